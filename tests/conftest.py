@@ -1,0 +1,34 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def orc_toy():
+    import oracle
+    import synth
+    return oracle.Oracle(**synth.PARAMS["toy"])
+
+
+@pytest.fixture(scope="session")
+def orc_mini():
+    import oracle
+    import synth
+    return oracle.Oracle(**synth.PARAMS["mini"])
+
+
+@pytest.fixture(scope="session")
+def orc_hyp():
+    import oracle
+    import synth
+    return oracle.Oracle(**synth.PARAMS["hyp"])
