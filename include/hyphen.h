@@ -1,0 +1,174 @@
+/*
+ * hyphen.h -- C ABI of the B200-native HyPHEN homomorphic-convolution hot path.
+ *
+ * HyPHEN: "HyPHEN: A Hybrid Packing Method and Its Optimizations for
+ * Homomorphic Encryption-Based Neural Networks" (arXiv 2302.02407).
+ * P:n below = line n of the paper source; "DESIGN R-x" = a reading
+ * of a point the paper leaves silent, listed in DESIGN.md "Readings".
+ *
+ * Problem statement: a client holds the secret key,
+ * encodes/encrypts an image and decrypts the result; a server holding weight
+ * plaintexts and evaluation keys runs the convolution layers on ciphertexts.
+ * Timing starts once weights and inputs are resident.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Scheme: RNS-CKKS over Z[X]/(X^N+1), N = 2^log_n, n = N/2 slots.
+ *  - Modulus chain ("chain index" t): q_0..q_{n_q-1} then p_0..p_{n_p-1}.
+ *    Hybrid key switching with dnum digits of alpha = ceil(n_q/dnum) q-limbs
+ *    (P:1232-1233); n_p = K special primes.
+ *  - Words: uint64, residues in [0, modulus).
+ *  - Polynomials are in the NTT (evaluation) domain, index k holding
+ *    a(psi^(2*br(k)+1)) (DESIGN R-NTT), unless a function says otherwise.
+ *  - Ciphertext at level l: device array [2][l+1][N] (c0 then c1), limb i on q_i.
+ *    Plaintext at level l: device array [l+1][N].
+ *    Evaluation (rotation) key: device array [dnum][2][n_q+n_p][N]
+ *    ([.][0] = b, [.][1] = a), generated at the full level and used at any
+ *    level l by reading q-limbs 0..l and the n_p p-limbs (DESIGN R-EVK).
+ *  - Ownership: every ciphertext/plaintext/key/workspace buffer is caller-
+ *    allocated device memory (in practice torch uint64/int64 tensors).  The
+ *    library never frees caller memory.  The context owns its read-only
+ *    tables (twiddles, basis-conversion constants), allocated at create time.
+ *  - Scratch: operations that need temporaries use the context workspace set
+ *    by hy_ctx_set_workspace(); hy_workspace_bytes() gives the size needed.
+ *  - Streams: every device call is asynchronous on the given cudaStream_t
+ *    (passed as void*; NULL = legacy default stream).  Calls on one context
+ *    must not run concurrently on different streams (they share the workspace).
+ *  - Errors: a hy_status is returned; outputs are unspecified on error and
+ *    hy_last_error() gives a thread-local message.  Preconditions are checked
+ *    on the host before any launch.  No exceptions cross the ABI.
+ */
+#ifndef HYPHEN_H_
+#define HYPHEN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HY_OK = 0,
+  HY_E_ARG = 1,             /* bad argument / null pointer / size */
+  HY_E_LEVEL_MISMATCH = 2,  /* operand levels differ (SPEC LevelMismatch) */
+  HY_E_LEVEL_EXHAUSTED = 3, /* level 0 operand to mul/rescale */
+  HY_E_SHAPE = 4,           /* shape / slot-count mismatch */
+  HY_E_CAPACITY = 5,        /* tensor does not fit the slots */
+  HY_E_FORMAT = 6,          /* unsupported packing / gap / transition */
+  HY_E_PLAN = 7,            /* conv plan inconsistent with the call */
+  HY_E_MISSING_KEY = 8,     /* no evaluation key given for a needed rotation */
+  HY_E_CUDA = 9,            /* CUDA runtime error */
+  HY_E_WORKSPACE = 10,      /* workspace missing or too small */
+  HY_E_NO_DEVICE = 11       /* no usable sm_100 device */
+} hy_status;
+
+typedef struct hy_ctx hy_ctx;
+
+typedef struct {
+  uint32_t log_n;          /* N = 2^log_n, 10 <= log_n <= 16 */
+  uint32_t n_q;            /* L+1 ciphertext primes (Set_hyp: 24) */
+  uint32_t n_p;            /* K special primes (>= alpha) */
+  uint32_t dnum;           /* key-switching digits (Set_hyp: 6) */
+  uint32_t hamming_weight; /* secret key weight (192) */
+  const uint32_t* q_bits;  /* n_q bit sizes (< 62) */
+  const uint32_t* p_bits;  /* n_p bit sizes (< 62) */
+} hy_params;
+
+/* ---- context ---------------------------------------------------------- */
+/* Generates the primes (DESIGN R-PRIMES: in chain order, the largest unused
+ * prime below 2^bits that is 1 mod 2N), roots (R-NTT) and all tables, and
+ * uploads them to `cuda_device`.  Fails with HY_E_NO_DEVICE when no CUDA
+ * device is present: there is no CPU fallback. */
+hy_status hy_ctx_create(const hy_params* params, int cuda_device, hy_ctx** out);
+void hy_ctx_destroy(hy_ctx* ctx);
+/* chain moduli: n_q + n_p words (host) */
+hy_status hy_ctx_moduli(const hy_ctx* ctx, uint64_t* out);
+uint32_t hy_ctx_alpha(const hy_ctx* ctx);
+uint32_t hy_ctx_n_digits(const hy_ctx* ctx, uint32_t level); /* beta = ceil((l+1)/alpha) */
+/* Bytes of workspace the context needs to run every operation up to level max_level
+ * with at most `max_terms` ciphertexts per batched call. */
+size_t hy_workspace_bytes(const hy_ctx* ctx, uint32_t max_level, uint32_t max_terms);
+hy_status hy_ctx_set_workspace(hy_ctx* ctx, void* d_ws, size_t bytes);
+const char* hy_last_error(void);
+/* number of kernels this context has launched since creation (for bench evidence) */
+uint64_t hy_ctx_launch_count(const hy_ctx* ctx);
+
+/* ---- transforms (exposed for parity tests of the sub-steps) ------------ */
+/* Negacyclic NTT / inverse NTT (P:97 ring; DESIGN R-NTT) of n_limbs limbs.
+ * d_in/d_out: [n_limbs][N] device (may alias); chain[u] = chain index of limb u (host array). */
+hy_status hy_ntt(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, const uint32_t* chain, uint32_t n_limbs,
+                 int inverse, void* stream);
+/* Automorphism X -> X^k in the NTT domain, same permutation on every limb.
+ * k: odd Galois element.  d_in/d_out [n_limbs][N], must not alias. */
+hy_status hy_automorph(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, uint32_t n_limbs, uint64_t k, void* stream);
+/* Galois element of a left rotation by r slots: 5^(r mod n) mod 2N. */
+uint64_t hy_galois_elt(const hy_ctx* ctx, int64_t r);
+
+/* ---- key switching pieces (DESIGN R-MODUP, R-MODDOWN) ------ */
+/* ModUp of one polynomial d given in the COEFFICIENT domain on q_0..q_l:
+ * d_ext out [beta][l+1+K][N] NTT domain; limbs of digit j's own primes are
+ * NTT(d) (fast basis conversion without correction elsewhere). */
+hy_status hy_modup(hy_ctx* ctx, uint32_t level, const uint64_t* d_coeff, uint64_t* d_ext, void* stream);
+/* u[c][t] = sum_j ext[j][t] * evk[j][c][chain(t)]  ([2][l+1+K][N] out). */
+hy_status hy_ks_inner_product(hy_ctx* ctx, uint32_t level, const uint64_t* d_ext, const uint64_t* d_evk,
+                              uint64_t* d_u, void* stream);
+/* ModDown of one polynomial [l+1+K][N] -> [l+1][N] (both NTT domain). */
+hy_status hy_moddown(hy_ctx* ctx, uint32_t level, const uint64_t* d_u, uint64_t* d_out, void* stream);
+
+/* ---- HRot: rotate LEFT by r slots, three variants (DESIGN R-HROT) - */
+/* plain: ModUp(kappa(c1)).  r = 0 (mod n) copies the input. */
+hy_status hy_hrot(hy_ctx* ctx, const uint64_t* d_evk, const uint64_t* d_ct, uint32_t level, int32_t r,
+                  uint64_t* d_out, void* stream);
+/* non-hoisted batch: out_i = HRot_{r_i}(ct_i) with key evk_i (host arrays of device pointers) */
+hy_status hy_hrot_batch(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* const* d_cts, uint32_t level,
+                        const int32_t* r, uint32_t n, uint64_t* const* d_outs, void* stream);
+/* hoisted (Slide_f): one ModUp of c1 shared by n rotations of the same ciphertext. */
+hy_status hy_hrot_hoisted(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* d_ct, uint32_t level,
+                          const int32_t* r, uint32_t n, uint64_t* const* d_outs, void* stream);
+/* lazy sum (Slide_1&Sum_f of reordered RAConv): sum_t HRot_{r_t}(ct_t) with the key-switch
+ * inner products accumulated over Q_l u P and ONE ModDown; r_t = 0 terms are added without switching
+ * (their evk pointer may be NULL). */
+hy_status hy_hrot_sum(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* const* d_cts, uint32_t level,
+                      const int32_t* r, uint32_t n, uint64_t* d_out, void* stream);
+
+/* ---- MulPt / AddCt / Rescale -------------------------------- */
+/* out = ct (.) pt limbwise; no auto-rescale (scale bookkeeping is the caller's). */
+hy_status hy_pmult(hy_ctx* ctx, const uint64_t* d_ct, const uint64_t* d_pt, uint32_t level, uint64_t* d_out,
+                   void* stream);
+/* MulFilter&Sum: out (+)= sum_i ct_i (.) pt_i, one reduction per output word.
+ * accumulate != 0 adds into d_out. */
+hy_status hy_pmult_acc(hy_ctx* ctx, const uint64_t* const* d_cts, const uint64_t* const* d_pts, uint32_t n,
+                       uint32_t level, uint64_t* d_out, int accumulate, void* stream);
+/* out = a + b over npoly polynomials ([npoly][l+1][N]); in-place allowed. */
+hy_status hy_add(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t npoly, uint32_t level,
+                 uint64_t* d_out, void* stream);
+/* Rescale (DESIGN R-RESCALE): [2][l+1][N] -> [2][l][N], exact round(c/q_l). */
+hy_status hy_rescale(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint64_t* d_out, void* stream);
+
+/* ---- client side: keys, encode, encrypt, decrypt (untimed) ------- */
+/* Rotation key for Galois element of a left rotation by r (DESIGN R-EVK, R-PRNG):
+ * secret from sk_seed, randomness from ek_seed.  d_evk: [dnum][2][n_q+n_p][N]. */
+hy_status hy_keygen_rot(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, int32_t r, uint64_t* d_evk, void* stream);
+hy_status hy_keygen_galois(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* d_evk, void* stream);
+/* Secret-key encryption of an NTT-domain plaintext at level l (DESIGN R-ENC). */
+hy_status hy_encrypt(hy_ctx* ctx, uint64_t sk_seed, uint64_t enc_seed, uint64_t ct_id, const uint64_t* d_pt,
+                     uint32_t level, uint64_t* d_ct, void* stream);
+/* m = c0 + c1*s (NTT domain). */
+hy_status hy_decrypt(hy_ctx* ctx, uint64_t sk_seed, const uint64_t* d_ct, uint32_t level, uint64_t* d_pt,
+                     void* stream);
+/* CKKS encode of n_slots <= N/2 real values (DESIGN R-ENCODE): exact integer scale,
+ * coefficients = round(scale * tau^{-1}(z)) computed in double-double precision,
+ * then reduced mod q_0..q_l and NTT'd into d_pt [l+1][N].  Synchronous w.r.t. the host buffer. */
+hy_status hy_encode(hy_ctx* ctx, const double* h_slots, uint32_t n_slots, uint64_t scale, uint32_t level,
+                    uint64_t* d_pt, void* stream);
+/* Host-only part of hy_encode: the N integer coefficients (no device needed). */
+hy_status hy_encode_coeffs(uint32_t log_n, const double* h_slots, uint32_t n_slots, uint64_t scale,
+                           int64_t* h_coeffs);
+/* Signed integer coefficients (host, N words) -> NTT-domain plaintext on q_0..q_l. */
+hy_status hy_pt_from_coeffs(hy_ctx* ctx, const int64_t* h_coeffs, uint32_t level, uint64_t* d_pt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYPHEN_H_ */

@@ -1,0 +1,288 @@
+"""paper_2302_02407_b200 -- B200-native HyPHEN homomorphic-convolution hot path.
+
+Thin Python binding over the C ABI of ``libhyphen.so`` (declared in
+``include/hyphen.h``).  Argument marshalling only: every step of the path runs
+in the library's sm_100a kernels.  PyTorch provides device memory (int64
+tensors holding the uint64 residues bit-for-bit), streams and process groups.
+There is no CPU fallback: when the library or a CUDA device is missing, the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhyphen.so")
+
+HY_ERRORS = {
+    0: "HY_OK", 1: "HY_E_ARG", 2: "HY_E_LEVEL_MISMATCH", 3: "HY_E_LEVEL_EXHAUSTED", 4: "HY_E_SHAPE",
+    5: "HY_E_CAPACITY", 6: "HY_E_FORMAT", 7: "HY_E_PLAN", 8: "HY_E_MISSING_KEY", 9: "HY_E_CUDA",
+    10: "HY_E_WORKSPACE", 11: "HY_E_NO_DEVICE",
+}
+
+
+class HyError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{HY_ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Params(C.Structure):
+    _fields_ = [("log_n", C.c_uint32), ("n_q", C.c_uint32), ("n_p", C.c_uint32), ("dnum", C.c_uint32),
+                ("hamming_weight", C.c_uint32), ("q_bits", C.POINTER(C.c_uint32)), ("p_bits", C.POINTER(C.c_uint32))]
+
+
+_lib = None
+_P = C.c_void_p
+_U64 = C.c_uint64
+_U32 = C.c_uint32
+_PP = C.POINTER(C.c_void_p)
+
+SIGNATURES = {
+    "hy_ctx_create": (C.c_int, [C.POINTER(_Params), C.c_int, C.POINTER(_P)]),
+    "hy_ctx_destroy": (None, [_P]),
+    "hy_ctx_moduli": (C.c_int, [_P, C.POINTER(_U64)]),
+    "hy_ctx_alpha": (_U32, [_P]),
+    "hy_ctx_n_digits": (_U32, [_P, _U32]),
+    "hy_workspace_bytes": (C.c_size_t, [_P, _U32, _U32]),
+    "hy_ctx_set_workspace": (C.c_int, [_P, _P, C.c_size_t]),
+    "hy_last_error": (C.c_char_p, []),
+    "hy_ctx_launch_count": (_U64, [_P]),
+    "hy_ntt": (C.c_int, [_P, _P, _P, C.POINTER(_U32), _U32, C.c_int, _P]),
+    "hy_automorph": (C.c_int, [_P, _P, _P, _U32, _U64, _P]),
+    "hy_galois_elt": (_U64, [_P, C.c_int64]),
+    "hy_modup": (C.c_int, [_P, _U32, _P, _P, _P]),
+    "hy_ks_inner_product": (C.c_int, [_P, _U32, _P, _P, _P, _P]),
+    "hy_moddown": (C.c_int, [_P, _U32, _P, _P, _P]),
+    "hy_hrot": (C.c_int, [_P, _P, _P, _U32, C.c_int32, _P, _P]),
+    "hy_hrot_batch": (C.c_int, [_P, _PP, _PP, _U32, C.POINTER(C.c_int32), _U32, _PP, _P]),
+    "hy_hrot_hoisted": (C.c_int, [_P, _PP, _P, _U32, C.POINTER(C.c_int32), _U32, _PP, _P]),
+    "hy_hrot_sum": (C.c_int, [_P, _PP, _PP, _U32, C.POINTER(C.c_int32), _U32, _P, _P]),
+    "hy_pmult": (C.c_int, [_P, _P, _P, _U32, _P, _P]),
+    "hy_pmult_acc": (C.c_int, [_P, _PP, _PP, _U32, _U32, _P, C.c_int, _P]),
+    "hy_add": (C.c_int, [_P, _P, _P, _U32, _U32, _P, _P]),
+    "hy_rescale": (C.c_int, [_P, _P, _U32, _P, _P]),
+    "hy_keygen_rot": (C.c_int, [_P, _U64, _U64, C.c_int32, _P, _P]),
+    "hy_keygen_galois": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
+    "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
+    "hy_decrypt": (C.c_int, [_P, _U64, _P, _U32, _P, _P]),
+    "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
+    "hy_encode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), _U32, _U64, C.POINTER(C.c_int64)]),
+    "hy_pt_from_coeffs": (C.c_int, [_P, C.POINTER(C.c_int64), _U32, _P, _P]),
+}
+
+
+def lib():
+    """Load libhyphen.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2302_02407_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(code: int):
+    if code != 0:
+        raise HyError(code, lib().hy_last_error().decode())
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def _ptr_array(ts):
+    a = (C.c_void_p * max(1, len(ts)))()
+    for i, t in enumerate(ts):
+        a[i] = _ptr(t)
+    return a
+
+
+def encode_coeffs(log_n: int, slots, scale: int) -> np.ndarray:
+    """Host-side CKKS encoding (DESIGN R-ENCODE): N signed integer coefficients."""
+    z = np.ascontiguousarray(slots, np.float64)
+    out = np.zeros(1 << log_n, np.int64)
+    _check(lib().hy_encode_coeffs(log_n, z.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale),
+                                  out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+class Context:
+    """One RNS-CKKS context on one CUDA device (see include/hyphen.h)."""
+
+    def __init__(self, log_n, q_bits, p_bits, dnum, h=192, device=0, max_level=None, **_):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.log_n, self.N, self.n = log_n, 1 << log_n, 1 << (log_n - 1)
+        self.n_q, self.n_p, self.dnum, self.h = len(q_bits), len(p_bits), dnum, h
+        self._qb = (C.c_uint32 * len(q_bits))(*q_bits)
+        self._pb = (C.c_uint32 * len(p_bits))(*p_bits)
+        prm = _Params(log_n, len(q_bits), len(p_bits), dnum, h, self._qb, self._pb)
+        h_ = C.c_void_p()
+        _check(lib().hy_ctx_create(C.byref(prm), device, C.byref(h_)))
+        self._c = h_
+        mods = (C.c_uint64 * (self.n_q + self.n_p))()
+        _check(lib().hy_ctx_moduli(self._c, mods))
+        self.moduli = [int(x) for x in mods]
+        self.q, self.p = self.moduli[: self.n_q], self.moduli[self.n_q:]
+        self.alpha = int(lib().hy_ctx_alpha(self._c))
+        self.max_level = self.n_q - 1 if max_level is None else max_level
+        nbytes = int(lib().hy_workspace_bytes(self._c, self.max_level, 1))
+        # key generation needs 3 (n_q+n_p) limbs; make sure the workspace covers it
+        nbytes = max(nbytes, (3 * (self.n_q + self.n_p) + 2) * self.N * 8 + (1 << 16))
+        self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device=self.device)
+        _check(lib().hy_ctx_set_workspace(self._c, self.ws.data_ptr(), self.ws.numel() * 8))
+
+    def __del__(self):
+        if getattr(self, "_c", None):
+            lib().hy_ctx_destroy(self._c)
+            self._c = None
+
+    # -- helpers ---------------------------------------------------------
+    def _stream(self):
+        return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def empty(self, *shape):
+        return self.torch.empty(*shape, dtype=self.torch.int64, device=self.device)
+
+    def zeros(self, *shape):
+        return self.torch.zeros(*shape, dtype=self.torch.int64, device=self.device)
+
+    def ct_shape(self, level):
+        return (2, level + 1, self.N)
+
+    def evk_shape(self):
+        return (self.dnum, 2, self.n_q + self.n_p, self.N)
+
+    def n_digits(self, level):
+        return int(lib().hy_ctx_n_digits(self._c, level))
+
+    def galois_elt(self, r: int) -> int:
+        return int(lib().hy_galois_elt(self._c, int(r)))
+
+    def launch_count(self) -> int:
+        return int(lib().hy_ctx_launch_count(self._c))
+
+    # -- transforms ------------------------------------------------------
+    def ntt(self, x, chain: Sequence[int], inverse=False, out=None):
+        out = self.empty(*x.shape) if out is None else out
+        ch = (C.c_uint32 * len(chain))(*chain)
+        _check(lib().hy_ntt(self._c, _ptr(x), _ptr(out), ch, len(chain), int(inverse), self._stream()))
+        return out
+
+    def automorph(self, x, k: int, out=None):
+        out = self.empty(*x.shape) if out is None else out
+        nl = x.numel() // self.N
+        _check(lib().hy_automorph(self._c, _ptr(x), _ptr(out), nl, int(k), self._stream()))
+        return out
+
+    # -- key switching ---------------------------------------------------
+    def modup(self, level, d_coeff):
+        ext = self.empty(self.n_digits(level), level + 1 + self.n_p, self.N)
+        _check(lib().hy_modup(self._c, level, _ptr(d_coeff), _ptr(ext), self._stream()))
+        return ext
+
+    def ks_inner_product(self, level, ext, evk):
+        u = self.empty(2, level + 1 + self.n_p, self.N)
+        _check(lib().hy_ks_inner_product(self._c, level, _ptr(ext), _ptr(evk), _ptr(u), self._stream()))
+        return u
+
+    def moddown(self, level, u_poly):
+        out = self.empty(level + 1, self.N)
+        _check(lib().hy_moddown(self._c, level, _ptr(u_poly), _ptr(out), self._stream()))
+        return out
+
+    def hrot(self, evk, ct, level, r, out=None):
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_hrot(self._c, _ptr(evk), _ptr(ct), level, int(r), _ptr(out), self._stream()))
+        return out
+
+    def hrot_batch(self, evks, cts, level, rs, outs=None):
+        outs = [self.empty(*self.ct_shape(level)) for _ in cts] if outs is None else outs
+        r = (C.c_int32 * len(rs))(*rs)
+        _check(lib().hy_hrot_batch(self._c, _ptr_array(evks), _ptr_array(cts), level, r, len(rs),
+                                   _ptr_array(outs), self._stream()))
+        return outs
+
+    def hrot_hoisted(self, evks, ct, level, rs, outs=None):
+        outs = [self.empty(*self.ct_shape(level)) for _ in rs] if outs is None else outs
+        r = (C.c_int32 * len(rs))(*rs)
+        _check(lib().hy_hrot_hoisted(self._c, _ptr_array(evks), _ptr(ct), level, r, len(rs),
+                                     _ptr_array(outs), self._stream()))
+        return outs
+
+    def hrot_sum(self, evks, cts, level, rs, out=None):
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        r = (C.c_int32 * len(rs))(*rs)
+        _check(lib().hy_hrot_sum(self._c, _ptr_array(evks), _ptr_array(cts), level, r, len(rs), _ptr(out),
+                                 self._stream()))
+        return out
+
+    # -- MulPt / AddCt / Rescale -----------------------------------------
+    def pmult(self, ct, pt, level, out=None):
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_pmult(self._c, _ptr(ct), _ptr(pt), level, _ptr(out), self._stream()))
+        return out
+
+    def pmult_acc(self, cts, pts, level, out=None, accumulate=False):
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_pmult_acc(self._c, _ptr_array(cts), _ptr_array(pts), len(cts), level, _ptr(out),
+                                  int(accumulate), self._stream()))
+        return out
+
+    def add(self, a, b, level, out=None, npoly=2):
+        out = self.empty(*a.shape) if out is None else out
+        _check(lib().hy_add(self._c, _ptr(a), _ptr(b), npoly, level, _ptr(out), self._stream()))
+        return out
+
+    def rescale(self, ct, level, out=None):
+        out = self.empty(*self.ct_shape(level - 1)) if out is None else out
+        _check(lib().hy_rescale(self._c, _ptr(ct), level, _ptr(out), self._stream()))
+        return out
+
+    # -- client side -----------------------------------------------------
+    def keygen_rot(self, sk_seed, ek_seed, r, out=None):
+        out = self.empty(*self.evk_shape()) if out is None else out
+        _check(lib().hy_keygen_rot(self._c, sk_seed, ek_seed, int(r), _ptr(out), self._stream()))
+        return out
+
+    def keygen_galois(self, sk_seed, ek_seed, k, out=None):
+        out = self.empty(*self.evk_shape()) if out is None else out
+        _check(lib().hy_keygen_galois(self._c, sk_seed, ek_seed, int(k), _ptr(out), self._stream()))
+        return out
+
+    def encrypt(self, sk_seed, enc_seed, ct_id, pt, level, out=None):
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_encrypt(self._c, sk_seed, enc_seed, ct_id, _ptr(pt), level, _ptr(out), self._stream()))
+        return out
+
+    def decrypt(self, sk_seed, ct, level, out=None):
+        out = self.empty(level + 1, self.N) if out is None else out
+        _check(lib().hy_decrypt(self._c, sk_seed, _ptr(ct), level, _ptr(out), self._stream()))
+        return out
+
+    def encode(self, slots, scale, level, out=None):
+        out = self.empty(level + 1, self.N) if out is None else out
+        z = np.ascontiguousarray(slots, np.float64)
+        _check(lib().hy_encode(self._c, z.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale), level,
+                               _ptr(out), self._stream()))
+        return out
+
+    def pt_from_coeffs(self, coeffs, level, out=None):
+        out = self.empty(level + 1, self.N) if out is None else out
+        cf = np.ascontiguousarray(coeffs, np.int64)
+        _check(lib().hy_pt_from_coeffs(self._c, cf.ctypes.data_as(C.POINTER(C.c_int64)), level, _ptr(out),
+                                       self._stream()))
+        return out

@@ -1,0 +1,123 @@
+// hy_internal.h -- context layout and launcher declarations shared by the
+// product's CUDA translation units.  Nothing here is visible through the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hyphen.h"
+
+namespace hy {
+
+constexpr int kMaxChain = 64;   // n_q + n_p
+constexpr int kMaxBatch = 256;  // limbs per batched NTT launch
+constexpr int kMaxDigits = 16;
+constexpr int kMaxExt = 48;     // l+1+K
+
+// Per-prime constants (device resident, indexed by chain index).
+struct PrimeConst {
+  uint64_t q;
+  uint64_t two_q;
+  uint64_t mu;          // floor(2^64 / q)            (Barrett for 64-bit words)
+  uint64_t r64;         // 2^64 mod q                 (128-bit reduction)
+  uint64_t r64_sh;      // Shoup companion of r64
+  uint64_t n_inv;       // N^{-1} mod q
+  uint64_t n_inv_sh;
+};
+
+// Basis-conversion constants for one (level, digit): ModUp  D_j -> other limbs.
+struct ModUpConst {
+  int lo, hi;                               // q-limb range of digit j
+  uint64_t hat_inv[8], hat_inv_sh[8];      // (D_j/q_i)^{-1} mod q_i
+  // (D_j/q_i) mod t for every ext limb u (u indexes Q_l u P), [u][i]
+  uint64_t hat_mod[kMaxExt][8];
+};
+
+struct ModDownConst {
+  uint64_t phat_inv[8], phat_inv_sh[8];    // (P/p_k)^{-1} mod p_k
+  uint64_t phat_mod[kMaxChain][8];         // (P/p_k) mod q_i
+  uint64_t p_inv[kMaxChain], p_inv_sh[kMaxChain];  // P^{-1} mod q_i
+};
+
+struct RescaleConst {  // for dropping q_l
+  uint64_t ql_inv[kMaxChain], ql_inv_sh[kMaxChain];  // q_l^{-1} mod q_i
+};
+
+struct DevTables {
+  const uint64_t* tw;      // [chain][N] psi^{br(k)}
+  const uint64_t* tw_sh;   // Shoup companions
+  const uint64_t* itw;     // [chain][N] psi^{-br(k)}
+  const uint64_t* itw_sh;
+  const PrimeConst* pc;    // [chain]
+};
+
+}  // namespace hy
+
+struct hy_ctx {
+  int device = 0;
+  uint32_t log_n = 0, N = 0, n_q = 0, n_p = 0, dnum = 0, alpha = 0, h = 0;
+  std::vector<uint64_t> mod;      // chain moduli
+  std::vector<uint64_t> psi;
+  hy::DevTables dt{};
+  void* d_tables = nullptr;       // single allocation behind dt
+  // per-level constant blocks (device), index = level
+  std::vector<hy::ModUpConst*> d_modup;      // [level] -> device array [beta]
+  std::vector<hy::ModDownConst*> d_moddown;  // [level]
+  std::vector<hy::RescaleConst*> d_rescale;  // [level] (drop q_level)
+  // host copies (used to fill launch parameters)
+  std::vector<std::vector<hy::ModUpConst>> h_modup;
+  std::vector<hy::ModDownConst> h_moddown;
+  std::vector<hy::RescaleConst> h_rescale;
+  // workspace
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  uint64_t launches = 0;
+};
+
+namespace hy {
+
+// error plumbing
+hy_status fail(hy_status s, const std::string& msg);
+hy_status cuda_check(const char* what);
+inline cudaStream_t st(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline uint32_t n_digits(const hy_ctx* c, uint32_t level) { return (level + 1 + c->alpha - 1) / c->alpha; }
+inline uint32_t ext_chain(const hy_ctx* c, uint32_t level, uint32_t u) {
+  return u <= level ? u : c->n_q + (u - level - 1);
+}
+
+// A batch of limbs for one launch: src/dst pointer and chain index per limb.
+struct LimbBatch {
+  const uint64_t* src[kMaxBatch];
+  uint64_t* dst[kMaxBatch];
+  uint8_t chain[kMaxBatch];
+  int n;
+};
+
+// NTT launchers (hy_ntt.cu)
+void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
+// convenience: contiguous [n][N] arrays with chain indices
+void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
+                cudaStream_t s);
+
+// elementwise / keyswitch launchers (hy_ops.cu / hy_keyswitch.cu)
+void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
+
+// workspace carving
+struct Ws {
+  uint8_t* p;
+  size_t left;
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    if (bytes > left) return nullptr;
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+
+}  // namespace hy

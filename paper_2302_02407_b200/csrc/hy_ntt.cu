@@ -1,0 +1,287 @@
+// hy_ntt.cu -- batched negacyclic NTT / inverse NTT for N = 2^10 .. 2^16 on sm_100a.
+//
+// Transform (DESIGN R-NTT): merged-twiddle Cooley-Tukey forward with
+// psi^{br(k)} twiddles, output in bit-reversed order (index k holds
+// a(psi^(2 br(k)+1))); Gentleman-Sande inverse.  At the stage whose butterfly
+// distance is t, the element x uses twiddle index (N + x) / (2t).
+//
+// Decomposition: N = R x 256 (R = N/256 rows of 256 contiguous words).
+//   pass A: the log2(R) stages with t >= 256 -- R-point transforms down the
+//           columns (x = r*256 + c);
+//   pass B: the 8 stages with t < 256 -- 256-point transforms along each row.
+// Forward = A then B; inverse = B then A (with the N^{-1} scaling fused in).
+// Each 256-point transform lives in registers, 8 words per thread, and moves
+// through shared memory twice (layouts L1 -> L2 -> L3) so that every stage is
+// a register-local butterfly: L1 owns bits {7,6,5}, L2 {4,3,2}, L3 {1,0}.
+#include "hy_arith.cuh"
+
+namespace hy {
+namespace {
+
+template <int LAY>
+__device__ __forceinline__ int elem(int l, int k) {
+  if (LAY == 1) return l + 32 * k;
+  if (LAY == 2) return 32 * (l >> 2) + 4 * k + (l & 3);
+  return 4 * (l + 32 * (k >> 2)) + (k & 3);
+}
+template <int LAY>
+__device__ __forceinline__ int kbit(int s) {
+  return LAY == 1 ? s - 5 : (LAY == 2 ? s - 2 : s);
+}
+
+// Run stages [s_lo, s_hi] (forward: descending, inverse: ascending) on the 8
+// register words of one thread in layout LAY.  Twiddle index = (base + e) >> (s+1).
+template <int LAY, bool FWD>
+__device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, int s_lo, uint32_t base,
+                                           const uint64_t* __restrict__ W, const uint64_t* __restrict__ Ws,
+                                           uint64_t q) {
+#pragma unroll
+  for (int it = 0; it <= s_hi - s_lo; ++it) {
+    const int s = FWD ? s_hi - it : s_lo + it;
+    const int kb = 1 << kbit<LAY>(s);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k & kb) continue;
+      const int e = elem<LAY>(l, k);
+      const uint32_t idx = (base + (uint32_t)e) >> (s + 1);
+      const uint64_t w = __ldg(W + idx), ws = __ldg(Ws + idx);
+      uint64_t a = x[k], b = x[k | kb];
+      if (FWD) {
+        uint64_t t = shoup(b, w, ws, q);
+        x[k] = add_mod(a, t, q);
+        x[k | kb] = sub_mod(a, t, q);
+      } else {
+        x[k] = add_mod(a, b, q);
+        x[k | kb] = shoup(sub_mod(a, b, q), w, ws, q);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
+
+// ---------------------------------------------------------------- pass B (rows)
+// CTA = 8 warps, one 256-word row per warp.  grid = (N/256/8, n_limbs)
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int logN) {
+  __shared__ uint64_t sm[8][272];
+  const int limb = blockIdx.y, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + w;
+  const size_t N = (size_t)1 << logN;
+  if (row >= (int)(N >> 8)) return;  // N = 2^10: 4 rows in an 8-warp CTA
+  const int t = b.chain[limb];
+  const uint64_t q = dt.pc[t].q;
+  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
+  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const uint64_t* src = b.src[limb] + (size_t)row * 256;
+  uint64_t* dst = b.dst[limb] + (size_t)row * 256;
+  uint64_t* S = sm[w];
+  const uint32_t base = (uint32_t)N + (uint32_t)row * 256;
+  uint64_t x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = src[elem<1>(l, k)];
+  if (FWD) {
+    run_stages<1, true>(x, l, 7, 5, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
+    run_stages<2, true>(x, l, 4, 2, base, W, Ws, q);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
+    run_stages<3, true>(x, l, 1, 0, base, W, Ws, q);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = S[pidx(elem<1>(l, k))];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
+    run_stages<3, false>(x, l, 1, 0, base, W, Ws, q);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
+    run_stages<2, false>(x, l, 4, 2, base, W, Ws, q);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<1>(l, k))];
+    run_stages<1, false>(x, l, 7, 5, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = x[k];
+  }
+}
+
+// ---------------------------------------------------------------- pass A (columns), R = 256
+// CTA = 512 threads: column c = tid & 15 of a 16-column strip, virtual lane l = tid >> 4.
+// grid = (256/16, n_limbs)
+template <bool FWD>
+__global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, int logN) {
+  __shared__ uint64_t sm[16 * 273];
+  const int limb = blockIdx.y, c = threadIdx.x & 15, l = threadIdx.x >> 4;
+  const int col = blockIdx.x * 16 + c;
+  const int t = b.chain[limb];
+  const size_t N = (size_t)1 << logN;
+  const PrimeConst& pc = dt.pc[t];
+  const uint64_t q = pc.q;
+  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
+  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const uint64_t* src = FWD ? b.src[limb] : b.dst[limb];  // inverse runs in place after pass B
+  uint64_t* dst = b.dst[limb];
+  uint64_t* S = sm + c * 273;
+  const uint32_t base = 256;  // R
+  uint64_t x[8];
+  if (FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<1>(l, k) * 256 + col];
+    run_stages<1, true>(x, l, 7, 5, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[elem<1>(l, k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+    run_stages<2, true>(x, l, 4, 2, base, W, Ws, q);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
+    run_stages<3, true>(x, l, 1, 0, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = x[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<3>(l, k) * 256 + col];
+    run_stages<3, false>(x, l, 1, 0, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[elem<3>(l, k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+    run_stages<2, false>(x, l, 4, 2, base, W, Ws, q);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = S[elem<1>(l, k)];
+    run_stages<1, false>(x, l, 7, 5, base, W, Ws, q);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      dst[(size_t)elem<1>(l, k) * 256 + col] = shoup(x[k], pc.n_inv, pc.n_inv_sh, q);
+  }
+}
+
+// ---------------------------------------------------------------- pass A, generic R < 256
+// CTA = 256 threads on a strip of 16 columns x R rows held in shared memory.
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables dt, int logN) {
+  __shared__ uint64_t sm[128 * 16];
+  const int limb = blockIdx.y;
+  const int logR = logN - 8, R = 1 << logR;
+  const int t = b.chain[limb];
+  const size_t N = (size_t)1 << logN;
+  const PrimeConst& pc = dt.pc[t];
+  const uint64_t q = pc.q;
+  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
+  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const uint64_t* src = FWD ? b.src[limb] : b.dst[limb];
+  uint64_t* dst = b.dst[limb];
+  const int col0 = blockIdx.x * 16;
+  for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
+    int r = i >> 4, c = i & 15;
+    sm[i] = src[(size_t)r * 256 + col0 + c];
+  }
+  __syncthreads();
+  for (int it = 0; it < logR; ++it) {
+    const int s = FWD ? logR - 1 - it : it;
+    const int half = 1 << s;
+    for (int bf = threadIdx.x; bf < (R / 2) * 16; bf += blockDim.x) {
+      int c = bf & 15, j = bf >> 4;                       // butterfly j in [0, R/2)
+      int r = ((j >> s) << (s + 1)) | (j & (half - 1));   // lower element row
+      uint32_t idx = (uint32_t)(R + r) >> (s + 1);
+      uint64_t w = W[idx], ws = Ws[idx];
+      uint64_t a = sm[r * 16 + c], bb = sm[(r + half) * 16 + c];
+      if (FWD) {
+        uint64_t tt = shoup(bb, w, ws, q);
+        sm[r * 16 + c] = add_mod(a, tt, q);
+        sm[(r + half) * 16 + c] = sub_mod(a, tt, q);
+      } else {
+        sm[r * 16 + c] = add_mod(a, bb, q);
+        sm[(r + half) * 16 + c] = shoup(sub_mod(a, bb, q), w, ws, q);
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
+    int r = i >> 4, c = i & 15;
+    uint64_t v = sm[i];
+    if (!FWD) v = shoup(v, pc.n_inv, pc.n_inv_sh, q);
+    dst[(size_t)r * 256 + col0 + c] = v;
+  }
+}
+
+}  // namespace
+
+void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
+  if (b.n == 0) return;
+  const int logN = (int)c->log_n;
+  const int R = (int)c->N / 256;
+  dim3 gB(R / 8 > 0 ? R / 8 : 1, b.n), gA(256 / 16, b.n);
+  if (!inverse) {
+    if (R == 256) k_ntt_cols256<true><<<gA, 512, 0, s>>>(b, c->dt, logN);
+    else k_ntt_cols_small<true><<<gA, 256, 0, s>>>(b, c->dt, logN);
+    // pass B runs in place on dst
+    LimbBatch b2 = b;
+    for (int i = 0; i < b.n; ++i) b2.src[i] = b.dst[i];
+    k_ntt_rows<true><<<gB, 256, 0, s>>>(b2, c->dt, logN);
+  } else {
+    k_ntt_rows<false><<<gB, 256, 0, s>>>(b, c->dt, logN);
+    if (R == 256) k_ntt_cols256<false><<<gA, 512, 0, s>>>(b, c->dt, logN);
+    else k_ntt_cols_small<false><<<gA, 256, 0, s>>>(b, c->dt, logN);
+  }
+  c->launches += 2;
+}
+
+void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
+                cudaStream_t s) {
+  LimbBatch b;
+  for (uint32_t done = 0; done < n;) {
+    uint32_t m = std::min<uint32_t>(n - done, kMaxBatch);
+    b.n = (int)m;
+    for (uint32_t i = 0; i < m; ++i) {
+      b.src[i] = in + (size_t)(done + i) * c->N;
+      b.dst[i] = out + (size_t)(done + i) * c->N;
+      b.chain[i] = (uint8_t)chain[done + i];
+    }
+    launch_ntt(c, b, inverse, s);
+    done += m;
+  }
+}
+
+}  // namespace hy
+
+extern "C" hy_status hy_ntt(hy_ctx* c, const uint64_t* d_in, uint64_t* d_out, const uint32_t* chain,
+                            uint32_t n_limbs, int inverse, void* stream) {
+  if (!c || !d_in || !d_out || !chain) return hy::fail(HY_E_ARG, "null argument");
+  for (uint32_t i = 0; i < n_limbs; ++i)
+    if (chain[i] >= c->n_q + c->n_p) return hy::fail(HY_E_ARG, "chain index out of range");
+  hy::ntt_contig(c, d_in, d_out, chain, n_limbs, inverse != 0, hy::st(stream));
+  return hy::cuda_check("hy_ntt");
+}

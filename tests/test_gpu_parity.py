@@ -1,0 +1,173 @@
+"""GPU parity: every RNS-CKKS step of the CUDA path vs the CPU oracle, bit-exact
+on every limb, through the C ABI (paper_2302_02407_b200 binding)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SK = synth.SEED_SK
+EK = synth.SEED_EVK
+
+
+def to_np(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def to_dev(a, ctx):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(ctx.device)
+
+
+@pytest.fixture(scope="module", params=["toy", "mini", "hyp"])
+def pair(request):
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS[request.param]
+    return request.param, hy.Context(**prm), oracle.Oracle(**prm)
+
+
+def rand_limbs(o, seed, chain):
+    g = np.random.default_rng(seed)
+    return np.stack([g.integers(0, int(o.moduli[t]), o.N, dtype=np.uint64) for t in chain])
+
+
+def test_moduli(pair):
+    _, ctx, o = pair
+    assert ctx.moduli == [int(x) for x in o.moduli]
+    assert ctx.alpha == o.alpha
+
+
+def test_ntt_forward_inverse(pair):
+    _, ctx, o = pair
+    chain = list(range(o.nq + o.np_))
+    a = rand_limbs(o, 1, chain)
+    A = to_np(ctx.ntt(to_dev(a, ctx), chain))
+    want = np.stack([o.ntt(a[t], t) for t in chain])
+    assert np.array_equal(A, want)
+    back = to_np(ctx.ntt(to_dev(A, ctx), chain, inverse=True))
+    assert np.array_equal(back, a)
+    # ragged batch with repeated primes
+    ch2 = [0, 0, chain[-1], 1]
+    b = rand_limbs(o, 2, ch2)
+    assert np.array_equal(to_np(ctx.ntt(to_dev(b, ctx), ch2)), np.stack([o.ntt(b[i], t) for i, t in enumerate(ch2)]))
+
+
+def test_automorph(pair):
+    _, ctx, o = pair
+    chain = [0, 1]
+    a = rand_limbs(o, 3, chain)
+    for r in [1, 5, -1, o.n - 3]:
+        k = o.galois_elt(r)
+        assert ctx.galois_elt(r) == k
+        A = np.stack([o.ntt(a[t], t) for t in chain])
+        got = to_np(ctx.automorph(to_dev(A, ctx), k))
+        want = np.stack([o.ntt(o.automorph_coeff(a[t], t, k), t) for t in chain])
+        assert np.array_equal(got, want)
+
+
+def test_keygen(pair):
+    name, ctx, o = pair
+    for r in ([1, -7] if name != "hyp" else [3]):
+        assert np.array_equal(to_np(ctx.keygen_rot(SK, EK, r)), o.keygen_rot(SK, EK, r))
+
+
+def test_encode_encrypt_decrypt(pair):
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    z = synth.slots_uniform(30, o.n)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    pt = ctx.encode(z, scale, level)
+    opt = o.encode(z, scale, level)
+    assert np.array_equal(to_np(pt), opt.data)
+    ct = ctx.encrypt(SK, 41, 7, pt, level)
+    oct_ = o.encrypt(SK, 41, 7, opt)
+    assert np.array_equal(to_np(ct), oct_.data)
+    dec = ctx.decrypt(SK, ct, level)
+    assert np.array_equal(to_np(dec), o.decrypt(SK, oct_).data)
+
+
+def test_modup_ip_moddown(pair):
+    name, ctx, o = pair
+    for level in sorted({o.nq - 1, 0, min(5, o.nq - 1)}):
+        d = rand_limbs(o, 10 + level, list(range(level + 1)))
+        ext = ctx.modup(level, to_dev(d, ctx))
+        oext = o.modup_coeff(level, d)
+        assert np.array_equal(to_np(ext), oext)
+        evk = o.keygen_rot(SK, EK, 1) if name != "hyp" else None
+        if evk is not None:
+            u = ctx.ks_inner_product(level, ext, to_dev(evk, ctx))
+            ou = o.ks_inner_product(level, oext, evk)
+            assert np.array_equal(to_np(u), ou)
+        chain = o.ext_chain(level)
+        uu = rand_limbs(o, 20 + level, chain)
+        assert np.array_equal(to_np(ctx.moddown(level, to_dev(uu, ctx))), o.moddown(level, uu))
+
+
+def _fresh_ct(ctx, o, name, level, seed):
+    z = synth.slots_uniform(seed, o.n)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    opt = o.encode(z, scale, level)
+    oct_ = o.encrypt(SK, 50, seed, opt)
+    return to_dev(oct_.data, ctx), oct_
+
+
+def test_hrot_plain_and_batch(pair):
+    name, ctx, o = pair
+    level = o.nq - 1
+    rs = [1, -1, 9] if name != "hyp" else [5]
+    evks = [o.keygen_rot(SK, EK, r) for r in rs]
+    d_evks = [to_dev(e, ctx) for e in evks]
+    cts = [_fresh_ct(ctx, o, name, level, 60 + i) for i in range(len(rs))]
+    for (dct, oct_), r, e, de in zip(cts, rs, evks, d_evks):
+        got = to_np(ctx.hrot(de, dct, level, r))
+        assert np.array_equal(got, o.hrot(oct_, e, r).data), r
+    outs = ctx.hrot_batch(d_evks, [c[0] for c in cts], level, rs)
+    for out, (dct, oct_), r, e in zip(outs, cts, rs, evks):
+        assert np.array_equal(to_np(out), o.hrot(oct_, e, r).data)
+    # r = 0 and r = n are copies
+    assert np.array_equal(to_np(ctx.hrot(d_evks[0], cts[0][0], level, 0)), cts[0][1].data)
+    assert np.array_equal(to_np(ctx.hrot(d_evks[0], cts[0][0], level, o.n)), cts[0][1].data)
+
+
+def test_hrot_hoisted(pair):
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    rs = [1, 0, -1, 8] if name != "hyp" else [1, 32, -64]
+    evks = [o.keygen_rot(SK, EK, r) if o.galois_elt(r) != 1 else None for r in rs]
+    dct, oct_ = _fresh_ct(ctx, o, name, level, 70)
+    d_evks = [to_dev(e, ctx) if e is not None else None for e in evks]
+    outs = ctx.hrot_hoisted(d_evks, dct, level, rs)
+    oo = o.hrot_hoisted(oct_, [e if e is not None else np.zeros(1, np.uint64) for e in evks], rs)
+    for a, b in zip(outs, oo):
+        assert np.array_equal(to_np(a), b.data)
+
+
+def test_hrot_sum(pair):
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 6
+    rs = [1, 0, -1, 7] if name != "hyp" else [1, 0, -9]
+    evks = [o.keygen_rot(SK, EK, r) if o.galois_elt(r) != 1 else None for r in rs]
+    cts = [_fresh_ct(ctx, o, name, level, 80 + i) for i in range(len(rs))]
+    got = ctx.hrot_sum([to_dev(e, ctx) if e is not None else None for e in evks], [c[0] for c in cts], level, rs)
+    want = o.hrot_sum([c[1] for c in cts], evks, rs)
+    assert np.array_equal(to_np(got), want.data)
+
+
+def test_pmult_add_rescale(pair):
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    a = rand_limbs(o, 90, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+    b = rand_limbs(o, 91, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+    pts = [rand_limbs(o, 92 + i, list(range(level + 1))) for i in range(3)]
+    A, B = oracle.Ct(a, level, 1.0), oracle.Ct(b, level, 1.0)
+    da, db = to_dev(a, ctx), to_dev(b, ctx)
+    dp = [to_dev(p, ctx) for p in pts]
+    assert np.array_equal(to_np(ctx.add(da, db, level)), o.add(A, B).data)
+    assert np.array_equal(to_np(ctx.pmult(da, dp[0], level)), o.pmult(A, oracle.Pt(pts[0], level, 1.0)).data)
+    acc = ctx.pmult_acc([da, db, da], dp, level)
+    want = o.add(o.add(o.pmult(A, oracle.Pt(pts[0], level, 1.0)), o.pmult(B, oracle.Pt(pts[1], level, 1.0))),
+                 o.pmult(A, oracle.Pt(pts[2], level, 1.0)))
+    assert np.array_equal(to_np(acc), want.data)
+    assert np.array_equal(to_np(ctx.rescale(da, level)), o.rescale(A).data)
