@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""bench.py -- HyPHEN hot-path benchmark on B200 (BASELINE.json config 2).
+
+Workload (BASELINE.json configs[1]): HRot / key-switch microbenchmark at
+N = 2^16 over the full limb chain of Set_hyp (L+1 = 24, dnum = 6, K = 4;
+P:1207-1208): one step = a batch of 64 non-hoisted rotations, ct_i rotated by
+r_i = i + 1 with its own evaluation key (64 x 168 MiB of keys resident in HBM,
+larger than L2, so no flush is needed).  The hoisted batch (ct_0 rotated by
+1..64 with one shared ModUp) is reported alongside.
+
+Metric: key switches per second (whole job, all ranks).  Multi-GPU: every rank
+runs its own independent batch (weak scaling, no data-path collective);
+timing is the max over ranks of the device time between barriers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+``--impl reference`` times the CPU oracle (oracle/, test infrastructure) on the
+host cores as the reference arm; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+BATCH = 64
+LEVEL = 23  # full chain: L+1 = 24 limbs
+METRIC = "HRot keyswitch/s at N=2^16 (HBM GB/s vs peak); ResNet-20 conv-layer ms at 1/2/4/8 GPU"
+UNIT = "keyswitch/s"
+N = 1 << 16
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- distributed
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------- CPU oracle timing
+def oracle_keyswitch_rate(n_rot: int, level: int = LEVEL, seed: int = 0):
+    """Time the CPU oracle's plain HRot at Set_hyp, on n_rot rotations (bounded sample).
+    Key material is seeded uniform residues: the oracle's work is data-independent."""
+    import oracle
+    o = oracle.Oracle(**synth.PARAMS["hyp"])
+    chain_all = list(range(o.nq + o.np_))
+    evk = synth.residues(seed, (o.dnum * 2, len(chain_all), o.N), [int(o.moduli[t]) for t in chain_all]) \
+        .reshape(o.dnum, 2, len(chain_all), o.N)
+    ct = synth.residues(seed + 1, (2, level + 1, o.N), o.q[: level + 1])
+    c = oracle.Ct(ct, level, 2.0**42)
+    t0 = time.perf_counter()
+    for i in range(n_rot):
+        o.hrot(c, evk, i + 1)
+    dt = time.perf_counter() - t0
+    return n_rot / dt, dt
+
+
+def run_reference(args, ws, rank):
+    """Reference arm: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    # warm-up (untimed) and K timed steps, each step = 1 plain HRot at full level (bounded sample)
+    for _ in range(args.warmup):
+        oracle_keyswitch_rate(1)
+    times = []
+    for s in range(args.steps):
+        rate, dt = oracle_keyswitch_rate(1, seed=s)
+        times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = 1000.0 / ms
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "C2 HRot keyswitch, N=2^16, Set_hyp L+1=24 dnum=6 K=4, plain (non-hoisted)",
+                   "sample": "1 plain HRot at full level per step (of the 64-rotation batch)",
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": "1 plain HRot per step, full level, OpenMP over limbs"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2302_02407_b200 as hy
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    prm = synth.PARAMS["hyp"]
+    ctx = hy.Context(**prm, device=local)
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    rs = [i + 1 for i in range(BATCH)]
+    # keys (server state) and inputs (client output), resident in HBM before timing
+    evks = [ctx.keygen_rot(sk, ek, r) for r in rs]
+    scale = 2 ** prm["log_scale"]
+    pt = ctx.encode(synth.slots_uniform(1000 + rank, ctx.n), scale, LEVEL)
+    cts = [ctx.encrypt(sk, synth.SEED_ENC, rank * BATCH + i, pt, LEVEL) for i in range(BATCH)]
+    outs = [ctx.empty(*ctx.ct_shape(LEVEL)) for _ in range(BATCH)]
+    houts = [ctx.empty(*ctx.ct_shape(LEVEL)) for _ in range(BATCH)]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.hrot_batch(evks, cts, LEVEL, rs, outs)
+
+    def step_hoisted():
+        ctx.hrot_hoisted(evks, cts[0], LEVEL, rs, houts)
+
+    def timed(fn, k, w):
+        for _ in range(w):
+            fn()
+        torch.cuda.synchronize()
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = ctx.launch_count()
+        prof = os.environ.get("HY_NCU_TIMED") == "1"  # ncu --profile-from-start off captures only this region
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
+        barrier(ws)
+        ms = e0.elapsed_time(e1) / k
+        return max_over_ranks(ms, ws), (ctx.launch_count() - l0) // k
+
+    with ClockSampler(local) as clk:
+        ms, launches = timed(step, args.steps, args.warmup)
+    clocks = clk.summary()
+    value = BATCH * ws * 1000.0 / ms
+
+    ms_h, _ = timed(step_hoisted, args.steps, max(1, args.warmup // 2))
+
+    # live per-family kernel timing over K instrumented steps (same stream, CUDA events)
+    fam = ctx.FAMILIES
+    ctx.time_kernels(sum(fam.values()))
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    breakdown = {}
+    for name, m in fam.items():
+        t, n, by = ctx.kernel_times(m)
+        if n:
+            breakdown[name] = {"ms_per_step": t / args.steps, "launches_per_step": n // args.steps,
+                               "alg_bytes_per_launch": by // n, "avg_us": 1000.0 * t / n}
+    ctx.time_kernels(0)
+    dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
+    d = breakdown[dominant]
+    pk = peaks()
+    achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
+    roof = {"bound": "hbm", "kernel_family": dominant, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": None,
+            "share_of_step": d["ms_per_step"] / ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
+    # ALU view of the NTT (the step's integer-bound work): butterflies/s vs measured Shoup rate
+    ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
+
+    # e2e through the public API with host buffers: pinned H2D of the 64 input cts, D2H of the outputs
+    e2e = None
+    if not args.no_e2e:
+        hin = [torch.empty_like(c, device="cpu").pin_memory() for c in cts]
+        hout = [torch.empty_like(c, device="cpu").pin_memory() for c in outs]
+        for h, c in zip(hin, cts):
+            h.copy_(c)
+        dcts = [torch.empty_like(c) for c in cts]
+
+        def e2e_step():
+            for h, d_ in zip(hin, dcts):
+                d_.copy_(h, non_blocking=True)
+            ctx.hrot_batch(evks, dcts, LEVEL, rs, outs)
+            for h, o in zip(hout, outs):
+                h.copy_(o, non_blocking=True)
+
+        ms_e2e, _ = timed(e2e_step, max(1, args.steps // 2), 1)
+        nb = sum(c.numel() * 8 for c in cts)
+        e2e = {"value": BATCH * ws * 1000.0 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "ms_per_step": ms_e2e,
+               "note": "H2D of the 64 input ciphertexts from pinned memory, hrot_batch, D2H of the 64 outputs; "
+                       "evaluation keys are server state, resident before timing (P:1030)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, dt = oracle_keyswitch_rate(args.cpu_rotations)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{args.cpu_rotations} plain HRot(s) at full level (Set_hyp, N=2^16), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "C2 HRot keyswitch microbenchmark, N=2^16, Set_hyp L+1=24 dnum=6 K=4, "
+                                   "batch of 64 plain (non-hoisted) rotations per step per GPU",
+                       "global_batch": BATCH * ws, "level": LEVEL, "parallelism": f"independent batches x{ws}",
+                       "l2": "inputs larger than L2 (64 x 168 MiB evaluation keys streamed per step)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "hoisted": {"value": BATCH * ws * 1000.0 / ms_h, "unit": UNIT, "ms_per_step": ms_h,
+                        "note": "ct_0 rotated by 1..64 with one shared ModUp (Slide_f pattern, P:369-375)"},
+            "kernel_breakdown": breakdown,
+            "ntt_ms_per_step": ntt_ms,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rotations", type=int, default=2)
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -93,6 +93,26 @@ hy_status hy_ctx_set_workspace(hy_ctx* ctx, void* d_ws, size_t bytes);
 const char* hy_last_error(void);
 /* number of kernels this context has launched since creation (for bench evidence) */
 uint64_t hy_ctx_launch_count(const hy_ctx* ctx);
+/* Live per-kernel-family timing: while family_mask != 0, every launch of a selected
+ * family is bracketed by CUDA events on its stream (clears previous records).
+ * hy_ctx_kernel_times() synchronizes on those events and returns the summed
+ * device time (ms), the launch count and the summed ALGORITHMIC bytes (the
+ * minimal reads + writes of each launch) of the
+ * families in family_mask. */
+enum {
+  HY_FAM_NTT_A = 1,     /* NTT pass over columns (stages with distance >= 256) */
+  HY_FAM_NTT_B = 2,     /* NTT pass over 256-word rows */
+  HY_FAM_MODUP = 4,     /* ModUp basis conversion */
+  HY_FAM_IP = 8,        /* key-switch inner product */
+  HY_FAM_MODDOWN = 16,  /* ModDown basis conversion + final combine */
+  HY_FAM_AUT = 32,      /* automorphism gather */
+  HY_FAM_ELEM = 64,     /* PMult / PMult-accumulate / add */
+  HY_FAM_RESCALE = 128,
+  HY_FAM_CLIENT = 256   /* keygen / encrypt / decrypt / encode upload */
+};
+hy_status hy_ctx_time_kernels(hy_ctx* ctx, uint32_t family_mask);
+hy_status hy_ctx_kernel_times(hy_ctx* ctx, uint32_t family_mask, double* total_ms, uint64_t* n_launches,
+                              uint64_t* alg_bytes);
 
 /* ---- transforms (exposed for parity tests of the sub-steps) ------------ */
 /* Negacyclic NTT / inverse NTT (P:97 ring; DESIGN R-NTT) of n_limbs limbs.

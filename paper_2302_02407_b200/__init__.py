@@ -52,6 +52,8 @@ SIGNATURES = {
     "hy_ctx_set_workspace": (C.c_int, [_P, _P, C.c_size_t]),
     "hy_last_error": (C.c_char_p, []),
     "hy_ctx_launch_count": (_U64, [_P]),
+    "hy_ctx_time_kernels": (C.c_int, [_P, _U32]),
+    "hy_ctx_kernel_times": (C.c_int, [_P, _U32, C.POINTER(C.c_double), C.POINTER(_U64), C.POINTER(_U64)]),
     "hy_ntt": (C.c_int, [_P, _P, _P, C.POINTER(_U32), _U32, C.c_int, _P]),
     "hy_automorph": (C.c_int, [_P, _P, _P, _U32, _U64, _P]),
     "hy_galois_elt": (_U64, [_P, C.c_int64]),
@@ -174,6 +176,18 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().hy_ctx_launch_count(self._c))
+
+    FAMILIES = {"ntt_a": 1, "ntt_b": 2, "modup": 4, "ip": 8, "moddown": 16, "aut": 32, "elem": 64,
+                "rescale": 128, "client": 256}
+
+    def time_kernels(self, mask: int):
+        _check(lib().hy_ctx_time_kernels(self._c, mask))
+
+    def kernel_times(self, mask: int):
+        """(total device ms, launches, algorithmic bytes) of the timed launches in `mask`."""
+        ms, n, by = C.c_double(), C.c_uint64(), C.c_uint64()
+        _check(lib().hy_ctx_kernel_times(self._c, mask, C.byref(ms), C.byref(n), C.byref(by)))
+        return ms.value, n.value, by.value
 
     # -- transforms ------------------------------------------------------
     def ntt(self, x, chain: Sequence[int], inverse=False, out=None):

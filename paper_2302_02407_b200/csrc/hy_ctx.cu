@@ -271,6 +271,7 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
 extern "C" void hy_ctx_destroy(hy_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   cudaFree(c->d_tables);
   for (auto p : c->d_modup) cudaFree(p);
   for (auto p : c->d_moddown) cudaFree(p);
@@ -308,5 +309,33 @@ extern "C" hy_status hy_ctx_set_workspace(hy_ctx* c, void* d_ws, size_t bytes) {
   if (!c) return hy::fail(HY_E_ARG, "null ctx");
   c->ws = (uint8_t*)d_ws;
   c->ws_bytes = bytes;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_ctx_time_kernels(hy_ctx* c, uint32_t family_mask) {
+  if (!c) return hy::fail(HY_E_ARG, "null ctx");
+  c->time_mask = family_mask;
+  c->timed.clear();
+  c->ev_used = 0;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_ctx_kernel_times(hy_ctx* c, uint32_t family_mask, double* total_ms, uint64_t* n_launches,
+                                        uint64_t* alg_bytes) {
+  if (!c || !total_ms || !n_launches || !alg_bytes) return hy::fail(HY_E_ARG, "null");
+  double tot = 0;
+  uint64_t n = 0, by = 0;
+  for (const auto& t : c->timed) {
+    if (!(t.fam & family_mask)) continue;
+    if (cudaEventSynchronize(t.b) != cudaSuccess) return hy::cuda_check("hy_ctx_kernel_times");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    tot += ms;
+    by += t.bytes;
+    ++n;
+  }
+  *total_ms = tot;
+  *n_launches = n;
+  *alg_bytes = by;
   return HY_OK;
 }

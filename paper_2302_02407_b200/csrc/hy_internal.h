@@ -74,6 +74,16 @@ struct hy_ctx {
   uint8_t* ws = nullptr;
   size_t ws_bytes = 0;
   uint64_t launches = 0;
+  // per-kernel-family CUDA-event timing (hy_ctx_time_kernels)
+  uint32_t time_mask = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct TimedPair {
+    uint32_t fam;
+    cudaEvent_t a, b;
+    uint64_t bytes;  // algorithmic bytes of the bracketed launch(es)
+  };
+  std::vector<TimedPair> timed;
 };
 
 namespace hy {
@@ -104,6 +114,45 @@ void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* ch
 
 // elementwise / keyswitch launchers (hy_ops.cu / hy_keyswitch.cu)
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
+
+// Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).
+enum Family : uint32_t {
+  FAM_NTT_A = 1, FAM_NTT_B = 2, FAM_MODUP = 4, FAM_IP = 8, FAM_MODDOWN = 16, FAM_AUT = 32, FAM_ELEM = 64,
+  FAM_RESCALE = 128, FAM_CLIENT = 256
+};
+
+inline cudaEvent_t pooled_event(hy_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+// Counts one launch (or n) and, when the family is being timed, brackets it
+// with CUDA events on the launching stream.
+struct KTimer {
+  hy_ctx* c;
+  uint32_t fam;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  uint64_t bytes = 0;  // algorithmic bytes (minimal reads + writes), set by the launcher
+  KTimer(hy_ctx* c_, uint32_t fam_, cudaStream_t s_, uint32_t n = 1) : c(c_), fam(fam_), s(s_) {
+    c->launches += n;
+    if (c->time_mask & fam) {
+      a = pooled_event(c);
+      b = pooled_event(c);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KTimer() {
+    if (b) {
+      cudaEventRecord(b, s);
+      c->timed.push_back({fam, a, b, bytes});
+    }
+  }
+};
 
 // workspace carving
 struct Ws {

@@ -26,8 +26,11 @@ namespace {
 
 constexpr int kT = 256;
 
+// IP operands: digit j's limb u is own[u] (the NTT-domain c1 the digits were
+// cut from) when u belongs to digit j, else ext[j][u].
 struct IPArgs {
-  const uint64_t* src[kMaxDigits][kMaxExt];
+  const uint64_t* ext;
+  const uint64_t* own;  // may be null: then every limb comes from ext
 };
 
 // out[l][p] (+)= in[l][perm_k(p)]; limb l uses prime chain (l % limbs_per_poly).
@@ -41,50 +44,88 @@ __global__ void k_automorph(const uint64_t* __restrict__ in, uint64_t* __restric
   out[off + p] = v;
 }
 
-// ModUp basis conversion.  grid (N/256, beta, ceil(E/4)).
+// Reduction constants of one prime, staged in shared memory.
+struct RedConst {
+  uint64_t q, two_q, mu, r64, r64_sh;
+};
+__device__ __forceinline__ uint64_t reduce128s(U128 x, const RedConst& p) {
+  uint64_t a = shoup_lazy(x.hi, p.r64, p.r64_sh, p.q);  // [0, 2q)
+  uint64_t b = x.lo - __umul64hi(x.lo, p.mu) * p.q;      // [0, 2q)
+  uint64_t s = csub(a + b, p.two_q);
+  return csub(s, p.q);
+}
+__device__ __forceinline__ void stage_red(RedConst& r, const PrimeConst& p) {
+  r.q = p.q;
+  r.two_q = p.two_q;
+  r.mu = p.mu;
+  r.r64 = p.r64;
+  r.r64_sh = p.r64_sh;
+}
+
+// ModUp basis conversion for digit j = blockIdx.y; one thread per coefficient x
+// produces every non-own limb of the digit.  grid (N/256, beta).
 // y_i = d_i (D_j/q_i)^{-1} mod q_i;  ext[j][u][x] = sum_i y_i [(D_j/q_i) mod t_u] mod t_u  (u not in digit j)
-__global__ void k_modup_bconv(const uint64_t* __restrict__ d, uint64_t* __restrict__ ext, const ModUpConst* mc,
-                              DevTables dt, int level, int n_q, int E, int logN) {
+// A = alpha (compile time); a partial last digit pads its missing sources with 0.
+template <int A>
+__global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict__ d, uint64_t* __restrict__ ext,
+                                                     const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
+                                                     int logN) {
+  __shared__ uint64_t s_hat[kMaxExt][A];
+  __shared__ RedConst s_red[kMaxExt];
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   const ModUpConst& m = mc[j];
   const int nsrc = m.hi - m.lo;
-  uint64_t y[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < nsrc) y[i] = shoup(d[(size_t)(m.lo + i) * N + x], m.hat_inv[i], m.hat_inv_sh[i], dt.pc[m.lo + i].q);
+  for (int i = threadIdx.x; i < E * A; i += blockDim.x) {
+    const int u = i / A, ii = i % A;
+    s_hat[u][ii] = ii < nsrc ? m.hat_mod[u][ii] : 0;
   }
+  for (int u = threadIdx.x; u < E; u += blockDim.x) stage_red(s_red[u], dt.pc[u <= level ? u : n_q + (u - level - 1)]);
+  uint64_t y[A];
 #pragma unroll
-  for (int uu = 0; uu < 4; ++uu) {
-    const int u = blockIdx.z * 4 + uu;
-    if (u >= E) break;
+  for (int i = 0; i < A; ++i)
+    y[i] = i < nsrc ? shoup(d[(size_t)(m.lo + i) * N + x], m.hat_inv[i], m.hat_inv_sh[i], dt.pc[m.lo + i].q) : 0;
+  __syncthreads();
+  uint64_t* out = ext + (size_t)j * E * N + x;
+  for (int u = 0; u < E; ++u) {
     if (u >= m.lo && u < m.hi) continue;
-    const int t = u <= level ? u : n_q + (u - level - 1);
     U128 acc{0, 0};
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nsrc) mac(acc, y[i], m.hat_mod[u][i]);
-    ext[((size_t)j * E + u) * N + x] = reduce128(acc, dt.pc[t]);
+    for (int i = 0; i < A; ++i) mac(acc, y[i], s_hat[u][i]);
+    out[(size_t)u * N] = reduce128s(acc, s_red[u]);
   }
 }
 
-// Key-switch inner product.  grid (N/256, E).
-// u[c][u][x] (+)= sum_j src[j][u][perm(x)] * evk[j][c][chain(u)][x]
-__global__ void k_ks_ip(IPArgs a, const uint64_t* __restrict__ evk, uint64_t* __restrict__ uo, DevTables dt,
-                        int level, int n_q, int L1, int E, int beta, uint64_t kperm, int logN, int accumulate) {
+// Key-switch inner product, B = beta digits (compile time).  grid (N/256, E).
+// u[c][u][x] (+)= sum_j src_j[u][perm(x)] * evk[j][c][chain(u)][x], where src_j[u] is the digit's own
+// limb of `own` (the NTT-domain c1 the digits were cut from) when u belongs to digit j, else ext[j][u].
+template <int B>
+__global__ void __launch_bounds__(256) k_ks_ip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ own,
+                                               const uint64_t* __restrict__ evk, uint64_t* __restrict__ uo,
+                                               DevTables dt, int level, int n_q, int L1, int E, int alpha,
+                                               uint64_t kperm, int logN, int accumulate) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const int u = blockIdx.y;
   const int t = u <= level ? u : n_q + (u - level - 1);
   const PrimeConst& p = dt.pc[t];
   const uint32_t xs = kperm != 1 ? aut_index(x, kperm, logN) : x;
-  U128 a0{0, 0}, a1{0, 0};
-  for (int j = 0; j < beta; ++j) {
-    const uint64_t v = a.src[j][u][xs];
+  const int own_digit = (own && u <= level) ? u / alpha : -1;
+  uint64_t v[B], e0[B], e1[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const uint64_t* src = (j == own_digit) ? own + (size_t)u * N : ext + ((size_t)j * E + u) * N;
+    v[j] = src[xs];
     const uint64_t* e = evk + ((size_t)(j * 2) * L1 + t) * N + x;
-    mac(a0, v, e[0]);
-    mac(a1, v, e[(size_t)L1 * N]);
+    e0[j] = __ldcs(e);
+    e1[j] = __ldcs(e + (size_t)L1 * N);
+  }
+  U128 a0{0, 0}, a1{0, 0};
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    mac(a0, v[j], e0[j]);
+    mac(a1, v[j], e1[j]);
   }
   uint64_t r0 = reduce128(a0, p), r1 = reduce128(a1, p);
   uint64_t* o0 = uo + (size_t)u * N + x;
@@ -97,27 +138,45 @@ __global__ void k_ks_ip(IPArgs a, const uint64_t* __restrict__ evk, uint64_t* __
   *o1 = r1;
 }
 
-// ModDown basis conversion P -> Q_l.  grid (N/256, npoly, ceil((l+1)/4)); v = iNTT(u on P) [npoly][K][N].
-__global__ void k_moddown_bconv(const uint64_t* __restrict__ v, uint64_t* __restrict__ w, const ModDownConst* md,
-                                DevTables dt, int level, int n_q, int K, int logN) {
+// ModDown basis conversion P -> Q_l, KP = K special primes (compile time).  grid (N/256, npoly);
+// v = iNTT(u on P) [npoly][K][N];  z_k = v_k (P/p_k)^{-1} mod p_k;  w[c][i] = sum_k z_k [(P/p_k) mod q_i] mod q_i.
+template <int KP>
+__global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restrict__ v, uint64_t* __restrict__ w,
+                                                       const ModDownConst* md, DevTables dt, int level, int n_q,
+                                                       int logN) {
+  __shared__ uint64_t s_hat[kMaxChain][KP];
+  __shared__ RedConst s_red[kMaxChain];
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
-  uint64_t z[8];
+  const int n = level + 1;
+  for (int i = threadIdx.x; i < n * KP; i += blockDim.x) s_hat[i / KP][i % KP] = md->phat_mod[i / KP][i % KP];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) stage_red(s_red[i], dt.pc[i]);
+  uint64_t z[KP];
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k < K) z[k] = shoup(v[((size_t)c * K + k) * N + x], md->phat_inv[k], md->phat_inv_sh[k], dt.pc[n_q + k].q);
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii) {
-    const int i = blockIdx.z * 4 + ii;
-    if (i > level) break;
+  for (int k = 0; k < KP; ++k)
+    z[k] = shoup(v[((size_t)c * KP + k) * N + x], md->phat_inv[k], md->phat_inv_sh[k], dt.pc[n_q + k].q);
+  __syncthreads();
+  uint64_t* out = w + (size_t)c * n * N + x;
+  for (int i = 0; i < n; ++i) {
     U128 acc{0, 0};
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < K) mac(acc, z[k], md->phat_mod[i][k]);
-    w[((size_t)c * (level + 1) + i) * N + x] = reduce128(acc, dt.pc[i]);
+    for (int k = 0; k < KP; ++k) mac(acc, z[k], s_hat[i][k]);
+    out[(size_t)i * N] = reduce128s(acc, s_red[i]);
   }
 }
+
+#define HY_DISPATCH_1_8(KERNEL, VAL, GRID, BLOCK, STREAM, ...)                      \
+  switch (VAL) {                                                                     \
+    case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 2: KERNEL<2><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 3: KERNEL<3><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 5: KERNEL<5><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 6: KERNEL<6><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    case 7: KERNEL<7><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
+    default: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
+  }
 
 // out[c][i] = (u[c][i] - w[c][i]) P^{-1} (+ add0[i][perm(x)] for c = 0) (+ add1[i][x] for c = 1).
 // grid (N/256, l+1, npoly)
@@ -162,16 +221,21 @@ hy_status carve(hy_ctx* c, uint32_t level, KsBufs& b) {
 void automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t nlimbs, uint32_t per_poly, uint64_t k,
                bool accumulate, cudaStream_t s) {
   dim3 g(c->N / kT, nlimbs);
+  KTimer kt(c, FAM_AUT, s);
+  kt.bytes = (uint64_t)nlimbs * c->N * 8 * (accumulate ? 3 : 2);
   k_automorph<<<g, kT, 0, s>>>(in, out, k, c->log_n, per_poly, accumulate ? 1 : 0, c->dt);
-  ++c->launches;
 }
 
 // d: coefficient-domain [l+1][N] -> ext [beta][E][N] (non-own limbs, NTT domain)
 void modup_core(hy_ctx* c, uint32_t level, const uint64_t* d, uint64_t* ext, cudaStream_t s) {
   const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
-  dim3 g(c->N / kT, beta, (E + 3) / 4);
-  k_modup_bconv<<<g, kT, 0, s>>>(d, ext, c->d_modup[level], c->dt, level, c->n_q, E, c->log_n);
-  ++c->launches;
+  dim3 g(c->N / kT, beta);
+  {
+    KTimer kt(c, FAM_MODUP, s);
+    kt.bytes = ((uint64_t)n + (uint64_t)beta * E - n) * c->N * 8;  // read d once, write non-own ext limbs
+    HY_DISPATCH_1_8(k_modup_bconv, c->alpha, g, kT, s, d, ext, c->d_modup[level], c->dt, (int)level, (int)c->n_q, E,
+                    (int)c->log_n);
+  }
   LimbBatch b;
   b.n = 0;
   for (int j = 0; j < beta; ++j) {
@@ -192,25 +256,18 @@ void modup_core(hy_ctx* c, uint32_t level, const uint64_t* d, uint64_t* ext, cud
   launch_ntt(c, b, false, s);
 }
 
-IPArgs ip_args(hy_ctx* c, uint32_t level, const uint64_t* ext, const uint64_t* own /* c1 NTT, or null */) {
-  IPArgs a{};
-  const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
-  for (int j = 0; j < beta; ++j) {
-    const auto& m = c->h_modup[level][j];
-    for (int u = 0; u < E; ++u) {
-      bool is_own = u >= m.lo && u < m.hi;
-      a.src[j][u] = (is_own && own) ? own + (size_t)u * c->N : ext + ((size_t)j * E + u) * c->N;
-    }
-  }
-  return a;
+IPArgs ip_args(hy_ctx*, uint32_t, const uint64_t* ext, const uint64_t* own /* c1 NTT, or null */) {
+  return IPArgs{ext, own};
 }
 
 void ip(hy_ctx* c, uint32_t level, const IPArgs& a, const uint64_t* evk, uint64_t* u, uint64_t kperm, bool acc,
         cudaStream_t s) {
   const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
   dim3 g(c->N / kT, E);
-  k_ks_ip<<<g, kT, 0, s>>>(a, evk, u, c->dt, level, c->n_q, c->n_q + c->n_p, E, beta, kperm, c->log_n, acc ? 1 : 0);
-  ++c->launches;
+  KTimer kt(c, FAM_IP, s);
+  kt.bytes = ((uint64_t)beta * E * 3 + 2ull * E * (acc ? 2 : 1)) * c->N * 8;  // ext + 2 evk polys in, u out
+  HY_DISPATCH_1_8(k_ks_ip, beta, g, kT, s, a.ext, a.own, evk, u, c->dt, (int)level, (int)c->n_q,
+                  (int)(c->n_q + c->n_p), E, (int)c->alpha, kperm, (int)c->log_n, acc ? 1 : 0);
 }
 
 // u [npoly][E][N] (NTT) -> out [npoly][l+1][N]
@@ -227,9 +284,13 @@ void moddown_core(hy_ctx* c, uint32_t level, int npoly, const uint64_t* u, uint6
       ++b.n;
     }
   launch_ntt(c, b, true, s);
-  dim3 g(c->N / kT, npoly, (n + 3) / 4);
-  k_moddown_bconv<<<g, kT, 0, s>>>(v, w, c->d_moddown[level], c->dt, level, c->n_q, K, c->log_n);
-  ++c->launches;
+  dim3 g(c->N / kT, npoly);
+  {
+    KTimer kt(c, FAM_MODDOWN, s);
+    kt.bytes = ((uint64_t)npoly * K + (uint64_t)npoly * n) * c->N * 8;
+    HY_DISPATCH_1_8(k_moddown_bconv, K, g, kT, s, v, w, c->d_moddown[level], c->dt, (int)level, (int)c->n_q,
+                    (int)c->log_n);
+  }
   b.n = 0;
   for (int cc = 0; cc < npoly; ++cc)
     for (int i = 0; i < n; ++i) {
@@ -241,8 +302,9 @@ void moddown_core(hy_ctx* c, uint32_t level, int npoly, const uint64_t* u, uint6
     }
   launch_ntt(c, b, false, s);
   dim3 g2(c->N / kT, n, npoly);
+  KTimer kt(c, FAM_MODDOWN, s);
+  kt.bytes = ((uint64_t)npoly * n * 3 + (add0 ? n : 0) + (add1 ? n : 0)) * c->N * 8;
   k_moddown_final<<<g2, kT, 0, s>>>(u, E, w, c->d_moddown[level], c->dt, level, out, add0, k0, add1, c->log_n);
-  ++c->launches;
 }
 
 void intt_poly(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t level, cudaStream_t s) {

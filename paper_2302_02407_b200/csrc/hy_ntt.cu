@@ -30,11 +30,14 @@ __device__ __forceinline__ int kbit(int s) {
 }
 
 // Run stages [s_lo, s_hi] (forward: descending, inverse: ascending) on the 8
-// register words of one thread in layout LAY.  Twiddle index = (base + e) >> (s+1).
+// register words of one thread in layout LAY.  Twiddles come from a shared-
+// memory "heap" table T[li], li = (256 + e) >> (s+1) in [1, 256), filled by
+// load_twiddles() for the 256-point transform at hand.
 template <int LAY, bool FWD>
-__device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, int s_lo, uint32_t base,
-                                           const uint64_t* __restrict__ W, const uint64_t* __restrict__ Ws,
+__device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, int s_lo,
+                                           const uint64_t* __restrict__ T, const uint64_t* __restrict__ Ts,
                                            uint64_t q) {
+  const uint64_t two_q = q << 1;
 #pragma unroll
   for (int it = 0; it <= s_hi - s_lo; ++it) {
     const int s = FWD ? s_hi - it : s_lo + it;
@@ -42,29 +45,47 @@ __device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, in
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (k & kb) continue;
-      const int e = elem<LAY>(l, k);
-      const uint32_t idx = (base + (uint32_t)e) >> (s + 1);
-      const uint64_t w = __ldg(W + idx), ws = __ldg(Ws + idx);
+      const int li = (256 + elem<LAY>(l, k)) >> (s + 1);
+      const uint64_t w = T[li], ws = Ts[li];
       uint64_t a = x[k], b = x[k | kb];
       if (FWD) {
-        uint64_t t = shoup(b, w, ws, q);
-        x[k] = add_mod(a, t, q);
-        x[k | kb] = sub_mod(a, t, q);
+        // Harvey lazy CT butterfly: inputs/outputs in [0, 4q)
+        a = csub(a, two_q);
+        const uint64_t t = shoup_lazy(b, w, ws, q);  // [0, 2q)
+        x[k] = a + t;
+        x[k | kb] = a + two_q - t;
       } else {
-        x[k] = add_mod(a, b, q);
-        x[k | kb] = shoup(sub_mod(a, b, q), w, ws, q);
+        // lazy GS butterfly: inputs/outputs in [0, 2q)
+        x[k] = csub(a + b, two_q);
+        x[k | kb] = shoup_lazy(a + two_q - b, w, ws, q);
       }
     }
+  }
+}
+
+// Fill the twiddle heap of one 256-point transform: T[li] = W[((hb - 1) << m) + li],
+// m = floor(log2 li).  hb = 1 for pass A (global index = li) and R + row for
+// pass B (global index = (N + row*256 + e) >> (s+1)).  nthr threads cooperate.
+__device__ __forceinline__ void load_twiddles(uint64_t* T, uint64_t* Ts, const uint64_t* __restrict__ W,
+                                              const uint64_t* __restrict__ Ws, uint32_t hb, int tid, int nthr) {
+  for (int li = tid; li < 256; li += nthr) {
+    if (li == 0) continue;
+    const int m = 31 - __clz(li);
+    const uint32_t g = ((hb - 1) << m) + (uint32_t)li;
+    T[li] = __ldg(W + g);
+    Ts[li] = __ldg(Ws + g);
   }
 }
 
 __device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
 
 // ---------------------------------------------------------------- pass B (rows)
-// CTA = 8 warps, one 256-word row per warp.  grid = (N/256/8, n_limbs)
+// CTA = 8 warps, one 256-word row per warp, dynamic smem = 8 x (272 data + 2 x 256 twiddles) words.
+// grid = (N/256/8, n_limbs)
+constexpr int kRowsSmemWords = 272 + 512;
 template <bool FWD>
 __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int logN) {
-  __shared__ uint64_t sm[8][272];
+  extern __shared__ uint64_t dsm[];
   const int limb = blockIdx.y, w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + w;
   const size_t N = (size_t)1 << logN;
@@ -75,53 +96,56 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
   const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
   const uint64_t* src = b.src[limb] + (size_t)row * 256;
   uint64_t* dst = b.dst[limb] + (size_t)row * 256;
-  uint64_t* S = sm[w];
-  const uint32_t base = (uint32_t)N + (uint32_t)row * 256;
+  uint64_t* S = dsm + w * kRowsSmemWords;
+  uint64_t* T = S + 272;
+  uint64_t* Ts = T + 256;
   uint64_t x[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = src[elem<1>(l, k)];
+  load_twiddles(T, Ts, W, Ws, (uint32_t)(N >> 8) + (uint32_t)row, l, 32);
+  __syncwarp();
   if (FWD) {
-    run_stages<1, true>(x, l, 7, 5, base, W, Ws, q);
+    run_stages<1, true>(x, l, 7, 5, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
-    run_stages<2, true>(x, l, 4, 2, base, W, Ws, q);
+    run_stages<2, true>(x, l, 4, 2, T, Ts, q);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
-    run_stages<3, true>(x, l, 1, 0, base, W, Ws, q);
+    run_stages<3, true>(x, l, 1, 0, T, Ts, q);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = S[pidx(elem<1>(l, k))];
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = csub(csub(S[pidx(elem<1>(l, k))], q << 1), q);  // [0,4q) -> [0,q)
   } else {
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
-    run_stages<3, false>(x, l, 1, 0, base, W, Ws, q);
+    run_stages<3, false>(x, l, 1, 0, T, Ts, q);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
-    run_stages<2, false>(x, l, 4, 2, base, W, Ws, q);
+    run_stages<2, false>(x, l, 4, 2, T, Ts, q);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<1>(l, k))];
-    run_stages<1, false>(x, l, 7, 5, base, W, Ws, q);
+    run_stages<1, false>(x, l, 7, 5, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = x[k];
   }
@@ -133,6 +157,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
 template <bool FWD>
 __global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, int logN) {
   __shared__ uint64_t sm[16 * 273];
+  __shared__ uint64_t T[256], Ts[256];
   const int limb = blockIdx.y, c = threadIdx.x & 15, l = threadIdx.x >> 4;
   const int col = blockIdx.x * 16 + c;
   const int t = b.chain[limb];
@@ -144,44 +169,48 @@ __global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, 
   const uint64_t* src = FWD ? b.src[limb] : b.dst[limb];  // inverse runs in place after pass B
   uint64_t* dst = b.dst[limb];
   uint64_t* S = sm + c * 273;
-  const uint32_t base = 256;  // R
   uint64_t x[8];
   if (FWD) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<1>(l, k) * 256 + col];
-    run_stages<1, true>(x, l, 7, 5, base, W, Ws, q);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<3>(l, k) * 256 + col];
+  }
+  load_twiddles(T, Ts, W, Ws, 1, threadIdx.x, blockDim.x);
+  __syncthreads();
+  if (FWD) {
+    run_stages<1, true>(x, l, 7, 5, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<1>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
-    run_stages<2, true>(x, l, 4, 2, base, W, Ws, q);
+    run_stages<2, true>(x, l, 4, 2, T, Ts, q);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
-    run_stages<3, true>(x, l, 1, 0, base, W, Ws, q);
+    run_stages<3, true>(x, l, 1, 0, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = x[k];
   } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<3>(l, k) * 256 + col];
-    run_stages<3, false>(x, l, 1, 0, base, W, Ws, q);
+    run_stages<3, false>(x, l, 1, 0, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<3>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
-    run_stages<2, false>(x, l, 4, 2, base, W, Ws, q);
+    run_stages<2, false>(x, l, 4, 2, T, Ts, q);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<1>(l, k)];
-    run_stages<1, false>(x, l, 7, 5, base, W, Ws, q);
+    run_stages<1, false>(x, l, 7, 5, T, Ts, q);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       dst[(size_t)elem<1>(l, k) * 256 + col] = shoup(x[k], pc.n_inv, pc.n_inv_sh, q);
@@ -206,7 +235,8 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
   const int col0 = blockIdx.x * 16;
   for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
     int r = i >> 4, c = i & 15;
-    sm[i] = src[(size_t)r * 256 + col0 + c];
+    uint64_t v = src[(size_t)r * 256 + col0 + c];
+    sm[i] = FWD ? v : csub(v, q);  // inverse input comes from pass B in [0, 2q)
   }
   __syncthreads();
   for (int it = 0; it < logR; ++it) {
@@ -241,22 +271,41 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
 
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
   if (b.n == 0) return;
+  constexpr int kRowsBytes = 8 * kRowsSmemWords * 8;
+  static bool attr_set = false;  // per process: the attribute is a property of the function
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_ntt_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowsBytes);
+    cudaFuncSetAttribute(k_ntt_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowsBytes);
+    attr_set = true;
+  }
   const int logN = (int)c->log_n;
   const int R = (int)c->N / 256;
   dim3 gB(R / 8 > 0 ? R / 8 : 1, b.n), gA(256 / 16, b.n);
+  const uint64_t pass_bytes = 2ull * b.n * c->N * 8;  // read + write every limb once
   if (!inverse) {
-    if (R == 256) k_ntt_cols256<true><<<gA, 512, 0, s>>>(b, c->dt, logN);
-    else k_ntt_cols_small<true><<<gA, 256, 0, s>>>(b, c->dt, logN);
+    {
+      KTimer kt(c, FAM_NTT_A, s);
+      kt.bytes = pass_bytes;
+      if (R == 256) k_ntt_cols256<true><<<gA, 512, 0, s>>>(b, c->dt, logN);
+      else k_ntt_cols_small<true><<<gA, 256, 0, s>>>(b, c->dt, logN);
+    }
     // pass B runs in place on dst
     LimbBatch b2 = b;
     for (int i = 0; i < b.n; ++i) b2.src[i] = b.dst[i];
-    k_ntt_rows<true><<<gB, 256, 0, s>>>(b2, c->dt, logN);
+    KTimer kt(c, FAM_NTT_B, s);
+    kt.bytes = pass_bytes;
+    k_ntt_rows<true><<<gB, 256, kRowsBytes, s>>>(b2, c->dt, logN);
   } else {
-    k_ntt_rows<false><<<gB, 256, 0, s>>>(b, c->dt, logN);
+    {
+      KTimer kt(c, FAM_NTT_B, s);
+      kt.bytes = pass_bytes;
+      k_ntt_rows<false><<<gB, 256, kRowsBytes, s>>>(b, c->dt, logN);
+    }
+    KTimer kt(c, FAM_NTT_A, s);
+    kt.bytes = pass_bytes;
     if (R == 256) k_ntt_cols256<false><<<gA, 512, 0, s>>>(b, c->dt, logN);
     else k_ntt_cols_small<false><<<gA, 256, 0, s>>>(b, c->dt, logN);
   }
-  c->launches += 2;
 }
 
 void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,

@@ -162,8 +162,10 @@ hy_status secret_ntt(hy_ctx* c, uint64_t seed, uint32_t nlimb, uint64_t* out, in
   cudaMemcpyAsync(d_s, h_s.data(), c->N, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);  // h_s is a pageable temporary
   dim3 g(c->N / kT, nlimb);
-  k_small_to_limbs<int8_t><<<g, kT, 0, s>>>(d_s, out, nullptr, c->dt, c->log_n);
-  ++c->launches;
+  {
+    KTimer kt(c, FAM_CLIENT, s);
+    k_small_to_limbs<int8_t><<<g, kT, 0, s>>>(d_s, out, nullptr, c->dt, c->log_n);
+  }
   std::vector<uint32_t> chain(nlimb);
   for (uint32_t i = 0; i < nlimb; ++i) chain[i] = i;
   ntt_contig(c, out, out, chain.data(), nlimb, false, s);
@@ -191,8 +193,9 @@ extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const u
       if (!tp.ct[i] || !tp.pt[i]) return fail(HY_E_ARG, "null term");
     }
     dim3 g(c->N / kT, level + 1, 2);
+    KTimer kt(c, FAM_ELEM, s);
+    kt.bytes = ((uint64_t)m * 3 * (level + 1) + 2ull * (level + 1) * ((accumulate || done > 0) ? 2 : 1)) * c->N * 8;
     k_pmult_acc<<<g, kT, 0, s>>>(tp, (int)m, out, c->dt, level, c->log_n, (accumulate || done > 0) ? 1 : 0);
-    ++c->launches;
     done += m;
   }
   return cuda_check("hy_pmult_acc");
@@ -210,8 +213,9 @@ extern "C" hy_status hy_add(hy_ctx* c, const uint64_t* a, const uint64_t* b, uin
   if (!c || !a || !b || !out) return fail(HY_E_ARG, "null");
   if (level >= c->n_q || npoly == 0) return fail(HY_E_ARG, "level/npoly out of range");
   dim3 g(c->N / kT, (level + 1) * npoly);
+  KTimer kt(c, FAM_ELEM, st(stream));
+  kt.bytes = 3ull * (level + 1) * npoly * c->N * 8;
   k_add<<<g, kT, 0, st(stream)>>>(a, b, out, c->dt, level + 1, c->log_n);
-  ++c->launches;
   return cuda_check("hy_add");
 }
 
@@ -235,8 +239,10 @@ extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, u
   }
   launch_ntt(c, b, true, s);
   dim3 g(c->N / kT, level, 2);
-  k_rescale_lift<<<g, kT, 0, s>>>(v, w, c->dt, level, c->log_n);
-  ++c->launches;
+  {
+    KTimer kt(c, FAM_RESCALE, s);
+    k_rescale_lift<<<g, kT, 0, s>>>(v, w, c->dt, level, c->log_n);
+  }
   b.n = 0;
   for (int p = 0; p < 2; ++p)
     for (uint32_t i = 0; i < level; ++i) {
@@ -247,8 +253,10 @@ extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, u
       ++b.n;
     }
   launch_ntt(c, b, false, s);
-  k_rescale_final<<<g, kT, 0, s>>>(ct, w, c->d_rescale[level], c->dt, level, out, c->log_n);
-  ++c->launches;
+  {
+    KTimer kt(c, FAM_RESCALE, s);
+    k_rescale_final<<<g, kT, 0, s>>>(ct, w, c->d_rescale[level], c->dt, level, out, c->log_n);
+  }
   return cuda_check("hy_rescale");
 }
 
@@ -275,10 +283,12 @@ extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_s
   std::vector<uint64_t> g(L1);
   for (uint32_t j = 0; j < c->dnum; ++j) {
     const uint64_t obj = (k << 8) | j;
-    k_sample_cbd<<<c->N / kT, kT, 0, s>>>(ek_seed, kDomEvkE, obj, e);
     dim3 gg(c->N / kT, L1);
-    k_small_to_limbs<int32_t><<<gg, kT, 0, s>>>(e, e_ntt, nullptr, c->dt, c->log_n);
-    c->launches += 2;
+    {
+      KTimer kt(c, FAM_CLIENT, s, 2);
+      k_sample_cbd<<<c->N / kT, kT, 0, s>>>(ek_seed, kDomEvkE, obj, e);
+      k_small_to_limbs<int32_t><<<gg, kT, 0, s>>>(e, e_ntt, nullptr, c->dt, c->log_n);
+    }
     ntt_contig(c, e_ntt, e_ntt, chain.data(), L1, false, s);
     // g_j = P on the q-limbs of digit j, 0 elsewhere (DESIGN R-EVK)
     for (uint32_t t = 0; t < L1; ++t) {
@@ -291,8 +301,10 @@ extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_s
       }
     }
     cudaMemcpyAsync(gm, g.data(), L1 * 8, cudaMemcpyHostToDevice, s);
-    k_evk_digit<<<gg, kT, 0, s>>>(evk, s_ntt, sk_ntt, e_ntt, ek_seed, obj, gm, (int)j, (int)L1, c->dt, c->log_n);
-    ++c->launches;
+    {
+      KTimer kt(c, FAM_CLIENT, s);
+      k_evk_digit<<<gg, kT, 0, s>>>(evk, s_ntt, sk_ntt, e_ntt, ek_seed, obj, gm, (int)j, (int)L1, c->dt, c->log_n);
+    }
     cudaStreamSynchronize(s);  // g is reused on the host
   }
   return cuda_check("hy_keygen_galois");
@@ -318,14 +330,17 @@ extern "C" hy_status hy_encrypt(hy_ctx* c, uint64_t sk_seed, uint64_t enc_seed, 
   int8_t* d_s = ws.take<int8_t>(N);
   if (!d_s) return fail(HY_E_WORKSPACE, "workspace too small");
   secret_ntt(c, sk_seed, n, s_ntt, d_s, s);
-  k_sample_cbd<<<c->N / kT, kT, 0, s>>>(enc_seed, kDomEncE, ct_id, e);
   dim3 g(c->N / kT, n);
-  k_small_to_limbs<int32_t><<<g, kT, 0, s>>>(e, e_ntt, nullptr, c->dt, c->log_n);
+  {
+    KTimer kt(c, FAM_CLIENT, s, 2);
+    k_sample_cbd<<<c->N / kT, kT, 0, s>>>(enc_seed, kDomEncE, ct_id, e);
+    k_small_to_limbs<int32_t><<<g, kT, 0, s>>>(e, e_ntt, nullptr, c->dt, c->log_n);
+  }
   std::vector<uint32_t> chain(n);
   for (uint32_t i = 0; i < n; ++i) chain[i] = i;
   ntt_contig(c, e_ntt, e_ntt, chain.data(), n, false, s);
+  KTimer kt(c, FAM_CLIENT, s);
   k_encrypt<<<g, kT, 0, s>>>(pt, s_ntt, e_ntt, enc_seed, ct_id, ct, c->dt, level, c->log_n);
-  c->launches += 3;
   return cuda_check("hy_encrypt");
 }
 
@@ -342,8 +357,8 @@ extern "C" hy_status hy_decrypt(hy_ctx* c, uint64_t sk_seed, const uint64_t* ct,
   if (!d_s) return fail(HY_E_WORKSPACE, "workspace too small");
   secret_ntt(c, sk_seed, n, s_ntt, d_s, s);
   dim3 g(c->N / kT, n);
+  KTimer kt(c, FAM_CLIENT, s);
   k_decrypt<<<g, kT, 0, s>>>(ct, s_ntt, pt, c->dt, level, c->log_n);
-  ++c->launches;
   return cuda_check("hy_decrypt");
 }
 
@@ -359,8 +374,10 @@ extern "C" hy_status hy_pt_from_coeffs(hy_ctx* c, const int64_t* h_coeffs, uint3
   cudaMemcpyAsync(d, h_coeffs, c->N * 8, cudaMemcpyHostToDevice, s);
   const uint32_t n = level + 1;
   dim3 g(c->N / kT, n);
-  k_small_to_limbs<int64_t><<<g, kT, 0, s>>>(d, pt, nullptr, c->dt, c->log_n);
-  ++c->launches;
+  {
+    KTimer kt(c, FAM_CLIENT, s);
+    k_small_to_limbs<int64_t><<<g, kT, 0, s>>>(d, pt, nullptr, c->dt, c->log_n);
+  }
   std::vector<uint32_t> chain(n);
   for (uint32_t i = 0; i < n; ++i) chain[i] = i;
   ntt_contig(c, pt, pt, chain.data(), n, false, s);
