@@ -57,4 +57,38 @@ __device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const PrimeC
 
 __device__ __forceinline__ uint32_t bitrev32(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
+// ---------------------------------------------------------------- FP64-pipe modular arithmetic
+// Residues of primes q < 2^48 are exact doubles.  B200 issues FP64 FMA at full
+// rate (64/clk/SM, measured 18.2 TFMA/s), so the NTT butterflies run on the FP64
+// pipe instead of the half-rate 64-bit IMAD chains (tools/microbench/fp_modmul.cu:
+// 1.66 vs 0.97 T modmul/s with full reduction).
+constexpr double kTwo52 = 4503599627370496.0;   // 2^52
+constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: (x + M) - M = rint(x) for |x| < 2^51
+
+__device__ __forceinline__ double u2d(uint64_t v) {  // v < 2^52
+  return __longlong_as_double((long long)(v | 0x4330000000000000ull)) - kTwo52;
+}
+__device__ __forceinline__ uint64_t d2u(double d) {  // d integer in [0, 2^52)
+  return (uint64_t)__double_as_longlong(d + kTwo52) & 0xFFFFFFFFFFFFFull;
+}
+// b*w mod q as an integer-valued double r with |r| <= 1.5 q, for |b| <= 16 q, 0 <= w < q < 2^48:
+// h + l = b*w exactly (FMA error term), c = rint(h/q), r = (h - c q) + l, every step exact.
+__device__ __forceinline__ double fmulmod(double b, double w, double q, double qinv) {
+  const double h = b * w;
+  const double l = fma(b, w, -h);
+  const double c = fma(h, qinv, kMagic) - kMagic;
+  return fma(-c, q, h) + l;
+}
+// v - rint(v/q) q, in [-q/2 - 1, q/2 + 1] for |v| < 2^51
+__device__ __forceinline__ double fred(double v, double q, double qinv) {
+  const double c = fma(v, qinv, kMagic) - kMagic;
+  return fma(-c, q, v);
+}
+// canonical residue in [0, q) for |v| < 2^51
+__device__ __forceinline__ double fcanon(double v, double q, double qinv) {
+  double r = fred(v, q, qinv);
+  r = r < 0.0 ? r + q : r;
+  return r >= q ? r - q : r;
+}
+
 }  // namespace hy

@@ -116,9 +116,9 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
   // primes (R-PRIMES)
   for (uint32_t t = 0; t < L; ++t) {
     uint32_t bits = t < c->n_q ? prm->q_bits[t] : prm->p_bits[t - c->n_q];
-    if (bits < 20 || bits > 61) {
+    if (bits < 20 || bits > 48) {  // the FP64-pipe NTT needs q < 2^48 (hy_ntt.cu)
       delete c;
-      return fail(HY_E_ARG, "prime bit sizes must be in [20,61]");
+      return fail(HY_E_ARG, "prime bit sizes must be in [20,48]");
     }
     uint64_t cand = (((1ull << bits) - 2) / twoN) * twoN + 1;
     for (;; cand -= twoN) {
@@ -149,7 +149,7 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
 
   // twiddle tables + prime constants, one allocation
   const size_t tw_words = (size_t)L * c->N;
-  std::vector<uint64_t> tw(tw_words), tws(tw_words), itw(tw_words), itws(tw_words);
+  std::vector<double> tw(tw_words), itw(tw_words);
   std::vector<PrimeConst> pc(L);
   std::vector<uint64_t> pw(c->N), ipw(c->N);
   for (uint32_t t = 0; t < L; ++t) {
@@ -161,10 +161,8 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
     }
     for (uint32_t k = 0; k < c->N; ++k) {
       size_t o = (size_t)t * c->N + k;
-      tw[o] = pw[brev(k, c->log_n)];
-      itw[o] = ipw[brev(k, c->log_n)];
-      tws[o] = shoup_pre(tw[o], q);
-      itws[o] = shoup_pre(itw[o], q);
+      tw[o] = (double)pw[brev(k, c->log_n)];
+      itw[o] = (double)ipw[brev(k, c->log_n)];
     }
     PrimeConst& p = pc[t];
     p.q = q;
@@ -174,23 +172,22 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
     p.r64_sh = shoup_pre(p.r64, q);
     p.n_inv = inv_h(c->N % q, q);
     p.n_inv_sh = shoup_pre(p.n_inv, q);
+    p.qd = (double)q;
+    p.qinv = 1.0 / (double)q;
+    p.n_inv_d = (double)p.n_inv;
   }
-  size_t bytes = 4 * tw_words * 8 + L * sizeof(PrimeConst);
+  size_t bytes = 2 * tw_words * 8 + L * sizeof(PrimeConst);
   if (cudaMalloc(&c->d_tables, bytes) != cudaSuccess) {
     delete c;
     return cuda_check("cudaMalloc tables");
   }
   uint64_t* base = (uint64_t*)c->d_tables;
   cudaMemcpy(base, tw.data(), tw_words * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(base + tw_words, tws.data(), tw_words * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(base + 2 * tw_words, itw.data(), tw_words * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(base + 3 * tw_words, itws.data(), tw_words * 8, cudaMemcpyHostToDevice);
-  cudaMemcpy(base + 4 * tw_words, pc.data(), L * sizeof(PrimeConst), cudaMemcpyHostToDevice);
-  c->dt.tw = base;
-  c->dt.tw_sh = base + tw_words;
-  c->dt.itw = base + 2 * tw_words;
-  c->dt.itw_sh = base + 3 * tw_words;
-  c->dt.pc = reinterpret_cast<const PrimeConst*>(base + 4 * tw_words);
+  cudaMemcpy(base + tw_words, itw.data(), tw_words * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(base + 2 * tw_words, pc.data(), L * sizeof(PrimeConst), cudaMemcpyHostToDevice);
+  c->dt.tw = reinterpret_cast<const double*>(base);
+  c->dt.itw = reinterpret_cast<const double*>(base + tw_words);
+  c->dt.pc = reinterpret_cast<const PrimeConst*>(base + 2 * tw_words);
 
   // basis-conversion constants per level
   const uint32_t K = c->n_p;

@@ -25,6 +25,9 @@ struct PrimeConst {
   uint64_t r64_sh;      // Shoup companion of r64
   uint64_t n_inv;       // N^{-1} mod q
   uint64_t n_inv_sh;
+  double qd;            // q as a double (exact: q < 2^48)
+  double qinv;          // 1/q rounded to double
+  double n_inv_d;       // N^{-1} mod q as a double
 };
 
 // Basis-conversion constants for one (level, digit): ModUp  D_j -> other limbs.
@@ -46,10 +49,8 @@ struct RescaleConst {  // for dropping q_l
 };
 
 struct DevTables {
-  const uint64_t* tw;      // [chain][N] psi^{br(k)}
-  const uint64_t* tw_sh;   // Shoup companions
-  const uint64_t* itw;     // [chain][N] psi^{-br(k)}
-  const uint64_t* itw_sh;
+  const double* tw;        // [chain][N] psi^{br(k)} (exact doubles, q < 2^48)
+  const double* itw;       // [chain][N] psi^{-br(k)}
   const PrimeConst* pc;    // [chain]
 };
 

@@ -44,34 +44,22 @@ __global__ void k_automorph(const uint64_t* __restrict__ in, uint64_t* __restric
   out[off + p] = v;
 }
 
-// Reduction constants of one prime, staged in shared memory.
-struct RedConst {
-  uint64_t q, two_q, mu, r64, r64_sh;
+// FP64 constants of one prime, staged in shared memory.
+struct FConst {
+  double q, qinv;
 };
-__device__ __forceinline__ uint64_t reduce128s(U128 x, const RedConst& p) {
-  uint64_t a = shoup_lazy(x.hi, p.r64, p.r64_sh, p.q);  // [0, 2q)
-  uint64_t b = x.lo - __umul64hi(x.lo, p.mu) * p.q;      // [0, 2q)
-  uint64_t s = csub(a + b, p.two_q);
-  return csub(s, p.q);
-}
-__device__ __forceinline__ void stage_red(RedConst& r, const PrimeConst& p) {
-  r.q = p.q;
-  r.two_q = p.two_q;
-  r.mu = p.mu;
-  r.r64 = p.r64;
-  r.r64_sh = p.r64_sh;
-}
 
 // ModUp basis conversion for digit j = blockIdx.y; one thread per coefficient x
 // produces every non-own limb of the digit.  grid (N/256, beta).
-// y_i = d_i (D_j/q_i)^{-1} mod q_i;  ext[j][u][x] = sum_i y_i [(D_j/q_i) mod t_u] mod t_u  (u not in digit j)
-// A = alpha (compile time); a partial last digit pads its missing sources with 0.
+// y_i = [d_i (D_j/q_i)^{-1}]_{q_i} in [0, q_i);  ext[j][u][x] = [sum_i y_i ((D_j/q_i) mod t_u)]_{t_u}.
+// Every product is reduced on the FP64 pipe (fmulmod, |term| <= 1.5 t), the A terms are summed
+// exactly and canonicalised once.  A = alpha (compile time); a partial last digit pads with 0.
 template <int A>
 __global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict__ d, uint64_t* __restrict__ ext,
                                                      const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
                                                      int logN) {
-  __shared__ uint64_t s_hat[kMaxExt][A];
-  __shared__ RedConst s_red[kMaxExt];
+  __shared__ double s_hat[kMaxExt][A];
+  __shared__ FConst s_fc[kMaxExt];
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
@@ -79,27 +67,39 @@ __global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict_
   const int nsrc = m.hi - m.lo;
   for (int i = threadIdx.x; i < E * A; i += blockDim.x) {
     const int u = i / A, ii = i % A;
-    s_hat[u][ii] = ii < nsrc ? m.hat_mod[u][ii] : 0;
+    s_hat[u][ii] = ii < nsrc ? (double)m.hat_mod[u][ii] : 0.0;
   }
-  for (int u = threadIdx.x; u < E; u += blockDim.x) stage_red(s_red[u], dt.pc[u <= level ? u : n_q + (u - level - 1)]);
-  uint64_t y[A];
+  for (int u = threadIdx.x; u < E; u += blockDim.x) {
+    const PrimeConst& pc = dt.pc[u <= level ? u : n_q + (u - level - 1)];
+    s_fc[u] = FConst{pc.qd, pc.qinv};
+  }
+  double y[A];
 #pragma unroll
-  for (int i = 0; i < A; ++i)
-    y[i] = i < nsrc ? shoup(d[(size_t)(m.lo + i) * N + x], m.hat_inv[i], m.hat_inv_sh[i], dt.pc[m.lo + i].q) : 0;
+  for (int i = 0; i < A; ++i) {
+    if (i < nsrc) {
+      const PrimeConst& pc = dt.pc[m.lo + i];
+      y[i] = fcanon(fmulmod(u2d(d[(size_t)(m.lo + i) * N + x]), (double)m.hat_inv[i], pc.qd, pc.qinv), pc.qd,
+                    pc.qinv);
+    } else {
+      y[i] = 0.0;
+    }
+  }
   __syncthreads();
   uint64_t* out = ext + (size_t)j * E * N + x;
   for (int u = 0; u < E; ++u) {
     if (u >= m.lo && u < m.hi) continue;
-    U128 acc{0, 0};
+    const FConst f = s_fc[u];
+    double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < A; ++i) mac(acc, y[i], s_hat[u][i]);
-    out[(size_t)u * N] = reduce128s(acc, s_red[u]);
+    for (int i = 0; i < A; ++i) acc += fmulmod(y[i], s_hat[u][i], f.q, f.qinv);
+    out[(size_t)u * N] = d2u(fcanon(acc, f.q, f.qinv));
   }
 }
 
 // Key-switch inner product, B = beta digits (compile time).  grid (N/256, E).
 // u[c][u][x] (+)= sum_j src_j[u][perm(x)] * evk[j][c][chain(u)][x], where src_j[u] is the digit's own
 // limb of `own` (the NTT-domain c1 the digits were cut from) when u belongs to digit j, else ext[j][u].
+// Products reduced on the FP64 pipe, summed exactly (|sum| <= 1.5 B t < 2^51), canonicalised once.
 template <int B>
 __global__ void __launch_bounds__(256) k_ks_ip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ own,
                                                const uint64_t* __restrict__ evk, uint64_t* __restrict__ uo,
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) k_ks_ip(const uint64_t* __restrict__ ext,
   const int u = blockIdx.y;
   const int t = u <= level ? u : n_q + (u - level - 1);
   const PrimeConst& p = dt.pc[t];
+  const double q = p.qd, qinv = p.qinv;
   const uint32_t xs = kperm != 1 ? aut_index(x, kperm, logN) : x;
   const int own_digit = (own && u <= level) ? u / alpha : -1;
   uint64_t v[B], e0[B], e1[B];
@@ -121,48 +122,53 @@ __global__ void __launch_bounds__(256) k_ks_ip(const uint64_t* __restrict__ ext,
     e0[j] = __ldcs(e);
     e1[j] = __ldcs(e + (size_t)L1 * N);
   }
-  U128 a0{0, 0}, a1{0, 0};
+  double a0 = 0.0, a1 = 0.0;
 #pragma unroll
   for (int j = 0; j < B; ++j) {
-    mac(a0, v[j], e0[j]);
-    mac(a1, v[j], e1[j]);
+    const double vj = u2d(v[j]);
+    a0 += fmulmod(vj, u2d(e0[j]), q, qinv);
+    a1 += fmulmod(vj, u2d(e1[j]), q, qinv);
   }
-  uint64_t r0 = reduce128(a0, p), r1 = reduce128(a1, p);
   uint64_t* o0 = uo + (size_t)u * N + x;
   uint64_t* o1 = uo + ((size_t)E + u) * N + x;
   if (accumulate) {
-    r0 = add_mod(r0, *o0, p.q);
-    r1 = add_mod(r1, *o1, p.q);
+    a0 += u2d(*o0);
+    a1 += u2d(*o1);
   }
-  *o0 = r0;
-  *o1 = r1;
+  *o0 = d2u(fcanon(a0, q, qinv));
+  *o1 = d2u(fcanon(a1, q, qinv));
 }
 
 // ModDown basis conversion P -> Q_l, KP = K special primes (compile time).  grid (N/256, npoly);
-// v = iNTT(u on P) [npoly][K][N];  z_k = v_k (P/p_k)^{-1} mod p_k;  w[c][i] = sum_k z_k [(P/p_k) mod q_i] mod q_i.
+// v = iNTT(u on P) [npoly][K][N];  z_k = [v_k (P/p_k)^{-1}]_{p_k} in [0, p_k);
+// w[c][i] = [sum_k z_k ((P/p_k) mod q_i)]_{q_i}.
 template <int KP>
 __global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restrict__ v, uint64_t* __restrict__ w,
                                                        const ModDownConst* md, DevTables dt, int level, int n_q,
                                                        int logN) {
-  __shared__ uint64_t s_hat[kMaxChain][KP];
-  __shared__ RedConst s_red[kMaxChain];
+  __shared__ double s_hat[kMaxChain][KP];
+  __shared__ FConst s_fc[kMaxChain];
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   const int n = level + 1;
-  for (int i = threadIdx.x; i < n * KP; i += blockDim.x) s_hat[i / KP][i % KP] = md->phat_mod[i / KP][i % KP];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) stage_red(s_red[i], dt.pc[i]);
-  uint64_t z[KP];
+  for (int i = threadIdx.x; i < n * KP; i += blockDim.x) s_hat[i / KP][i % KP] = (double)md->phat_mod[i / KP][i % KP];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_fc[i] = FConst{dt.pc[i].qd, dt.pc[i].qinv};
+  double z[KP];
 #pragma unroll
-  for (int k = 0; k < KP; ++k)
-    z[k] = shoup(v[((size_t)c * KP + k) * N + x], md->phat_inv[k], md->phat_inv_sh[k], dt.pc[n_q + k].q);
+  for (int k = 0; k < KP; ++k) {
+    const PrimeConst& pc = dt.pc[n_q + k];
+    z[k] = fcanon(fmulmod(u2d(v[((size_t)c * KP + k) * N + x]), (double)md->phat_inv[k], pc.qd, pc.qinv), pc.qd,
+                  pc.qinv);
+  }
   __syncthreads();
   uint64_t* out = w + (size_t)c * n * N + x;
   for (int i = 0; i < n; ++i) {
-    U128 acc{0, 0};
+    const FConst f = s_fc[i];
+    double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < KP; ++k) mac(acc, z[k], s_hat[i][k]);
-    out[(size_t)i * N] = reduce128s(acc, s_red[i]);
+    for (int k = 0; k < KP; ++k) acc += fmulmod(z[k], s_hat[i][k], f.q, f.qinv);
+    out[(size_t)i * N] = d2u(fcanon(acc, f.q, f.qinv));
   }
 }
 

@@ -13,6 +13,8 @@
 // Each 256-point transform lives in registers, 8 words per thread, and moves
 // through shared memory twice (layouts L1 -> L2 -> L3) so that every stage is
 // a register-local butterfly: L1 owns bits {7,6,5}, L2 {4,3,2}, L3 {1,0}.
+// Arithmetic runs on the FP64 pipe (hy_arith.cuh fmulmod): residues are loaded
+// as uint64, converted exactly to doubles, and stored back canonical in [0, q).
 #include "hy_arith.cuh"
 
 namespace hy {
@@ -30,14 +32,15 @@ __device__ __forceinline__ int kbit(int s) {
 }
 
 // Run stages [s_lo, s_hi] (forward: descending, inverse: ascending) on the 8
-// register words of one thread in layout LAY.  Twiddles come from a shared-
-// memory "heap" table T[li], li = (256 + e) >> (s+1) in [1, 256), filled by
-// load_twiddles() for the 256-point transform at hand.
+// register values of one thread in layout LAY, on the FP64 pipe.  Twiddles come
+// from a shared-memory "heap" table T[li], li = (256 + e) >> (s+1) in [1, 256).
+//   forward (CT):  a' = a + b w, b' = a - b w   with |b w mod q| <= 1.5 q, no reduction
+//                  inside a pass (|v| < q + 8 * 1.5 q < 16 q, see fmulmod);
+//   inverse (GS):  a' = a + b, b' = (a - b) w; sums double per stage, so every
+//                  register round ends with a reduction (fred) of all 8 values.
 template <int LAY, bool FWD>
-__device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, int s_lo,
-                                           const uint64_t* __restrict__ T, const uint64_t* __restrict__ Ts,
-                                           uint64_t q) {
-  const uint64_t two_q = q << 1;
+__device__ __forceinline__ void run_stages(double (&x)[8], int l, int s_hi, int s_lo, const double* __restrict__ T,
+                                           double q, double qinv) {
 #pragma unroll
   for (int it = 0; it <= s_hi - s_lo; ++it) {
     const int s = FWD ? s_hi - it : s_lo + it;
@@ -45,109 +48,105 @@ __device__ __forceinline__ void run_stages(uint64_t (&x)[8], int l, int s_hi, in
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (k & kb) continue;
-      const int li = (256 + elem<LAY>(l, k)) >> (s + 1);
-      const uint64_t w = T[li], ws = Ts[li];
-      uint64_t a = x[k], b = x[k | kb];
+      const double w = T[(256 + elem<LAY>(l, k)) >> (s + 1)];
+      const double a = x[k], b = x[k | kb];
       if (FWD) {
-        // Harvey lazy CT butterfly: inputs/outputs in [0, 4q)
-        a = csub(a, two_q);
-        const uint64_t t = shoup_lazy(b, w, ws, q);  // [0, 2q)
+        const double t = fmulmod(b, w, q, qinv);
         x[k] = a + t;
-        x[k | kb] = a + two_q - t;
+        x[k | kb] = a - t;
       } else {
-        // lazy GS butterfly: inputs/outputs in [0, 2q)
-        x[k] = csub(a + b, two_q);
-        x[k | kb] = shoup_lazy(a + two_q - b, w, ws, q);
+        x[k] = a + b;
+        x[k | kb] = fmulmod(a - b, w, q, qinv);
       }
     }
+  }
+  if (!FWD) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fred(x[k], q, qinv);
   }
 }
 
 // Fill the twiddle heap of one 256-point transform: T[li] = W[((hb - 1) << m) + li],
 // m = floor(log2 li).  hb = 1 for pass A (global index = li) and R + row for
 // pass B (global index = (N + row*256 + e) >> (s+1)).  nthr threads cooperate.
-__device__ __forceinline__ void load_twiddles(uint64_t* T, uint64_t* Ts, const uint64_t* __restrict__ W,
-                                              const uint64_t* __restrict__ Ws, uint32_t hb, int tid, int nthr) {
+__device__ __forceinline__ void load_twiddles(double* T, const double* __restrict__ W, uint32_t hb, int tid,
+                                              int nthr) {
   for (int li = tid; li < 256; li += nthr) {
     if (li == 0) continue;
     const int m = 31 - __clz(li);
-    const uint32_t g = ((hb - 1) << m) + (uint32_t)li;
-    T[li] = __ldg(W + g);
-    Ts[li] = __ldg(Ws + g);
+    T[li] = __ldg(W + ((hb - 1) << m) + (uint32_t)li);
   }
 }
 
 __device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
 
 // ---------------------------------------------------------------- pass B (rows)
-// CTA = 8 warps, one 256-word row per warp, dynamic smem = 8 x (272 data + 2 x 256 twiddles) words.
-// grid = (N/256/8, n_limbs)
-constexpr int kRowsSmemWords = 272 + 512;
+// CTA = 8 warps, one 256-word row per warp.  grid = (N/256/8, n_limbs)
 template <bool FWD>
 __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int logN) {
-  extern __shared__ uint64_t dsm[];
+  __shared__ double sm[8][272];
+  __shared__ double tws[8][256];
   const int limb = blockIdx.y, w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + w;
   const size_t N = (size_t)1 << logN;
   if (row >= (int)(N >> 8)) return;  // N = 2^10: 4 rows in an 8-warp CTA
   const int t = b.chain[limb];
-  const uint64_t q = dt.pc[t].q;
-  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
-  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const PrimeConst& pc = dt.pc[t];
+  const double q = pc.qd, qinv = pc.qinv;
+  const double* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
   const uint64_t* src = b.src[limb] + (size_t)row * 256;
   uint64_t* dst = b.dst[limb] + (size_t)row * 256;
-  uint64_t* S = dsm + w * kRowsSmemWords;
-  uint64_t* T = S + 272;
-  uint64_t* Ts = T + 256;
-  uint64_t x[8];
+  double* S = sm[w];
+  double* T = tws[w];
+  double x[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) x[k] = src[elem<1>(l, k)];
-  load_twiddles(T, Ts, W, Ws, (uint32_t)(N >> 8) + (uint32_t)row, l, 32);
+  for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+  load_twiddles(T, W, (uint32_t)(N >> 8) + (uint32_t)row, l, 32);
   __syncwarp();
   if (FWD) {
-    run_stages<1, true>(x, l, 7, 5, T, Ts, q);
+    run_stages<1, true>(x, l, 7, 5, T, q, qinv);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
-    run_stages<2, true>(x, l, 4, 2, T, Ts, q);
+    run_stages<2, true>(x, l, 4, 2, T, q, qinv);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
-    run_stages<3, true>(x, l, 1, 0, T, Ts, q);
+    run_stages<3, true>(x, l, 1, 0, T, q, qinv);
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
+    for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = fcanon(x[k], q, qinv);
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = csub(csub(S[pidx(elem<1>(l, k))], q << 1), q);  // [0,4q) -> [0,q)
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2u(S[pidx(elem<1>(l, k))]);
   } else {
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
-    run_stages<3, false>(x, l, 1, 0, T, Ts, q);
+    run_stages<3, false>(x, l, 1, 0, T, q, qinv);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
-    run_stages<2, false>(x, l, 4, 2, T, Ts, q);
+    run_stages<2, false>(x, l, 4, 2, T, q, qinv);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<1>(l, k))];
-    run_stages<1, false>(x, l, 7, 5, T, Ts, q);
+    run_stages<1, false>(x, l, 7, 5, T, q, qinv);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = x[k];
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2u(fcanon(x[k], q, qinv));
   }
 }
 
@@ -156,87 +155,85 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
 // grid = (256/16, n_limbs)
 template <bool FWD>
 __global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, int logN) {
-  __shared__ uint64_t sm[16 * 273];
-  __shared__ uint64_t T[256], Ts[256];
+  __shared__ double sm[16 * 273];
+  __shared__ double T[256];
   const int limb = blockIdx.y, c = threadIdx.x & 15, l = threadIdx.x >> 4;
   const int col = blockIdx.x * 16 + c;
   const int t = b.chain[limb];
   const size_t N = (size_t)1 << logN;
   const PrimeConst& pc = dt.pc[t];
-  const uint64_t q = pc.q;
-  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
-  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const double q = pc.qd, qinv = pc.qinv;
+  const double* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
   const uint64_t* src = FWD ? b.src[limb] : b.dst[limb];  // inverse runs in place after pass B
   uint64_t* dst = b.dst[limb];
-  uint64_t* S = sm + c * 273;
-  uint64_t x[8];
+  double* S = sm + c * 273;
+  double x[8];
   if (FWD) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<1>(l, k) * 256 + col];
+    for (int k = 0; k < 8; ++k) x[k] = u2d(src[(size_t)elem<1>(l, k) * 256 + col]);
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = src[(size_t)elem<3>(l, k) * 256 + col];
+    for (int k = 0; k < 8; ++k) x[k] = u2d(src[(size_t)elem<3>(l, k) * 256 + col]);
   }
-  load_twiddles(T, Ts, W, Ws, 1, threadIdx.x, blockDim.x);
+  load_twiddles(T, W, 1, threadIdx.x, blockDim.x);
   __syncthreads();
   if (FWD) {
-    run_stages<1, true>(x, l, 7, 5, T, Ts, q);
+    run_stages<1, true>(x, l, 7, 5, T, q, qinv);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<1>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
-    run_stages<2, true>(x, l, 4, 2, T, Ts, q);
+    run_stages<2, true>(x, l, 4, 2, T, q, qinv);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
-    run_stages<3, true>(x, l, 1, 0, T, Ts, q);
+    run_stages<3, true>(x, l, 1, 0, T, q, qinv);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = x[k];
+    for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = d2u(fcanon(x[k], q, qinv));
   } else {
-    run_stages<3, false>(x, l, 1, 0, T, Ts, q);
+    run_stages<3, false>(x, l, 1, 0, T, q, qinv);
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<3>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
-    run_stages<2, false>(x, l, 4, 2, T, Ts, q);
+    run_stages<2, false>(x, l, 4, 2, T, q, qinv);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = S[elem<1>(l, k)];
-    run_stages<1, false>(x, l, 7, 5, T, Ts, q);
+    run_stages<1, false>(x, l, 7, 5, T, q, qinv);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      dst[(size_t)elem<1>(l, k) * 256 + col] = shoup(x[k], pc.n_inv, pc.n_inv_sh, q);
+      dst[(size_t)elem<1>(l, k) * 256 + col] = d2u(fcanon(fmulmod(x[k], pc.n_inv_d, q, qinv), q, qinv));
   }
 }
 
 // ---------------------------------------------------------------- pass A, generic R < 256
-// CTA = 256 threads on a strip of 16 columns x R rows held in shared memory.
+// CTA = 256 threads on a strip of 16 columns x R rows held in shared memory (exact
+// canonical arithmetic per butterfly: only used for N < 2^16).
 template <bool FWD>
 __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables dt, int logN) {
-  __shared__ uint64_t sm[128 * 16];
+  __shared__ double sm[128 * 16];
   const int limb = blockIdx.y;
   const int logR = logN - 8, R = 1 << logR;
   const int t = b.chain[limb];
   const size_t N = (size_t)1 << logN;
   const PrimeConst& pc = dt.pc[t];
-  const uint64_t q = pc.q;
-  const uint64_t* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
-  const uint64_t* Ws = (FWD ? dt.tw_sh : dt.itw_sh) + (size_t)t * N;
+  const double q = pc.qd, qinv = pc.qinv;
+  const double* W = (FWD ? dt.tw : dt.itw) + (size_t)t * N;
   const uint64_t* src = FWD ? b.src[limb] : b.dst[limb];
   uint64_t* dst = b.dst[limb];
   const int col0 = blockIdx.x * 16;
   for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
     int r = i >> 4, c = i & 15;
-    uint64_t v = src[(size_t)r * 256 + col0 + c];
-    sm[i] = FWD ? v : csub(v, q);  // inverse input comes from pass B in [0, 2q)
+    sm[i] = u2d(src[(size_t)r * 256 + col0 + c]);
   }
   __syncthreads();
   for (int it = 0; it < logR; ++it) {
@@ -245,25 +242,24 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
     for (int bf = threadIdx.x; bf < (R / 2) * 16; bf += blockDim.x) {
       int c = bf & 15, j = bf >> 4;                       // butterfly j in [0, R/2)
       int r = ((j >> s) << (s + 1)) | (j & (half - 1));   // lower element row
-      uint32_t idx = (uint32_t)(R + r) >> (s + 1);
-      uint64_t w = W[idx], ws = Ws[idx];
-      uint64_t a = sm[r * 16 + c], bb = sm[(r + half) * 16 + c];
+      const double w = W[(uint32_t)(R + r) >> (s + 1)];
+      const double a = sm[r * 16 + c], bb = sm[(r + half) * 16 + c];
       if (FWD) {
-        uint64_t tt = shoup(bb, w, ws, q);
-        sm[r * 16 + c] = add_mod(a, tt, q);
-        sm[(r + half) * 16 + c] = sub_mod(a, tt, q);
+        const double tt = fmulmod(bb, w, q, qinv);
+        sm[r * 16 + c] = fred(a + tt, q, qinv);
+        sm[(r + half) * 16 + c] = fred(a - tt, q, qinv);
       } else {
-        sm[r * 16 + c] = add_mod(a, bb, q);
-        sm[(r + half) * 16 + c] = shoup(sub_mod(a, bb, q), w, ws, q);
+        sm[r * 16 + c] = fred(a + bb, q, qinv);
+        sm[(r + half) * 16 + c] = fmulmod(a - bb, w, q, qinv);
       }
     }
     __syncthreads();
   }
   for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
     int r = i >> 4, c = i & 15;
-    uint64_t v = sm[i];
-    if (!FWD) v = shoup(v, pc.n_inv, pc.n_inv_sh, q);
-    dst[(size_t)r * 256 + col0 + c] = v;
+    double v = sm[i];
+    if (!FWD) v = fmulmod(v, pc.n_inv_d, q, qinv);
+    dst[(size_t)r * 256 + col0 + c] = d2u(fcanon(v, q, qinv));
   }
 }
 
@@ -271,13 +267,6 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
 
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
   if (b.n == 0) return;
-  constexpr int kRowsBytes = 8 * kRowsSmemWords * 8;
-  static bool attr_set = false;  // per process: the attribute is a property of the function
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_ntt_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowsBytes);
-    cudaFuncSetAttribute(k_ntt_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowsBytes);
-    attr_set = true;
-  }
   const int logN = (int)c->log_n;
   const int R = (int)c->N / 256;
   dim3 gB(R / 8 > 0 ? R / 8 : 1, b.n), gA(256 / 16, b.n);
@@ -294,12 +283,12 @@ void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
     for (int i = 0; i < b.n; ++i) b2.src[i] = b.dst[i];
     KTimer kt(c, FAM_NTT_B, s);
     kt.bytes = pass_bytes;
-    k_ntt_rows<true><<<gB, 256, kRowsBytes, s>>>(b2, c->dt, logN);
+    k_ntt_rows<true><<<gB, 256, 0, s>>>(b2, c->dt, logN);
   } else {
     {
       KTimer kt(c, FAM_NTT_B, s);
       kt.bytes = pass_bytes;
-      k_ntt_rows<false><<<gB, 256, kRowsBytes, s>>>(b, c->dt, logN);
+      k_ntt_rows<false><<<gB, 256, 0, s>>>(b, c->dt, logN);
     }
     KTimer kt(c, FAM_NTT_A, s);
     kt.bytes = pass_bytes;

@@ -14,11 +14,11 @@ from __future__ import annotations
 import numpy as np
 
 PARAMS = {
-    # P:1028 (h = 192), DESIGN R-PRIMES (bit sizes), R-SCALE (log_scale)
-    "toy": dict(log_n=12, q_bits=[50, 40, 40], p_bits=[50], dnum=3, h=64, log_scale=40),
-    "hyp": dict(log_n=16, q_bits=[50] + [42] * 23, p_bits=[50] * 4, dnum=6, h=192, log_scale=42),
+    # P:1028 (h = 192), DESIGN R-PRIMES (bit sizes, all <= 48 bits), R-SCALE (log_scale)
+    "toy": dict(log_n=12, q_bits=[48, 40, 40], p_bits=[48], dnum=3, h=64, log_scale=40),
+    "hyp": dict(log_n=16, q_bits=[48] + [42] * 23, p_bits=[48] * 4, dnum=6, h=192, log_scale=42),
     # small full-featured set used by fast CPU tests (alpha = 2, partial last digit)
-    "mini": dict(log_n=10, q_bits=[50, 40, 40, 40, 40], p_bits=[50, 50], dnum=3, h=32, log_scale=40),
+    "mini": dict(log_n=10, q_bits=[48, 40, 40, 40, 40], p_bits=[48, 48], dnum=3, h=32, log_scale=40),
 }
 
 SEED_SK = 3        # secret-key seed of BASELINE config 1

@@ -1,0 +1,28 @@
+"""Key metrics + stall breakdown of an ncu report (first kernel)."""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(out.splitlines()))
+h, v = r[0], r[2]
+d = dict(zip(h, v))
+keys = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+        "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+for k in keys:
+    if k in d:
+        print(f"  {k:65s} {d[k]}")
+st = [(k, float(x.replace(",", ""))) for k, x in d.items()
+      if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued") and x]
+st = [(k, x) for k, x in st if x > 0]
+tot = sum(x for _, x in st)
+print("  stalls:", ", ".join(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100*x/tot:.0f}%" for k, x in sorted(st, key=lambda t: -t[1])[:8]))
