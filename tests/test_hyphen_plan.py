@@ -1,0 +1,116 @@
+"""Pins of the oracle's HyPHEN layer plans (CPU only): the float slot simulator
+running each plan equals conv2d (Alg. 1), the rotation counts
+equal the paper's cost table and its SISO totals."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import hyphen as H
+
+N_SLOTS = 32768
+
+# ResNet-20 CIFAR-10 layers (tb:resnet 20 parameter), Optimal plan (1,2)/(2,4)/(4,8)
+R20 = {
+    "stem":     H.ConvSpec(3, 16, 32, 3, 1, 32, 1, 1, 2, "CA"),
+    "L1_ca":    H.ConvSpec(16, 16, 32, 3, 1, 32, 1, 1, 2, "CA"),
+    "L1_ra":    H.ConvSpec(16, 16, 32, 3, 1, 32, 1, 2, 1, "RA"),
+    "L2_ds":    H.ConvSpec(16, 32, 32, 3, 2, 32, 1, 1, 2, "CA"),
+    "L2_pconv": H.ConvSpec(16, 32, 32, 1, 2, 32, 1, 1, 2, "CA"),
+    "L2_ca":    H.ConvSpec(32, 32, 16, 3, 1, 32, 2, 2, 4, "CA"),
+    "L2_ra":    H.ConvSpec(32, 32, 16, 3, 1, 32, 2, 4, 2, "RA"),
+    "L3_ds":    H.ConvSpec(32, 64, 16, 3, 2, 32, 2, 2, 4, "CA"),
+    "L3_pconv": H.ConvSpec(32, 64, 16, 1, 2, 32, 2, 2, 4, "CA"),
+    "L3_ca":    H.ConvSpec(64, 64, 8, 3, 1, 32, 4, 4, 8, "CA"),
+    "L3_ra":    H.ConvSpec(64, 64, 8, 3, 1, 32, 4, 8, 4, "RA"),
+}
+
+
+def _run(spec, seed=0):
+    X = synth.image(seed, spec.ci, spec.w)
+    K = synth.conv_weight(seed + 1, spec.co, spec.ci, spec.f)
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    ys = H.simulate(plan, H.pack(X, plan.fin))
+    return X, K, plan, ys
+
+
+@pytest.mark.parametrize("name", list(R20))
+def test_simulated_plan_equals_conv2d(name):
+    spec = R20[name]
+    X, K, plan, ys = _run(spec)
+    want = H.conv2d(X, K, spec.s)
+    got = H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo)
+    assert not np.isnan(got).any()
+    assert np.max(np.abs(got - want)) < 1e-9
+    # every replica carries the same values (R_g / R_a replication)
+    rmax = plan.fout.d
+    for rep in range(rmax):
+        assert np.max(np.abs(H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo, rep) - want)) < 1e-9
+
+
+def test_toy_raconv_config1():
+    """BASELINE config 1: 3x3 RAConv 4->4 on 8x8 at N = 2^12 (n = 2048 slots)."""
+    spec = H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048)
+    X, K, plan, ys = _run(spec, 1)
+    assert plan.n_in == 4 and plan.n_out == 1
+    got = H.unpack(ys, plan.fout, 4, 8, 8)
+    assert np.max(np.abs(got - H.conv2d(X, K))) < 1e-9
+    assert sorted(r % 2048 for r in plan.taps if r) == sorted(r % 2048 for r in [-9, -8, -7, -1, 1, 7, 8, 9])
+
+
+def test_pack_unpack_roundtrip():
+    for fmt, C, w in [(H.Fmt("CA", N_SLOTS, 32, 2, 2, 4), 32, 16), (H.Fmt("RA", N_SLOTS, 32, 4, 8, 4), 64, 8),
+                      (H.Fmt("CA", N_SLOTS, 64, 1, 1, 1), 64, 56)]:
+        X = synth.image(3, C, w)
+        assert np.array_equal(H.unpack(H.pack(X, fmt), fmt, C, w, w), X)
+
+
+@pytest.mark.parametrize("cn,m,d,f", [(16, 1, 2, 3), (8, 2, 2, 3), (16, 2, 4, 3), (8, 4, 4, 3), (16, 4, 8, 1)])
+def test_rotation_complexity_table(cn, m, d, f):
+    """Table 'Cost of homomorphic convolutions' with c_i = c_o = m c_n (n_i = 1 for CAConv)."""
+    c = m * cn
+    g = int(math.isqrt(m * d)) if math.isqrt(m * d) ** 2 == m * d else int(math.isqrt(m * d // 2))
+    wp = int(math.isqrt(N_SLOTS // cn // (m * d // (g * g))))
+    spec = H.ConvSpec(c, c, wp // g, f, 1, wp, g, m, d, "CA")
+    p = H.plan_caconv(spec, synth.conv_weight(0, c, c, f))
+    assert p.n_in == 1 and p.n_out == m * cn // d
+    assert p.counts["Slide"] == f * f - 1
+    assert p.counts["RaS"] == (m * cn // d) * int(math.log2(cn))
+    assert p.counts["RaS_g"] == (m * cn // d) * int(math.log2(m))
+    assert p.counts["IR_g"] == (m * cn // d) * int(math.log2(m))
+    # RAConv_Reorder on the CAConv output: n_i = m c_n / d, Slide f^2 - 1 (vs naive n_i (f^2-1)), RaS 0
+    rspec = H.ConvSpec(c, c, wp // g, f, 1, wp, g, d, m, "RA")
+    r = H.plan_raconv(rspec, synth.conv_weight(1, c, c, f))
+    assert r.n_in == m * cn // d and r.n_out == 1
+    assert r.counts["Slide"] == f * f - 1 and r.counts["RaS"] == 0
+    assert r.counts["RaS_g"] == int(math.log2(d)) and r.counts["IR_g"] == int(math.log2(d))
+
+
+def test_siso_totals_resnet20_and_resnet18():
+    """SISO rotations of the Optimal plans: 152 for ResNet-20, 1024 for ResNet-18 (tb:Rot and Boot P:1159)."""
+    slide = 0
+    # 3x3 convs of ResNet-20: stem; 3 basic blocks (CA, RA) per stage, the first CA of stages 2/3 is the dsconv
+    mults = {"stem": 1, "L1_ca": 3, "L1_ra": 3, "L2_ds": 1, "L2_ca": 2, "L2_ra": 3, "L3_ds": 1, "L3_ca": 2, "L3_ra": 3}
+    assert sum(mults.values()) == 19
+    for name, mult in mults.items():
+        spec = R20[name]
+        p =H.plan_caconv(spec, synth.conv_weight(0, spec.co, spec.ci, 3)) if spec.algo == "CA" else \
+            H.plan_raconv(spec, synth.conv_weight(0, spec.co, spec.ci, 3))
+        slide += mult * p.counts["Slide"]
+    assert slide == 152
+    # ResNet-18: plan (1,1)/(2,2)/(4,4)/(8,8), images padded 56/28/14/7 -> 64/32/16/8 (DESIGN R-LAYOUT)
+    r18 = []
+    for L, (c, w, g) in enumerate([(64, 56, 1), (128, 28, 2), (256, 14, 4), (512, 7, 8)]):
+        if L == 0:
+            r18 += [H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA"), H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "RA")] * 2
+        else:
+            pc, pw, pg = [(64, 56, 1), (128, 28, 2), (256, 14, 4)][L - 1]
+            r18 += [H.ConvSpec(pc, c, pw, 3, 2, 64, pg, pg, pg, "CA"), H.ConvSpec(c, c, w, 3, 1, 64, g, g, g, "RA"),
+                    H.ConvSpec(c, c, w, 3, 1, 64, g, g, g, "CA"), H.ConvSpec(c, c, w, 3, 1, 64, g, g, g, "RA")]
+    total = 0
+    for s in r18:
+        K = np.zeros((s.co, s.ci, 3, 3))
+        p = H.plan_caconv(s, K, False) if s.algo == "CA" else H.plan_raconv(s, K, False)
+        total += p.counts["Slide"]
+    assert len(r18) == 16 and total == 1024
