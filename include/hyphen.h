@@ -166,6 +166,62 @@ hy_status hy_add(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t
 /* Rescale (DESIGN R-RESCALE): [2][l+1][N] -> [2][l][N], exact round(c/q_l). */
 hy_status hy_rescale(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint64_t* d_out, void* stream);
 
+/* ---- HyPHEN convolution layers ------------------------------- */
+/* Slot layout (DESIGN R-LAYOUT): physical width wp (power of two), gap g, cell kappa in
+ * [0, m d) with digits (g_c, g_r, e_idx) at slot offsets (1, wp, wp^2), e = m d / g^2 image
+ * sub-blocks per channel block of B = e wp^2 slots, c_n = (N/2) / B blocks.
+ *   CA(m, d) (pi_CA): C_g index mu = kappa % m, R_g index rho = kappa / m;
+ *            ciphertext i holds channel i c_n m + b m + mu in block b.
+ *   RA(m, d) (pi_RA): mu = kappa / d, rho = kappa % d; ciphertext i holds channel
+ *            i m + mu, replicated in every block (R_a) and every rho (R_g).
+ * CAConv maps CA(m, d) -> RA(d, m) (stride 1) or RA(2d, 2m) at gap 2g (stride 2, needs m = g;
+ * DESIGN R-DSCONV); RAConv (reordered) maps RA(m, d) -> CA(d, m), stride 1. */
+typedef enum { HY_CONV_CA = 0, HY_CONV_RA = 1 } hy_conv_algo;
+typedef struct {
+  uint32_t ci, co;   /* input / output channels */
+  uint32_t w;        /* input image width = height (logical pixels) */
+  uint32_t f;        /* odd filter width, zero padding (f-1)/2 (Fig. 2(a)) */
+  uint32_t stride;   /* 1, or 2 for CAConv */
+  uint32_t wp;       /* physical width W_p >= w * gap */
+  uint32_t gap;      /* input gap g */
+  uint32_t m, d;     /* |C_g|, |R_g| of the INPUT format */
+  uint32_t algo;     /* hy_conv_algo */
+} hy_conv_spec;
+typedef struct hy_conv_plan hy_conv_plan;
+/* Rotation amounts, weight/mask plaintext contents and counts for one layer.  Errors:
+ * HY_E_SHAPE (bad sizes), HY_E_FORMAT (non power of two, m d % g^2, unsupported stride-2
+ * layout), HY_E_CAPACITY (image or block does not fit the N/2 slots). */
+hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spec, hy_conv_plan** out); /* host only */
+void hy_conv_plan_destroy(hy_conv_plan* plan);
+/* n_in / n_out ciphertexts, n_pt weight plaintexts (+1 mask plaintext when has_mask),
+ * n_rot distinct nonzero rotation amounts mod N/2 in ascending order (rots: n_rot entries,
+ * the order keys are passed in), counts[5] = Slide, RaS, RaS_g, IR_g rotations and PMults
+ * of the whole layer (table 'Cost of homomorphic convolutions').  Any output
+ * pointer may be NULL. */
+hy_status hy_conv_plan_query(const hy_conv_plan* plan, uint32_t* n_in, uint32_t* n_out, uint32_t* n_pt,
+                             uint32_t* has_mask, uint32_t* n_rot, int32_t* rots, uint32_t* counts);
+/* Slot values (host, N/2 doubles) of weight plaintext idx < n_pt, or of the mask (idx == n_pt).
+ * K: host [co][ci][f][f] float64. */
+hy_status hy_conv_weight_slots(const hy_conv_plan* plan, const double* K, uint32_t idx, double* slots);
+/* Device words of the encoded weights at input level l: n_pt x [l+1][N] then the mask [l][N]. */
+size_t hy_conv_weight_words(const hy_ctx* ctx, const hy_conv_plan* plan, uint32_t level);
+/* Device scratch words hy_caconv / hy_raconv need at input level l. */
+size_t hy_conv_scratch_words(const hy_ctx* ctx, const hy_conv_plan* plan, uint32_t level);
+/* Encode every weight plaintext at scale q_l (level l) and the mask at scale q_{l-1} (level
+ * l-1), so each rescale returns the ciphertext scale exactly (DESIGN R-SCALE). */
+hy_status hy_conv_encode_weights(hy_ctx* ctx, const hy_conv_plan* plan, const double* K, uint32_t level,
+                                 uint64_t* d_pts, void* stream);
+/* Run the layer on n_in input ciphertexts at level l, producing outputs [out_begin, out_end)
+ * (the multi-GPU shard) at level l - 1 - has_mask.  d_evks: one key per rotation amount in
+ * hy_conv_plan_query order.  Outputs must not alias inputs.  HY_E_PLAN when the plan's algo
+ * does not match the call. */
+hy_status hy_caconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
+                    const uint64_t* const* d_in, uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch,
+                    uint32_t out_begin, uint32_t out_end, uint64_t* const* d_out, void* stream);
+hy_status hy_raconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
+                    const uint64_t* const* d_in, uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch,
+                    uint32_t out_begin, uint32_t out_end, uint64_t* const* d_out, void* stream);
+
 /* ---- client side: keys, encode, encrypt, decrypt (untimed) ------- */
 /* Rotation key for Galois element of a left rotation by r (DESIGN R-EVK, R-PRNG):
  * secret from sk_seed, randomness from ek_seed.  d_evk: [dnum][2][n_q+n_p][N]. */

@@ -380,10 +380,16 @@ class EncConv:
     def encode(self, v, level):
         return self.o.encode(v, self.o.q[level], level)
 
-    def run(self, cts):
+    def run(self, cts, outputs=None):
+        """outputs: optional list of output ciphertext indices to compute (sampling); default all."""
         o, p, sp = self.o, self.plan, self.plan.spec
         level = cts[0].level
-        wpts = {k: self.encode(v, level) for k, v in p.weights.items()}
+        outs_wanted = list(range(p.n_out)) if outputs is None else list(outputs)
+        if sp.algo == "CA":
+            grp = set(outs_wanted) if sp.s == 1 else {g for J in outs_wanted for g in (2 * J, 2 * J + 1)}
+        else:
+            grp = set(outs_wanted)
+        wpts = {k: self.encode(v, level) for k, v in p.weights.items() if k[0] in grp}
         if sp.algo == "CA":
             rs = [r for r in p.taps]
             slid = []
@@ -391,8 +397,8 @@ class EncConv:
                 nz = [r for r in rs if r % o.n]
                 rot_cts = dict(zip(nz, o.hrot_hoisted(x, [self.key(r) for r in nz], nz)))
                 slid.append([rot_cts[r] if r % o.n else x for r in rs])
-            groups = []
-            for j in range(p.n_groups):
+            groups = {}
+            for j in sorted(grp):
                 acc = None
                 for i in range(p.n_in):
                     for t in range(len(rs)):
@@ -401,17 +407,18 @@ class EncConv:
                 acc = o.rescale(acc)
                 acc = self.ras(acc, p.ras)
                 acc = self.ras(acc, p.ras_g)
-                groups.append(acc)
+                groups[j] = acc
             if sp.s == 1:
                 outs = []
-                for acc in groups:
+                for j in outs_wanted:
+                    acc = groups[j]
                     if p.mask is not None:
                         acc = o.rescale(o.pmult(acc, self.encode(p.mask, acc.level)))
                         acc = self.ras(acc, p.ir_g)
                     outs.append(acc)
                 return outs
             outs = []
-            for J in range(p.n_out):
+            for J in outs_wanted:
                 lv = groups[2 * J].level
                 mpt = self.encode(p.mask, lv)
                 a = o.rescale(o.pmult(groups[2 * J], mpt))
@@ -420,7 +427,7 @@ class EncConv:
                 outs.append(self.ras(y, p.ir_g))
             return outs
         outs = []
-        for oo in range(p.n_out):
+        for oo in outs_wanted:
             accs = []
             for t in range(len(p.taps)):
                 acc = None

@@ -36,6 +36,10 @@ class _Params(C.Structure):
                 ("hamming_weight", C.c_uint32), ("q_bits", C.POINTER(C.c_uint32)), ("p_bits", C.POINTER(C.c_uint32))]
 
 
+class _ConvSpec(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("ci", "co", "w", "f", "stride", "wp", "gap", "m", "d", "algo")]
+
+
 _lib = None
 _P = C.c_void_p
 _U64 = C.c_uint64
@@ -75,6 +79,16 @@ SIGNATURES = {
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
     "hy_encode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), _U32, _U64, C.POINTER(C.c_int64)]),
     "hy_pt_from_coeffs": (C.c_int, [_P, C.POINTER(C.c_int64), _U32, _P, _P]),
+    "hy_conv_plan_create": (C.c_int, [_U32, C.POINTER(_ConvSpec), C.POINTER(_P)]),
+    "hy_conv_plan_destroy": (None, [_P]),
+    "hy_conv_plan_query": (C.c_int, [_P, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
+                                      C.POINTER(_U32), C.POINTER(C.c_int32), C.POINTER(_U32)]),
+    "hy_conv_weight_slots": (C.c_int, [_P, C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
+    "hy_conv_weight_words": (C.c_size_t, [_P, _P, _U32]),
+    "hy_conv_scratch_words": (C.c_size_t, [_P, _P, _U32]),
+    "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), _U32, _P, _P]),
+    "hy_caconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
+    "hy_raconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
 }
 
 
@@ -300,3 +314,68 @@ class Context:
         _check(lib().hy_pt_from_coeffs(self._c, cf.ctypes.data_as(C.POINTER(C.c_int64)), level, _ptr(out),
                                        self._stream()))
         return out
+
+
+class ConvPlan:
+    """A HyPHEN convolution layer (CAConv / RAConv_Reorder) on one context (include/hyphen.h)."""
+
+    CA, RA = 0, 1
+
+    def __init__(self, ctx, ci, co, w, f, stride, wp, gap, m, d, algo, log_n=None):
+        """ctx may be None (host-only plan inspection) when log_n is given."""
+        self.ctx = ctx
+        self.n = 1 << ((log_n if log_n is not None else ctx.log_n) - 1)
+        self.algo = {"CA": 0, "RA": 1}.get(algo, algo)
+        spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo)
+        h = C.c_void_p()
+        _check(lib().hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
+        self._p = h
+        ni, no, npt, hm, nr = (C.c_uint32() for _ in range(5))
+        counts = (C.c_uint32 * 5)()
+        _check(lib().hy_conv_plan_query(self._p, C.byref(ni), C.byref(no), C.byref(npt), C.byref(hm), C.byref(nr),
+                                        None, counts))
+        rots = (C.c_int32 * max(1, nr.value))()
+        _check(lib().hy_conv_plan_query(self._p, None, None, None, None, None, rots, None))
+        self.n_in, self.n_out, self.n_pt, self.has_mask = ni.value, no.value, npt.value, bool(hm.value)
+        self.rots = [int(rots[i]) for i in range(nr.value)]
+        self.counts = dict(zip(["Slide", "RaS", "RaS_g", "IR_g", "PMult"], [int(x) for x in counts]))
+        self.f = f
+
+    def __del__(self):
+        if getattr(self, "_p", None):
+            lib().hy_conv_plan_destroy(self._p)
+            self._p = None
+
+    def weight_slots(self, K, idx):
+        K = np.ascontiguousarray(K, np.float64)
+        out = np.zeros(self.n)
+        _check(lib().hy_conv_weight_slots(self._p, K.ctypes.data_as(C.POINTER(C.c_double)), idx,
+                                          out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def out_level(self, level):
+        return level - 1 - int(self.has_mask)
+
+    def encode_weights(self, K, level):
+        words = int(lib().hy_conv_weight_words(self.ctx._c, self._p, level))
+        pts = self.ctx.empty(words)
+        K = np.ascontiguousarray(K, np.float64)
+        _check(lib().hy_conv_encode_weights(self.ctx._c, self._p, K.ctypes.data_as(C.POINTER(C.c_double)), level,
+                                            _ptr(pts), self.ctx._stream()))
+        return pts
+
+    def scratch(self, level):
+        return self.ctx.empty(int(lib().hy_conv_scratch_words(self.ctx._c, self._p, level)))
+
+    def run(self, evks, cts, level, pts, scratch=None, out_begin=0, out_end=None, outs=None):
+        """evks: dict rotation amount (mod n) -> key tensor, or a list in self.rots order."""
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        out_end = self.n_out if out_end is None else out_end
+        lo = self.out_level(level)
+        outs = [self.ctx.empty(*self.ctx.ct_shape(lo)) for _ in range(out_end - out_begin)] if outs is None else outs
+        scratch = self.scratch(level) if scratch is None else scratch
+        fn = lib().hy_caconv if self.algo == 0 else lib().hy_raconv
+        _check(fn(self.ctx._c, self._p, _ptr_array(evks), _ptr_array(cts), level, _ptr(pts), _ptr(scratch),
+                  out_begin, out_end, _ptr_array(outs), self.ctx._stream()))
+        return outs

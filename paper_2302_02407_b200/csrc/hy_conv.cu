@@ -1,0 +1,457 @@
+// hy_conv.cu -- HyPHEN convolution layers on the device: CAConv and
+// RAConv_Reorder over 2D-gap packed ciphertexts, including
+// stride-2 downsampling (Fig. 2(d)) -- the plan (rotation amounts, weight and mask
+// slot vectors) is built on the host, every homomorphic step runs in the library's
+// kernels (hoisted HRot, PMult-accumulate, lazy HRotSum, rescale, HRot+add).
+//
+// Slot layout (DESIGN.md R-LAYOUT): physical width W_p, gap g, cell kappa in [0, m d)
+// with low->high digits (g_c, g_r, e_idx) at slot offsets (1, W_p, W_p^2); channel block
+// size B = e W_p^2 (e = m d / g^2), c_n = n / B blocks.
+//   CA(m, d): mu = kappa % m, rho = kappa / m; ciphertext i holds channel i c_n m + b m + mu.
+//   RA(m, d): mu = kappa / d, rho = kappa % d; ciphertext i holds channel i m + mu in every block.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "hy_internal.h"
+
+namespace {
+
+int lg2(uint64_t x) {
+  int v = 0;
+  while ((1ull << v) < x) ++v;
+  return v;
+}
+bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+struct Layout {
+  bool ca;
+  int64_t n, wp, g, m, d;
+  int64_t I() const { return wp * wp; }
+  int64_t e() const { return m * d / (g * g); }
+  int64_t B() const { return e() * I(); }
+  int64_t cn() const { return n / B(); }
+  // slot distance of cell bit k
+  int64_t stride(int k) const {
+    const int lgg = lg2(g);
+    if (k < lgg) return 1ll << k;
+    if (k < 2 * lgg) return wp << (k - lgg);
+    return I() << (k - 2 * lgg);
+  }
+  struct Pos {
+    int64_t b, h, w, kappa;
+  };
+  Pos at(int64_t s) const {
+    const int64_t b = s / B(), r = s % B();
+    const int64_t ei = r / I(), pr = (r % I()) / wp, pc = r % wp;
+    return {b, pr / g, pc / g, (pc % g) + g * ((pr % g) + g * ei)};
+  }
+  int64_t mu(int64_t kappa) const { return ca ? kappa % m : kappa / d; }
+  int64_t rho(int64_t kappa) const { return ca ? kappa / m : kappa % d; }
+  int64_t channel(int64_t ct, const Pos& p) const {
+    return ca ? ct * cn() * m + p.b * m + mu(p.kappa) : ct * m + mu(p.kappa);
+  }
+  int64_t cts_for(int64_t c) const {
+    const int64_t per = ca ? cn() * m : m;
+    return (c + per - 1) / per;
+  }
+};
+
+}  // namespace
+
+struct hy_conv_plan {
+  hy_conv_spec s;
+  int64_t n, pad, wo;
+  Layout in, out;
+  std::vector<int64_t> taps;
+  int64_t n_in, n_groups, n_out;
+  std::vector<int64_t> ras, ras_g, ir_g;
+  bool has_mask = false, has_combine = false;
+  int64_t combine = 0;
+  std::vector<int64_t> rots;  // distinct nonzero rotation amounts mod n (key order)
+  uint32_t counts[5] = {0, 0, 0, 0, 0};
+  int64_t n_pt() const { return n_groups * n_in * (int64_t)s.f * s.f; }
+};
+
+namespace {
+
+int64_t tap_amount(const hy_conv_plan& p, int j1, int j2) {
+  return ((int64_t)j1 - p.pad) * p.s.gap * p.s.wp + ((int64_t)j2 - p.pad) * p.s.gap;
+}
+
+// weight slot vector of plaintext idx (or the mask when idx == n_pt)
+void weight_slots(const hy_conv_plan& p, const double* K, int64_t idx, double* v) {
+  const hy_conv_spec& s = p.s;
+  const int64_t f2 = (int64_t)s.f * s.f;
+  if (idx == p.n_pt()) {  // IR_g mask
+    for (int64_t x = 0; x < p.n; ++x) {
+      bool keep;
+      if (s.algo == HY_CONV_CA && s.stride == 1) {
+        keep = p.in.mu(p.in.at(x).kappa) == 0;
+      } else if (s.algo == HY_CONV_CA) {  // dsconv: new-cell bits [0, lg m), lg g, 2 lg g + 1 all zero
+        const int64_t k2 = p.out.at(x).kappa;
+        const int lgg = lg2(s.gap);
+        keep = true;
+        for (int k = 0; k < lg2(s.m); ++k) keep &= !((k2 >> k) & 1);
+        keep &= !((k2 >> lgg) & 1) && !((k2 >> (2 * lgg + 1)) & 1);
+      } else {
+        keep = p.out.rho(p.out.at(x).kappa) == 0;
+      }
+      v[x] = keep ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const int64_t t = idx % f2, i = (idx / f2) % p.n_in, grp = idx / f2 / p.n_in;
+  const int j1 = (int)(t / s.f), j2 = (int)(t % s.f);
+  auto K_at = [&](int64_t o, int64_t c) { return K[((o * s.ci + c) * s.f + j1) * s.f + j2]; };
+  std::fill(v, v + p.n, 0.0);
+  if (s.algo == HY_CONV_CA) {
+    for (int64_t x = 0; x < p.n; ++x) {
+      const Layout::Pos q = p.in.at(x);
+      const int64_t mu = p.in.mu(q.kappa), rho = p.in.rho(q.kappa);
+      const int64_t c = i * p.in.cn() * s.m + q.b * s.m + mu;
+      int64_t o;
+      bool out_ok;
+      if (s.stride == 1) {
+        o = grp * s.d + rho;
+        out_ok = q.h < p.wo && q.w < p.wo;
+      } else {
+        const int64_t lo = rho % s.gap, hi = rho / s.gap;
+        o = (grp / 2) * (2 * (int64_t)s.d) + lo + (int64_t)s.gap * (grp & 1) + 2 * (int64_t)s.gap * hi;
+        out_ok = !(q.h & 1) && !(q.w & 1) && q.h / 2 < p.wo && q.w / 2 < p.wo;
+      }
+      const int64_t sh = q.h + j1 - p.pad, sw = q.w + j2 - p.pad;
+      if (out_ok && sh >= 0 && sh < s.w && sw >= 0 && sw < s.w && c < s.ci && o < s.co) v[x] = K_at(o, c);
+    }
+  } else {
+    // RAConv: plain SISO weight W for output ct grp, then inversely rotated W' = Rot_{-r_t}(W) (Alg. 2)
+    const int64_t r = p.taps[t];
+    for (int64_t x = 0; x < p.n; ++x) {
+      const Layout::Pos q = p.out.at(x);
+      const int64_t mu = p.out.mu(q.kappa), rho = p.out.rho(q.kappa);
+      const int64_t oc = grp * p.out.cn() * p.out.m + q.b * p.out.m + mu;
+      const int64_t c = i * s.m + rho;
+      const int64_t sh = q.h + j1 - p.pad, sw = q.w + j2 - p.pad;
+      if (q.h < p.wo && q.w < p.wo && sh >= 0 && sh < s.w && sw >= 0 && sw < s.w && c < s.ci && oc < s.co)
+        v[((x + r) % p.n + p.n) % p.n] = K_at(oc, c);  // W'[x + r] = W[x]
+    }
+  }
+}
+
+// ------------------------------------------------------------------ device orchestration
+struct Ctx {
+  hy_ctx* c;
+  const hy_conv_plan* p;
+  const uint64_t* const* evks;
+  cudaStream_t s;
+  const uint64_t* key(int64_t r) const {
+    const int64_t rr = ((r % p->n) + p->n) % p->n;
+    auto it = std::lower_bound(p->rots.begin(), p->rots.end(), rr);
+    return (it != p->rots.end() && *it == rr) ? evks[it - p->rots.begin()] : nullptr;
+  }
+};
+
+hy_status ras_inplace(const Ctx& x, uint64_t* ct, uint32_t level, const std::vector<int64_t>& rs) {
+  for (int64_t r : rs) {
+    hy_status st = hy::hrot_plain(x.c, x.key(r), ct, level, (int32_t)r, ct, x.s, ct);
+    if (st != HY_OK) return st;
+  }
+  return HY_OK;
+}
+
+}  // namespace
+
+using namespace hy;
+
+extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spec, hy_conv_plan** out) {
+  if (!spec || !out || log_n < 4 || log_n > 17) return fail(HY_E_ARG, "null / log_n");
+  const hy_conv_spec& s = *spec;
+  if (s.f % 2 == 0 || s.f == 0 || (s.stride != 1 && s.stride != 2) || !s.ci || !s.co || !s.w)
+    return fail(HY_E_SHAPE, "conv spec: odd f, stride 1 or 2, nonzero sizes");
+  if (!pow2(s.wp) || !pow2(s.gap) || !pow2(s.m) || !pow2(s.d)) return fail(HY_E_FORMAT, "W_p, g, m, d must be powers of two");
+  if ((uint64_t)s.m * s.d % ((uint64_t)s.gap * s.gap)) return fail(HY_E_FORMAT, "m d must be a multiple of g^2");
+  if ((uint64_t)s.w * s.gap > s.wp) return fail(HY_E_CAPACITY, "image does not fit the physical width");
+  auto* p = new hy_conv_plan();
+  p->s = s;
+  p->n = (1ll << log_n) / 2;
+  p->pad = (s.f - 1) / 2;
+  p->wo = (s.w + s.stride - 1) / s.stride;
+  const int64_t e = (int64_t)s.m * s.d / ((int64_t)s.gap * s.gap);
+  if ((int64_t)s.wp * s.wp * e > p->n || p->n % ((int64_t)s.wp * s.wp * e)) {
+    delete p;
+    return fail(HY_E_CAPACITY, "channel block does not divide the slot count");
+  }
+  if (s.algo == HY_CONV_CA) {
+    p->in = Layout{true, p->n, s.wp, s.gap, s.m, s.d};
+    if (s.stride == 1) {
+      p->out = Layout{false, p->n, s.wp, s.gap, s.d, s.m};
+    } else {
+      if (s.m != s.gap) {
+        delete p;
+        return fail(HY_E_FORMAT, "stride-2 CAConv needs m == g (DESIGN R-DSCONV)");
+      }
+      p->out = Layout{false, p->n, s.wp, 2 * (int64_t)s.gap, 2 * (int64_t)s.d, 2 * (int64_t)s.m};
+    }
+    p->n_in = p->in.cts_for(s.ci);
+    p->n_groups = (s.co + s.d - 1) / s.d;
+    if (s.stride == 2) p->n_groups += p->n_groups % 2;
+    for (int k = 0; k < lg2(p->in.cn()); ++k) p->ras.push_back(p->in.B() << k);
+    for (int k = 0; k < lg2(s.m); ++k) p->ras_g.push_back(p->in.stride(k));
+    if (s.stride == 1) {
+      p->n_out = p->n_groups;
+      p->has_mask = s.m > 1;
+      if (p->has_mask)
+        for (int k = 0; k < lg2(s.m); ++k) p->ir_g.push_back(-p->in.stride(k));
+    } else {
+      const int lgg = lg2(s.gap);
+      p->n_out = p->n_groups / 2;
+      p->has_mask = true;
+      p->has_combine = true;
+      p->combine = -p->out.stride(2 * lgg + 1);
+      for (int k = 0; k <= lgg; ++k) p->ir_g.push_back(-p->out.stride(k));
+    }
+  } else {
+    if (s.stride != 1) {
+      delete p;
+      return fail(HY_E_FORMAT, "RAConv is stride 1 (downsampling happens in CAConv)");
+    }
+    p->in = Layout{false, p->n, s.wp, s.gap, s.m, s.d};
+    p->out = Layout{true, p->n, s.wp, s.gap, s.d, s.m};
+    p->n_in = p->in.cts_for(s.ci);
+    p->n_out = p->n_groups = p->out.cts_for(s.co);
+    for (int k = 0; k < lg2(p->out.d); ++k) p->ras_g.push_back(p->out.stride(lg2(p->out.m) + k));
+    p->has_mask = p->out.d > 1;
+    if (p->has_mask)
+      for (int64_t r : p->ras_g) p->ir_g.push_back(-r);
+  }
+  for (uint32_t j1 = 0; j1 < s.f; ++j1)
+    for (uint32_t j2 = 0; j2 < s.f; ++j2) p->taps.push_back(tap_amount(*p, j1, j2));
+  std::vector<int64_t> all = p->taps;
+  all.insert(all.end(), p->ras.begin(), p->ras.end());
+  all.insert(all.end(), p->ras_g.begin(), p->ras_g.end());
+  all.insert(all.end(), p->ir_g.begin(), p->ir_g.end());
+  if (p->has_combine) all.push_back(p->combine);
+  for (int64_t r : all) {
+    const int64_t rr = ((r % p->n) + p->n) % p->n;
+    if (rr) p->rots.push_back(rr);
+  }
+  std::sort(p->rots.begin(), p->rots.end());
+  p->rots.erase(std::unique(p->rots.begin(), p->rots.end()), p->rots.end());
+  int64_t nz_taps = 0;
+  for (int64_t r : p->taps) nz_taps += (r % p->n) != 0;
+  const bool ca = s.algo == HY_CONV_CA;
+  p->counts[0] = (uint32_t)(nz_taps * (ca ? p->n_in : p->n_out));
+  p->counts[1] = (uint32_t)(p->ras.size() * p->n_groups);
+  p->counts[2] = (uint32_t)(p->ras_g.size() * p->n_groups);
+  p->counts[3] = (uint32_t)(p->ir_g.size() * p->n_out + (p->has_combine ? p->n_out : 0));
+  p->counts[4] = (uint32_t)p->n_pt();
+  *out = p;
+  return HY_OK;
+}
+
+extern "C" void hy_conv_plan_destroy(hy_conv_plan* p) { delete p; }
+
+extern "C" hy_status hy_conv_plan_query(const hy_conv_plan* p, uint32_t* n_in, uint32_t* n_out, uint32_t* n_pt,
+                                        uint32_t* has_mask, uint32_t* n_rot, int32_t* rots, uint32_t* counts) {
+  if (!p) return fail(HY_E_ARG, "null plan");
+  if (n_in) *n_in = (uint32_t)p->n_in;
+  if (n_out) *n_out = (uint32_t)p->n_out;
+  if (n_pt) *n_pt = (uint32_t)p->n_pt();
+  if (has_mask) *has_mask = p->has_mask;
+  if (n_rot) *n_rot = (uint32_t)p->rots.size();
+  if (rots)
+    for (size_t i = 0; i < p->rots.size(); ++i) rots[i] = (int32_t)p->rots[i];
+  if (counts) memcpy(counts, p->counts, sizeof(p->counts));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_conv_weight_slots(const hy_conv_plan* p, const double* K, uint32_t idx, double* slots) {
+  if (!p || !K || !slots) return fail(HY_E_ARG, "null");
+  if ((int64_t)idx > p->n_pt() || ((int64_t)idx == p->n_pt() && !p->has_mask)) return fail(HY_E_ARG, "index");
+  weight_slots(*p, K, idx, slots);
+  return HY_OK;
+}
+
+extern "C" size_t hy_conv_weight_words(const hy_ctx* c, const hy_conv_plan* p, uint32_t level) {
+  if (!c || !p) return 0;
+  return ((size_t)p->n_pt() * (level + 1) + (p->has_mask ? level : 0)) * c->N;
+}
+
+extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, uint32_t level) {
+  if (!c || !p) return 0;
+  const size_t ct = 2ull * (level + 1) * c->N;
+  const size_t f2 = (size_t)p->s.f * p->s.f;
+  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 4) * ct;  // slid inputs + acc + 2 groups + tmp
+  return (f2 + 2) * ct;                                          // tap accumulators + tmp
+}
+
+extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, const double* K, uint32_t level,
+                                            uint64_t* d_pts, void* stream) {
+  if (!c || !p || !K || !d_pts) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
+  const int64_t npt = p->n_pt() + (p->has_mask ? 1 : 0);
+  std::vector<std::vector<int64_t>> coeffs(npt, std::vector<int64_t>(c->N));
+  hy_status err = HY_OK;
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t k = 0; k < npt; ++k) {
+    std::vector<double> v(p->n);
+    weight_slots(*p, K, k, v.data());
+    const bool mask = k == p->n_pt();
+    // weights at scale q_level, the mask at q_{level-1}: each rescale restores the ciphertext scale
+    const uint64_t scale = mask ? c->mod[level - 1] : c->mod[level];
+    hy_status st = hy_encode_coeffs(c->log_n, v.data(), (uint32_t)p->n, scale, coeffs[k].data());
+    if (st != HY_OK) {
+#pragma omp critical
+      err = st;
+    }
+  }
+  if (err != HY_OK) return fail(err, "weight encoding failed");
+  for (int64_t k = 0; k < npt; ++k) {
+    const bool mask = k == p->n_pt();
+    uint64_t* dst = d_pts + (size_t)k * (level + 1) * c->N;
+    hy_status st = hy_pt_from_coeffs(c, coeffs[k].data(), mask ? level - 1 : level, dst, stream);
+    if (st != HY_OK) return st;
+  }
+  return cuda_check("hy_conv_encode_weights");
+}
+
+namespace {
+
+hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
+                   uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
+                   uint64_t* const* out, void* stream) {
+  if (!c || !p || !evks || !in || !pts || !scratch || !out) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
+  if (ob > oe || oe > p->n_out) return fail(HY_E_PLAN, "output range outside the plan");
+  for (int64_t i = 0; i < p->n_in; ++i)
+    if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
+  Ctx x{c, p, evks, st(stream)};
+  const size_t N = c->N, f2 = (size_t)p->s.f * p->s.f;
+  const size_t ct_l = 2 * (level + 1) * N;
+  const uint64_t* wpt = pts;                                       // [n_pt][level+1][N]
+  const uint64_t* mask = pts + (size_t)p->n_pt() * (level + 1) * N;  // [level][N]
+  auto W = [&](int64_t grp, int64_t i, int64_t t) { return wpt + (size_t)((grp * p->n_in + i) * f2 + t) * (level + 1) * N; };
+  std::vector<const uint64_t*> cts, ps;
+  hy_status stt;
+  if (p->s.algo == HY_CONV_CA) {
+    // Slide_f: hoisted rotations of every input
+    std::vector<std::vector<const uint64_t*>> slid(p->n_in, std::vector<const uint64_t*>(f2));
+    uint64_t* sbuf = scratch;
+    for (int64_t i = 0; i < p->n_in; ++i) {
+      std::vector<int32_t> rs;
+      std::vector<const uint64_t*> ks;
+      std::vector<uint64_t*> outs;
+      for (size_t t = 0; t < f2; ++t) {
+        if (p->taps[t] % p->n == 0) {
+          slid[i][t] = in[i];
+          continue;
+        }
+        uint64_t* o = sbuf + ((size_t)i * f2 + t) * ct_l;
+        slid[i][t] = o;
+        rs.push_back((int32_t)p->taps[t]);
+        ks.push_back(x.key(p->taps[t]));
+        outs.push_back(o);
+      }
+      if (!rs.empty()) {
+        stt = hy_hrot_hoisted(c, ks.data(), in[i], level, rs.data(), (uint32_t)rs.size(), outs.data(), stream);
+        if (stt != HY_OK) return stt;
+      }
+    }
+    uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;
+    uint64_t* ga = acc + ct_l;
+    uint64_t* gb = ga + ct_l;
+    auto siso_group = [&](int64_t grp, uint64_t* dst) -> hy_status {  // MulFilter&Sum_f, rescale, RaS, RaS_g
+      cts.clear();
+      ps.clear();
+      for (int64_t i = 0; i < p->n_in; ++i)
+        for (size_t t = 0; t < f2; ++t) {
+          cts.push_back(slid[i][t]);
+          ps.push_back(W(grp, i, t));
+        }
+      hy_status s1 = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, acc, 0, stream);
+      if (s1 == HY_OK) s1 = hy_rescale(c, acc, level, dst, stream);
+      if (s1 == HY_OK) s1 = ras_inplace(x, dst, level - 1, p->ras);
+      if (s1 == HY_OK) s1 = ras_inplace(x, dst, level - 1, p->ras_g);
+      return s1;
+    };
+    for (uint32_t j = ob; j < oe; ++j) {
+      if (p->s.stride == 1) {
+        if (!p->has_mask) {
+          stt = siso_group(j, out[j - ob]);
+          if (stt != HY_OK) return stt;
+          continue;
+        }
+        stt = siso_group(j, ga);
+        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
+        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, out[j - ob], stream);
+        if (stt == HY_OK) stt = ras_inplace(x, out[j - ob], level - 2, p->ir_g);
+        if (stt != HY_OK) return stt;
+      } else {  // dsconv: two SISO groups merged into the doubled gap (DESIGN R-DSCONV)
+        const size_t ct_m = 2 * (size_t)level * N;
+        uint64_t* a = gb;
+        uint64_t* bb = gb + ct_m;
+        stt = siso_group(2 * j, ga);
+        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
+        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, a, stream);
+        if (stt == HY_OK) stt = siso_group(2 * j + 1, ga);
+        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
+        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, bb, stream);
+        if (stt == HY_OK) stt = hrot_plain(c, x.key(p->combine), bb, level - 2, (int32_t)p->combine, out[j - ob], x.s, a);
+        if (stt == HY_OK) stt = ras_inplace(x, out[j - ob], level - 2, p->ir_g);
+        if (stt != HY_OK) return stt;
+      }
+    }
+    return cuda_check("hy_caconv");
+  }
+  // RAConv_Reorder: MulFilter&Sum_{c_i} into f^2 accumulators, one lazy Slide_1&Sum_f, rescale, RaS_g, IR_g
+  uint64_t* accs = scratch;
+  uint64_t* tmp = scratch + f2 * ct_l;
+  std::vector<const uint64_t*> acc_ptrs(f2), keys(f2);
+  std::vector<int32_t> rs(f2);
+  for (size_t t = 0; t < f2; ++t) {
+    acc_ptrs[t] = accs + t * ct_l;
+    rs[t] = (int32_t)p->taps[t];
+    keys[t] = (p->taps[t] % p->n) ? x.key(p->taps[t]) : nullptr;
+  }
+  for (uint32_t o = ob; o < oe; ++o) {
+    for (size_t t = 0; t < f2; ++t) {
+      cts.clear();
+      ps.clear();
+      for (int64_t i = 0; i < p->n_in; ++i) {
+        cts.push_back(in[i]);
+        ps.push_back(W(o, i, t));
+      }
+      stt = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, accs + t * ct_l, 0, stream);
+      if (stt != HY_OK) return stt;
+    }
+    stt = hy_hrot_sum(c, keys.data(), acc_ptrs.data(), level, rs.data(), (uint32_t)f2, tmp, stream);
+    uint64_t* dst = p->has_mask ? accs : out[o - ob];
+    if (stt == HY_OK) stt = hy_rescale(c, tmp, level, dst, stream);
+    if (stt == HY_OK) stt = ras_inplace(x, dst, level - 1, p->ras_g);
+    if (stt == HY_OK && p->has_mask) {
+      stt = hy_pmult(c, dst, mask, level - 1, tmp, stream);
+      if (stt == HY_OK) stt = hy_rescale(c, tmp, level - 1, out[o - ob], stream);
+      if (stt == HY_OK) stt = ras_inplace(x, out[o - ob], level - 2, p->ir_g);
+    }
+    if (stt != HY_OK) return stt;
+  }
+  return cuda_check("hy_raconv");
+}
+
+}  // namespace
+
+extern "C" hy_status hy_caconv(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
+                               const uint64_t* const* in, uint32_t level, const uint64_t* pts, uint64_t* scratch,
+                               uint32_t out_begin, uint32_t out_end, uint64_t* const* out, void* stream) {
+  if (p && p->s.algo != HY_CONV_CA) return fail(HY_E_PLAN, "plan is not a CAConv plan");
+  return conv_run(c, p, evks, in, level, pts, scratch, out_begin, out_end, out, stream);
+}
+
+extern "C" hy_status hy_raconv(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
+                               const uint64_t* const* in, uint32_t level, const uint64_t* pts, uint64_t* scratch,
+                               uint32_t out_begin, uint32_t out_end, uint64_t* const* out, void* stream) {
+  if (p && p->s.algo != HY_CONV_RA) return fail(HY_E_PLAN, "plan is not an RAConv plan");
+  return conv_run(c, p, evks, in, level, pts, scratch, out_begin, out_end, out, stream);
+}

@@ -114,6 +114,9 @@ void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* ch
                 cudaStream_t s);
 
 // elementwise / keyswitch launchers (hy_ops.cu / hy_keyswitch.cu)
+// out = HRot_r(ct) (+ addct); out may alias ct and addct (hy_keyswitch.cu)
+hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
+                     cudaStream_t s, const uint64_t* addct);
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
 
 // Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).

@@ -184,12 +184,13 @@ __global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restric
     default: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
   }
 
-// out[c][i] = (u[c][i] - w[c][i]) P^{-1} (+ add0[i][perm(x)] for c = 0) (+ add1[i][x] for c = 1).
+// out[c][i] = (u[c][i] - w[c][i]) P^{-1} (+ add0[i][perm(x)] for c = 0) (+ add1[i][x] for c = 1)
+//             (+ addct[c][i][x] for both polys).  out may alias addct (read before write, same x).
 // grid (N/256, l+1, npoly)
 __global__ void k_moddown_final(const uint64_t* __restrict__ u, int E, const uint64_t* __restrict__ w,
-                                const ModDownConst* md, DevTables dt, int level, uint64_t* __restrict__ out,
+                                const ModDownConst* md, DevTables dt, int level, uint64_t* out,
                                 const uint64_t* __restrict__ add0, uint64_t k0, const uint64_t* __restrict__ add1,
-                                int logN) {
+                                const uint64_t* addct, int logN) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y, c = blockIdx.z;
@@ -201,7 +202,9 @@ __global__ void k_moddown_final(const uint64_t* __restrict__ u, int E, const uin
     val = add_mod(val, add0[(size_t)i * N + xs], q);
   }
   if (c == 1 && add1) val = add_mod(val, add1[(size_t)i * N + x], q);
-  out[((size_t)c * (level + 1) + i) * N + x] = val;
+  const size_t o = ((size_t)c * (level + 1) + i) * N + x;
+  if (addct) val = add_mod(val, addct[o], q);
+  out[o] = val;
 }
 
 // ---------------------------------------------------------------- host-side building blocks
@@ -278,7 +281,8 @@ void ip(hy_ctx* c, uint32_t level, const IPArgs& a, const uint64_t* evk, uint64_
 
 // u [npoly][E][N] (NTT) -> out [npoly][l+1][N]
 void moddown_core(hy_ctx* c, uint32_t level, int npoly, const uint64_t* u, uint64_t* out, const uint64_t* add0,
-                  uint64_t k0, const uint64_t* add1, uint64_t* v, uint64_t* w, cudaStream_t s) {
+                  uint64_t k0, const uint64_t* add1, uint64_t* v, uint64_t* w, cudaStream_t s,
+                  const uint64_t* addct = nullptr) {
   const int n = level + 1, E = n + c->n_p, K = c->n_p;
   LimbBatch b;
   b.n = 0;
@@ -309,8 +313,9 @@ void moddown_core(hy_ctx* c, uint32_t level, int npoly, const uint64_t* u, uint6
   launch_ntt(c, b, false, s);
   dim3 g2(c->N / kT, n, npoly);
   KTimer kt(c, FAM_MODDOWN, s);
-  kt.bytes = ((uint64_t)npoly * n * 3 + (add0 ? n : 0) + (add1 ? n : 0)) * c->N * 8;
-  k_moddown_final<<<g2, kT, 0, s>>>(u, E, w, c->d_moddown[level], c->dt, level, out, add0, k0, add1, c->log_n);
+  kt.bytes = ((uint64_t)npoly * n * (addct ? 4 : 3) + (add0 ? n : 0) + (add1 ? n : 0)) * c->N * 8;
+  k_moddown_final<<<g2, kT, 0, s>>>(u, E, w, c->d_moddown[level], c->dt, level, out, add0, k0, add1, addct,
+                                    c->log_n);
 }
 
 void intt_poly(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t level, cudaStream_t s) {
@@ -330,12 +335,21 @@ hy_status check_level(hy_ctx* c, uint32_t level) {
   return HY_OK;
 }
 
+}  // namespace
+
+// out = HRot_r(ct) (+ addct).  out may alias addct (and ct, since ct is consumed into the
+// workspace before the final write).
 hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
-                     cudaStream_t s) {
+                     cudaStream_t s, const uint64_t* addct) {
   const uint64_t k = hy_galois_elt(c, r);
   const size_t n = level + 1, N = c->N;
   if (k == 1) {
-    if (out != ct) cudaMemcpyAsync(out, ct, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+    if (addct) {  // out = ct + addct
+      if (out != addct) cudaMemcpyAsync(out, addct, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+      automorph(c, ct, out, 2 * n, n, 1, true, s);
+    } else if (out != ct) {
+      cudaMemcpyAsync(out, ct, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+    }
     return HY_OK;
   }
   if (!evk) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
@@ -347,10 +361,11 @@ hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_
   modup_core(c, level, b.d, b.ext, s);
   IPArgs a = ip_args(c, level, b.ext, b.rc + n * N);
   ip(c, level, a, evk, b.u, 1, false, s);
-  moddown_core(c, level, 2, b.u, out, b.rc, 1, nullptr, b.v, b.w, s);
+  moddown_core(c, level, 2, b.u, out, b.rc, 1, nullptr, b.v, b.w, s, addct);
   return HY_OK;
 }
 
+namespace {
 }  // namespace
 
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s) {
@@ -420,7 +435,7 @@ extern "C" hy_status hy_hrot(hy_ctx* c, const uint64_t* evk, const uint64_t* ct,
   if (s0 != HY_OK) return s0;
   if (!ct || !out) return fail(HY_E_ARG, "null");
   if (ct == out) return fail(HY_E_ARG, "hrot cannot run in place");
-  s0 = hrot_plain(c, evk, ct, level, r, out, st(stream));
+  s0 = hrot_plain(c, evk, ct, level, r, out, st(stream), nullptr);
   if (s0 != HY_OK) return s0;
   return cuda_check("hy_hrot");
 }
@@ -432,7 +447,7 @@ extern "C" hy_status hy_hrot_batch(hy_ctx* c, const uint64_t* const* evks, const
   if (!evks || !cts || !r || !outs) return fail(HY_E_ARG, "null");
   for (uint32_t i = 0; i < n; ++i) {
     if (cts[i] == outs[i]) return fail(HY_E_ARG, "hrot cannot run in place");
-    s0 = hrot_plain(c, evks[i], cts[i], level, r[i], outs[i], st(stream));
+    s0 = hrot_plain(c, evks[i], cts[i], level, r[i], outs[i], st(stream), nullptr);
     if (s0 != HY_OK) return s0;
   }
   return cuda_check("hy_hrot_batch");

@@ -1,0 +1,92 @@
+"""GPU parity of the HyPHEN conv layers (hy_caconv / hy_raconv through the C ABI)
+against the oracle's encrypted execution of its own plan: bit-exact on every RNS
+limb.  Toy layers (N = 2^12) run in full; ResNet-20 layers at Set_hyp (N = 2^16)
+are checked on sampled output ciphertexts at the conv levels (l+1 = 10 / 7)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import hyphen as H
+from test_hyphen_plan import R20
+
+pytestmark = pytest.mark.gpu
+SK, EK = synth.SEED_SK, synth.SEED_EVK
+
+
+def to_np(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def ctx_toy():
+    import paper_2302_02407_b200 as hy
+    return hy.Context(**synth.PARAMS["toy"])
+
+
+@pytest.fixture(scope="module")
+def ctx_hyp():
+    import paper_2302_02407_b200 as hy
+    return hy.Context(**synth.PARAMS["hyp"])
+
+
+def gpu_layer(ctx, spec, X, K, level, scale, out_begin=0, out_end=None):
+    import paper_2302_02407_b200 as hy
+    p = hy.ConvPlan(ctx, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo)
+    fin = H.Fmt("CA" if spec.algo == "CA" else "RA", spec.n, spec.wp, spec.g, spec.m, spec.d)
+    cts = [ctx.encrypt(SK, 900, i, ctx.encode(v, scale, level), level) for i, v in enumerate(H.pack(X, fin))]
+    evks = {r: ctx.keygen_rot(SK, EK, r) for r in p.rots}
+    pts = p.encode_weights(K, level)
+    outs = p.run(evks, cts, level, pts, out_begin=out_begin, out_end=out_end)
+    return p, outs
+
+
+def oracle_layer(o, spec, X, K, level, scale, outputs=None):
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    cts = [o.encrypt(SK, 900, i, o.encode(v, scale, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+    wanted = range(plan.n_out) if outputs is None else outputs
+    need = set()
+    for r in H.rotation_amounts(plan, o.n):
+        need.add(r)
+    evks = {r: o.keygen_rot(SK, EK, r) for r in need}
+    return plan, H.EncConv(o, plan, evks).run(cts, list(wanted))
+
+
+TOY = [
+    H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048),
+    H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "CA", n=2048),
+    H.ConvSpec(8, 8, 8, 3, 1, 8, 1, 1, 2, "CA", n=2048),
+    H.ConvSpec(8, 8, 8, 3, 1, 8, 1, 2, 1, "RA", n=2048),
+    H.ConvSpec(8, 8, 4, 3, 1, 8, 2, 2, 4, "CA", n=2048),
+    H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048),
+    H.ConvSpec(4, 8, 8, 1, 2, 8, 1, 1, 2, "CA", n=2048),
+]
+
+
+@pytest.mark.parametrize("spec", TOY, ids=["C1_raconv", "ca11", "ca12", "ra21", "ca_g2", "dsconv", "pconv"])
+def test_toy_layers_bit_exact(ctx_toy, orc_toy, spec):
+    level = orc_toy.nq - 1
+    X = synth.image(11, spec.ci, spec.w)
+    K = synth.conv_weight(12, spec.co, spec.ci, spec.f)
+    p, outs = gpu_layer(ctx_toy, spec, X, K, level, 2 ** 40)
+    plan, ref = oracle_layer(orc_toy, spec, X, K, level, 2 ** 40)
+    assert len(outs) == len(ref) == plan.n_out
+    for a, b in zip(outs, ref):
+        assert np.array_equal(to_np(a), b.data)
+    # and the decryption is the plaintext convolution (2^-10, north star)
+    dec = [np.real(orc_toy.decode(orc_toy.decrypt(SK, oracle.Ct(to_np(a), b.level, b.scale)))) for a, b in zip(outs, ref)]
+    got = H.unpack(dec, plan.fout, spec.co, spec.wo, spec.wo)
+    want = H.conv2d(X, K, spec.s)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10
+
+
+@pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1])])
+def test_resnet20_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
+    spec = R20[name]
+    level = 9 if spec.algo == "CA" else 6      # l+1 = 10 for CAConv, 7 for RAConv (DESIGN R-LEVELS)
+    X = synth.image(21, spec.ci, spec.w)
+    K = synth.conv_weight(22, spec.co, spec.ci, spec.f)
+    j = outputs[0]
+    p, outs = gpu_layer(ctx_hyp, spec, X, K, level, 2 ** 42, j, j + 1)
+    plan, ref = oracle_layer(orc_hyp, spec, X, K, level, 2 ** 42, outputs)
+    assert np.array_equal(to_np(outs[0]), ref[0].data)

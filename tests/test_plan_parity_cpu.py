@@ -1,0 +1,41 @@
+"""The product's host-side conv plans (C++) against the oracle's (numpy), CPU only:
+identical rotation amounts, counts and bit-identical weight / mask slot vectors."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import hyphen as H
+from test_hyphen_plan import R20
+
+
+@pytest.fixture(scope="module")
+def hy():
+    from paper_2302_02407_b200 import build
+    build.build()
+    import paper_2302_02407_b200 as hy
+    return hy
+
+
+CASES = dict(R20)
+CASES["C1_raconv"] = H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048)
+CASES["toy_dsconv"] = H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048)
+CASES["r18_L4_ra"] = H.ConvSpec(512, 512, 7, 3, 1, 64, 8, 8, 8, "RA")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_plan_matches_oracle(hy, name):
+    s = CASES[name]
+    K = synth.conv_weight(7, s.co, s.ci, s.f)
+    log_n = (2 * s.n).bit_length() - 1
+    p = hy.ConvPlan(None, s.ci, s.co, s.w, s.f, s.s, s.wp, s.g, s.m, s.d, s.algo, log_n=log_n)
+    big = s.ci * s.co > 64 * 64
+    o = (H.plan_caconv if s.algo == "CA" else H.plan_raconv)(s, K, with_weights=not big)
+    assert (p.n_in, p.n_out) == (o.n_in, o.n_out)
+    assert p.rots == H.rotation_amounts(o, s.n)
+    assert p.counts == o.counts
+    assert p.has_mask == (o.mask is not None)
+    keys = sorted(o.weights) if not big else []
+    for idx, key in enumerate(keys):
+        assert np.array_equal(p.weight_slots(K, idx), o.weights[key]), (name, key)
+    if o.mask is not None:
+        assert np.array_equal(p.weight_slots(K, p.n_pt), o.mask)
