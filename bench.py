@@ -180,6 +180,75 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- ResNet-20 conv layers
+# (name, (ci, co, w, f, stride, wp, gap, m, d, algo), multiplicity in ResNet-20): tb:resnet 20 parameter
+# (P:1045-1050), Optimal (m, d) plan (1,2)/(2,4)/(4,8), DESIGN R-LAYOUT / R-DSCONV.
+R20_LAYERS = [
+    ("stem", (3, 16, 32, 3, 1, 32, 1, 1, 2, "CA"), 1),
+    ("L1_ca", (16, 16, 32, 3, 1, 32, 1, 1, 2, "CA"), 3),
+    ("L1_ra", (16, 16, 32, 3, 1, 32, 1, 2, 1, "RA"), 3),
+    ("L2_ds", (16, 32, 32, 3, 2, 32, 1, 1, 2, "CA"), 1),
+    ("L2_pconv", (16, 32, 32, 1, 2, 32, 1, 1, 2, "CA"), 1),
+    ("L2_ca", (32, 32, 16, 3, 1, 32, 2, 2, 4, "CA"), 2),
+    ("L2_ra", (32, 32, 16, 3, 1, 32, 2, 4, 2, "RA"), 3),
+    ("L3_ds", (32, 64, 16, 3, 2, 32, 2, 2, 4, "CA"), 1),
+    ("L3_pconv", (32, 64, 16, 1, 2, 32, 2, 2, 4, "CA"), 1),
+    ("L3_ca", (64, 64, 8, 3, 1, 32, 4, 4, 8, "CA"), 2),
+    ("L3_ra", (64, 64, 8, 3, 1, 32, 4, 8, 4, "RA"), 3),
+]
+CA_LEVEL, RA_LEVEL = 9, 6  # l+1 = 10 / 7 limbs (DESIGN R-LEVELS)
+
+
+def bench_conv(ctx, ws, rank, steps, warmup, timed):
+    """Per-layer device time of every ResNet-20 conv layer type (fresh encryption at its scheduled
+    level, outputs sharded over ranks + all-gathered), and the network's conv total."""
+    import torch
+
+    import paper_2302_02407_b200 as hy
+    from paper_2302_02407_b200.dist import all_gather_cts, shard
+
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    keys = {}
+    layers = {}
+    total = 0.0
+    for li, (name, spec, mult) in enumerate(R20_LAYERS):
+        ci, co, w, f, s, wp, g, m, d, algo = spec
+        p = hy.ConvPlan(ctx, ci, co, w, f, s, wp, g, m, d, algo)
+        level = CA_LEVEL if algo == "CA" else RA_LEVEL
+        for r in p.rots:
+            if r not in keys:
+                keys[r] = ctx.keygen_rot(sk, ek, r)
+        K = synth.conv_weight(2000 + li, co, ci, f)
+        pts = p.encode_weights(K, level)
+        scale = 2 ** synth.PARAMS["hyp"]["log_scale"]
+        cts = [ctx.encrypt(sk, synth.SEED_ENC, 10_000 + 100 * li + i,
+                           ctx.encode(synth.slots_uniform(3000 + 100 * li + i, ctx.n), scale, level), level)
+               for i in range(p.n_in)]
+        b, e = shard(p.n_out, rank, ws)
+        lo = p.out_level(level)
+        outs = [ctx.empty(*ctx.ct_shape(lo)) for _ in range(e - b)]
+        scratch = p.scratch(level)
+        like = ctx.empty(*ctx.ct_shape(lo))
+        evks = [keys[r] for r in p.rots]
+
+        def step():
+            if e > b:
+                p.run(evks, cts, level, pts, scratch, b, e, outs)
+            if ws > 1:
+                all_gather_cts(outs, p.n_out, like)
+
+        ms, launches = timed(step, steps, warmup)
+        layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
+                        "rotations": p.counts, "gpu_launches": launches}
+        total += mult * ms
+        del pts, cts, outs, scratch
+        torch.cuda.empty_cache()
+    return {"layers": layers, "total_ms": total, "n_gpus": ws,
+            "note": "sum over the 19 3x3 convs + 2 pconv of per-layer device time (max over ranks), each layer on a "
+                    "fresh encryption at its scheduled level; bootstrapping/activation excluded (P:1095-1101 conv "
+                    "columns: 0.52 s on A100, context only)"}
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, ws, rank, local):
     import torch
@@ -252,14 +321,30 @@ def run_ours(args, ws, rank, local):
                                "alg_bytes_per_launch": by // n, "avg_us": 1000.0 * t / n}
     ctx.time_kernels(0)
     dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
-    d = breakdown[dominant]
     pk = peaks()
-    achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
-    roof = {"bound": "hbm", "kernel_family": dominant, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"], "traffic": None,
-            "share_of_step": d["ms_per_step"] / ms,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
-    # ALU view of the NTT (the step's integer-bound work): butterflies/s vs measured Shoup rate
+
+    def hbm_roof(fam_name):
+        d = breakdown[fam_name]
+        achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
+        return {"bound": "hbm", "kernel_family": fam_name, "achieved": achieved, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "share_of_step": d["ms_per_step"] / ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
+
+    def alu_roof(fam_name):
+        # NTT pass: 8 stages x N/2 butterflies x 8 FP64-pipe ops (fmulmod 6 + add + sub) per limb (DESIGN 5)
+        d = breakdown[fam_name]
+        limbs = d["alg_bytes_per_launch"] / (2 * N * 8)
+        ops = limbs * 8 * (N // 2) * 8
+        achieved = ops / (d["avg_us"] * 1e-6) / 1e12
+        peak = 148 * 64 * 1.965e9 / 1e12  # FP64 lanes x SMs x max clock (guide unit counts); measured 18.2
+        return {"bound": "alu", "kernel_family": fam_name, "achieved": achieved, "peak": peak,
+                "unit": "TFP64op/s", "frac": achieved / peak, "traffic": None,
+                "share_of_step": d["ms_per_step"] / ms,
+                "peak_source": "148 SM x 64 FP64 lanes x 1.965 GHz (DESIGN.md section 5); one DFMA/DMUL/DADD = 1 op"}
+
+    roof = alu_roof(dominant) if dominant.startswith("ntt") else hbm_roof(dominant)
+    roof_ip = hbm_roof("ip") if "ip" in breakdown else None
     ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
 
     # e2e through the public API with host buffers: pinned H2D of the 64 input cts, D2H of the outputs
@@ -285,6 +370,12 @@ def run_ours(args, ws, rank, local):
                "note": "H2D of the 64 input ciphertexts from pinned memory, hrot_batch, D2H of the 64 outputs; "
                        "evaluation keys are server state, resident before timing (P:1030)"}
 
+    conv = None
+    if not args.no_conv:
+        del evks, cts, outs, houts
+        torch.cuda.empty_cache()
+        conv = bench_conv(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, dt = oracle_keyswitch_rate(args.cpu_rotations)
@@ -301,6 +392,8 @@ def run_ours(args, ws, rank, local):
                        "global_batch": BATCH * ws, "level": LEVEL, "parallelism": f"independent batches x{ws}",
                        "l2": "inputs larger than L2 (64 x 168 MiB evaluation keys streamed per step)"},
             "roofline": roof,
+            "roofline_ip": roof_ip,
+            "resnet20_conv": conv,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -322,6 +415,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rotations", type=int, default=2)
+    ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 conv-layer timings")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
