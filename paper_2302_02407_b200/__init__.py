@@ -136,7 +136,7 @@ def encode_coeffs(log_n: int, slots, scale: int) -> np.ndarray:
 class Context:
     """One RNS-CKKS context on one CUDA device (see include/hyphen.h)."""
 
-    def __init__(self, log_n, q_bits, p_bits, dnum, h=192, device=0, max_level=None, **_):
+    def __init__(self, log_n, q_bits, p_bits, dnum, h=192, device=0, max_level=None, max_batch=16, **_):
         import torch
 
         self.torch = torch
@@ -155,9 +155,8 @@ class Context:
         self.q, self.p = self.moduli[: self.n_q], self.moduli[self.n_q:]
         self.alpha = int(lib().hy_ctx_alpha(self._c))
         self.max_level = self.n_q - 1 if max_level is None else max_level
-        nbytes = int(lib().hy_workspace_bytes(self._c, self.max_level, 1))
-        # key generation needs 3 (n_q+n_p) limbs; make sure the workspace covers it
-        nbytes = max(nbytes, (3 * (self.n_q + self.n_p) + 2) * self.N * 8 + (1 << 16))
+        # workspace for up to `max_batch` key switches per batched launch (library cap: 16)
+        nbytes = int(lib().hy_workspace_bytes(self._c, self.max_level, max_batch))
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device=self.device)
         _check(lib().hy_ctx_set_workspace(self._c, self.ws.data_ptr(), self.ws.numel() * 8))
 

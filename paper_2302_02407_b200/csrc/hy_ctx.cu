@@ -6,6 +6,7 @@
 //             unused prime below 2^bits with p == 1 (mod 2N).
 //   R-NTT     psi = smallest primitive 2N-th root of unity mod p; forward NTT
 //             output index k holds a(psi^(2 br(k) + 1)).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -295,11 +296,13 @@ extern "C" uint64_t hy_galois_elt(const hy_ctx* c, int64_t r) {
 extern "C" size_t hy_workspace_bytes(const hy_ctx* c, uint32_t max_level, uint32_t max_terms) {
   if (!c) return 0;
   if (max_level >= c->n_q) max_level = c->n_q - 1;
-  (void)max_terms;
-  size_t n = max_level + 1, E = n + c->n_p, beta = hy::n_digits(c, max_level);
-  // rot ct (2n) + d (n) + ext (beta*E) + u (2E) + u_acc (2E) + v (2K) + w (2n) + misc (4n)
-  size_t limbs = 2 * n + n + beta * E + 2 * E + 2 * E + 2 * c->n_p + 2 * n + 4 * n + 8;
-  return limbs * (size_t)c->N * 8 + 64 * 256;
+  // max_terms key switches per batched launch (capped at 16), plus one accumulator ciphertext;
+  // at least enough for key generation (3 (n_q + n_p) limbs + small buffers)
+  const size_t items = std::max<uint32_t>(1, std::min<uint32_t>(max_terms, 16));
+  const size_t n = max_level + 1;
+  const size_t ks = items * hy::ks_item_bytes(c, max_level) + 2 * n * (size_t)c->N * 8 + 4096;
+  const size_t keygen = (3 * (size_t)(c->n_q + c->n_p) + 2) * c->N * 8 + 65536;
+  return std::max(ks, keygen);
 }
 
 extern "C" hy_status hy_ctx_set_workspace(hy_ctx* c, void* d_ws, size_t bytes) {

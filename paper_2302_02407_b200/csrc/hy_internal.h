@@ -117,6 +117,12 @@ void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* ch
 // out = HRot_r(ct) (+ addct); out may alias ct and addct (hy_keyswitch.cu)
 hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
                      cudaStream_t s, const uint64_t* addct);
+// batched plain HRot: out_g = HRot_{r_g}(ct_g) (+ addct_g); identical evk pointers share one key stream
+hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* const* ct, uint32_t level,
+                     const int32_t* r, uint32_t n_items, uint64_t* const* out, const uint64_t* const* addct,
+                     cudaStream_t s);
+// workspace bytes of one batched key-switch item at `level`
+size_t ks_item_bytes(const hy_ctx* c, uint32_t level);
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
 
 // Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).

@@ -6,9 +6,16 @@
 //   hoisted : d = iNTT(c_1) once; ModUp once; per r the IP reads the extended
 //             digits through the NTT-domain permutation of kappa_k (Halevi-Shoup)
 //   lazy sum: per term plain ModUp + IP accumulated over Q_l u P; ONE ModDown.
+//
+// Batched engine: every stage runs on up to kG key switches per launch (items g),
+// so a batch of rotations costs one launch per stage instead of one per rotation,
+// and items that share an evaluation key (RaS of all output groups of a conv
+// layer) stream that key from HBM once for the whole batch.
+//
 // Data layout (HBM): ct [2][l+1][N], ext [beta][l+1+K][N], u [2][l+1+K][N], evk
 // [dnum][2][n_q+n_p][N]; every limb is N contiguous uint64 (coalesced rows).
 #include <algorithm>
+#include <vector>
 
 #include "hy_arith.cuh"
 
@@ -25,23 +32,41 @@ __device__ __forceinline__ uint32_t aut_index(uint32_t p, uint64_t k, int logN) 
 namespace {
 
 constexpr int kT = 256;
+constexpr int kG = 16;  // key switches per batched launch
 
-// IP operands: digit j's limb u is own[u] (the NTT-domain c1 the digits were
-// cut from) when u belongs to digit j, else ext[j][u].
-struct IPArgs {
-  const uint64_t* ext;
-  const uint64_t* own;  // may be null: then every limb comes from ext
+template <class T>
+struct Arr {
+  T p[kG];
 };
 
-// out[l][p] (+)= in[l][perm_k(p)]; limb l uses prime chain (l % limbs_per_poly).
-__global__ void k_automorph(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t k, int logN,
-                            int limbs_per_poly, int accumulate, DevTables dt) {
+// ---------------------------------------------------------------- automorphism
+// item g: out_g[l][x] (+)= in_g[l][perm_{k_g}(x)]; limb l on prime l % per_poly.  grid (N/256, limbs, G)
+// (Arr parameters are __grid_constant__: indexed by blockIdx / loop counters straight out of the
+// parameter bank instead of being copied to a per-thread local-memory frame.)
+__global__ void k_automorph(const __grid_constant__ Arr<const uint64_t*> in, const __grid_constant__ Arr<uint64_t*> out,
+                            const __grid_constant__ Arr<uint64_t> k, int logN, int per_poly,
+                            int accumulate, DevTables dt) {
   const size_t N = (size_t)1 << logN;
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.z;
   const size_t off = (size_t)blockIdx.y * N;
-  uint64_t v = in[off + aut_index(p, k, logN)];
-  if (accumulate) v = add_mod(v, out[off + p], dt.pc[blockIdx.y % limbs_per_poly].q);
-  out[off + p] = v;
+  uint64_t v = in.p[g][off + aut_index(x, k.p[g], logN)];
+  if (accumulate) v = add_mod(v, out.p[g][off + x], dt.pc[blockIdx.y % per_poly].q);
+  out.p[g][off + x] = v;
+}
+
+// out[l][x] (+)= sum_g in_g[l][perm_{k_g}(x)] (race-free reduction of G permuted polynomials).
+// grid (N/256, limbs)
+__global__ void k_automorph_sum(const __grid_constant__ Arr<const uint64_t*> in,
+                                const __grid_constant__ Arr<uint64_t> k, int G, uint64_t* __restrict__ out,
+                                int logN, int per_poly, DevTables dt) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t off = (size_t)blockIdx.y * N;
+  const uint64_t q = dt.pc[blockIdx.y % per_poly].q;
+  uint64_t v = out[off + x];
+  for (int g = 0; g < G; ++g) v = add_mod(v, in.p[g][off + aut_index(x, k.p[g], logN)], q);
+  out[off + x] = v;
 }
 
 // FP64 constants of one prime, staged in shared memory.
@@ -49,13 +74,15 @@ struct FConst {
   double q, qinv;
 };
 
-// ModUp basis conversion for digit j = blockIdx.y; one thread per coefficient x
-// produces every non-own limb of the digit.  grid (N/256, beta).
+// ---------------------------------------------------------------- ModUp basis conversion
+// Item g = blockIdx.z, digit j = blockIdx.y; one thread per coefficient x produces every
+// non-own limb of the digit.  grid (N/256, beta, G).
 // y_i = [d_i (D_j/q_i)^{-1}]_{q_i} in [0, q_i);  ext[j][u][x] = [sum_i y_i ((D_j/q_i) mod t_u)]_{t_u}.
 // Every product is reduced on the FP64 pipe (fmulmod, |term| <= 1.5 t), the A terms are summed
 // exactly and canonicalised once.  A = alpha (compile time); a partial last digit pads with 0.
 template <int A>
-__global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict__ d, uint64_t* __restrict__ ext,
+__global__ void __launch_bounds__(256) k_modup_bconv(const __grid_constant__ Arr<const uint64_t*> dd,
+                                                     const __grid_constant__ Arr<uint64_t*> ee,
                                                      const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
                                                      int logN) {
   __shared__ double s_hat[kMaxExt][A];
@@ -63,6 +90,8 @@ __global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict_
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
+  const uint64_t* d = dd.p[blockIdx.z];
+  uint64_t* ext = ee.p[blockIdx.z];
   const ModUpConst& m = mc[j];
   const int nsrc = m.hi - m.lo;
   for (int i = threadIdx.x; i < E * A; i += blockDim.x) {
@@ -96,54 +125,102 @@ __global__ void __launch_bounds__(256) k_modup_bconv(const uint64_t* __restrict_
   }
 }
 
-// Key-switch inner product, B = beta digits (compile time).  grid (N/256, E).
-// u[c][u][x] (+)= sum_j src_j[u][perm(x)] * evk[j][c][chain(u)][x], where src_j[u] is the digit's own
-// limb of `own` (the NTT-domain c1 the digits were cut from) when u belongs to digit j, else ext[j][u].
-// Products reduced on the FP64 pipe, summed exactly (|sum| <= 1.5 B t < 2^51), canonicalised once.
-template <int B>
-__global__ void __launch_bounds__(256) k_ks_ip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ own,
-                                               const uint64_t* __restrict__ evk, uint64_t* __restrict__ uo,
-                                               DevTables dt, int level, int n_q, int L1, int E, int alpha,
-                                               uint64_t kperm, int logN, int accumulate) {
+// ---------------------------------------------------------------- key-switch inner product
+// B = beta digits (compile time).
+// u_g[c][u][x] (+)= sum_j src_g,j[u][perm_g(x)] * evk_g[j][c][chain(u)][x], where src_g,j[u] is the
+// digit's own limb of own_g (the NTT-domain c1 the digits were cut from) when u belongs to digit j,
+// else ext_g[j][u].
+//   default: grid (N/256, E, G), one item per z-slice;
+//   SHARED : grid (N/256, E), each thread loops over the items with evk_0 held in registers, so the
+//            key is streamed from HBM once for the whole batch;
+//   SUM    : grid (N/256, E), all items accumulate into u_0 (the lazy HRotSum), race-free because
+//            one thread owns (u, x).
+// Products reduced on the FP64 pipe and summed exactly (|sum| <= 1.5 B t < 2^53), canonicalised once
+// per item (SUM: each item's sum is re-centred with fred before the cross-item sum).
+template <int B, bool SHARED, bool SUM>
+__global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const uint64_t*> ext,
+                                               const __grid_constant__ Arr<const uint64_t*> own,
+                                               const __grid_constant__ Arr<const uint64_t*> evk,
+                                               const __grid_constant__ Arr<uint64_t*> uo,
+                                               const __grid_constant__ Arr<uint64_t> kperm, int G, DevTables dt,
+                                               int level, int n_q, int L1, int E, int alpha, int logN,
+                                               int accumulate) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const int u = blockIdx.y;
   const int t = u <= level ? u : n_q + (u - level - 1);
   const PrimeConst& p = dt.pc[t];
   const double q = p.qd, qinv = p.qinv;
-  const uint32_t xs = kperm != 1 ? aut_index(x, kperm, logN) : x;
-  const int own_digit = (own && u <= level) ? u / alpha : -1;
-  uint64_t v[B], e0[B], e1[B];
+  const int own_digit = u <= level ? u / alpha : -1;
+  double e0[B], e1[B];
+  if (SHARED) {
 #pragma unroll
-  for (int j = 0; j < B; ++j) {
-    const uint64_t* src = (j == own_digit) ? own + (size_t)u * N : ext + ((size_t)j * E + u) * N;
-    v[j] = src[xs];
-    const uint64_t* e = evk + ((size_t)(j * 2) * L1 + t) * N + x;
-    e0[j] = __ldcs(e);
-    e1[j] = __ldcs(e + (size_t)L1 * N);
+    for (int j = 0; j < B; ++j) {
+      const uint64_t* e = evk.p[0] + ((size_t)(j * 2) * L1 + t) * N + x;
+      e0[j] = u2d(__ldcs(e));
+      e1[j] = u2d(__ldcs(e + (size_t)L1 * N));
+    }
   }
-  double a0 = 0.0, a1 = 0.0;
+  double s0 = 0.0, s1 = 0.0;
+  const int g0 = (SHARED || SUM) ? 0 : (int)blockIdx.z;
+  const int g1 = (SHARED || SUM) ? G : g0 + 1;
+  for (int g = g0; g < g1; ++g) {
+    const uint32_t xs = kperm.p[g] != 1 ? aut_index(x, kperm.p[g], logN) : x;
+    uint64_t v[B];
 #pragma unroll
-  for (int j = 0; j < B; ++j) {
-    const double vj = u2d(v[j]);
-    a0 += fmulmod(vj, u2d(e0[j]), q, qinv);
-    a1 += fmulmod(vj, u2d(e1[j]), q, qinv);
+    for (int j = 0; j < B; ++j) {
+      const uint64_t* src = (j == own_digit && own.p[g]) ? own.p[g] + (size_t)u * N
+                                                          : ext.p[g] + ((size_t)j * E + u) * N;
+      v[j] = src[xs];
+    }
+    if (!SHARED) {
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const uint64_t* e = evk.p[g] + ((size_t)(j * 2) * L1 + t) * N + x;
+        e0[j] = u2d(__ldcs(e));
+        e1[j] = u2d(__ldcs(e + (size_t)L1 * N));
+      }
+    }
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const double vj = u2d(v[j]);
+      a0 += fmulmod(vj, e0[j], q, qinv);
+      a1 += fmulmod(vj, e1[j], q, qinv);
+    }
+    if (SUM) {
+      s0 += fred(a0, q, qinv);
+      s1 += fred(a1, q, qinv);
+      continue;
+    }
+    uint64_t* o0 = uo.p[g] + (size_t)u * N + x;
+    uint64_t* o1 = uo.p[g] + ((size_t)E + u) * N + x;
+    if (accumulate) {
+      a0 += u2d(*o0);
+      a1 += u2d(*o1);
+    }
+    *o0 = d2u(fcanon(a0, q, qinv));
+    *o1 = d2u(fcanon(a1, q, qinv));
   }
-  uint64_t* o0 = uo + (size_t)u * N + x;
-  uint64_t* o1 = uo + ((size_t)E + u) * N + x;
-  if (accumulate) {
-    a0 += u2d(*o0);
-    a1 += u2d(*o1);
+  if (SUM) {
+    uint64_t* o0 = uo.p[0] + (size_t)u * N + x;
+    uint64_t* o1 = uo.p[0] + ((size_t)E + u) * N + x;
+    if (accumulate) {
+      s0 += u2d(*o0);
+      s1 += u2d(*o1);
+    }
+    *o0 = d2u(fcanon(s0, q, qinv));
+    *o1 = d2u(fcanon(s1, q, qinv));
   }
-  *o0 = d2u(fcanon(a0, q, qinv));
-  *o1 = d2u(fcanon(a1, q, qinv));
 }
 
-// ModDown basis conversion P -> Q_l, KP = K special primes (compile time).  grid (N/256, npoly);
-// v = iNTT(u on P) [npoly][K][N];  z_k = [v_k (P/p_k)^{-1}]_{p_k} in [0, p_k);
-// w[c][i] = [sum_k z_k ((P/p_k) mod q_i)]_{q_i}.
+// ---------------------------------------------------------------- ModDown
+// P -> Q_l basis conversion, KP = K special primes (compile time).  grid (N/256, npoly, G);
+// v_g = iNTT(u_g on P) [npoly][K][N];  z_k = [v_k (P/p_k)^{-1}]_{p_k} in [0, p_k);
+// w_g[c][i] = [sum_k z_k ((P/p_k) mod q_i)]_{q_i}.
 template <int KP>
-__global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restrict__ v, uint64_t* __restrict__ w,
+__global__ void __launch_bounds__(256) k_moddown_bconv(const __grid_constant__ Arr<const uint64_t*> vv,
+                                                       const __grid_constant__ Arr<uint64_t*> ww,
                                                        const ModDownConst* md, DevTables dt, int level, int n_q,
                                                        int logN) {
   __shared__ double s_hat[kMaxChain][KP];
@@ -151,6 +228,8 @@ __global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restric
   const size_t N = (size_t)1 << logN;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
+  const uint64_t* v = vv.p[blockIdx.z];
+  uint64_t* w = ww.p[blockIdx.z];
   const int n = level + 1;
   for (int i = threadIdx.x; i < n * KP; i += blockDim.x) s_hat[i / KP][i % KP] = (double)md->phat_mod[i / KP][i % KP];
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_fc[i] = FConst{dt.pc[i].qd, dt.pc[i].qinv};
@@ -172,6 +251,33 @@ __global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restric
   }
 }
 
+// out_g[c][i] = (u_g[c][i] - w_g[c][i]) P^{-1} (+ add0_g[i][perm_g(x)] for c = 0) (+ add1_g[i][x] for c = 1)
+//               (+ addct_g[c][i][x]).  out_g may alias addct_g (read before write, same x).
+// grid (N/256, l+1, npoly * G), blockIdx.z = g * npoly + c
+struct FinalArgs {
+  Arr<const uint64_t*> u, w, add0, add1, addct;
+  Arr<uint64_t*> out;
+  Arr<uint64_t> k0;
+};
+__global__ void k_moddown_final(const __grid_constant__ FinalArgs a, int npoly, int E, const ModDownConst* md,
+                                DevTables dt, int level,
+                                int logN) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, g = blockIdx.z / npoly, c = blockIdx.z % npoly;
+  const uint64_t q = dt.pc[i].q;
+  uint64_t val = sub_mod(a.u.p[g][((size_t)c * E + i) * N + x], a.w.p[g][((size_t)c * (level + 1) + i) * N + x], q);
+  val = shoup(val, md->p_inv[i], md->p_inv_sh[i], q);
+  if (c == 0 && a.add0.p[g]) {
+    const uint32_t xs = a.k0.p[g] != 1 ? aut_index(x, a.k0.p[g], logN) : x;
+    val = add_mod(val, a.add0.p[g][(size_t)i * N + xs], q);
+  }
+  if (c == 1 && a.add1.p[g]) val = add_mod(val, a.add1.p[g][(size_t)i * N + x], q);
+  const size_t o = ((size_t)c * (level + 1) + i) * N + x;
+  if (a.addct.p[g]) val = add_mod(val, a.addct.p[g][o], q);
+  a.out.p[g][o] = val;
+}
+
 #define HY_DISPATCH_1_8(KERNEL, VAL, GRID, BLOCK, STREAM, ...)                      \
   switch (VAL) {                                                                     \
     case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;               \
@@ -184,149 +290,229 @@ __global__ void __launch_bounds__(256) k_moddown_bconv(const uint64_t* __restric
     default: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
   }
 
-// out[c][i] = (u[c][i] - w[c][i]) P^{-1} (+ add0[i][perm(x)] for c = 0) (+ add1[i][x] for c = 1)
-//             (+ addct[c][i][x] for both polys).  out may alias addct (read before write, same x).
-// grid (N/256, l+1, npoly)
-__global__ void k_moddown_final(const uint64_t* __restrict__ u, int E, const uint64_t* __restrict__ w,
-                                const ModDownConst* md, DevTables dt, int level, uint64_t* out,
-                                const uint64_t* __restrict__ add0, uint64_t k0, const uint64_t* __restrict__ add1,
-                                const uint64_t* addct, int logN) {
-  const size_t N = (size_t)1 << logN;
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y, c = blockIdx.z;
-  const uint64_t q = dt.pc[i].q;
-  uint64_t val = sub_mod(u[((size_t)c * E + i) * N + x], w[((size_t)c * (level + 1) + i) * N + x], q);
-  val = shoup(val, md->p_inv[i], md->p_inv_sh[i], q);
-  if (c == 0 && add0) {
-    const uint32_t xs = k0 != 1 ? aut_index(x, k0, logN) : x;
-    val = add_mod(val, add0[(size_t)i * N + xs], q);
+#define HY_DISPATCH_IP(SH, SM)                                                                              \
+  switch (beta) {                                                                                           \
+    case 1: k_ks_ip<1, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 2: k_ks_ip<2, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 3: k_ks_ip<3, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 4: k_ks_ip<4, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 5: k_ks_ip<5, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 6: k_ks_ip<6, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    case 7: k_ks_ip<7, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                                \
+    default: k_ks_ip<8, SH, SM><<<g, kT, 0, s>>>(ARGS); break;                                               \
   }
-  if (c == 1 && add1) val = add_mod(val, add1[(size_t)i * N + x], q);
-  const size_t o = ((size_t)c * (level + 1) + i) * N + x;
-  if (addct) val = add_mod(val, addct[o], q);
-  out[o] = val;
-}
 
 // ---------------------------------------------------------------- host-side building blocks
-struct KsBufs {
-  uint64_t *rc, *d, *ext, *u, *v, *w, *acc;
+// Per-item key-switch workspace.
+struct KsItem {
+  uint64_t *rc, *d, *ext, *u, *v, *w;
 };
 
-hy_status carve(hy_ctx* c, uint32_t level, KsBufs& b) {
+size_t item_words(const hy_ctx* c, uint32_t level) {
+  const size_t n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
+  return (2 * n + n + beta * E + 2 * E + 2 * c->n_p + 2 * n) * c->N + 6 * 32;
+}
+
+// carve G item workspaces plus one [2][l+1][N] accumulator
+hy_status carve(hy_ctx* c, uint32_t level, int G, KsItem* it, uint64_t** acc) {
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set (hy_ctx_set_workspace)");
   const size_t N = c->N, n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
   Ws ws{c->ws, c->ws_bytes};
-  b.rc = ws.take<uint64_t>(2 * n * N);
-  b.d = ws.take<uint64_t>(n * N);
-  b.ext = ws.take<uint64_t>(beta * E * N);
-  b.u = ws.take<uint64_t>(2 * E * N);
-  b.v = ws.take<uint64_t>(2 * c->n_p * N);
-  b.w = ws.take<uint64_t>(2 * n * N);
-  b.acc = ws.take<uint64_t>(2 * n * N);
-  if (!b.acc) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  for (int g = 0; g < G; ++g) {
+    it[g].rc = ws.take<uint64_t>(2 * n * N);
+    it[g].d = ws.take<uint64_t>(n * N);
+    it[g].ext = ws.take<uint64_t>(beta * E * N);
+    it[g].u = ws.take<uint64_t>(2 * E * N);
+    it[g].v = ws.take<uint64_t>(2 * c->n_p * N);
+    it[g].w = ws.take<uint64_t>(2 * n * N);
+    if (!it[g].w) return fail(HY_E_WORKSPACE, "workspace too small for this level / batch");
+  }
+  if (acc) {
+    *acc = ws.take<uint64_t>(2 * n * N);
+    if (!*acc) return fail(HY_E_WORKSPACE, "workspace too small for this level / batch");
+  }
   return HY_OK;
+}
+
+// how many items fit the workspace at this level (<= kG)
+int max_items(const hy_ctx* c, uint32_t level) {
+  const size_t per = item_words(c, level) * 8 + 6 * 256;
+  const size_t acc = 2 * (level + 1) * (size_t)c->N * 8 + 256;
+  if (c->ws_bytes <= acc) return 0;
+  return (int)std::min<size_t>(kG, (c->ws_bytes - acc) / per);
+}
+
+void automorph_batch(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* out, const uint64_t* k,
+                     uint32_t nlimbs, uint32_t per_poly, bool accumulate, cudaStream_t s) {
+  if (G == 0) return;
+  Arr<const uint64_t*> ai{};
+  Arr<uint64_t*> ao{};
+  Arr<uint64_t> ak{};
+  for (int g = 0; g < G; ++g) {
+    ai.p[g] = in[g];
+    ao.p[g] = out[g];
+    ak.p[g] = k[g];
+  }
+  dim3 grid(c->N / kT, nlimbs, G);
+  KTimer kt(c, FAM_AUT, s);
+  kt.bytes = (uint64_t)G * nlimbs * c->N * 8 * (accumulate ? 3 : 2);
+  k_automorph<<<grid, kT, 0, s>>>(ai, ao, ak, c->log_n, per_poly, accumulate ? 1 : 0, c->dt);
 }
 
 void automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t nlimbs, uint32_t per_poly, uint64_t k,
                bool accumulate, cudaStream_t s) {
-  dim3 g(c->N / kT, nlimbs);
-  KTimer kt(c, FAM_AUT, s);
-  kt.bytes = (uint64_t)nlimbs * c->N * 8 * (accumulate ? 3 : 2);
-  k_automorph<<<g, kT, 0, s>>>(in, out, k, c->log_n, per_poly, accumulate ? 1 : 0, c->dt);
+  automorph_batch(c, 1, &in, &out, &k, nlimbs, per_poly, accumulate, s);
 }
 
-// d: coefficient-domain [l+1][N] -> ext [beta][E][N] (non-own limbs, NTT domain)
-void modup_core(hy_ctx* c, uint32_t level, const uint64_t* d, uint64_t* ext, cudaStream_t s) {
+// NTT of many limbs given by (pointer, chain) lists, in launches of <= kMaxBatch limbs
+struct LimbList {
+  std::vector<uint64_t*> src, dst;
+  std::vector<uint8_t> chain;
+  void add(const uint64_t* a, uint64_t* b, uint32_t t) {
+    src.push_back(const_cast<uint64_t*>(a));
+    dst.push_back(b);
+    chain.push_back((uint8_t)t);
+  }
+};
+void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
+  LimbBatch b;
+  for (size_t done = 0; done < L.src.size();) {
+    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
+    b.n = (int)m;
+    for (size_t i = 0; i < m; ++i) {
+      b.src[i] = L.src[done + i];
+      b.dst[i] = L.dst[done + i];
+      b.chain[i] = L.chain[done + i];
+    }
+    launch_ntt(c, b, inverse, s);
+    done += m;
+  }
+}
+
+// d_g: coefficient-domain [l+1][N] -> ext_g [beta][E][N] (non-own limbs, NTT domain)
+void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext, cudaStream_t s) {
   const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
-  dim3 g(c->N / kT, beta);
+  Arr<const uint64_t*> ad{};
+  Arr<uint64_t*> ae{};
+  for (int g = 0; g < G; ++g) {
+    ad.p[g] = d[g];
+    ae.p[g] = ext[g];
+  }
+  dim3 grid(c->N / kT, beta, G);
   {
     KTimer kt(c, FAM_MODUP, s);
-    kt.bytes = ((uint64_t)n + (uint64_t)beta * E - n) * c->N * 8;  // read d once, write non-own ext limbs
-    HY_DISPATCH_1_8(k_modup_bconv, c->alpha, g, kT, s, d, ext, c->d_modup[level], c->dt, (int)level, (int)c->n_q, E,
-                    (int)c->log_n);
+    kt.bytes = (uint64_t)G * ((uint64_t)n + (uint64_t)beta * E - n) * c->N * 8;
+    HY_DISPATCH_1_8(k_modup_bconv, c->alpha, grid, kT, s, ad, ae, c->d_modup[level], c->dt, (int)level,
+                    (int)c->n_q, E, (int)c->log_n);
   }
-  LimbBatch b;
-  b.n = 0;
-  for (int j = 0; j < beta; ++j) {
-    const auto& m = c->h_modup[level][j];
-    for (int u = 0; u < E; ++u) {
-      if (u >= m.lo && u < m.hi) continue;
-      if (b.n == kMaxBatch) {
-        launch_ntt(c, b, false, s);
-        b.n = 0;
+  LimbList L;
+  for (int g = 0; g < G; ++g)
+    for (int j = 0; j < beta; ++j) {
+      const auto& m = c->h_modup[level][j];
+      for (int u = 0; u < E; ++u) {
+        if (u >= m.lo && u < m.hi) continue;
+        uint64_t* p = ext[g] + ((size_t)j * E + u) * c->N;
+        L.add(p, p, ext_chain(c, level, u));
       }
-      uint64_t* p = ext + ((size_t)j * E + u) * c->N;
-      b.src[b.n] = p;
-      b.dst[b.n] = p;
-      b.chain[b.n] = (uint8_t)ext_chain(c, level, u);
-      ++b.n;
     }
-  }
-  launch_ntt(c, b, false, s);
+  ntt_list(c, L, false, s);
 }
 
-IPArgs ip_args(hy_ctx*, uint32_t, const uint64_t* ext, const uint64_t* own /* c1 NTT, or null */) {
-  return IPArgs{ext, own};
-}
-
-void ip(hy_ctx* c, uint32_t level, const IPArgs& a, const uint64_t* evk, uint64_t* u, uint64_t kperm, bool acc,
-        cudaStream_t s) {
+// IP of G items.  shared: all items use evk[0]; sum: all items accumulate into u[0].
+void ip_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* ext, const uint64_t* const* own,
+              const uint64_t* const* evk, uint64_t* const* u, const uint64_t* kperm, bool acc, bool shared, bool sum,
+              cudaStream_t s) {
   const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
-  dim3 g(c->N / kT, E);
+  Arr<const uint64_t*> ae{}, ao{}, ak{};
+  Arr<uint64_t*> au{};
+  Arr<uint64_t> ap{};
+  for (int g = 0; g < G; ++g) {
+    ae.p[g] = ext[g];
+    ao.p[g] = own ? own[g] : nullptr;
+    ak.p[g] = evk[shared ? 0 : g];
+    au.p[g] = u[sum ? 0 : g];
+    ap.p[g] = kperm ? kperm[g] : 1;
+  }
+  dim3 g(c->N / kT, E, (shared || sum) ? 1 : G);
   KTimer kt(c, FAM_IP, s);
-  kt.bytes = ((uint64_t)beta * E * 3 + 2ull * E * (acc ? 2 : 1)) * c->N * 8;  // ext + 2 evk polys in, u out
-  HY_DISPATCH_1_8(k_ks_ip, beta, g, kT, s, a.ext, a.own, evk, u, c->dt, (int)level, (int)c->n_q,
-                  (int)(c->n_q + c->n_p), E, (int)c->alpha, kperm, (int)c->log_n, acc ? 1 : 0);
+  const uint64_t keys = shared ? 1 : G, outs = sum ? 1 : G;
+  kt.bytes = ((uint64_t)G * beta * E + keys * 2ull * beta * E + outs * 2ull * E * (acc ? 2 : 1)) * c->N * 8;
+#define ARGS ae, ao, ak, au, ap, G, c->dt, (int)level, (int)c->n_q, (int)(c->n_q + c->n_p), E, (int)c->alpha, \
+             (int)c->log_n, acc ? 1 : 0
+  if (shared && !sum) {
+    HY_DISPATCH_IP(true, false)
+  } else if (!shared && sum) {
+    HY_DISPATCH_IP(false, true)
+  } else if (shared && sum) {
+    HY_DISPATCH_IP(true, true)
+  } else {
+    HY_DISPATCH_IP(false, false)
+  }
+#undef ARGS
 }
 
-// u [npoly][E][N] (NTT) -> out [npoly][l+1][N]
-void moddown_core(hy_ctx* c, uint32_t level, int npoly, const uint64_t* u, uint64_t* out, const uint64_t* add0,
-                  uint64_t k0, const uint64_t* add1, uint64_t* v, uint64_t* w, cudaStream_t s,
-                  const uint64_t* addct = nullptr) {
+// ModDown of G items: u_g [npoly][E][N] (NTT) -> out_g [npoly][l+1][N], with the final addends.
+struct DownItem {
+  const uint64_t* u;
+  uint64_t* out;
+  const uint64_t* add0;
+  uint64_t k0;
+  const uint64_t* add1;
+  const uint64_t* addct;
+  uint64_t *v, *w;  // scratch
+};
+void moddown_batch(hy_ctx* c, uint32_t level, int npoly, int G, const DownItem* it, cudaStream_t s) {
   const int n = level + 1, E = n + c->n_p, K = c->n_p;
-  LimbBatch b;
-  b.n = 0;
-  for (int cc = 0; cc < npoly; ++cc)
-    for (int k = 0; k < K; ++k) {
-      b.src[b.n] = u + ((size_t)cc * E + n + k) * c->N;
-      b.dst[b.n] = v + ((size_t)cc * K + k) * c->N;
-      b.chain[b.n] = (uint8_t)(c->n_q + k);
-      ++b.n;
-    }
-  launch_ntt(c, b, true, s);
-  dim3 g(c->N / kT, npoly);
+  LimbList L;
+  for (int g = 0; g < G; ++g)
+    for (int cc = 0; cc < npoly; ++cc)
+      for (int k = 0; k < K; ++k)
+        L.add(it[g].u + ((size_t)cc * E + n + k) * c->N, it[g].v + ((size_t)cc * K + k) * c->N, c->n_q + k);
+  ntt_list(c, L, true, s);
+  Arr<const uint64_t*> av{};
+  Arr<uint64_t*> aw{};
+  for (int g = 0; g < G; ++g) {
+    av.p[g] = it[g].v;
+    aw.p[g] = it[g].w;
+  }
+  dim3 grid(c->N / kT, npoly, G);
   {
     KTimer kt(c, FAM_MODDOWN, s);
-    kt.bytes = ((uint64_t)npoly * K + (uint64_t)npoly * n) * c->N * 8;
-    HY_DISPATCH_1_8(k_moddown_bconv, K, g, kT, s, v, w, c->d_moddown[level], c->dt, (int)level, (int)c->n_q,
+    kt.bytes = (uint64_t)G * ((uint64_t)npoly * K + (uint64_t)npoly * n) * c->N * 8;
+    HY_DISPATCH_1_8(k_moddown_bconv, K, grid, kT, s, av, aw, c->d_moddown[level], c->dt, (int)level, (int)c->n_q,
                     (int)c->log_n);
   }
-  b.n = 0;
-  for (int cc = 0; cc < npoly; ++cc)
-    for (int i = 0; i < n; ++i) {
-      uint64_t* p = w + ((size_t)cc * n + i) * c->N;
-      b.src[b.n] = p;
-      b.dst[b.n] = p;
-      b.chain[b.n] = (uint8_t)i;
-      ++b.n;
-    }
-  launch_ntt(c, b, false, s);
-  dim3 g2(c->N / kT, n, npoly);
+  LimbList L2;
+  for (int g = 0; g < G; ++g)
+    for (int cc = 0; cc < npoly; ++cc)
+      for (int i = 0; i < n; ++i) {
+        uint64_t* p = it[g].w + ((size_t)cc * n + i) * c->N;
+        L2.add(p, p, i);
+      }
+  ntt_list(c, L2, false, s);
+  FinalArgs a{};
+  uint64_t extra = 0;
+  for (int g = 0; g < G; ++g) {
+    a.u.p[g] = it[g].u;
+    a.w.p[g] = it[g].w;
+    a.out.p[g] = it[g].out;
+    a.add0.p[g] = it[g].add0;
+    a.k0.p[g] = it[g].k0;
+    a.add1.p[g] = it[g].add1;
+    a.addct.p[g] = it[g].addct;
+    extra += (it[g].add0 ? n : 0) + (it[g].add1 ? n : 0) + (it[g].addct ? (uint64_t)npoly * n : 0);
+  }
+  dim3 g2(c->N / kT, n, npoly * G);
   KTimer kt(c, FAM_MODDOWN, s);
-  kt.bytes = ((uint64_t)npoly * n * (addct ? 4 : 3) + (add0 ? n : 0) + (add1 ? n : 0)) * c->N * 8;
-  k_moddown_final<<<g2, kT, 0, s>>>(u, E, w, c->d_moddown[level], c->dt, level, out, add0, k0, add1, addct,
-                                    c->log_n);
+  kt.bytes = ((uint64_t)G * npoly * n * 3 + extra) * c->N * 8;
+  k_moddown_final<<<g2, kT, 0, s>>>(a, npoly, E, c->d_moddown[level], c->dt, (int)level, (int)c->log_n);
 }
 
-void intt_poly(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t level, cudaStream_t s) {
-  LimbBatch b;
-  b.n = level + 1;
-  for (uint32_t i = 0; i <= level; ++i) {
-    b.src[i] = in + (size_t)i * c->N;
-    b.dst[i] = out + (size_t)i * c->N;
-    b.chain[i] = (uint8_t)i;
-  }
-  launch_ntt(c, b, true, s);
+void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* out, uint32_t level, cudaStream_t s) {
+  LimbList L;
+  for (int g = 0; g < G; ++g)
+    for (uint32_t i = 0; i <= level; ++i) L.add(in[g] + (size_t)i * c->N, out[g] + (size_t)i * c->N, i);
+  ntt_list(c, L, true, s);
 }
 
 hy_status check_level(hy_ctx* c, uint32_t level) {
@@ -337,40 +523,79 @@ hy_status check_level(hy_ctx* c, uint32_t level) {
 
 }  // namespace
 
-// out = HRot_r(ct) (+ addct).  out may alias addct (and ct, since ct is consumed into the
-// workspace before the final write).
-hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
-                     cudaStream_t s, const uint64_t* addct) {
-  const uint64_t k = hy_galois_elt(c, r);
+// Plain HRot of G ciphertexts: out_g = HRot_{r_g}(ct_g) (+ addct_g).  evk may repeat (shared key).
+// out_g may alias ct_g and addct_g (ct_g is consumed into the workspace before the final write).
+hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* const* ct, uint32_t level,
+                     const int32_t* r, uint32_t n_items, uint64_t* const* out, const uint64_t* const* addct,
+                     cudaStream_t s) {
   const size_t n = level + 1, N = c->N;
-  if (k == 1) {
-    if (addct) {  // out = ct + addct
-      if (out != addct) cudaMemcpyAsync(out, addct, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
-      automorph(c, ct, out, 2 * n, n, 1, true, s);
-    } else if (out != ct) {
-      cudaMemcpyAsync(out, ct, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+  // rotations by 0 first (copies / adds), then key switches in chunks
+  std::vector<uint32_t> ks;
+  for (uint32_t i = 0; i < n_items; ++i) {
+    const uint64_t k = hy_galois_elt(c, r[i]);
+    if (k != 1) {
+      if (!evk[i]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
+      ks.push_back(i);
+      continue;
     }
-    return HY_OK;
+    const uint64_t* a = addct ? addct[i] : nullptr;
+    if (a) {  // out = ct + addct
+      if (out[i] != a) cudaMemcpyAsync(out[i], a, 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+      automorph(c, ct[i], out[i], 2 * n, n, 1, true, s);
+    } else if (out[i] != ct[i]) {
+      cudaMemcpyAsync(out[i], ct[i], 2 * n * N * 8, cudaMemcpyDeviceToDevice, s);
+    }
   }
-  if (!evk) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
-  KsBufs b;
-  hy_status st = carve(c, level, b);
-  if (st != HY_OK) return st;
-  automorph(c, ct, b.rc, 2 * n, n, k, false, s);
-  intt_poly(c, b.rc + n * N, b.d, level, s);
-  modup_core(c, level, b.d, b.ext, s);
-  IPArgs a = ip_args(c, level, b.ext, b.rc + n * N);
-  ip(c, level, a, evk, b.u, 1, false, s);
-  moddown_core(c, level, 2, b.u, out, b.rc, 1, nullptr, b.v, b.w, s, addct);
+  const int cap = max_items(c, level);
+  if (!ks.empty() && cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  for (size_t done = 0; done < ks.size();) {
+    const int G = (int)std::min<size_t>(ks.size() - done, cap);
+    hy_status st0 = carve(c, level, G, it, nullptr);
+    if (st0 != HY_OK) return st0;
+    const uint64_t* cin[kG];
+    uint64_t* rc[kG];
+    const uint64_t* rc1[kG];
+    uint64_t* d[kG];
+    uint64_t* ext[kG];
+    uint64_t* u[kG];
+    const uint64_t* keys[kG];
+    uint64_t kk[kG];
+    DownItem di[kG];
+    bool shared = true;
+    for (int g = 0; g < G; ++g) {
+      const uint32_t i = ks[done + g];
+      cin[g] = ct[i];
+      rc[g] = it[g].rc;
+      rc1[g] = it[g].rc + n * N;
+      d[g] = it[g].d;
+      ext[g] = it[g].ext;
+      u[g] = it[g].u;
+      keys[g] = evk[i];
+      kk[g] = hy_galois_elt(c, r[i]);
+      shared &= evk[i] == evk[ks[done]];
+      di[g] = DownItem{it[g].u, out[i], it[g].rc, 1, nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w};
+    }
+    automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
+    intt_polys(c, G, rc1, d, level, s);
+    modup_batch(c, level, G, d, ext, s);
+    ip_batch(c, level, G, ext, rc1, keys, u, nullptr, false, shared && G > 1, false, s);
+    moddown_batch(c, level, 2, G, di, s);
+    done += G;
+  }
   return HY_OK;
 }
 
-namespace {
-}  // namespace
+hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
+                     cudaStream_t s, const uint64_t* addct) {
+  return hrot_multi(c, &evk, &ct, level, &r, 1, &out, addct ? &addct : nullptr, s);
+}
 
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s) {
   automorph(c, in, out, n_limbs, n_limbs, k, false, s);
 }
+
+size_t ks_item_bytes(const hy_ctx* c, uint32_t level) { return item_words(c, level) * 8 + 6 * 256; }
 
 }  // namespace hy
 
@@ -390,21 +615,15 @@ extern "C" hy_status hy_modup(hy_ctx* c, uint32_t level, const uint64_t* d, uint
   if (s0 != HY_OK) return s0;
   if (!d || !ext) return fail(HY_E_ARG, "null");
   cudaStream_t s = st(stream);
-  modup_core(c, level, d, ext, s);
+  modup_batch(c, level, 1, &d, &ext, s);
   // own-digit limbs: NTT(d)
   const int E = level + 1 + c->n_p;
-  LimbBatch b;
-  b.n = 0;
+  LimbList L;
   for (uint32_t j = 0; j < n_digits(c, level); ++j) {
     const auto& m = c->h_modup[level][j];
-    for (int i = m.lo; i < m.hi; ++i) {
-      b.src[b.n] = d + (size_t)i * c->N;
-      b.dst[b.n] = ext + ((size_t)j * E + i) * c->N;
-      b.chain[b.n] = (uint8_t)i;
-      ++b.n;
-    }
+    for (int i = m.lo; i < m.hi; ++i) L.add(d + (size_t)i * c->N, ext + ((size_t)j * E + i) * c->N, i);
   }
-  launch_ntt(c, b, false, s);
+  ntt_list(c, L, false, s);
   return cuda_check("hy_modup");
 }
 
@@ -413,8 +632,7 @@ extern "C" hy_status hy_ks_inner_product(hy_ctx* c, uint32_t level, const uint64
   hy_status s0 = check_level(c, level);
   if (s0 != HY_OK) return s0;
   if (!ext || !evk || !u) return fail(HY_E_ARG, "null");
-  IPArgs a = ip_args(c, level, ext, nullptr);
-  ip(c, level, a, evk, u, 1, false, st(stream));
+  ip_batch(c, level, 1, &ext, nullptr, &evk, &u, nullptr, false, false, false, st(stream));
   return cuda_check("hy_ks_inner_product");
 }
 
@@ -422,10 +640,11 @@ extern "C" hy_status hy_moddown(hy_ctx* c, uint32_t level, const uint64_t* u, ui
   hy_status s0 = check_level(c, level);
   if (s0 != HY_OK) return s0;
   if (!u || !out) return fail(HY_E_ARG, "null");
-  KsBufs b;
-  hy_status st0 = carve(c, level, b);
-  if (st0 != HY_OK) return st0;
-  moddown_core(c, level, 1, u, out, nullptr, 1, nullptr, b.v, b.w, st(stream));
+  KsItem it[1];
+  s0 = carve(c, level, 1, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  DownItem di{u, out, nullptr, 1, nullptr, nullptr, it[0].v, it[0].w};
+  moddown_batch(c, level, 1, 1, &di, st(stream));
   return cuda_check("hy_moddown");
 }
 
@@ -445,11 +664,10 @@ extern "C" hy_status hy_hrot_batch(hy_ctx* c, const uint64_t* const* evks, const
   hy_status s0 = check_level(c, level);
   if (s0 != HY_OK) return s0;
   if (!evks || !cts || !r || !outs) return fail(HY_E_ARG, "null");
-  for (uint32_t i = 0; i < n; ++i) {
+  for (uint32_t i = 0; i < n; ++i)
     if (cts[i] == outs[i]) return fail(HY_E_ARG, "hrot cannot run in place");
-    s0 = hrot_plain(c, evks[i], cts[i], level, r[i], outs[i], st(stream), nullptr);
-    if (s0 != HY_OK) return s0;
-  }
+  s0 = hrot_multi(c, evks, cts, level, r, n, outs, nullptr, st(stream));
+  if (s0 != HY_OK) return s0;
   return cuda_check("hy_hrot_batch");
 }
 
@@ -460,30 +678,46 @@ extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, con
   if (!evks || !ct || !r || !outs) return fail(HY_E_ARG, "null");
   cudaStream_t s = st(stream);
   const size_t nl = level + 1, N = c->N;
-  KsBufs b;
-  s0 = carve(c, level, b);
-  if (s0 != HY_OK) return s0;
-  bool need_ks = false;
+  std::vector<uint32_t> ks;
   for (uint32_t i = 0; i < n; ++i) {
     if (outs[i] == ct) return fail(HY_E_ARG, "hrot cannot run in place");
-    if (hy_galois_elt(c, r[i]) != 1) {
-      need_ks = true;
-      if (!evks[i]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
-    }
-  }
-  if (need_ks) {
-    intt_poly(c, ct + nl * N, b.d, level, s);
-    modup_core(c, level, b.d, b.ext, s);
-  }
-  IPArgs a = ip_args(c, level, b.ext, ct + nl * N);
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint64_t k = hy_galois_elt(c, r[i]);
-    if (k == 1) {
+    if (hy_galois_elt(c, r[i]) == 1) {
       cudaMemcpyAsync(outs[i], ct, 2 * nl * N * 8, cudaMemcpyDeviceToDevice, s);
       continue;
     }
-    ip(c, level, a, evks[i], b.u, k, false, s);
-    moddown_core(c, level, 2, b.u, outs[i], ct, k, nullptr, b.v, b.w, s);
+    if (!evks[i]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
+    ks.push_back(i);
+  }
+  if (ks.empty()) return cuda_check("hy_hrot_hoisted");
+  const int cap = max_items(c, level);
+  if (cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  s0 = carve(c, level, cap, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  // one ModUp of c1 into item 0's buffers, shared by every rotation
+  const uint64_t* c1 = ct + nl * N;
+  intt_polys(c, 1, &c1, &it[0].d, level, s);
+  modup_batch(c, level, 1, (const uint64_t* const*)&it[0].d, &it[0].ext, s);
+  for (size_t done = 0; done < ks.size();) {
+    const int G = (int)std::min<size_t>(ks.size() - done, cap);
+    const uint64_t* ext[kG];
+    const uint64_t* own[kG];
+    const uint64_t* keys[kG];
+    uint64_t* u[kG];
+    uint64_t kk[kG];
+    DownItem di[kG];
+    for (int g = 0; g < G; ++g) {
+      const uint32_t i = ks[done + g];
+      ext[g] = it[0].ext;
+      own[g] = c1;
+      keys[g] = evks[i];
+      u[g] = it[g].u;
+      kk[g] = hy_galois_elt(c, r[i]);
+      di[g] = DownItem{it[g].u, outs[i], ct, kk[g], nullptr, nullptr, it[g].v, it[g].w};
+    }
+    ip_batch(c, level, G, ext, own, keys, u, kk, false, false, false, s);
+    moddown_batch(c, level, 2, G, di, s);
+    done += G;
   }
   return cuda_check("hy_hrot_hoisted");
 }
@@ -495,37 +729,78 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
   if (!evks || !cts || !r || !out || n == 0) return fail(HY_E_ARG, "null / empty");
   cudaStream_t s = st(stream);
   const size_t nl = level + 1, N = c->N;
-  KsBufs b;
-  s0 = carve(c, level, b);
-  if (s0 != HY_OK) return s0;
+  std::vector<uint32_t> ks, zero;
   for (uint32_t t = 0; t < n; ++t) {
     if (cts[t] == out) return fail(HY_E_ARG, "output aliases an input");
-    if (hy_galois_elt(c, r[t]) != 1 && !evks[t]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
-  }
-  uint64_t* acc0 = b.acc;          // sum of kappa(c0_t) and unrotated c0_t
-  uint64_t* acc1 = b.acc + nl * N; // sum of unrotated c1_t
-  cudaMemsetAsync(b.acc, 0, 2 * nl * N * 8, s);
-  bool first = true, any1 = false;
-  for (uint32_t t = 0; t < n; ++t) {
-    const uint64_t k = hy_galois_elt(c, r[t]);
-    if (k == 1) {
-      automorph(c, cts[t], acc0, nl, nl, 1, true, s);
-      automorph(c, cts[t] + nl * N, acc1, nl, nl, 1, true, s);
-      any1 = true;
-      continue;
+    if (hy_galois_elt(c, r[t]) == 1) {
+      zero.push_back(t);
+    } else {
+      if (!evks[t]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
+      ks.push_back(t);
     }
-    automorph(c, cts[t], acc0, nl, nl, k, true, s);
-    automorph(c, cts[t] + nl * N, b.rc, nl, nl, k, false, s);
-    intt_poly(c, b.rc, b.d, level, s);
-    modup_core(c, level, b.d, b.ext, s);
-    IPArgs a = ip_args(c, level, b.ext, b.rc);
-    ip(c, level, a, evks[t], b.u, 1, !first, s);
+  }
+  const int cap = max_items(c, level);
+  if (cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  uint64_t* acc = nullptr;
+  s0 = carve(c, level, cap, it, &acc);
+  if (s0 != HY_OK) return s0;
+  uint64_t* acc0 = acc;           // sum of kappa(c0_t) (and unrotated c0_t)
+  uint64_t* acc1 = acc + nl * N;  // sum of unrotated c1_t
+  cudaMemsetAsync(acc, 0, 2 * nl * N * 8, s);
+  // r = 0 terms: added without key switching
+  for (uint32_t t : zero) {
+    automorph(c, cts[t], acc0, nl, nl, 1, true, s);
+    automorph(c, cts[t] + nl * N, acc1, nl, nl, 1, true, s);
+  }
+  bool first = true;
+  for (size_t done = 0; done < ks.size();) {
+    const int G = (int)std::min<size_t>(ks.size() - done, cap);
+    const uint64_t* c0[kG];
+    const uint64_t* c1[kG];
+    uint64_t* rc1[kG];
+    const uint64_t* rc1c[kG];
+    uint64_t* d[kG];
+    uint64_t* ext[kG];
+    const uint64_t* keys[kG];
+    uint64_t kk[kG];
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t = ks[done + g];
+      c0[g] = cts[t];
+      c1[g] = cts[t] + nl * N;
+      rc1[g] = it[g].rc;
+      rc1c[g] = it[g].rc;
+      d[g] = it[g].d;
+      ext[g] = it[g].ext;
+      keys[g] = evks[t];
+      kk[g] = hy_galois_elt(c, r[t]);
+    }
+    // acc0 += sum_g kappa_g(c0_g), race-free in one kernel
+    {
+      Arr<const uint64_t*> ai{};
+      Arr<uint64_t> ak{};
+      for (int g = 0; g < G; ++g) {
+        ai.p[g] = c0[g];
+        ak.p[g] = kk[g];
+      }
+      dim3 grid(c->N / kT, nl);
+      KTimer kt(c, FAM_AUT, s);
+      kt.bytes = ((uint64_t)G + 2) * nl * N * 8;
+      k_automorph_sum<<<grid, kT, 0, s>>>(ai, ak, G, acc0, c->log_n, (int)nl, c->dt);
+    }
+    automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
+    intt_polys(c, G, rc1c, d, level, s);
+    modup_batch(c, level, G, d, ext, s);
+    uint64_t* u0 = it[0].u;
+    ip_batch(c, level, G, ext, rc1c, keys, &u0, nullptr, !first, false, true, s);
     first = false;
+    done += G;
   }
   if (first) {  // no key switching at all: out = accumulated sum
-    cudaMemcpyAsync(out, b.acc, 2 * nl * N * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(out, acc, 2 * nl * N * 8, cudaMemcpyDeviceToDevice, s);
   } else {
-    moddown_core(c, level, 2, b.u, out, acc0, 1, any1 ? acc1 : nullptr, b.v, b.w, s);
+    DownItem di{it[0].u, out, acc0, 1, zero.empty() ? nullptr : acc1, nullptr, it[0].v, it[0].w};
+    moddown_batch(c, level, 2, 1, &di, s);
   }
   return cuda_check("hy_hrot_sum");
 }
