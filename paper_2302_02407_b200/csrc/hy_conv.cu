@@ -283,7 +283,8 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   if (!c || !p) return 0;
   const size_t ct = 2ull * (level + 1) * c->N;
   const size_t f2 = (size_t)p->s.f * p->s.f;
-  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 4) * ct;  // slid inputs + acc + 2 groups + tmp
+  // CA: slid inputs + acc + (up to) two ciphertexts per SISO group (group sums, masked groups)
+  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 1 + 2 * p->n_groups) * ct;
   return (f2 + 2) * ct;                                          // tap accumulators + tmp
 }
 
@@ -359,50 +360,72 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
         if (stt != HY_OK) return stt;
       }
     }
+    // All SISO groups of the requested outputs advance together, so every RaS / RaS_g / IR_g step
+    // is one batched HRot whose evaluation key is streamed once for all groups.
+    const bool ds = p->s.stride == 2;
+    std::vector<int64_t> grps;
+    for (uint32_t j = ob; j < oe; ++j) {
+      if (ds) {
+        grps.push_back(2 * j);
+        grps.push_back(2 * j + 1);
+      } else {
+        grps.push_back(j);
+      }
+    }
+    const size_t G = grps.size();
     uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;
-    uint64_t* ga = acc + ct_l;
-    uint64_t* gb = ga + ct_l;
-    auto siso_group = [&](int64_t grp, uint64_t* dst) -> hy_status {  // MulFilter&Sum_f, rescale, RaS, RaS_g
+    uint64_t* gbuf = acc + ct_l;                                  // G group ciphertexts (level - 1)
+    const size_t ct_m = 2 * (size_t)level * N;
+    std::vector<uint64_t*> gp(G);
+    for (size_t g = 0; g < G; ++g)
+      gp[g] = (!p->has_mask && !ds) ? out[g] : gbuf + g * ct_m;  // no mask: write the output directly
+    for (size_t g = 0; g < G; ++g) {                              // MulFilter&Sum_f, rescale
       cts.clear();
       ps.clear();
       for (int64_t i = 0; i < p->n_in; ++i)
         for (size_t t = 0; t < f2; ++t) {
           cts.push_back(slid[i][t]);
-          ps.push_back(W(grp, i, t));
+          ps.push_back(W(grps[g], i, t));
         }
-      hy_status s1 = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, acc, 0, stream);
-      if (s1 == HY_OK) s1 = hy_rescale(c, acc, level, dst, stream);
-      if (s1 == HY_OK) s1 = ras_inplace(x, dst, level - 1, p->ras);
-      if (s1 == HY_OK) s1 = ras_inplace(x, dst, level - 1, p->ras_g);
-      return s1;
-    };
-    for (uint32_t j = ob; j < oe; ++j) {
-      if (p->s.stride == 1) {
-        if (!p->has_mask) {
-          stt = siso_group(j, out[j - ob]);
-          if (stt != HY_OK) return stt;
-          continue;
-        }
-        stt = siso_group(j, ga);
-        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
-        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, out[j - ob], stream);
-        if (stt == HY_OK) stt = ras_inplace(x, out[j - ob], level - 2, p->ir_g);
-        if (stt != HY_OK) return stt;
-      } else {  // dsconv: two SISO groups merged into the doubled gap (DESIGN R-DSCONV)
-        const size_t ct_m = 2 * (size_t)level * N;
-        uint64_t* a = gb;
-        uint64_t* bb = gb + ct_m;
-        stt = siso_group(2 * j, ga);
-        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
-        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, a, stream);
-        if (stt == HY_OK) stt = siso_group(2 * j + 1, ga);
-        if (stt == HY_OK) stt = hy_pmult(c, ga, mask, level - 1, acc, stream);
-        if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, bb, stream);
-        if (stt == HY_OK) stt = hrot_plain(c, x.key(p->combine), bb, level - 2, (int32_t)p->combine, out[j - ob], x.s, a);
-        if (stt == HY_OK) stt = ras_inplace(x, out[j - ob], level - 2, p->ir_g);
-        if (stt != HY_OK) return stt;
-      }
+      stt = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, acc, 0, stream);
+      if (stt == HY_OK) stt = hy_rescale(c, acc, level, gp[g], stream);
+      if (stt != HY_OK) return stt;
     }
+    auto ras_all = [&](std::vector<uint64_t*>& v, uint32_t lvl, const std::vector<int64_t>& rs) -> hy_status {
+      for (int64_t r : rs) {
+        std::vector<const uint64_t*> keys(v.size(), x.key(r)), in_c(v.begin(), v.end());
+        std::vector<int32_t> rr(v.size(), (int32_t)r);
+        hy_status s1 = hrot_multi(c, keys.data(), in_c.data(), lvl, rr.data(), (uint32_t)v.size(), v.data(),
+                                  in_c.data(), x.s);
+        if (s1 != HY_OK) return s1;
+      }
+      return HY_OK;
+    };
+    stt = ras_all(gp, level - 1, p->ras);                          // RaS over C_a
+    if (stt == HY_OK) stt = ras_all(gp, level - 1, p->ras_g);      // RaS_g over C_g
+    if (stt != HY_OK || (!p->has_mask && !ds)) return stt == HY_OK ? cuda_check("hy_caconv") : stt;
+    // IR_g: mask (one level) ...
+    std::vector<uint64_t*> masked(G);
+    for (size_t g = 0; g < G; ++g) {
+      masked[g] = ds ? gbuf + (G + g) * ct_m : out[g];
+      stt = hy_pmult(c, gp[g], mask, level - 1, acc, stream);
+      if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, masked[g], stream);
+      if (stt != HY_OK) return stt;
+    }
+    std::vector<uint64_t*> fin(out, out + (oe - ob));
+    if (ds) {  // ... merge the two groups of each output into the doubled gap (DESIGN R-DSCONV) ...
+      const size_t J = oe - ob;
+      std::vector<const uint64_t*> keys(J, x.key(p->combine)), b(J), a(J);
+      std::vector<int32_t> rr(J, (int32_t)p->combine);
+      for (size_t j = 0; j < J; ++j) {
+        a[j] = masked[2 * j];
+        b[j] = masked[2 * j + 1];
+      }
+      stt = hrot_multi(c, keys.data(), b.data(), level - 2, rr.data(), (uint32_t)J, fin.data(), a.data(), x.s);
+      if (stt != HY_OK) return stt;
+    }
+    stt = ras_all(fin, level - 2, p->ir_g);                        // ... and replicate
+    if (stt != HY_OK) return stt;
     return cuda_check("hy_caconv");
   }
   // RAConv_Reorder: MulFilter&Sum_{c_i} into f^2 accumulators, one lazy Slide_1&Sum_f, rescale, RaS_g, IR_g
