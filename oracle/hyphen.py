@@ -43,10 +43,16 @@ class Fmt:
     g: int       # gap
     m: int       # |C_g|
     d: int       # |R_g|
+    S: int = 1   # PRCR row segments |S|; 1 = plain rows
 
     @property
     def I(self):
         return self.wp * self.wp
+
+    @property
+    def F(self):
+        """slots per row segment (the PRCR fragment size)."""
+        return self.I // self.S
 
     @property
     def e(self):
@@ -74,7 +80,8 @@ class Fmt:
         return self.I << (bit - 2 * lg)
 
     def decompose(self):
-        """per slot: block b, logical pixel (h, w), cell kappa."""
+        """per slot: block b, logical pixel (h, w), cell kappa (rows stay at their natural positions
+        under PRCR; only the channel occupying each row segment changes)."""
         s = np.arange(self.n)
         b, r = s // self.B, s % self.B
         e_idx, pr, pc = r // self.I, (r % self.I) // self.wp, r % self.wp
@@ -82,20 +89,36 @@ class Fmt:
         kappa = gc + self.g * (gr + self.g * e_idx)
         return b, h, w, kappa
 
+    def segment(self):
+        """global row-segment position G = b S + s of every slot (PRCR; requires e = 1)."""
+        s = np.arange(self.n)
+        return s // self.F
+
     def mu_rho(self, kappa):
         if self.kind == "CA":
             return kappa % self.m, kappa // self.m
         return kappa // self.d, kappa % self.d
 
     def channel(self, i: int):
-        """channel held by every slot of ciphertext i (before the `< C` cut)."""
+        """channel held by every slot of ciphertext i (before the `< C` cut).
+        pi_CA' (CA, S > 1, PRCR): ciphertexts come in families of S; member im of family k holds, at
+        global segment G, row segment (G mod S) of channel k c_n S m + ((G + im) mod c_n S) m + mu --
+        the fragments are organised circularly, so member im sees the family's weight
+        plaintext rotated by im fragments (PRot)."""
         b, h, w, kappa = self.decompose()
         mu, _ = self.mu_rho(kappa)
         if self.kind == "CA":
+            if self.S > 1:
+                assert self.e == 1, "PRCR needs e = 1"
+                fam, im = divmod(i, self.S)
+                G = self.segment()
+                return fam * self.cn * self.S * self.m + ((G + im) % (self.cn * self.S)) * self.m + mu
             return i * self.cn * self.m + b * self.m + mu
         return i * self.m + mu
 
     def n_ct(self, c: int) -> int:
+        if self.kind == "CA" and self.S > 1:
+            return self.S * -(-c // (self.cn * self.S * self.m))
         per = self.cn * self.m if self.kind == "CA" else self.m
         return -(-c // per)
 
@@ -164,10 +187,18 @@ class ConvSpec:
     d: int
     algo: str       # "CA" or "RA"
     n: int = 32768
+    S: int = 1      # PRCR segments |S|; 1 = no PRCR
 
     @property
     def pad(self):
         return (self.f - 1) // 2
+
+    def check_prcr(self):
+        """PRCR needs whole rows per segment: S | W_p / g, stride 1, and e = m d / g^2 = 1 (DESIGN R-PRCR)."""
+        if self.S > 1:
+            assert self.s == 1 and (self.wp // self.g) % self.S == 0, "PRCR: S must divide W_p / g, stride 1"
+            assert self.m * self.d == self.g * self.g, "PRCR: needs e = 1"
+            assert self.wp // self.g >= self.w + self.pad, "PRCR: needs >= pad zero rows/columns of padding"
 
     @property
     def wo(self):
@@ -192,6 +223,27 @@ class Plan:
     combine: int | None = None                     # dsconv: rotation merging two groups
     counts: dict = field(default_factory=dict)
 
+    def wkey(self, grp: int, i: int, t: int):
+        """(stored weight key, PRot amount) used for SISO group / output `grp`, input ct i, tap t.
+        Without PRCR every (grp, i, t) has its own plaintext and no PRot.  With PRCR a family
+        of S ciphertexts shares one plaintext P holding, per slot, the filter value of the channel at
+        that global row segment (no pixel masks); the effective weight is PRot(P, shift) with
+          CA input member im:  shift = r_t + im F   (P indexed by the source slot of the tap),
+          RA output member im: shift = im F - r_t   (the inverse rotation of Alg. 2 folded in).
+        Out-of-image sources read the zero padding; invalid output pixels are zeroed by the mask step
+        (DESIGN R-PRCR)."""
+        S = self.spec.S
+        if S == 1:
+            return (grp, i, t), 0
+        if self.spec.algo == "CA":
+            return (grp, i // S, t), self.taps[t] + (i % S) * self.fin.F
+        return (grp // S, i, t), (grp % S) * self.fout.F - self.taps[t]
+
+    def effective(self, grp: int, i: int, t: int):
+        """the slot vector actually multiplied with (rotated) input i for group/output grp, tap t."""
+        key, sh = self.wkey(grp, i, t)
+        return rot(self.weights[key], sh)
+
 
 def _tap(j1, j2, spec: ConvSpec, g: int):
     return (j1 - spec.pad) * g * spec.wp + (j2 - spec.pad) * g
@@ -203,10 +255,11 @@ def plan_caconv(spec: ConvSpec, K: np.ndarray, with_weights: bool = True) -> Pla
     Stride 2 (dsconv/pconv, Fig. 2(d)): valid outputs at even pixels; IR_g merges two SISO groups
     into the doubled gap (DESIGN R-DSCONV)."""
     assert spec.algo == "CA" and spec.s in (1, 2)
-    fin = Fmt("CA", spec.n, spec.wp, spec.g, spec.m, spec.d)
+    spec.check_prcr()
+    fin = Fmt("CA", spec.n, spec.wp, spec.g, spec.m, spec.d, spec.S)
     lg = ilog2(spec.g)
     if spec.s == 1:
-        fout = Fmt("RA", spec.n, spec.wp, spec.g, spec.d, spec.m)
+        fout = Fmt("RA", spec.n, spec.wp, spec.g, spec.d, spec.m, spec.S)
     else:
         assert spec.m == spec.g, "dsconv IR needs m == g (DESIGN R-DSCONV)"
         fout = Fmt("RA", spec.n, spec.wp, 2 * spec.g, 2 * spec.d, 2 * spec.m)
@@ -231,21 +284,34 @@ def plan_caconv(spec: ConvSpec, K: np.ndarray, with_weights: bool = True) -> Pla
             rho_lo, rho_hi = rho % spec.g, rho // spec.g
             mu_new = rho_lo + (spec.g * (j & 1)) + (2 * spec.g) * rho_hi
             o = (j // 2) * (2 * d) + mu_new
-        for i in range(n_in):
-            c = i * cn * m + b * m + mu
-            for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
-                sh, sw = h + j1 - spec.pad, w + j2 - spec.pad
-                ok = out_ok & (sh >= 0) & (sh < spec.w) & (sw >= 0) & (sw < spec.w) & (c < spec.ci) & (o < spec.co)
-                v = np.zeros(spec.n)
-                v[ok] = K[o[ok], c[ok], j1, j2]
-                weights[(j, i, t)] = v
+        if spec.S == 1:
+            for i in range(n_in):
+                c = i * cn * m + b * m + mu
+                for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
+                    sh, sw = h + j1 - spec.pad, w + j2 - spec.pad
+                    ok = out_ok & (sh >= 0) & (sh < spec.w) & (sw >= 0) & (sw < spec.w) & (c < spec.ci) & (o < spec.co)
+                    v = np.zeros(spec.n)
+                    v[ok] = K[o[ok], c[ok], j1, j2]
+                    weights[(j, i, t)] = v
+        else:
+            # PRCR: one plaintext per family k in source coordinates: slot q holds the filter value of the
+            # channel at global segment G(q) of member 0, i.e. k c_n S m + G m + mu (DESIGN R-PRCR)
+            for k in range(n_in // spec.S):
+                c = k * cn * spec.S * m + fin.segment() * m + mu
+                ok = (c < spec.ci) & (o < spec.co)
+                for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
+                    v = np.zeros(spec.n)
+                    v[ok] = K[o[ok], c[ok], j1, j2]
+                    weights[(j, k, t)] = v
     p = Plan(spec, fin, fout, taps, weights, n_in, n_groups, 0)
     p.ras = [fin.B << k for k in range(ilog2(cn))]
     p.ras_g = [fin.stride(k) for k in range(ilog2(m))]
     if spec.s == 1:
         p.n_out = n_groups
-        if m > 1:
-            p.mask = (mu == 0).astype(np.float64)
+        if m > 1 or spec.S > 1:
+            # IR_g mask (mu = 0); PRCR also zeroes the invalid output pixels here (DESIGN R-PRCR)
+            keep = (mu == 0) & (out_ok if spec.S > 1 else True)
+            p.mask = keep.astype(np.float64)
             p.ir_g = [-fin.stride(k) for k in range(ilog2(m))]
     else:
         p.n_out = n_groups // 2
@@ -269,8 +335,9 @@ def plan_raconv(spec: ConvSpec, K: np.ndarray, with_weights: bool = True) -> Pla
     inversely rotated plaintexts W' = Rot(W, -r_t) (DESIGN R-ALG2), then Slide_1&Sum_f as one lazy
     HRotSum, RaS_g and IR_g over the R_g bits of the output format."""
     assert spec.algo == "RA" and spec.s == 1
-    fin = Fmt("RA", spec.n, spec.wp, spec.g, spec.m, spec.d)
-    fout = Fmt("CA", spec.n, spec.wp, spec.g, spec.d, spec.m)
+    spec.check_prcr()
+    fin = Fmt("RA", spec.n, spec.wp, spec.g, spec.m, spec.d, spec.S)
+    fout = Fmt("CA", spec.n, spec.wp, spec.g, spec.d, spec.m, spec.S)
     m_out, d_out = spec.d, spec.m
     cn = fout.cn
     n_in = fin.n_ct(spec.ci)
@@ -280,20 +347,34 @@ def plan_raconv(spec: ConvSpec, K: np.ndarray, with_weights: bool = True) -> Pla
     taps = [_tap(j1, j2, spec, spec.g) for j1 in range(spec.f) for j2 in range(spec.f)]
     out_ok = (h < spec.wo) & (w < spec.wo)
     weights = {}
-    for o in range(n_out if with_weights else 0):
-        oc = o * cn * m_out + b * m_out + mu
-        for i in range(n_in):
-            c = i * spec.m + rho
-            for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
-                sh, sw = h + j1 - spec.pad, w + j2 - spec.pad
-                ok = out_ok & (sh >= 0) & (sh < spec.w) & (sw >= 0) & (sw < spec.w) & (c < spec.ci) & (oc < spec.co)
-                v = np.zeros(spec.n)
-                v[ok] = K[oc[ok], c[ok], j1, j2]
-                weights[(o, i, t)] = np.roll(v, taps[t])   # W' = Rot_{-r_t}(W): W'[p] = W[p - r_t]
+    if spec.S == 1:
+        for o in range(n_out if with_weights else 0):
+            oc = o * cn * m_out + b * m_out + mu
+            for i in range(n_in):
+                c = i * spec.m + rho
+                for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
+                    sh, sw = h + j1 - spec.pad, w + j2 - spec.pad
+                    ok = out_ok & (sh >= 0) & (sh < spec.w) & (sw >= 0) & (sw < spec.w) & (c < spec.ci) & (oc < spec.co)
+                    v = np.zeros(spec.n)
+                    v[ok] = K[oc[ok], c[ok], j1, j2]
+                    weights[(o, i, t)] = np.roll(v, taps[t])   # W' = Rot_{-r_t}(W): W'[p] = W[p - r_t]
+    else:
+        # PRCR: one plaintext per output family k (member-0 channel view, no pixel masks); the
+        # inverse rotation of Alg. 2 and the member's fragment shift become one PRot (DESIGN R-PRCR)
+        for k in range(n_out // spec.S if with_weights else 0):
+            oc = k * cn * spec.S * m_out + fout.segment() * m_out + mu
+            for i in range(n_in):
+                c = i * spec.m + rho
+                ok = (c < spec.ci) & (oc < spec.co)
+                for t, (j1, j2) in enumerate((a, bb) for a in range(spec.f) for bb in range(spec.f)):
+                    v = np.zeros(spec.n)
+                    v[ok] = K[oc[ok], c[ok], j1, j2]
+                    weights[(k, i, t)] = v
     p = Plan(spec, fin, fout, taps, weights, n_in, n_out, n_out)
     p.ras_g = [fout.stride(ilog2(m_out) + k) for k in range(ilog2(d_out))]
-    if d_out > 1:
-        p.mask = (rho == 0).astype(np.float64)
+    if d_out > 1 or spec.S > 1:
+        keep = (rho == 0) & (out_ok if spec.S > 1 else True)
+        p.mask = keep.astype(np.float64)
         p.ir_g = [-s for s in p.ras_g]
     p.counts = {"Slide": len([r for r in taps if r != 0]) * n_out, "RaS": 0, "RaS_g": len(p.ras_g) * n_out,
                 "IR_g": len(p.ir_g) * n_out, "PMult": n_out * n_in * spec.f * spec.f}
@@ -316,7 +397,7 @@ def simulate(plan: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
             acc = np.zeros(sp.n)
             for i in range(plan.n_in):
                 for t in range(len(plan.taps)):
-                    acc = acc + slid[i][t] * plan.weights[(j, i, t)]
+                    acc = acc + slid[i][t] * plan.effective(j, i, t)
             for r in plan.ras:
                 acc = acc + rot(acc, r)
             for r in plan.ras_g:
@@ -342,7 +423,7 @@ def simulate(plan: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
         return outs
     outs = []
     for o in range(plan.n_out):
-        accs = [sum(xs[i] * plan.weights[(o, i, t)] for i in range(plan.n_in)) for t in range(len(plan.taps))]
+        accs = [sum(xs[i] * plan.effective(o, i, t) for i in range(plan.n_in)) for t in range(len(plan.taps))]
         out = sum(rot(a, r) for a, r in zip(accs, plan.taps))
         for r in plan.ras_g:
             out = out + rot(out, r)
@@ -380,6 +461,23 @@ class EncConv:
     def encode(self, v, level):
         return self.o.encode(v, self.o.q[level], level)
 
+    def prot(self, pt, r):
+        """PRot: plaintext rotation by r = the automorphism kappa_{5^r} of the plaintext polynomial,
+        done the obvious way (iNTT, coefficient map, NTT) limb by limb."""
+        import oracle as _o
+        if r % self.o.n == 0:
+            return pt
+        k = self.o.galois_elt(r)
+        data = np.stack([self.o.ntt(self.o.automorph_coeff(self.o.intt(pt.data[i], i), i, k), i)
+                         for i in range(pt.level + 1)])
+        return _o.Pt(data, pt.level, pt.scale)
+
+    def weight(self, wpts, cache, grp, i, t):
+        key, pr = self.plan.wkey(grp, i, t)
+        if (key, pr) not in cache:
+            cache[(key, pr)] = self.prot(wpts[key], pr)
+        return cache[(key, pr)]
+
     def run(self, cts, outputs=None):
         """outputs: optional list of output ciphertext indices to compute (sampling); default all."""
         o, p, sp = self.o, self.plan, self.plan.spec
@@ -389,7 +487,9 @@ class EncConv:
             grp = set(outs_wanted) if sp.s == 1 else {g for J in outs_wanted for g in (2 * J, 2 * J + 1)}
         else:
             grp = set(outs_wanted)
-        wpts = {k: self.encode(v, level) for k, v in p.weights.items() if k[0] in grp}
+        need = {p.wkey(g, i, t)[0] for g in grp for i in range(p.n_in) for t in range(len(p.taps))}
+        wpts = {k: self.encode(v, level) for k, v in p.weights.items() if k in need}
+        cache = {}
         if sp.algo == "CA":
             rs = [r for r in p.taps]
             slid = []
@@ -402,7 +502,7 @@ class EncConv:
                 acc = None
                 for i in range(p.n_in):
                     for t in range(len(rs)):
-                        term = o.pmult(slid[i][t], wpts[(j, i, t)])
+                        term = o.pmult(slid[i][t], self.weight(wpts, cache, j, i, t))
                         acc = term if acc is None else o.add(acc, term)
                 acc = o.rescale(acc)
                 acc = self.ras(acc, p.ras)
@@ -432,7 +532,7 @@ class EncConv:
             for t in range(len(p.taps)):
                 acc = None
                 for i in range(p.n_in):
-                    term = o.pmult(cts[i], wpts[(oo, i, t)])
+                    term = o.pmult(cts[i], self.weight(wpts, cache, oo, i, t))
                     acc = term if acc is None else o.add(acc, term)
                 accs.append(acc)
             keys = [self.key(r) if r % o.n else None for r in p.taps]

@@ -114,3 +114,31 @@ def test_siso_totals_resnet20_and_resnet18():
         p = H.plan_caconv(s, K, False) if s.algo == "CA" else H.plan_raconv(s, K, False)
         total += p.counts["Slide"]
     assert len(r18) == 16 and total == 1024
+
+
+# PRCR: ResNet-18-like layers with |S| row segments (DESIGN R-PRCR)
+PRCR = {
+    "r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8),
+    "r18_L1_ra_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "RA", S=8),
+    "r18_L2_ca_S4": H.ConvSpec(128, 128, 28, 3, 1, 64, 2, 2, 2, "CA", S=4),
+    "r18_L2_ra_S4": H.ConvSpec(128, 128, 28, 3, 1, 64, 2, 2, 2, "RA", S=4),
+    "toy_ca_S2": H.ConvSpec(8, 8, 6, 3, 1, 8, 1, 1, 1, "CA", n=2048, S=2),
+    "r18_L4_ca_S8": H.ConvSpec(512, 512, 7, 3, 1, 64, 8, 8, 8, "CA", S=8),
+}
+
+
+@pytest.mark.parametrize("name", list(PRCR))
+def test_prcr_plan_equals_conv2d(name):
+    spec = PRCR[name]
+    X, K, plan, ys = _run(spec, 3)
+    got = H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo)
+    assert not np.isnan(got).any()
+    assert np.max(np.abs(got - H.conv2d(X, K))) < 1e-9
+    # weight plaintexts / S (one plaintext reused |S| times), same rotation counts
+    plain = H.ConvSpec(**{**spec.__dict__, "S": 1})
+    p0 = (H.plan_caconv if spec.algo == "CA" else H.plan_raconv)(plain, K, with_weights=False)
+    n_pt_plain = p0.n_groups * p0.n_in * spec.f ** 2
+    if spec.ci % (plan.fin.cn * spec.S * spec.m) == 0:   # full families: same work, weights / S
+        assert len(plan.weights) * spec.S == n_pt_plain
+        assert plan.counts == p0.counts
+    assert plan.mask is not None

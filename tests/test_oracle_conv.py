@@ -31,7 +31,9 @@ def run_encrypted(o, spec, seed, level):
     H.ConvSpec(8, 8, 8, 3, 1, 8, 1, 2, 1, "RA", n=2048),   # RaS_g + IR_g over R_g
     H.ConvSpec(8, 8, 4, 3, 1, 8, 2, 2, 4, "CA", n=2048),   # gap 2: RaS_g + mask + IR_g over C_g
     H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048),   # dsconv: gap 1 -> 2
-], ids=["C1_raconv", "caconv_11", "caconv_12", "raconv_21", "caconv_g2", "dsconv"])
+    H.ConvSpec(64, 8, 6, 3, 1, 8, 1, 1, 1, "CA", n=2048, S=2),   # PRCR CAConv (full family)
+    H.ConvSpec(8, 64, 6, 3, 1, 8, 1, 1, 1, "RA", n=2048, S=2),   # PRCR RAConv
+], ids=["C1_raconv", "caconv_11", "caconv_12", "raconv_21", "caconv_g2", "dsconv", "prcr_ca", "prcr_ra"])
 def test_encrypted_conv_matches_conv2d(orc_toy, spec):
     o = orc_toy
     got, want, outs, plan = run_encrypted(o, spec, 5, o.nq - 1)
