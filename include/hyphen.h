@@ -186,6 +186,11 @@ typedef struct {
   uint32_t gap;      /* input gap g */
   uint32_t m, d;     /* |C_g|, |R_g| of the INPUT format */
   uint32_t algo;     /* hy_conv_algo */
+  uint32_t segments; /* PRCR |S|; 0 or 1 = off.  With S > 1 (DESIGN R-PRCR): the CA side
+                        is pi_CA' -- ciphertexts in families of S, member im holding at global row
+                        segment G (F = wp^2/S slots) rows of channel k c_n S m + ((G + im) mod c_n S) m + mu;
+                        one weight plaintext per family, used as PRot(P, shift); needs S | wp/gap,
+                        e = 1, stride 1, wp/gap >= w + (f-1)/2; adds an output-valid mask step. */
 } hy_conv_spec;
 typedef struct hy_conv_plan hy_conv_plan;
 /* Rotation amounts, weight/mask plaintext contents and counts for one layer.  Errors:

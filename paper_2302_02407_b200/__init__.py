@@ -37,7 +37,8 @@ class _Params(C.Structure):
 
 
 class _ConvSpec(C.Structure):
-    _fields_ = [(k, C.c_uint32) for k in ("ci", "co", "w", "f", "stride", "wp", "gap", "m", "d", "algo")]
+    _fields_ = [(k, C.c_uint32) for k in ("ci", "co", "w", "f", "stride", "wp", "gap", "m", "d", "algo",
+                                          "segments")]
 
 
 _lib = None
@@ -320,12 +321,12 @@ class ConvPlan:
 
     CA, RA = 0, 1
 
-    def __init__(self, ctx, ci, co, w, f, stride, wp, gap, m, d, algo, log_n=None):
+    def __init__(self, ctx, ci, co, w, f, stride, wp, gap, m, d, algo, log_n=None, S=1):
         """ctx may be None (host-only plan inspection) when log_n is given."""
         self.ctx = ctx
         self.n = 1 << ((log_n if log_n is not None else ctx.log_n) - 1)
         self.algo = {"CA": 0, "RA": 1}.get(algo, algo)
-        spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo)
+        spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo, S)
         h = C.c_void_p()
         _check(lib().hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
         self._p = h

@@ -57,6 +57,15 @@ __device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const PrimeC
 
 __device__ __forceinline__ uint32_t bitrev32(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
+// NTT-domain index permutation of the automorphism kappa_k: out[p] = in[perm(p)],
+// 2 br(perm(p)) + 1 = (2 br(p) + 1) k mod 2N.  Used for ciphertext rotations and for PRot of
+// plaintexts fused into their consumers as a gather.
+__device__ __forceinline__ uint32_t aut_index(uint32_t p, uint64_t k, int logN) {
+  uint32_t e = 2 * bitrev32(p, logN) + 1;
+  uint32_t e2 = (uint32_t)(((uint64_t)e * k) & ((2ull << logN) - 1));
+  return bitrev32((e2 - 1) >> 1, logN);
+}
+
 // ---------------------------------------------------------------- FP64-pipe modular arithmetic
 // Residues of primes q < 2^48 are exact doubles.  B200 issues FP64 FMA at full
 // rate (64/clk/SM, measured 18.2 TFMA/s), so the NTT butterflies run on the FP64

@@ -29,7 +29,9 @@ bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
 struct Layout {
   bool ca;
   int64_t n, wp, g, m, d;
+  int64_t S = 1;  // PRCR row segments (pi_CA' when ca && S > 1)
   int64_t I() const { return wp * wp; }
+  int64_t F() const { return I() / S; }  // slots per row segment (fragment)
   int64_t e() const { return m * d / (g * g); }
   int64_t B() const { return e() * I(); }
   int64_t cn() const { return n / B(); }
@@ -50,10 +52,18 @@ struct Layout {
   }
   int64_t mu(int64_t kappa) const { return ca ? kappa % m : kappa / d; }
   int64_t rho(int64_t kappa) const { return ca ? kappa / m : kappa % d; }
-  int64_t channel(int64_t ct, const Pos& p) const {
-    return ca ? ct * cn() * m + p.b * m + mu(p.kappa) : ct * m + mu(p.kappa);
+  // pi_CA' (PRCR): member im of family k holds, at global row segment G = slot / F, rows of channel
+  // k c_n S m + ((G + im) mod c_n S) m + mu -- fragments organised circularly
+  int64_t channel(int64_t ct, const Pos& p, int64_t slot) const {
+    if (!ca) return ct * m + mu(p.kappa);
+    if (S > 1) {
+      const int64_t fam = ct / S, im = ct % S, G = slot / F();
+      return fam * cn() * S * m + ((G + im) % (cn() * S)) * m + mu(p.kappa);
+    }
+    return ct * cn() * m + p.b * m + mu(p.kappa);
   }
   int64_t cts_for(int64_t c) const {
+    if (ca && S > 1) return S * ((c + cn() * S * m - 1) / (cn() * S * m));
     const int64_t per = ca ? cn() * m : m;
     return (c + per - 1) / per;
   }
@@ -72,7 +82,20 @@ struct hy_conv_plan {
   int64_t combine = 0;
   std::vector<int64_t> rots;  // distinct nonzero rotation amounts mod n (key order)
   uint32_t counts[5] = {0, 0, 0, 0, 0};
-  int64_t n_pt() const { return n_groups * n_in * (int64_t)s.f * s.f; }
+  int64_t S = 1;              // PRCR segments
+  int64_t f2() const { return (int64_t)s.f * s.f; }
+  // stored weight plaintexts: CA [group][input or family][tap]; RA [output or family][input][tap]
+  int64_t n_w_in() const { return s.algo == HY_CONV_CA ? n_in / S : n_in; }
+  int64_t n_w_grp() const { return s.algo == HY_CONV_CA ? n_groups : n_groups / S; }
+  int64_t n_pt() const { return n_w_grp() * n_w_in() * f2(); }
+  // (stored plaintext index, PRot amount) of term (group/output grp, input ct i, tap t):
+  // PRCR shares one plaintext per family, member im using PRot(P, r_t + im F) on the CA input
+  // side and PRot(P, im F - r_t) on the RA output side (DESIGN R-PRCR)
+  std::pair<int64_t, int64_t> term(int64_t grp, int64_t i, int64_t t) const {
+    if (S == 1) return {(grp * n_in + i) * f2() + t, 0};
+    if (s.algo == HY_CONV_CA) return {(grp * n_w_in() + i / S) * f2() + t, taps[t] + (i % S) * in.F()};
+    return {((grp / S) * n_in + i) * f2() + t, (grp % S) * out.F() - taps[t]};
+  }
 };
 
 namespace {
@@ -89,7 +112,8 @@ void weight_slots(const hy_conv_plan& p, const double* K, int64_t idx, double* v
     for (int64_t x = 0; x < p.n; ++x) {
       bool keep;
       if (s.algo == HY_CONV_CA && s.stride == 1) {
-        keep = p.in.mu(p.in.at(x).kappa) == 0;
+        const Layout::Pos q = p.in.at(x);
+        keep = p.in.mu(q.kappa) == 0 && (p.S == 1 || (q.h < p.wo && q.w < p.wo));  // PRCR: valid outputs
       } else if (s.algo == HY_CONV_CA) {  // dsconv: new-cell bits [0, lg m), lg g, 2 lg g + 1 all zero
         const int64_t k2 = p.out.at(x).kappa;
         const int lgg = lg2(s.gap);
@@ -97,16 +121,37 @@ void weight_slots(const hy_conv_plan& p, const double* K, int64_t idx, double* v
         for (int k = 0; k < lg2(s.m); ++k) keep &= !((k2 >> k) & 1);
         keep &= !((k2 >> lgg) & 1) && !((k2 >> (2 * lgg + 1)) & 1);
       } else {
-        keep = p.out.rho(p.out.at(x).kappa) == 0;
+        const Layout::Pos q = p.out.at(x);
+        keep = p.out.rho(q.kappa) == 0 && (p.S == 1 || (q.h < p.wo && q.w < p.wo));
       }
       v[x] = keep ? 1.0 : 0.0;
     }
     return;
   }
-  const int64_t t = idx % f2, i = (idx / f2) % p.n_in, grp = idx / f2 / p.n_in;
+  const int64_t t = idx % f2, i = (idx / f2) % p.n_w_in(), grp = idx / f2 / p.n_w_in();
   const int j1 = (int)(t / s.f), j2 = (int)(t % s.f);
   auto K_at = [&](int64_t o, int64_t c) { return K[((o * s.ci + c) * s.f + j1) * s.f + j2]; };
   std::fill(v, v + p.n, 0.0);
+  if (p.S > 1) {
+    // PRCR: member-0 view, no pixel masks -- out-of-image sources read zero padding and invalid
+    // outputs are zeroed by the mask step (DESIGN R-PRCR).  CA: grp = group, i = family;
+    // RA: grp = output family, i = input ciphertext.
+    for (int64_t x = 0; x < p.n; ++x) {
+      const int64_t G = x / p.in.F();
+      if (s.algo == HY_CONV_CA) {
+        const Layout::Pos q = p.in.at(x);
+        const int64_t mu = p.in.mu(q.kappa), rho = p.in.rho(q.kappa);
+        const int64_t c = i * p.in.cn() * p.S * s.m + G * s.m + mu, o = grp * s.d + rho;
+        if (c < s.ci && o < s.co) v[x] = K_at(o, c);
+      } else {
+        const Layout::Pos q = p.out.at(x);
+        const int64_t mu = p.out.mu(q.kappa), rho = p.out.rho(q.kappa);
+        const int64_t oc = grp * p.out.cn() * p.S * p.out.m + G * p.out.m + mu, c = i * s.m + rho;
+        if (c < s.ci && oc < s.co) v[x] = K_at(oc, c);
+      }
+    }
+    return;
+  }
   if (s.algo == HY_CONV_CA) {
     for (int64_t x = 0; x < p.n; ++x) {
       const Layout::Pos q = p.in.at(x);
@@ -183,8 +228,20 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
     delete p;
     return fail(HY_E_CAPACITY, "channel block does not divide the slot count");
   }
+  p->S = s.segments > 1 ? s.segments : 1;
+  if (p->S > 1) {  // PRCR preconditions (DESIGN R-PRCR)
+    const char* why = nullptr;
+    if (!pow2(p->S) || (s.wp / s.gap) % p->S) why = "PRCR: |S| must be a power of two dividing wp/gap";
+    else if (e != 1) why = "PRCR: needs m d = g^2 (e = 1)";
+    else if (s.stride != 1) why = "PRCR: stride 1 only";
+    else if ((int64_t)s.wp / s.gap < (int64_t)s.w + p->pad) why = "PRCR: needs (f-1)/2 rows/columns of zero padding";
+    if (why) {
+      delete p;
+      return fail(HY_E_FORMAT, why);
+    }
+  }
   if (s.algo == HY_CONV_CA) {
-    p->in = Layout{true, p->n, s.wp, s.gap, s.m, s.d};
+    p->in = Layout{true, p->n, s.wp, s.gap, s.m, s.d, p->S};
     if (s.stride == 1) {
       p->out = Layout{false, p->n, s.wp, s.gap, s.d, s.m};
     } else {
@@ -201,9 +258,8 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
     for (int k = 0; k < lg2(s.m); ++k) p->ras_g.push_back(p->in.stride(k));
     if (s.stride == 1) {
       p->n_out = p->n_groups;
-      p->has_mask = s.m > 1;
-      if (p->has_mask)
-        for (int k = 0; k < lg2(s.m); ++k) p->ir_g.push_back(-p->in.stride(k));
+      p->has_mask = s.m > 1 || p->S > 1;  // PRCR also zeroes invalid output pixels in the mask step
+      for (int k = 0; k < lg2(s.m); ++k) p->ir_g.push_back(-p->in.stride(k));
     } else {
       const int lgg = lg2(s.gap);
       p->n_out = p->n_groups / 2;
@@ -217,14 +273,13 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
       delete p;
       return fail(HY_E_FORMAT, "RAConv is stride 1 (downsampling happens in CAConv)");
     }
-    p->in = Layout{false, p->n, s.wp, s.gap, s.m, s.d};
-    p->out = Layout{true, p->n, s.wp, s.gap, s.d, s.m};
+    p->in = Layout{false, p->n, s.wp, s.gap, s.m, s.d, p->S};
+    p->out = Layout{true, p->n, s.wp, s.gap, s.d, s.m, p->S};
     p->n_in = p->in.cts_for(s.ci);
     p->n_out = p->n_groups = p->out.cts_for(s.co);
     for (int k = 0; k < lg2(p->out.d); ++k) p->ras_g.push_back(p->out.stride(lg2(p->out.m) + k));
-    p->has_mask = p->out.d > 1;
-    if (p->has_mask)
-      for (int64_t r : p->ras_g) p->ir_g.push_back(-r);
+    p->has_mask = p->out.d > 1 || p->S > 1;
+    for (int64_t r : p->ras_g) p->ir_g.push_back(-r);
   }
   for (uint32_t j1 = 0; j1 < s.f; ++j1)
     for (uint32_t j2 = 0; j2 < s.f; ++j2) p->taps.push_back(tap_amount(*p, j1, j2));
@@ -246,7 +301,7 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
   p->counts[1] = (uint32_t)(p->ras.size() * p->n_groups);
   p->counts[2] = (uint32_t)(p->ras_g.size() * p->n_groups);
   p->counts[3] = (uint32_t)(p->ir_g.size() * p->n_out + (p->has_combine ? p->n_out : 0));
-  p->counts[4] = (uint32_t)p->n_pt();
+  p->counts[4] = (uint32_t)(p->n_groups * p->n_in * p->f2());  // PMult terms (PRCR reuses plaintexts)
   *out = p;
   return HY_OK;
 }
@@ -333,8 +388,15 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
   const size_t ct_l = 2 * (level + 1) * N;
   const uint64_t* wpt = pts;                                       // [n_pt][level+1][N]
   const uint64_t* mask = pts + (size_t)p->n_pt() * (level + 1) * N;  // [level][N]
-  auto W = [&](int64_t grp, int64_t i, int64_t t) { return wpt + (size_t)((grp * p->n_in + i) * f2 + t) * (level + 1) * N; };
+  // term (group/output grp, input i, tap t) -> stored plaintext and the Galois element of its PRot
   std::vector<const uint64_t*> cts, ps;
+  std::vector<uint64_t> pk;
+  auto add_term = [&](const uint64_t* ct, int64_t grp, int64_t i, int64_t t) {
+    const auto tm = p->term(grp, i, t);
+    cts.push_back(ct);
+    ps.push_back(wpt + (size_t)tm.first * (level + 1) * N);
+    pk.push_back(hy_galois_elt(c, tm.second));
+  };
   hy_status stt;
   if (p->s.algo == HY_CONV_CA) {
     // Slide_f: hoisted rotations of every input
@@ -382,12 +444,10 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
     for (size_t g = 0; g < G; ++g) {                              // MulFilter&Sum_f, rescale
       cts.clear();
       ps.clear();
+      pk.clear();
       for (int64_t i = 0; i < p->n_in; ++i)
-        for (size_t t = 0; t < f2; ++t) {
-          cts.push_back(slid[i][t]);
-          ps.push_back(W(grps[g], i, t));
-        }
-      stt = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, acc, 0, stream);
+        for (size_t t = 0; t < f2; ++t) add_term(slid[i][t], grps[g], i, t);
+      stt = pmult_acc_prot(c, cts.data(), ps.data(), pk.data(), (uint32_t)cts.size(), level, acc, 0, stream);
       if (stt == HY_OK) stt = hy_rescale(c, acc, level, gp[g], stream);
       if (stt != HY_OK) return stt;
     }
@@ -442,11 +502,10 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
     for (size_t t = 0; t < f2; ++t) {
       cts.clear();
       ps.clear();
-      for (int64_t i = 0; i < p->n_in; ++i) {
-        cts.push_back(in[i]);
-        ps.push_back(W(o, i, t));
-      }
-      stt = hy_pmult_acc(c, cts.data(), ps.data(), (uint32_t)cts.size(), level, accs + t * ct_l, 0, stream);
+      pk.clear();
+      for (int64_t i = 0; i < p->n_in; ++i) add_term(in[i], o, i, t);
+      stt = pmult_acc_prot(c, cts.data(), ps.data(), pk.data(), (uint32_t)cts.size(), level, accs + t * ct_l, 0,
+                           stream);
       if (stt != HY_OK) return stt;
     }
     stt = hy_hrot_sum(c, keys.data(), acc_ptrs.data(), level, rs.data(), (uint32_t)f2, tmp, stream);

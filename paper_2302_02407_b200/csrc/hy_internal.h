@@ -123,6 +123,9 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
                      cudaStream_t s);
 // workspace bytes of one batched key-switch item at `level`
 size_t ks_item_bytes(const hy_ctx* c, uint32_t level);
+// out (+)= sum_i ct_i (.) PRot_{k_i}(pt_i), k_i Galois elements (1 = none), PRot fused as a gather (hy_ops.cu)
+hy_status pmult_acc_prot(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, const uint64_t* ks,
+                         uint32_t n, uint32_t level, uint64_t* out, int accumulate, void* stream);
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
 
 // Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).

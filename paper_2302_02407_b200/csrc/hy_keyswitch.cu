@@ -20,15 +20,6 @@
 #include "hy_arith.cuh"
 
 namespace hy {
-
-// NTT-domain index permutation of kappa_k: out[p] = in[perm(p)],
-// 2 br(perm(p)) + 1 = (2 br(p) + 1) k mod 2N.
-__device__ __forceinline__ uint32_t aut_index(uint32_t p, uint64_t k, int logN) {
-  uint32_t e = 2 * bitrev32(p, logN) + 1;
-  uint32_t e2 = (uint32_t)(((uint64_t)e * k) & ((2ull << logN) - 1));
-  return bitrev32((e2 - 1) >> 1, logN);
-}
-
 namespace {
 
 constexpr int kT = 256;

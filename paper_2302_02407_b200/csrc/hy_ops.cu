@@ -16,10 +16,11 @@ constexpr int kMaxTerms = 64;
 struct TermPtrs {
   const uint64_t* ct[kMaxTerms];
   const uint64_t* pt[kMaxTerms];
+  uint64_t prot[kMaxTerms];  // Galois element of a PRot applied to pt (1 = none), fused as a gather
 };
 
 // out[p][i][x] (+)= sum_m ct_m[p][i][x] * pt_m[i][x] mod q_i.  grid (N/256, l+1, 2)
-__global__ void k_pmult_acc(TermPtrs tp, int nterm, uint64_t* __restrict__ out, DevTables dt, int level, int logN,
+__global__ void k_pmult_acc(const __grid_constant__ TermPtrs tp, int nterm, uint64_t* __restrict__ out, DevTables dt, int level, int logN,
                             int accumulate) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -28,7 +29,10 @@ __global__ void k_pmult_acc(TermPtrs tp, int nterm, uint64_t* __restrict__ out, 
   const size_t o = ((size_t)p * n + i) * N + x;
   const PrimeConst& pc = dt.pc[i];
   U128 acc{0, 0};
-  for (int m = 0; m < nterm; ++m) mac(acc, tp.ct[m][o], tp.pt[m][(size_t)i * N + x]);
+  for (int m = 0; m < nterm; ++m) {
+    const uint32_t xs = tp.prot[m] != 1 ? aut_index(x, tp.prot[m], logN) : x;
+    mac(acc, tp.ct[m][o], tp.pt[m][(size_t)i * N + xs]);
+  }
   uint64_t r = reduce128(acc, pc);
   if (accumulate) r = add_mod(r, out[o], pc.q);
   out[o] = r;
@@ -177,8 +181,10 @@ hy_status secret_ntt(hy_ctx* c, uint64_t seed, uint32_t nlimb, uint64_t* out, in
 
 using namespace hy;
 
-extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, uint32_t n,
-                                  uint32_t level, uint64_t* out, int accumulate, void* stream) {
+namespace hy {
+// out (+)= sum_i ct_i (.) PRot_{k_i}(pt_i)   (k_i = Galois element, 1 = no rotation)
+hy_status pmult_acc_prot(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, const uint64_t* ks,
+                         uint32_t n, uint32_t level, uint64_t* out, int accumulate, void* stream) {
   if (!c || !cts || !pts || !out) return fail(HY_E_ARG, "null");
   if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
   if (n == 0 && !accumulate) return fail(HY_E_ARG, "empty product sum");
@@ -190,6 +196,7 @@ extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const u
     for (uint32_t i = 0; i < m; ++i) {
       tp.ct[i] = cts[done + i];
       tp.pt[i] = pts[done + i];
+      tp.prot[i] = ks ? ks[done + i] : 1;
       if (!tp.ct[i] || !tp.pt[i]) return fail(HY_E_ARG, "null term");
     }
     dim3 g(c->N / kT, level + 1, 2);
@@ -199,6 +206,12 @@ extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const u
     done += m;
   }
   return cuda_check("hy_pmult_acc");
+}
+}  // namespace hy
+
+extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, uint32_t n,
+                                  uint32_t level, uint64_t* out, int accumulate, void* stream) {
+  return hy::pmult_acc_prot(c, cts, pts, nullptr, n, level, out, accumulate, stream);
 }
 
 extern "C" hy_status hy_pmult(hy_ctx* c, const uint64_t* ct, const uint64_t* pt, uint32_t level, uint64_t* out,

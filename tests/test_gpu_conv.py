@@ -32,8 +32,9 @@ def ctx_hyp():
 
 def gpu_layer(ctx, spec, X, K, level, scale, out_begin=0, out_end=None):
     import paper_2302_02407_b200 as hy
-    p = hy.ConvPlan(ctx, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo)
-    fin = H.Fmt("CA" if spec.algo == "CA" else "RA", spec.n, spec.wp, spec.g, spec.m, spec.d)
+    p = hy.ConvPlan(ctx, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo,
+                    S=spec.S)
+    fin = H.Fmt("CA" if spec.algo == "CA" else "RA", spec.n, spec.wp, spec.g, spec.m, spec.d, spec.S)
     cts = [ctx.encrypt(SK, 900, i, ctx.encode(v, scale, level), level) for i, v in enumerate(H.pack(X, fin))]
     evks = {r: ctx.keygen_rot(SK, EK, r) for r in p.rots}
     pts = p.encode_weights(K, level)
@@ -60,10 +61,13 @@ TOY = [
     H.ConvSpec(8, 8, 4, 3, 1, 8, 2, 2, 4, "CA", n=2048),
     H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048),
     H.ConvSpec(4, 8, 8, 1, 2, 8, 1, 1, 2, "CA", n=2048),
+    H.ConvSpec(64, 8, 6, 3, 1, 8, 1, 1, 1, "CA", n=2048, S=2),
+    H.ConvSpec(8, 64, 6, 3, 1, 8, 1, 1, 1, "RA", n=2048, S=2),
 ]
 
 
-@pytest.mark.parametrize("spec", TOY, ids=["C1_raconv", "ca11", "ca12", "ra21", "ca_g2", "dsconv", "pconv"])
+@pytest.mark.parametrize("spec", TOY, ids=["C1_raconv", "ca11", "ca12", "ra21", "ca_g2", "dsconv", "pconv",
+                                           "prcr_ca", "prcr_ra"])
 def test_toy_layers_bit_exact(ctx_toy, orc_toy, spec):
     level = orc_toy.nq - 1
     X = synth.image(11, spec.ci, spec.w)
@@ -80,9 +84,12 @@ def test_toy_layers_bit_exact(ctx_toy, orc_toy, spec):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10
 
 
-@pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1])])
-def test_resnet20_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
-    spec = R20[name]
+R18_PRCR = {"r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8)}
+
+
+@pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1]), ("r18_L1_ca_S8", [5])])
+def test_resnet_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
+    spec = R20[name] if name in R20 else R18_PRCR[name]
     level = 9 if spec.algo == "CA" else 6      # l+1 = 10 for CAConv, 7 for RAConv (DESIGN R-LEVELS)
     X = synth.image(21, spec.ci, spec.w)
     K = synth.conv_weight(22, spec.co, spec.ci, spec.f)

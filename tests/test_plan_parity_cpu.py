@@ -5,7 +5,7 @@ import pytest
 
 import synth
 from oracle import hyphen as H
-from test_hyphen_plan import R20
+from test_hyphen_plan import PRCR, R20
 
 
 @pytest.fixture(scope="module")
@@ -20,6 +20,7 @@ CASES = dict(R20)
 CASES["C1_raconv"] = H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048)
 CASES["toy_dsconv"] = H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048)
 CASES["r18_L4_ra"] = H.ConvSpec(512, 512, 7, 3, 1, 64, 8, 8, 8, "RA")
+CASES.update(PRCR)
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -27,7 +28,7 @@ def test_plan_matches_oracle(hy, name):
     s = CASES[name]
     K = synth.conv_weight(7, s.co, s.ci, s.f)
     log_n = (2 * s.n).bit_length() - 1
-    p = hy.ConvPlan(None, s.ci, s.co, s.w, s.f, s.s, s.wp, s.g, s.m, s.d, s.algo, log_n=log_n)
+    p = hy.ConvPlan(None, s.ci, s.co, s.w, s.f, s.s, s.wp, s.g, s.m, s.d, s.algo, log_n=log_n, S=s.S)
     big = s.ci * s.co > 64 * 64
     o = (H.plan_caconv if s.algo == "CA" else H.plan_raconv)(s, K, with_weights=not big)
     assert (p.n_in, p.n_out) == (o.n_in, o.n_out)
