@@ -198,10 +198,23 @@ R20_LAYERS = [
 ]
 CA_LEVEL, RA_LEVEL = 9, 6  # l+1 = 10 / 7 limbs (DESIGN R-LEVELS)
 
+# ResNet-18 ImageNet stride-1 conv layers with PRCR |S| = 8, plan (1,1)/(2,2)/(4,4)/(8,8)
+# (P:1164), widths 56/28/14/7 padded to 64/32/16/8 per gap (W_p = 64).  Multiplicity = 3x3 convs of each type.
+R18_LAYERS = [
+    ("L1_ca", (64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", 8), 2),
+    ("L1_ra", (64, 64, 56, 3, 1, 64, 1, 1, 1, "RA", 8), 2),
+    ("L2_ca", (128, 128, 28, 3, 1, 64, 2, 2, 2, "CA", 8), 1),
+    ("L2_ra", (128, 128, 28, 3, 1, 64, 2, 2, 2, "RA", 8), 2),
+    ("L3_ca", (256, 256, 14, 3, 1, 64, 4, 4, 4, "CA", 8), 1),
+    ("L3_ra", (256, 256, 14, 3, 1, 64, 4, 4, 4, "RA", 8), 2),
+    ("L4_ca", (512, 512, 7, 3, 1, 64, 8, 8, 8, "CA", 8), 1),
+    ("L4_ra", (512, 512, 7, 3, 1, 64, 8, 8, 8, "RA", 8), 2),
+]
 
-def bench_conv(ctx, ws, rank, steps, warmup, timed):
-    """Per-layer device time of every ResNet-20 conv layer type (fresh encryption at its scheduled
-    level, outputs sharded over ranks + all-gathered), and the network's conv total."""
+
+def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet-20"):
+    """Per-layer device time of every conv layer type (fresh encryption at its scheduled level,
+    outputs sharded over ranks + all-gathered), and the network's conv total."""
     import torch
 
     import paper_2302_02407_b200 as hy
@@ -211,9 +224,10 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed):
     keys = {}
     layers = {}
     total = 0.0
-    for li, (name, spec, mult) in enumerate(R20_LAYERS):
-        ci, co, w, f, s, wp, g, m, d, algo = spec
-        p = hy.ConvPlan(ctx, ci, co, w, f, s, wp, g, m, d, algo)
+    for li, (name, spec, mult) in enumerate(layers_def or R20_LAYERS):
+        ci, co, w, f, s, wp, g, m, d, algo = spec[:10]
+        S = spec[10] if len(spec) > 10 else 1
+        p = hy.ConvPlan(ctx, ci, co, w, f, s, wp, g, m, d, algo, S=S)
         level = CA_LEVEL if algo == "CA" else RA_LEVEL
         for r in p.rots:
             if r not in keys:
@@ -239,14 +253,19 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed):
 
         ms, launches = timed(step, steps, warmup)
         layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
-                        "rotations": p.counts, "gpu_launches": launches}
+                        "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S}
         total += mult * ms
         del pts, cts, outs, scratch
         torch.cuda.empty_cache()
-    return {"layers": layers, "total_ms": total, "n_gpus": ws,
-            "note": "sum over the 19 3x3 convs + 2 pconv of per-layer device time (max over ranks), each layer on a "
-                    "fresh encryption at its scheduled level; bootstrapping/activation excluded (P:1095-1101 conv "
-                    "columns: 0.52 s on A100, context only)"}
+    if net == "ResNet-20":
+        note = ("sum over the 19 3x3 convs + 2 pconv of per-layer device time (max over ranks), each layer on a "
+                "fresh encryption at its scheduled level; bootstrapping/activation excluded (P:1095-1101 conv "
+                "columns: 0.52 s on A100, context only)")
+    else:
+        note = ("sum over the 14 stride-1 3x3 convs (PRCR |S|=8) of per-layer device time; the 3 dsconv and 3 pconv "
+                "layers are not included (stride-2 weights are not PRCR-compressible in our design, DESIGN R-PRCR); "
+                "context: ResNet-18 conv 7.59 s on A100 (P:1095-1096)")
+    return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -370,11 +389,12 @@ def run_ours(args, ws, rank, local):
                "note": "H2D of the 64 input ciphertexts from pinned memory, hrot_batch, D2H of the 64 outputs; "
                        "evaluation keys are server state, resident before timing (P:1030)"}
 
-    conv = None
+    conv = conv18 = None
     if not args.no_conv:
         del evks, cts, outs, houts
         torch.cuda.empty_cache()
         conv = bench_conv(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
+        conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18")
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -394,6 +414,7 @@ def run_ours(args, ws, rank, local):
             "roofline": roof,
             "roofline_ip": roof_ip,
             "resnet20_conv": conv,
+            "resnet18_conv": conv18,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -415,7 +436,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rotations", type=int, default=2)
-    ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 conv-layer timings")
+    ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 / ResNet-18 conv-layer timings")
+    ap.add_argument("--no-r18", action="store_true", help="skip the ResNet-18 (PRCR) conv-layer timings")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
