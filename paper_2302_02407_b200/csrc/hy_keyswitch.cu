@@ -326,11 +326,17 @@ hy_status carve(hy_ctx* c, uint32_t level, int G, KsItem* it, uint64_t** acc) {
 }
 
 // how many items fit the workspace at this level (<= kG)
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 int max_items(const hy_ctx* c, uint32_t level) {
   const size_t per = item_words(c, level) * 8 + 6 * 256;
   const size_t acc = 2 * (level + 1) * (size_t)c->N * 8 + 256;
   if (c->ws_bytes <= acc) return 0;
-  return (int)std::min<size_t>(kG, (c->ws_bytes - acc) / per);
+  static const int cap = std::max(1, std::min(kG, env_int("HY_KS_BATCH", kG)));
+  return (int)std::min<size_t>(cap, (c->ws_bytes - acc) / per);
 }
 
 void automorph_batch(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* out, const uint64_t* k,
@@ -367,8 +373,10 @@ struct LimbList {
 };
 void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
   LimbBatch b;
+  // chunks small enough that pass A's output is still in L2 when pass B reads it
+  static const size_t chunk = std::max(1, std::min(kMaxBatch, env_int("HY_NTT_CHUNK", kMaxBatch)));
   for (size_t done = 0; done < L.src.size();) {
-    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
+    const size_t m = std::min<size_t>(L.src.size() - done, chunk);
     b.n = (int)m;
     for (size_t i = 0; i < m; ++i) {
       b.src[i] = L.src[done + i];
