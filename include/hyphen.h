@@ -108,7 +108,8 @@ enum {
   HY_FAM_AUT = 32,      /* automorphism gather */
   HY_FAM_ELEM = 64,     /* PMult / PMult-accumulate / add */
   HY_FAM_RESCALE = 128,
-  HY_FAM_CLIENT = 256   /* keygen / encrypt / decrypt / encode upload */
+  HY_FAM_CLIENT = 256,  /* keygen / encrypt / decrypt / encode upload */
+  HY_FAM_NTT_IP = 512   /* ModUp NTT row pass fused with the key-switch inner product */
 };
 hy_status hy_ctx_time_kernels(hy_ctx* ctx, uint32_t family_mask);
 hy_status hy_ctx_kernel_times(hy_ctx* ctx, uint32_t family_mask, double* total_ms, uint64_t* n_launches,

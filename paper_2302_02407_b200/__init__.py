@@ -192,7 +192,7 @@ class Context:
         return int(lib().hy_ctx_launch_count(self._c))
 
     FAMILIES = {"ntt_a": 1, "ntt_b": 2, "modup": 4, "ip": 8, "moddown": 16, "aut": 32, "elem": 64,
-                "rescale": 128, "client": 256}
+                "rescale": 128, "client": 256, "ntt_ip": 512}
 
     def time_kernels(self, mask: int):
         _check(lib().hy_ctx_time_kernels(self._c, mask))

@@ -109,6 +109,23 @@ struct LimbBatch {
 
 // NTT launchers (hy_ntt.cu)
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
+// forward pass A only (the column stages); the row stages are then run by launch_ntt_rows_ip
+void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s);
+
+constexpr int kG = 16;  // key switches per batched launch
+
+// Fused ModUp NTT row pass + key-switch inner product (hy_ntt.cu), per item g:
+//   u_g[c][u] (+)= sum_j NTT_rows(ext_g[j][u]) (.) evk_g[j][c][chain(u)]   (own digit: own_g[u] as is)
+// ext_g[j][u] holds the column-pass output of the digit's non-own limbs.  sum: every item accumulates
+// into u[0] (lazy HRotSum).  Items with the same evk pointer reuse the key rows through L2.
+struct RowsIpArgs {
+  const uint64_t* ext[kG];
+  const uint64_t* own[kG];
+  const uint64_t* evk[kG];
+  uint64_t* u[kG];
+};
+void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
+                        cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices
 void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
                 cudaStream_t s);
@@ -131,7 +148,7 @@ void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_l
 // Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).
 enum Family : uint32_t {
   FAM_NTT_A = 1, FAM_NTT_B = 2, FAM_MODUP = 4, FAM_IP = 8, FAM_MODDOWN = 16, FAM_AUT = 32, FAM_ELEM = 64,
-  FAM_RESCALE = 128, FAM_CLIENT = 256
+  FAM_RESCALE = 128, FAM_CLIENT = 256, FAM_NTT_IP = 512
 };
 
 inline cudaEvent_t pooled_event(hy_ctx* c) {

@@ -23,7 +23,7 @@ namespace hy {
 namespace {
 
 constexpr int kT = 256;
-constexpr int kG = 16;  // key switches per batched launch
+// kG (key switches per batched launch) lives in hy_internal.h
 
 template <class T>
 struct Arr {
@@ -387,9 +387,25 @@ void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
     done += m;
   }
 }
+void ntt_cols_list(hy_ctx* c, const LimbList& L, cudaStream_t s) {
+  LimbBatch b;
+  for (size_t done = 0; done < L.src.size();) {
+    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
+    b.n = (int)m;
+    for (size_t i = 0; i < m; ++i) {
+      b.src[i] = L.src[done + i];
+      b.dst[i] = L.dst[done + i];
+      b.chain[i] = L.chain[done + i];
+    }
+    launch_ntt_cols(c, b, s);
+    done += m;
+  }
+}
 
-// d_g: coefficient-domain [l+1][N] -> ext_g [beta][E][N] (non-own limbs, NTT domain)
-void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext, cudaStream_t s) {
+// d_g: coefficient-domain [l+1][N] -> ext_g [beta][E][N] (non-own limbs, NTT domain).
+// cols_only: stop after the NTT column pass (the row pass is fused into the IP, launch_ntt_rows_ip).
+void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext, cudaStream_t s,
+                 bool cols_only = false) {
   const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
   Arr<const uint64_t*> ad{};
   Arr<uint64_t*> ae{};
@@ -414,7 +430,29 @@ void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uin
         L.add(p, p, ext_chain(c, level, u));
       }
     }
-  ntt_list(c, L, false, s);
+  if (cols_only) ntt_cols_list(c, L, s);
+  else ntt_list(c, L, false, s);
+}
+
+// ModUp (column pass only) + fused row pass / IP of G items (hy_ntt.cu launch_ntt_rows_ip)
+void modup_ip_fused(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext,
+                    const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
+                    cudaStream_t s) {
+  modup_batch(c, level, G, d, ext, s, true);
+  RowsIpArgs ra{};
+  for (int g = 0; g < G; ++g) {
+    ra.ext[g] = ext[g];
+    ra.own[g] = own[g];
+    ra.evk[g] = evk[g];
+    ra.u[g] = u[sum ? 0 : g];
+  }
+  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s);
+}
+
+// HY_FUSE_IP=0 runs the unfused ModUp NTT + IP (kept for A/B measurements)
+bool fuse_ip() {
+  static const bool on = env_int("HY_FUSE_IP", 1) != 0;
+  return on;
 }
 
 // IP of G items.  shared: all items use evk[0]; sum: all items accumulate into u[0].
@@ -577,8 +615,12 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
     }
     automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
     intt_polys(c, G, rc1, d, level, s);
-    modup_batch(c, level, G, d, ext, s);
-    ip_batch(c, level, G, ext, rc1, keys, u, nullptr, false, shared && G > 1, false, s);
+    if (fuse_ip()) {
+      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s);
+    } else {
+      modup_batch(c, level, G, d, ext, s);
+      ip_batch(c, level, G, ext, rc1, keys, u, nullptr, false, shared && G > 1, false, s);
+    }
     moddown_batch(c, level, 2, G, di, s);
     done += G;
   }
@@ -789,9 +831,13 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
     }
     automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
     intt_polys(c, G, rc1c, d, level, s);
-    modup_batch(c, level, G, d, ext, s);
     uint64_t* u0 = it[0].u;
-    ip_batch(c, level, G, ext, rc1c, keys, &u0, nullptr, !first, false, true, s);
+    if (fuse_ip()) {
+      modup_ip_fused(c, level, G, d, ext, rc1c, keys, &u0, !first, true, s);
+    } else {
+      modup_batch(c, level, G, d, ext, s);
+      ip_batch(c, level, G, ext, rc1c, keys, &u0, nullptr, !first, false, true, s);
+    }
     first = false;
     done += G;
   }

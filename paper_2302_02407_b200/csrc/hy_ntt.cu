@@ -15,6 +15,9 @@
 // a register-local butterfly: L1 owns bits {7,6,5}, L2 {4,3,2}, L3 {1,0}.
 // Arithmetic runs on the FP64 pipe (hy_arith.cuh fmulmod): residues are loaded
 // as uint64, converted exactly to doubles, and stored back canonical in [0, q).
+#include <algorithm>
+#include <cstdlib>
+
 #include "hy_arith.cuh"
 
 namespace hy {
@@ -263,7 +266,188 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
   }
 }
 
+// ---------------------------------------------------------------- pass B fused with the key-switch IP
+// The forward row stages of one 256-word row, layout L1 in -> layout L3 out (values |v| < 13 q,
+// not canonicalised), S = the warp's transpose buffer, T = the row's twiddle heap.
+__device__ __forceinline__ void rows_forward_l3(double (&x)[8], int l, double* S, const double* T, double q,
+                                                double qinv) {
+  run_stages<1, true>(x, l, 7, 5, T, q, qinv);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
+  run_stages<2, true>(x, l, 4, 2, T, q, qinv);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
+  run_stages<3, true>(x, l, 1, 0, T, q, qinv);
+  __syncwarp();
+}
+
+// Layout L3 holds words 4(l + 32h) + m (m < 4) in x[4h + m]: two 32-byte runs per lane.
+__device__ __forceinline__ void load_l3(const uint64_t* __restrict__ p, int l, ulonglong2 (&v)[4], bool stream) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const ulonglong2* a = reinterpret_cast<const ulonglong2*>(p + 4 * (l + 32 * h) + 2 * i);
+      v[2 * h + i] = stream ? __ldcs(a) : *a;
+    }
+}
+__device__ __forceinline__ double l3_word(const ulonglong2 (&v)[4], int k) {
+  const ulonglong2 w = v[k >> 1];
+  return u2d((k & 1) ? w.y : w.x);
+}
+__device__ __forceinline__ void store_l3(uint64_t* p, int l, const double (&x)[8], double q, double qinv,
+                                         bool accumulate) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      ulonglong2* a = reinterpret_cast<ulonglong2*>(p + 4 * (l + 32 * h) + 2 * i);
+      double lo = x[4 * h + 2 * i], hi = x[4 * h + 2 * i + 1];
+      if (accumulate) {
+        const ulonglong2 o = *a;
+        lo += u2d(o.x);
+        hi += u2d(o.y);
+      }
+      *a = make_ulonglong2(d2u(fcanon(lo, q, qinv)), d2u(fcanon(hi, q, qinv)));
+    }
+}
+
+// One warp per (item g, extended limb u, row): for every digit j it runs the row stages of
+// ext_g[j][u] (the column pass already done; the own digit's limb own_g[u] is already in the NTT
+// domain) and multiplies the result, still in registers, by the evk rows of (j, c = 0, 1).  The B
+// products per word are reduced with fmulmod (|.| <= 1.5 t) and summed exactly (< 2^53), then
+// canonicalised once; the NTT'd digits never reach HBM.  The twiddle heap of (chain(u), row) is
+// loaded once and serves all B digits.  grid (G or 1 (SUM), R/8, E), CTA = 8 warps = 8 rows; the
+// item index is the fastest grid dimension so that items sharing a key hit its rows in L2.
+// SUM: one warp loops over all G items and accumulates into u[0] (each item's sum re-centred with
+// fred first), race-free because one warp owns (u, row).
+template <int B, bool SUM>
+__global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ RowsIpArgs a, int G, DevTables dt,
+                                                        int level, int n_q, int L1, int E, int alpha, int logN,
+                                                        int accumulate) {
+  __shared__ double sm[8][272];
+  __shared__ double tws[8][256];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t N = (size_t)1 << logN;
+  const int R = (int)(N >> 8);
+  const int row = blockIdx.y * 8 + w, u = blockIdx.z;
+  if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
+  const int t = u <= level ? u : n_q + (u - level - 1);
+  const PrimeConst& pc = dt.pc[t];
+  const double q = pc.qd, qinv = pc.qinv;
+  const int own_digit = u <= level ? u / alpha : -1;
+  double* S = sm[w];
+  double* T = tws[w];
+  load_twiddles(T, dt.tw + (size_t)t * N, (uint32_t)R + (uint32_t)row, l, 32);
+  __syncwarp();
+  const size_t roff = (size_t)row * 256;
+  double s0[8], s1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s0[k] = s1[k] = 0.0;
+  const int g0 = SUM ? 0 : (int)blockIdx.x, g1 = SUM ? G : g0 + 1;
+  for (int g = g0; g < g1; ++g) {
+    double a0[8], a1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < B; ++j) {
+      const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + t) * N + roff;
+      ulonglong2 k0[4], k1[4];
+      load_l3(e0, l, k0, true);
+      load_l3(e0 + (size_t)L1 * N, l, k1, true);
+      double x[8];
+      if (j == own_digit) {
+        ulonglong2 v[4];
+        load_l3(a.own[g] + (size_t)u * N + roff, l, v, false);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = l3_word(v, k);
+      } else {
+        const uint64_t* src = a.ext[g] + ((size_t)j * E + u) * N + roff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+        rows_forward_l3(x, l, S, T, q, qinv);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a0[k] += fmulmod(x[k], l3_word(k0, k), q, qinv);
+        a1[k] += fmulmod(x[k], l3_word(k1, k), q, qinv);
+      }
+    }
+    if (SUM) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        s0[k] += fred(a0[k], q, qinv);
+        s1[k] += fred(a1[k], q, qinv);
+      }
+    } else {
+      store_l3(a.u[g] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
+      store_l3(a.u[g] + ((size_t)E + u) * N + roff, l, a1, q, qinv, accumulate);
+    }
+  }
+  if (SUM) {
+    store_l3(a.u[0] + (size_t)u * N + roff, l, s0, q, qinv, accumulate);
+    store_l3(a.u[0] + ((size_t)E + u) * N + roff, l, s1, q, qinv, accumulate);
+  }
+}
+
 }  // namespace
+
+void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
+  if (b.n == 0) return;
+  const int logN = (int)c->log_n;
+  dim3 gA(256 / 16, b.n);
+  KTimer kt(c, FAM_NTT_A, s);
+  kt.bytes = 2ull * b.n * c->N * 8;
+  if (c->N == 65536) k_ntt_cols256<true><<<gA, 512, 0, s>>>(b, c->dt, logN);
+  else k_ntt_cols_small<true><<<gA, 256, 0, s>>>(b, c->dt, logN);
+}
+
+void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
+                        cudaStream_t s) {
+  if (G <= 0) return;
+  const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
+  int keys = 0;
+  for (int g = 0; g < G; ++g) {
+    bool seen = false;
+    for (int h = 0; h < g; ++h) seen |= a.evk[h] == a.evk[g];
+    keys += seen ? 0 : 1;
+  }
+  dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, E);
+  KTimer kt(c, FAM_NTT_IP, s);
+  // algorithmic bytes: every digit limb in once, each distinct key once, the outputs (read back too
+  // when accumulating)
+  const uint64_t outs = sum ? 1 : G;
+  kt.bytes = ((uint64_t)G * beta * E + (uint64_t)keys * 2 * beta * E + outs * 2 * E * (accumulate ? 2 : 1)) * c->N * 8;
+  const int L1 = (int)(c->n_q + c->n_p);
+#define HY_RIP(BB)                                                                                             \
+  case BB:                                                                                                     \
+    if (sum)                                                                                                   \
+      k_ntt_rows_ip<BB, true><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E, (int)c->alpha, \
+                                                   (int)c->log_n, accumulate ? 1 : 0);                         \
+    else                                                                                                       \
+      k_ntt_rows_ip<BB, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,              \
+                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0);         \
+    break;
+  switch (beta) {
+    HY_RIP(1)
+    HY_RIP(2)
+    HY_RIP(3)
+    HY_RIP(4)
+    HY_RIP(5)
+    HY_RIP(6)
+    HY_RIP(7)
+    default:
+      HY_RIP(8)
+  }
+#undef HY_RIP
+}
 
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
   if (b.n == 0) return;
