@@ -126,6 +126,21 @@ struct RowsIpArgs {
 };
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
                         cudaStream_t s);
+
+// Fused ModDown NTT row pass + epilogue (hy_ntt.cu), per item g and poly c < npoly:
+//   out_g[c][i] = (u_g[c][i] - NTT_rows(w_g[c][i])) P^{-1} (+ add0_g[i][kappa_k0(x)] for c = 0)
+//                 (+ add1_g[i] for c = 1) (+ addct_g[c][i]),   i <= level
+// w_g[c][i] holds the column-pass output of the P -> Q_l conversion.  out_g may alias addct_g.
+struct RowsFinalArgs {
+  const uint64_t* u[kG];
+  const uint64_t* w[kG];
+  const uint64_t* add0[kG];
+  const uint64_t* add1[kG];
+  const uint64_t* addct[kG];
+  uint64_t* out[kG];
+  uint64_t k0[kG];
+};
+void launch_ntt_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, int npoly, uint32_t level, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices
 void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
                 cudaStream_t s);

@@ -449,9 +449,13 @@ void modup_ip_fused(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, 
   launch_ntt_rows_ip(c, ra, G, level, sum, acc, s);
 }
 
-// HY_FUSE_IP=0 runs the unfused ModUp NTT + IP (kept for A/B measurements)
+// HY_FUSE_IP=0 / HY_FUSE_MD=0 run the unfused ModUp NTT + IP / ModDown NTT + epilogue (A/B measurements)
 bool fuse_ip() {
   static const bool on = env_int("HY_FUSE_IP", 1) != 0;
+  return on;
+}
+bool fuse_moddown() {
+  static const bool on = env_int("HY_FUSE_MD", 1) != 0;
   return on;
 }
 
@@ -526,6 +530,21 @@ void moddown_batch(hy_ctx* c, uint32_t level, int npoly, int G, const DownItem* 
         uint64_t* p = it[g].w + ((size_t)cc * n + i) * c->N;
         L2.add(p, p, i);
       }
+  if (fuse_moddown()) {  // column pass, then the row pass fused with the epilogue
+    ntt_cols_list(c, L2, s);
+    RowsFinalArgs ra{};
+    for (int g = 0; g < G; ++g) {
+      ra.u[g] = it[g].u;
+      ra.w[g] = it[g].w;
+      ra.add0[g] = it[g].add0;
+      ra.k0[g] = it[g].k0;
+      ra.add1[g] = it[g].add1;
+      ra.addct[g] = it[g].addct;
+      ra.out[g] = it[g].out;
+    }
+    launch_ntt_rows_final(c, ra, G, npoly, level, s);
+    return;
+  }
   ntt_list(c, L2, false, s);
   FinalArgs a{};
   uint64_t extra = 0;
@@ -593,27 +612,34 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
     const uint64_t* cin[kG];
     uint64_t* rc[kG];
     const uint64_t* rc1[kG];
+    uint64_t* rc1w[kG];
     uint64_t* d[kG];
     uint64_t* ext[kG];
     uint64_t* u[kG];
     const uint64_t* keys[kG];
     uint64_t kk[kG];
     DownItem di[kG];
-    bool shared = true;
+    bool shared = true, alias = false;
+    for (int g = 0; g < G; ++g)  // an output overwriting any input c0 of the batch forbids the late gather
+      for (int h = 0; h < G; ++h) alias |= out[ks[done + g]] == ct[ks[done + h]];
     for (int g = 0; g < G; ++g) {
       const uint32_t i = ks[done + g];
       cin[g] = ct[i];
       rc[g] = it[g].rc;
-      rc1[g] = it[g].rc + n * N;
+      rc1[g] = rc1w[g] = it[g].rc + n * N;
       d[g] = it[g].d;
       ext[g] = it[g].ext;
       u[g] = it[g].u;
       keys[g] = evk[i];
       kk[g] = hy_galois_elt(c, r[i]);
       shared &= evk[i] == evk[ks[done]];
-      di[g] = DownItem{it[g].u, out[i], it[g].rc, 1, nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w};
+      // kappa(c0) is gathered by the ModDown epilogue straight from ct (unless out aliases ct)
+      di[g] = alias ? DownItem{it[g].u, out[i], it[g].rc, 1, nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w}
+                    : DownItem{it[g].u, out[i], ct[i], kk[g], nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w};
+      if (!alias) cin[g] = ct[i] + n * N;
     }
-    automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
+    if (alias) automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
+    else automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
     intt_polys(c, G, rc1, d, level, s);
     if (fuse_ip()) {
       modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s);

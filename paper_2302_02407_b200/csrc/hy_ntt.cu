@@ -397,7 +397,76 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------- pass B fused with the ModDown epilogue
+// One warp per (item g, poly c, limb i <= level, row): the row stages of w_g[c][i] (column pass done),
+// then in layout L3: (u - w) P^{-1} (fmulmod, |u - w| < 14 q) plus the optional addends, canonicalised
+// once.  grid (R/8, l+1, npoly * G), blockIdx.z = g * npoly + c.
+__global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ RowsFinalArgs a, int npoly, int E,
+                                                        const ModDownConst* md, DevTables dt, int level, int logN) {
+  __shared__ double sm[8][272];
+  __shared__ double tws[8][256];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t N = (size_t)1 << logN;
+  const int R = (int)(N >> 8);
+  const int row = blockIdx.x * 8 + w, i = blockIdx.y;
+  const int g = blockIdx.z / npoly, c = blockIdx.z % npoly;
+  if (row >= R) return;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  double* S = sm[w];
+  double* T = tws[w];
+  load_twiddles(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l, 32);
+  const size_t roff = (size_t)row * 256;
+  const uint64_t* src = a.w[g] + ((size_t)c * (level + 1) + i) * N + roff;
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+  __syncwarp();
+  rows_forward_l3(x, l, S, T, q, qinv);
+  ulonglong2 uv[4];
+  load_l3(a.u[g] + ((size_t)c * E + i) * N + roff, l, uv, false);
+  const double pinv = (double)md->p_inv[i];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = fmulmod(l3_word(uv, k) - x[k], pinv, q, qinv);
+  if (c == 0 && a.add0[g]) {
+    const uint64_t* a0 = a.add0[g] + (size_t)i * N;
+    const uint64_t k0 = a.k0[g];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+      x[k] += u2d(a0[k0 != 1 ? aut_index(xi, k0, logN) : xi]);
+    }
+  }
+  if (c == 1 && a.add1[g]) {
+    ulonglong2 v[4];
+    load_l3(a.add1[g] + (size_t)i * N + roff, l, v, false);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+  }
+  uint64_t* o = a.out[g] + ((size_t)c * (level + 1) + i) * N + roff;
+  if (a.addct[g]) {
+    ulonglong2 v[4];
+    load_l3(a.addct[g] + ((size_t)c * (level + 1) + i) * N + roff, l, v, false);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+  }
+  store_l3(o, l, x, q, qinv, false);
+}
+
 }  // namespace
+
+void launch_ntt_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, int npoly, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  const int n = (int)level + 1, E = n + (int)c->n_p, R = (int)(c->N / 256);
+  uint64_t extra = 0;
+  for (int g = 0; g < G; ++g)
+    extra += (a.add0[g] ? n : 0) + (a.add1[g] ? n : 0) + (a.addct[g] ? (uint64_t)npoly * n : 0);
+  dim3 grid(R / 8 > 0 ? R / 8 : 1, n, npoly * G);
+  KTimer kt(c, FAM_MODDOWN, s);
+  // w (column-pass output) and u in, out written, plus the addends
+  kt.bytes = ((uint64_t)G * npoly * n * 3 + extra) * c->N * 8;
+  k_ntt_rows_final<<<grid, 256, 0, s>>>(a, npoly, E, c->d_moddown[level], c->dt, (int)level, (int)c->log_n);
+}
 
 void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
   if (b.n == 0) return;
