@@ -15,6 +15,9 @@
 // a register-local butterfly: L1 owns bits {7,6,5}, L2 {4,3,2}, L3 {1,0}.
 // Arithmetic runs on the FP64 pipe (hy_arith.cuh fmulmod): residues are loaded
 // as uint64, converted exactly to doubles, and stored back canonical in [0, q).
+// Between the two passes the limb holds the raw bits of fred-reduced doubles
+// (|v| <= q/2 + 1), so neither pass pays for canonicalisation / conversion there;
+// only the fused row kernels below and the second pass read that format.
 #include <algorithm>
 #include <cstdlib>
 
@@ -22,6 +25,10 @@
 
 namespace hy {
 namespace {
+
+// intermediate (between-pass) format: raw double bits
+__device__ __forceinline__ double raw2d(uint64_t v) { return __longlong_as_double((long long)v); }
+__device__ __forceinline__ uint64_t d2raw(double d) { return (uint64_t)__double_as_longlong(d); }
 
 template <int LAY>
 __device__ __forceinline__ int elem(int l, int k) {
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
   double* T = tws[w];
   double x[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+  for (int k = 0; k < 8; ++k) x[k] = FWD ? raw2d(src[elem<1>(l, k)]) : u2d(src[elem<1>(l, k)]);
   load_twiddles(T, W, (uint32_t)(N >> 8) + (uint32_t)row, l, 32);
   __syncwarp();
   if (FWD) {
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
     for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<1>(l, k))];
     run_stages<1, false>(x, l, 7, 5, T, q, qinv);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2u(fcanon(x[k], q, qinv));
+    for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2raw(x[k]);
   }
 }
 
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, 
     for (int k = 0; k < 8; ++k) x[k] = u2d(src[(size_t)elem<1>(l, k) * 256 + col]);
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = u2d(src[(size_t)elem<3>(l, k) * 256 + col]);
+    for (int k = 0; k < 8; ++k) x[k] = raw2d(src[(size_t)elem<3>(l, k) * 256 + col]);
   }
   load_twiddles(T, W, 1, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(512) k_ntt_cols256(LimbBatch b, DevTables dt, 
     for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
     run_stages<3, true>(x, l, 1, 0, T, q, qinv);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = d2u(fcanon(x[k], q, qinv));
+    for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256 + col] = d2raw(fred(x[k], q, qinv));
   } else {
     run_stages<3, false>(x, l, 1, 0, T, q, qinv);
 #pragma unroll
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
   const int col0 = blockIdx.x * 16;
   for (int i = threadIdx.x; i < R * 16; i += blockDim.x) {
     int r = i >> 4, c = i & 15;
-    sm[i] = u2d(src[(size_t)r * 256 + col0 + c]);
+    sm[i] = FWD ? u2d(src[(size_t)r * 256 + col0 + c]) : raw2d(src[(size_t)r * 256 + col0 + c]);
   }
   __syncthreads();
   for (int it = 0; it < logR; ++it) {
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
     int r = i >> 4, c = i & 15;
     double v = sm[i];
     if (!FWD) v = fmulmod(v, pc.n_inv_d, q, qinv);
-    dst[(size_t)r * 256 + col0 + c] = d2u(fcanon(v, q, qinv));
+    dst[(size_t)r * 256 + col0 + c] = FWD ? d2raw(v) : d2u(fcanon(v, q, qinv));
   }
 }
 
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
       } else {
         const uint64_t* src = a.ext[g] + ((size_t)j * E + u) * N + roff;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+        for (int k = 0; k < 8; ++k) x[k] = raw2d(src[elem<1>(l, k)]);
         rows_forward_l3(x, l, S, T, q, qinv);
       }
 #pragma unroll
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
   const uint64_t* src = a.w[g] + ((size_t)c * (level + 1) + i) * N + roff;
   double x[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) x[k] = u2d(src[elem<1>(l, k)]);
+  for (int k = 0; k < 8; ++k) x[k] = raw2d(src[elem<1>(l, k)]);
   __syncwarp();
   rows_forward_l3(x, l, S, T, q, qinv);
   ulonglong2 uv[4];
