@@ -141,6 +141,19 @@ struct RowsFinalArgs {
   uint64_t k0[kG];
 };
 void launch_ntt_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, int npoly, uint32_t level, cudaStream_t s);
+
+// Fused ModUp column kernel (hy_ntt.cu), per item g, digit j and 16-column strip:
+//   d_i = inverse column pass of src_g[i] (i in digit j; src_g = c1 after the inverse row pass),
+//   y_i = [d_i (D_j/q_i)^{-1}]_{q_i},  ext_g[j][u] = forward column pass of [sum_i y_i (D_j/q_i)]_{t_u}
+// for every non-own limb u; ext is left in the between-pass format for launch_ntt_rows_ip / rows.
+struct ModUpColsArgs {
+  const uint64_t* src[kG];
+  uint64_t* ext[kG];
+};
+void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
+bool modup_cols_ok(const hy_ctx* c);  // N = 2^16 and alpha <= 4
+// one NTT row pass (forward: reads the between-pass format; inverse: writes it)
+void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices
 void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
                 cudaStream_t s);

@@ -387,6 +387,20 @@ void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
     done += m;
   }
 }
+void rows_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
+  LimbBatch b;
+  for (size_t done = 0; done < L.src.size();) {
+    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
+    b.n = (int)m;
+    for (size_t i = 0; i < m; ++i) {
+      b.src[i] = L.src[done + i];
+      b.dst[i] = L.dst[done + i];
+      b.chain[i] = L.chain[done + i];
+    }
+    launch_ntt_rows(c, b, inverse, s);
+    done += m;
+  }
+}
 void ntt_cols_list(hy_ctx* c, const LimbList& L, cudaStream_t s) {
   LimbBatch b;
   for (size_t done = 0; done < L.src.size();) {
@@ -434,11 +448,29 @@ void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uin
   else ntt_list(c, L, false, s);
 }
 
-// ModUp (column pass only) + fused row pass / IP of G items (hy_ntt.cu launch_ntt_rows_ip)
-void modup_ip_fused(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext,
+void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* out, uint32_t level, cudaStream_t s);
+
+// ModUp + IP of G items from the NTT-domain c1 (own): inverse row pass into d, then the fused
+// iNTT-column / BConv / NTT-column kernel (N = 2^16; else iNTT + BConv + column pass), then the fused
+// row pass / IP (hy_ntt.cu)
+void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
                     cudaStream_t s) {
-  modup_batch(c, level, G, d, ext, s, true);
+  if (modup_cols_ok(c)) {
+    LimbList L;
+    for (int g = 0; g < G; ++g)
+      for (uint32_t i = 0; i <= level; ++i) L.add(own[g] + (size_t)i * c->N, d[g] + (size_t)i * c->N, i);
+    rows_list(c, L, true, s);
+    ModUpColsArgs ma{};
+    for (int g = 0; g < G; ++g) {
+      ma.src[g] = d[g];
+      ma.ext[g] = ext[g];
+    }
+    launch_modup_cols(c, ma, G, level, s);
+  } else {
+    intt_polys(c, G, own, d, level, s);
+    modup_batch(c, level, G, d, ext, s, true);
+  }
   RowsIpArgs ra{};
   for (int g = 0; g < G; ++g) {
     ra.ext[g] = ext[g];
@@ -640,10 +672,10 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
     }
     if (alias) automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
     else automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
-    intt_polys(c, G, rc1, d, level, s);
     if (fuse_ip()) {
       modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s);
     } else {
+      intt_polys(c, G, rc1, d, level, s);
       modup_batch(c, level, G, d, ext, s);
       ip_batch(c, level, G, ext, rc1, keys, u, nullptr, false, shared && G > 1, false, s);
     }
@@ -856,11 +888,11 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
       k_automorph_sum<<<grid, kT, 0, s>>>(ai, ak, G, acc0, c->log_n, (int)nl, c->dt);
     }
     automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
-    intt_polys(c, G, rc1c, d, level, s);
     uint64_t* u0 = it[0].u;
     if (fuse_ip()) {
       modup_ip_fused(c, level, G, d, ext, rc1c, keys, &u0, !first, true, s);
     } else {
+      intt_polys(c, G, rc1c, d, level, s);
       modup_batch(c, level, G, d, ext, s);
       ip_batch(c, level, G, ext, rc1c, keys, &u0, nullptr, !first, false, true, s);
     }

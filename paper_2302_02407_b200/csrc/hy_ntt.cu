@@ -460,7 +460,150 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
   store_l3(o, l, x, q, qinv, false);
 }
 
+// ---------------------------------------------------------------- ModUp: iNTT column pass + BConv + NTT column pass
+// CTA = 512 threads on one 16-column strip (thread: column c = tid & 15, lane l = tid >> 4, as in
+// k_ntt_cols256) of item g = blockIdx.z, digit j = blockIdx.y.  Phase i < A: inverse column stages of
+// source limb lo + i, ending in layout L1 with y_i = [d_i (D_j/q_i)^{-1}]_{q_i} (canonical: the fast
+// BConv lifts y_i as an integer in [0, q_i)) kept in registers; N^{-1} is folded into that constant.
+// Then one phase per non-own limb u: x = fred(sum_i fmulmod(y_i, (D_j/q_i) mod t_u)) (|x| <= t/2 + 1)
+// goes straight into the forward column stages and is stored fred-reduced (between-pass format).
+// The coefficient-domain digit and the un-transformed BConv output never reach HBM.  The next phase's
+// twiddle heap is fetched into a register during the current phase (double-buffered T).
+template <int A>
+__global__ void __launch_bounds__(512, 1) k_modup_cols(const __grid_constant__ ModUpColsArgs a,
+                                                       const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
+                                                       int logN) {
+  __shared__ double sm[16 * 273];
+  __shared__ double T[2][256];
+  __shared__ double s_hat[kMaxExt][A];
+  const int c = threadIdx.x & 15, l = threadIdx.x >> 4, tid = threadIdx.x;
+  const int col = blockIdx.x * 16 + c, j = blockIdx.y, g = blockIdx.z;
+  const size_t N = (size_t)1 << logN;
+  const ModUpConst& m = mc[j];
+  const int lo = m.lo, nsrc = m.hi - m.lo, nph = E;  // nsrc inverse phases + (E - nsrc) targets
+  for (int i = tid; i < E * A; i += blockDim.x) {
+    const int u = i / A, ii = i % A;
+    s_hat[u][ii] = ii < nsrc ? (double)m.hat_mod[u][ii] : 0.0;
+  }
+  // phase p -> (chain index, twiddle table); phases [0, nsrc) inverse, then the targets in order
+  auto target = [&](int p) {  // p >= nsrc: the (p - nsrc)-th ext limb outside [lo, hi)
+    const int k = p - nsrc;
+    return k < lo ? k : k + nsrc;
+  };
+  auto table = [&](int p) -> const double* {
+    if (p < nsrc) return dt.itw + (size_t)(lo + p) * N;
+    const int u = target(p);
+    return dt.tw + (size_t)(u <= level ? u : n_q + (u - level - 1)) * N;
+  };
+  if (tid > 0 && tid < 256) T[0][tid] = table(0)[tid];
+  double* S = sm + c * 273;
+  double y[A][8];
+#pragma unroll
+  for (int i = 0; i < A; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) y[i][k] = 0.0;
+  __syncthreads();
+  for (int p = 0; p < nph; ++p) {
+    const double tw_next = (p + 1 < nph && tid > 0 && tid < 256) ? table(p + 1)[tid] : 0.0;
+    const double* Tp = T[p & 1];
+    double x[8];
+    if (p < nsrc) {  // inverse column pass of source limb lo + p
+      const PrimeConst& pc = dt.pc[lo + p];
+      const double q = pc.qd, qinv = pc.qinv;
+      const uint64_t* src = a.src[g] + (size_t)(lo + p) * N + col;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = raw2d(src[(size_t)elem<3>(l, k) * 256]);
+      run_stages<3, false>(x, l, 1, 0, Tp, q, qinv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S[elem<3>(l, k)] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+      run_stages<2, false>(x, l, 4, 2, Tp, q, qinv);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = S[elem<1>(l, k)];
+      run_stages<1, false>(x, l, 7, 5, Tp, q, qinv);
+      const double cst = fcanon(fmulmod(pc.n_inv_d, (double)m.hat_inv[p], q, qinv), q, qinv);
+#pragma unroll
+      for (int i = 0; i < A; ++i)
+        if (i == p) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) y[i][k] = fcanon(fmulmod(x[k], cst, q, qinv), q, qinv);
+        }
+    } else {  // BConv to limb u, then the forward column pass
+      const int u = target(p);
+      const PrimeConst& pc = dt.pc[u <= level ? u : n_q + (u - level - 1)];
+      const double q = pc.qd, qinv = pc.qinv;
+      double h[A];
+#pragma unroll
+      for (int i = 0; i < A; ++i) h[i] = s_hat[u][i];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < A; ++i) acc += fmulmod(y[i][k], h[i], q, qinv);
+        x[k] = fred(acc, q, qinv);
+      }
+      run_stages<1, true>(x, l, 7, 5, Tp, q, qinv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S[elem<1>(l, k)] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+      run_stages<2, true>(x, l, 4, 2, Tp, q, qinv);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
+      run_stages<3, true>(x, l, 1, 0, Tp, q, qinv);
+      uint64_t* dst = a.ext[g] + ((size_t)j * E + u) * N + col;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256] = d2raw(fred(x[k], q, qinv));
+    }
+    if (tid > 0 && tid < 256) T[(p + 1) & 1][tid] = tw_next;
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+bool modup_cols_ok(const hy_ctx* c) { return c->N == 65536 && c->alpha <= 4; }
+
+void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
+  if (b.n == 0) return;
+  const int R = (int)c->N / 256;
+  dim3 gB(R / 8 > 0 ? R / 8 : 1, b.n);
+  KTimer kt(c, FAM_NTT_B, s);
+  kt.bytes = 2ull * b.n * c->N * 8;
+  if (inverse) k_ntt_rows<false><<<gB, 256, 0, s>>>(b, c->dt, (int)c->log_n);
+  else k_ntt_rows<true><<<gB, 256, 0, s>>>(b, c->dt, (int)c->log_n);
+}
+
+void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level);
+  dim3 grid(16, beta, G);
+  KTimer kt(c, FAM_MODUP, s);
+  // algorithmic bytes: the l+1 limbs of c1 in, beta x (E - alpha) limbs out (the last digit may be short)
+  uint64_t outs = 0;
+  for (int j = 0; j < beta; ++j) outs += E - (c->h_modup[level][j].hi - c->h_modup[level][j].lo);
+  kt.bytes = (uint64_t)G * (n + outs) * c->N * 8;
+  const ModUpConst* mc = c->d_modup[level];
+  const int nq = (int)c->n_q, lg = (int)c->log_n, lv = (int)level;
+  switch (c->alpha) {
+    case 1: k_modup_cols<1><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 2: k_modup_cols<2><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 3: k_modup_cols<3><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 4: k_modup_cols<4><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    default: break;  // callers check modup_cols_ok
+  }
+}
 
 void launch_ntt_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, int npoly, uint32_t level, cudaStream_t s) {
   if (G <= 0) return;
