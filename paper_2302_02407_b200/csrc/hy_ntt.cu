@@ -461,8 +461,9 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- ModUp: iNTT column pass + BConv + NTT column pass
-// CTA = 512 threads on one 16-column strip (thread: column c = tid & 15, lane l = tid >> 4, as in
-// k_ntt_cols256) of item g = blockIdx.z, digit j = blockIdx.y.  Phase i < A: inverse column stages of
+// CTA = 256 threads on one 8-column strip (thread: column c = tid & 7, lane l = tid >> 3; the
+// k_ntt_cols256 scheme at half width, so that two CTAs of 126-register threads share an SM and one
+// CTA's barriers are covered by the other's work) of item g = blockIdx.z, digit j = blockIdx.y.  Phase i < A: inverse column stages of
 // source limb lo + i, ending in layout L1 with y_i = [d_i (D_j/q_i)^{-1}]_{q_i} (canonical: the fast
 // BConv lifts y_i as an integer in [0, q_i)) kept in registers; N^{-1} is folded into that constant.
 // Then one phase per non-own limb u: x = fred(sum_i fmulmod(y_i, (D_j/q_i) mod t_u)) (|x| <= t/2 + 1)
@@ -470,14 +471,14 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
 // The coefficient-domain digit and the un-transformed BConv output never reach HBM.  The next phase's
 // twiddle heap is fetched into a register during the current phase (double-buffered T).
 template <int A>
-__global__ void __launch_bounds__(512, 1) k_modup_cols(const __grid_constant__ ModUpColsArgs a,
+__global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ ModUpColsArgs a,
                                                        const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
                                                        int logN) {
-  __shared__ double sm[16 * 273];
+  __shared__ double sm[8 * 273];
   __shared__ double T[2][256];
   __shared__ double s_hat[kMaxExt][A];
-  const int c = threadIdx.x & 15, l = threadIdx.x >> 4, tid = threadIdx.x;
-  const int col = blockIdx.x * 16 + c, j = blockIdx.y, g = blockIdx.z;
+  const int c = threadIdx.x & 7, l = threadIdx.x >> 3, tid = threadIdx.x;
+  const int col = blockIdx.x * 8 + c, j = blockIdx.y, g = blockIdx.z;
   const size_t N = (size_t)1 << logN;
   const ModUpConst& m = mc[j];
   const int lo = m.lo, nsrc = m.hi - m.lo, nph = E;  // nsrc inverse phases + (E - nsrc) targets
@@ -588,7 +589,7 @@ void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s
 void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
   if (G <= 0) return;
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level);
-  dim3 grid(16, beta, G);
+  dim3 grid(32, beta, G);
   KTimer kt(c, FAM_MODUP, s);
   // algorithmic bytes: the l+1 limbs of c1 in, beta x (E - alpha) limbs out (the last digit may be short)
   uint64_t outs = 0;
@@ -597,10 +598,10 @@ void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level,
   const ModUpConst* mc = c->d_modup[level];
   const int nq = (int)c->n_q, lg = (int)c->log_n, lv = (int)level;
   switch (c->alpha) {
-    case 1: k_modup_cols<1><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 2: k_modup_cols<2><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 3: k_modup_cols<3><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 4: k_modup_cols<4><<<grid, 512, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 1: k_modup_cols<1><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 2: k_modup_cols<2><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 3: k_modup_cols<3><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 4: k_modup_cols<4><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
     default: break;  // callers check modup_cols_ok
   }
 }
