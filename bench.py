@@ -50,6 +50,20 @@ def peaks():
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
+# --------------------------------------------------------------------------- ncu traffic
+def ncu_traffic(fam_name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the family's kernel, from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+    except OSError:
+        return None
+    e = t.get("families", {}).get(fam_name)
+    return None if e is None else {"bytes_per_launch": e["dram_bytes"], "kernel": e["kernel"],
+                                   "items_per_launch": e.get("items"), "source": t.get("source")}
+
+
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -346,24 +360,43 @@ def run_ours(args, ws, rank, local):
         d = breakdown[fam_name]
         achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
         return {"bound": "hbm", "kernel_family": fam_name, "achieved": achieved, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(fam_name),
                 "share_of_step": d["ms_per_step"] / ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
 
-    def alu_roof(fam_name):
-        # NTT pass: 8 stages x N/2 butterflies x 8 FP64-pipe ops (fmulmod 6 + add + sub) per limb (DESIGN 5)
+    fp64_peak = 148 * 64 * 1.965e9 / 1e12  # FP64 lanes x SMs x max clock (B200 unit counts)
+
+    def alu_roof(fam_name, ops_per_launch, what):
         d = breakdown[fam_name]
-        limbs = d["alg_bytes_per_launch"] / (2 * N * 8)
-        ops = limbs * 8 * (N // 2) * 8
-        achieved = ops / (d["avg_us"] * 1e-6) / 1e12
-        peak = 148 * 64 * 1.965e9 / 1e12  # FP64 lanes x SMs x max clock (guide unit counts); measured 18.2
-        return {"bound": "alu", "kernel_family": fam_name, "achieved": achieved, "peak": peak,
-                "unit": "TFP64op/s", "frac": achieved / peak, "traffic": None,
-                "share_of_step": d["ms_per_step"] / ms,
+        achieved = ops_per_launch / (d["avg_us"] * 1e-6) / 1e12
+        return {"bound": "alu", "kernel_family": fam_name, "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFP64op/s", "frac": achieved / fp64_peak, "traffic": ncu_traffic(fam_name),
+                "share_of_step": d["ms_per_step"] / ms, "work": what,
                 "peak_source": "148 SM x 64 FP64 lanes x 1.965 GHz (DESIGN.md section 5); one DFMA/DMUL/DADD = 1 op"}
 
-    roof = alu_roof(dominant) if dominant.startswith("ntt") else hbm_roof(dominant)
-    roof_ip = hbm_roof("ip") if "ip" in breakdown else None
+    # algorithmic FP64-pipe work: an NTT column / row pass = 8 stages x N/2
+    # butterflies x 8 ops (fmulmod 6 + add + sub); a fast-BConv output word = alpha fmulmods + alpha-1 adds
+    # + one fred (3 ops) = 7 alpha + 2
+    alpha, kp = 4, 4
+    n_l = LEVEL + 1
+    E = n_l + kp
+    digits = [min(alpha, n_l - j * alpha) for j in range((n_l + alpha - 1) // alpha)]
+    pass_ops = 8 * (N // 2) * 8
+    modup_item = n_l * pass_ops + sum((E - a) * (pass_ops + N * (7 * a + 2)) for a in digits)
+    roofs = {}
+    if "modup" in breakdown:
+        items = BATCH // breakdown["modup"]["launches_per_step"]
+        roofs["modup"] = alu_roof("modup", items * modup_item,
+                                  "fused ModUp columns: (l+1) inverse column passes + per digit (E - alpha) x "
+                                  "(BConv word + forward column pass), per item")
+    for f in ("ntt_ip", "ip", "moddown", "aut"):
+        if f in breakdown:
+            roofs[f] = hbm_roof(f)
+    for f in ("ntt_a", "ntt_b"):
+        if f in breakdown:
+            limbs = breakdown[f]["alg_bytes_per_launch"] / (2 * N * 8)
+            roofs[f] = alu_roof(f, limbs * pass_ops, "NTT pass: 8 stages x N/2 butterflies x 8 ops per limb")
+    roof = roofs.get(dominant) or hbm_roof(dominant)
     ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
 
     # e2e through the public API with host buffers: pinned H2D of the 64 input cts, D2H of the outputs
@@ -412,7 +445,7 @@ def run_ours(args, ws, rank, local):
                        "global_batch": BATCH * ws, "level": LEVEL, "parallelism": f"independent batches x{ws}",
                        "l2": "inputs larger than L2 (64 x 168 MiB evaluation keys streamed per step)"},
             "roofline": roof,
-            "roofline_ip": roof_ip,
+            "roofline_families": roofs,
             "resnet20_conv": conv,
             "resnet18_conv": conv18,
             "cpu_baseline": cpu,
