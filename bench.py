@@ -266,8 +266,19 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
                 all_gather_cts(outs, p.n_out, like)
 
         ms, launches = timed(step, steps, warmup)
+        # one extra instrumented run: device ms per kernel family (CUDA events on the launching stream)
+        ctx.time_kernels(sum(ctx.FAMILIES.values()))
+        step()
+        torch.cuda.synchronize()
+        fams = {}
+        for fn, fm in ctx.FAMILIES.items():
+            t, n, _ = ctx.kernel_times(fm)
+            if n:
+                fams[fn] = round(t, 3)
+        ctx.time_kernels(0)
         layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
-                        "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S}
+                        "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S,
+                        "family_ms": fams}
         total += mult * ms
         del pts, cts, outs, scratch
         torch.cuda.empty_cache()

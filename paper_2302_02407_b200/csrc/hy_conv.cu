@@ -198,9 +198,33 @@ struct Ctx {
   }
 };
 
-hy_status ras_inplace(const Ctx& x, uint64_t* ct, uint32_t level, const std::vector<int64_t>& rs) {
+// x_g += HRot_r(x_g) for every r in rs, in order, for all ciphertexts x_g at once: each step is one
+// batched HRot whose evaluation key is shared by every item (RaS / RaS_g / IR_g)
+hy_status ras_all(const Ctx& x, const std::vector<uint64_t*>& v, uint32_t level, const std::vector<int64_t>& rs) {
+  if (v.empty()) return HY_OK;
   for (int64_t r : rs) {
-    hy_status st = hy::hrot_plain(x.c, x.key(r), ct, level, (int32_t)r, ct, x.s, ct);
+    std::vector<const uint64_t*> keys(v.size(), x.key(r)), in_c(v.begin(), v.end());
+    std::vector<int32_t> rr(v.size(), (int32_t)r);
+    hy_status st = hy::hrot_multi(x.c, keys.data(), in_c.data(), level, rr.data(), (uint32_t)v.size(), v.data(),
+                              in_c.data(), x.s);
+    if (st != HY_OK) return st;
+  }
+  return HY_OK;
+}
+
+// out_g = Rescale(ct_g (.) mask) for all g, in blocks of 8 through the temporaries tmp[0..7]
+hy_status mask_rescale(const Ctx& x, const std::vector<uint64_t*>& v, const uint64_t* mask, uint32_t level,
+                       uint64_t* tmp, size_t tmp_stride, const std::vector<uint64_t*>& outs) {
+  for (size_t g0 = 0; g0 < v.size(); g0 += 8) {
+    const size_t M = std::min<size_t>(8, v.size() - g0);
+    std::vector<const uint64_t*> in(v.begin() + g0, v.begin() + g0 + M);
+    std::vector<uint64_t*> t(M);
+    for (size_t m = 0; m < M; ++m) t[m] = tmp + m * tmp_stride;
+    hy_status st = hy::pmult_many(x.c, in.data(), (uint32_t)M, mask, level, t.data(), x.s);
+    if (st == HY_OK) {
+      std::vector<const uint64_t*> tc(t.begin(), t.end());
+      st = hy::rescale_multi(x.c, tc.data(), (uint32_t)M, level, outs.data() + g0, x.s);
+    }
     if (st != HY_OK) return st;
   }
   return HY_OK;
@@ -339,8 +363,9 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   const size_t ct = 2ull * (level + 1) * c->N;
   const size_t f2 = (size_t)p->s.f * p->s.f;
   // CA: slid inputs + acc + (up to) two ciphertexts per SISO group (group sums, masked groups)
-  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 1 + 2 * p->n_groups) * ct;
-  return (f2 + 2) * ct;                                          // tap accumulators + tmp
+  // (8 = one block of MulFilter&Sum accumulators)
+  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + 2 * p->n_groups) * ct;
+  return (p->n_out * (f2 + 1) + 8) * ct;                          // tap accumulators + one sum per output
 }
 
 extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, const double* K, uint32_t level,
@@ -388,14 +413,14 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
   const size_t ct_l = 2 * (level + 1) * N;
   const uint64_t* wpt = pts;                                       // [n_pt][level+1][N]
   const uint64_t* mask = pts + (size_t)p->n_pt() * (level + 1) * N;  // [level][N]
-  // term (group/output grp, input i, tap t) -> stored plaintext and the Galois element of its PRot
-  std::vector<const uint64_t*> cts, ps;
-  std::vector<uint64_t> pk;
-  auto add_term = [&](const uint64_t* ct, int64_t grp, int64_t i, int64_t t) {
+  // MulFilter&Sum as dense blocks of <= 8 outputs: term (output m, operand j) -> stored plaintext index
+  // and the Galois element of its PRot; each operand ciphertext is read once per block
+  std::vector<uint32_t> bidx;
+  std::vector<uint64_t> bgal;
+  auto set_term = [&](size_t m, size_t J, size_t j, int64_t grp, int64_t i, int64_t t) {
     const auto tm = p->term(grp, i, t);
-    cts.push_back(ct);
-    ps.push_back(wpt + (size_t)tm.first * (level + 1) * N);
-    pk.push_back(hy_galois_elt(c, tm.second));
+    bidx[m * J + j] = (uint32_t)tm.first;
+    bgal[m * J + j] = hy_galois_elt(c, tm.second);
   };
   hy_status stt;
   if (p->s.algo == HY_CONV_CA) {
@@ -435,43 +460,44 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
       }
     }
     const size_t G = grps.size();
-    uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;
-    uint64_t* gbuf = acc + ct_l;                                  // G group ciphertexts (level - 1)
+    uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;          // 8 block accumulators
+    uint64_t* gbuf = acc + 8 * ct_l;                              // G group ciphertexts (level - 1)
     const size_t ct_m = 2 * (size_t)level * N;
     std::vector<uint64_t*> gp(G);
     for (size_t g = 0; g < G; ++g)
       gp[g] = (!p->has_mask && !ds) ? out[g] : gbuf + g * ct_m;  // no mask: write the output directly
-    for (size_t g = 0; g < G; ++g) {                              // MulFilter&Sum_f, rescale
-      cts.clear();
-      ps.clear();
-      pk.clear();
-      for (int64_t i = 0; i < p->n_in; ++i)
-        for (size_t t = 0; t < f2; ++t) add_term(slid[i][t], grps[g], i, t);
-      stt = pmult_acc_prot(c, cts.data(), ps.data(), pk.data(), (uint32_t)cts.size(), level, acc, 0, stream);
-      if (stt == HY_OK) stt = hy_rescale(c, acc, level, gp[g], stream);
+    // MulFilter&Sum_f over every (tap, input) operand, 8 groups per block, then rescale.  Operands are
+    // tap-major so that a PRCR family's inputs (same stored plaintext) are adjacent.
+    const size_t J = (size_t)p->n_in * f2;
+    std::vector<const uint64_t*> ops(J);
+    for (size_t t = 0; t < f2; ++t)
+      for (int64_t i = 0; i < p->n_in; ++i) ops[t * p->n_in + i] = slid[i][t];
+    for (size_t g0 = 0; g0 < G; g0 += 8) {
+      const size_t M = std::min<size_t>(8, G - g0);
+      bidx.assign(M * J, 0);
+      bgal.assign(M * J, 1);
+      std::vector<uint64_t*> accs(M);
+      for (size_t m = 0; m < M; ++m) {
+        accs[m] = acc + m * ct_l;
+        for (size_t t = 0; t < f2; ++t)
+          for (int64_t i = 0; i < p->n_in; ++i) set_term(m, J, t * p->n_in + i, grps[g0 + m], i, (int64_t)t);
+      }
+      stt = pmult_block(c, ops.data(), (uint32_t)J, accs.data(), (uint32_t)M, wpt, bidx.data(), bgal.data(), level,
+                        0, stream);
+      if (stt == HY_OK) {
+        std::vector<const uint64_t*> ac(accs.begin(), accs.end());
+        stt = rescale_multi(c, ac.data(), (uint32_t)M, level, gp.data() + g0, x.s);
+      }
       if (stt != HY_OK) return stt;
     }
-    auto ras_all = [&](std::vector<uint64_t*>& v, uint32_t lvl, const std::vector<int64_t>& rs) -> hy_status {
-      for (int64_t r : rs) {
-        std::vector<const uint64_t*> keys(v.size(), x.key(r)), in_c(v.begin(), v.end());
-        std::vector<int32_t> rr(v.size(), (int32_t)r);
-        hy_status s1 = hrot_multi(c, keys.data(), in_c.data(), lvl, rr.data(), (uint32_t)v.size(), v.data(),
-                                  in_c.data(), x.s);
-        if (s1 != HY_OK) return s1;
-      }
-      return HY_OK;
-    };
-    stt = ras_all(gp, level - 1, p->ras);                          // RaS over C_a
-    if (stt == HY_OK) stt = ras_all(gp, level - 1, p->ras_g);      // RaS_g over C_g
+    stt = ras_all(x, gp, level - 1, p->ras);                        // RaS over C_a
+    if (stt == HY_OK) stt = ras_all(x, gp, level - 1, p->ras_g);    // RaS_g over C_g
     if (stt != HY_OK || (!p->has_mask && !ds)) return stt == HY_OK ? cuda_check("hy_caconv") : stt;
     // IR_g: mask (one level) ...
     std::vector<uint64_t*> masked(G);
-    for (size_t g = 0; g < G; ++g) {
-      masked[g] = ds ? gbuf + (G + g) * ct_m : out[g];
-      stt = hy_pmult(c, gp[g], mask, level - 1, acc, stream);
-      if (stt == HY_OK) stt = hy_rescale(c, acc, level - 1, masked[g], stream);
-      if (stt != HY_OK) return stt;
-    }
+    for (size_t g = 0; g < G; ++g) masked[g] = ds ? gbuf + (G + g) * ct_m : out[g];
+    stt = mask_rescale(x, gp, mask, level - 1, acc, ct_l, masked);
+    if (stt != HY_OK) return stt;
     std::vector<uint64_t*> fin(out, out + (oe - ob));
     if (ds) {  // ... merge the two groups of each output into the doubled gap (DESIGN R-DSCONV) ...
       const size_t J = oe - ob;
@@ -484,41 +510,58 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
       stt = hrot_multi(c, keys.data(), b.data(), level - 2, rr.data(), (uint32_t)J, fin.data(), a.data(), x.s);
       if (stt != HY_OK) return stt;
     }
-    stt = ras_all(fin, level - 2, p->ir_g);                        // ... and replicate
+    stt = ras_all(x, fin, level - 2, p->ir_g);                     // ... and replicate
     if (stt != HY_OK) return stt;
     return cuda_check("hy_caconv");
   }
   // RAConv_Reorder: MulFilter&Sum_{c_i} into f^2 accumulators, one lazy Slide_1&Sum_f, rescale, RaS_g, IR_g
+  // accumulators [output][tap], filled as dense blocks of 8 outputs per tap: each input ciphertext is read
+  // once per (tap, block), and a PRCR family's outputs (same stored plaintext) share a block
   uint64_t* accs = scratch;
-  uint64_t* tmp = scratch + f2 * ct_l;
-  std::vector<const uint64_t*> acc_ptrs(f2), keys(f2);
+  uint64_t* tmp = scratch + (size_t)(oe - ob) * f2 * ct_l;
+  std::vector<const uint64_t*> keys(f2);
   std::vector<int32_t> rs(f2);
   for (size_t t = 0; t < f2; ++t) {
-    acc_ptrs[t] = accs + t * ct_l;
     rs[t] = (int32_t)p->taps[t];
     keys[t] = (p->taps[t] % p->n) ? x.key(p->taps[t]) : nullptr;
   }
-  for (uint32_t o = ob; o < oe; ++o) {
-    for (size_t t = 0; t < f2; ++t) {
-      cts.clear();
-      ps.clear();
-      pk.clear();
-      for (int64_t i = 0; i < p->n_in; ++i) add_term(in[i], o, i, t);
-      stt = pmult_acc_prot(c, cts.data(), ps.data(), pk.data(), (uint32_t)cts.size(), level, accs + t * ct_l, 0,
-                           stream);
+  const size_t J = (size_t)p->n_in;
+  for (size_t t = 0; t < f2; ++t)
+    for (uint32_t o0 = ob; o0 < oe; o0 += 8) {
+      const size_t M = std::min<size_t>(8, oe - o0);
+      bidx.assign(M * J, 0);
+      bgal.assign(M * J, 1);
+      std::vector<uint64_t*> outs(M);
+      for (size_t m = 0; m < M; ++m) {
+        outs[m] = accs + ((o0 + m - ob) * f2 + t) * ct_l;
+        for (size_t i = 0; i < J; ++i) set_term(m, J, i, o0 + m, (int64_t)i, (int64_t)t);
+      }
+      stt = pmult_block(c, in, (uint32_t)J, outs.data(), (uint32_t)M, wpt, bidx.data(), bgal.data(), level, 0,
+                        stream);
       if (stt != HY_OK) return stt;
     }
-    stt = hy_hrot_sum(c, keys.data(), acc_ptrs.data(), level, rs.data(), (uint32_t)f2, tmp, stream);
-    uint64_t* dst = p->has_mask ? accs : out[o - ob];
-    if (stt == HY_OK) stt = hy_rescale(c, tmp, level, dst, stream);
-    if (stt == HY_OK) stt = ras_inplace(x, dst, level - 1, p->ras_g);
-    if (stt == HY_OK && p->has_mask) {
-      stt = hy_pmult(c, dst, mask, level - 1, tmp, stream);
-      if (stt == HY_OK) stt = hy_rescale(c, tmp, level - 1, out[o - ob], stream);
-      if (stt == HY_OK) stt = ras_inplace(x, out[o - ob], level - 2, p->ir_g);
-    }
+  // one lazy Slide_1&Sum_f per output (Alg. P:727-733), then every later step batched over the outputs
+  const size_t no = oe - ob;
+  std::vector<const uint64_t*> sums(no);
+  std::vector<uint64_t*> dst(no);
+  for (uint32_t o = ob; o < oe; ++o) {
+    uint64_t* oacc = accs + (size_t)(o - ob) * f2 * ct_l;
+    std::vector<const uint64_t*> acc_ptrs(f2);
+    for (size_t t = 0; t < f2; ++t) acc_ptrs[t] = oacc + t * ct_l;
+    uint64_t* sum = tmp + (size_t)(o - ob) * ct_l;
+    stt = hy_hrot_sum(c, keys.data(), acc_ptrs.data(), level, rs.data(), (uint32_t)f2, sum, stream);
     if (stt != HY_OK) return stt;
+    sums[o - ob] = sum;
+    dst[o - ob] = p->has_mask ? oacc : out[o - ob];  // the output's consumed tap accumulators
   }
+  stt = rescale_multi(c, sums.data(), (uint32_t)no, level, dst.data(), x.s);
+  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g);
+  if (stt == HY_OK && p->has_mask) {
+    std::vector<uint64_t*> fin(out, out + no);
+    stt = mask_rescale(x, dst, mask, level - 1, tmp, ct_l, fin);
+    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g);
+  }
+  if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv");
 }
 

@@ -109,6 +109,25 @@ struct LimbBatch {
 
 // NTT launchers (hy_ntt.cu)
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
+
+// Any number of limbs as (src, dst, chain) lists, launched in LimbBatch chunks (hy_ntt.cu)
+struct LimbList {
+  std::vector<uint64_t*> src, dst;
+  std::vector<uint8_t> chain;
+  void add(const uint64_t* a, uint64_t* b, uint32_t t) {
+    src.push_back(const_cast<uint64_t*>(a));
+    dst.push_back(b);
+    chain.push_back((uint8_t)t);
+  }
+};
+void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s);  // both passes
+void rows_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s);  // row pass only
+void ntt_cols_list(hy_ctx* c, const LimbList& L, cudaStream_t s);            // forward column pass only
+// batched rescale / mask product (hy_ops.cu); rescale outputs must not alias inputs
+hy_status rescale_multi(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint32_t level, uint64_t* const* outs,
+                        cudaStream_t s);
+hy_status pmult_many(hy_ctx* c, const uint64_t* const* cts, uint32_t n, const uint64_t* pt, uint32_t level,
+                     uint64_t* const* outs, cudaStream_t s);
 // forward pass A only (the column stages); the row stages are then run by launch_ntt_rows_ip
 void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s);
 
@@ -172,6 +191,11 @@ size_t ks_item_bytes(const hy_ctx* c, uint32_t level);
 hy_status pmult_acc_prot(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, const uint64_t* ks,
                          uint32_t n, uint32_t level, uint64_t* out, int accumulate, void* stream);
 void launch_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t n_limbs, uint64_t k, cudaStream_t s);
+// dense MulFilter&Sum block (hy_ops.cu): out_m (+)= sum_j ct_j (.) PRot_{gal[m*J+j]}(pt_base[pt_idx[m*J+j]]),
+// M <= 8 outputs, any J (chunks of 64 operands)
+hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_t* const* outs, uint32_t M,
+                      const uint64_t* pt_base, const uint32_t* pt_idx, const uint64_t* gal, uint32_t level,
+                      int accumulate, void* stream);
 
 // Kernel families for live CUDA-event timing (values of HY_FAM_* in hyphen.h).
 enum Family : uint32_t {

@@ -361,61 +361,6 @@ void automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, uint32_t nlimbs, ui
   automorph_batch(c, 1, &in, &out, &k, nlimbs, per_poly, accumulate, s);
 }
 
-// NTT of many limbs given by (pointer, chain) lists, in launches of <= kMaxBatch limbs
-struct LimbList {
-  std::vector<uint64_t*> src, dst;
-  std::vector<uint8_t> chain;
-  void add(const uint64_t* a, uint64_t* b, uint32_t t) {
-    src.push_back(const_cast<uint64_t*>(a));
-    dst.push_back(b);
-    chain.push_back((uint8_t)t);
-  }
-};
-void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
-  LimbBatch b;
-  // chunks small enough that pass A's output is still in L2 when pass B reads it
-  static const size_t chunk = std::max(1, std::min(kMaxBatch, env_int("HY_NTT_CHUNK", kMaxBatch)));
-  for (size_t done = 0; done < L.src.size();) {
-    const size_t m = std::min<size_t>(L.src.size() - done, chunk);
-    b.n = (int)m;
-    for (size_t i = 0; i < m; ++i) {
-      b.src[i] = L.src[done + i];
-      b.dst[i] = L.dst[done + i];
-      b.chain[i] = L.chain[done + i];
-    }
-    launch_ntt(c, b, inverse, s);
-    done += m;
-  }
-}
-void rows_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) {
-  LimbBatch b;
-  for (size_t done = 0; done < L.src.size();) {
-    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
-    b.n = (int)m;
-    for (size_t i = 0; i < m; ++i) {
-      b.src[i] = L.src[done + i];
-      b.dst[i] = L.dst[done + i];
-      b.chain[i] = L.chain[done + i];
-    }
-    launch_ntt_rows(c, b, inverse, s);
-    done += m;
-  }
-}
-void ntt_cols_list(hy_ctx* c, const LimbList& L, cudaStream_t s) {
-  LimbBatch b;
-  for (size_t done = 0; done < L.src.size();) {
-    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
-    b.n = (int)m;
-    for (size_t i = 0; i < m; ++i) {
-      b.src[i] = L.src[done + i];
-      b.dst[i] = L.dst[done + i];
-      b.chain[i] = L.chain[done + i];
-    }
-    launch_ntt_cols(c, b, s);
-    done += m;
-  }
-}
-
 // d_g: coefficient-domain [l+1][N] -> ext_g [beta][E][N] (non-own limbs, NTT domain).
 // cols_only: stop after the NTT column pass (the row pass is fused into the IP, launch_ntt_rows_ip).
 void modup_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* d, uint64_t* const* ext, cudaStream_t s,

@@ -701,6 +701,30 @@ void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
   }
 }
 
+namespace {
+enum class Pass { Both, Rows, Cols };
+void run_list(hy_ctx* c, const LimbList& L, bool inverse, Pass pass, cudaStream_t s) {
+  LimbBatch b;
+  for (size_t done = 0; done < L.src.size();) {
+    const size_t m = std::min<size_t>(L.src.size() - done, kMaxBatch);
+    b.n = (int)m;
+    for (size_t i = 0; i < m; ++i) {
+      b.src[i] = L.src[done + i];
+      b.dst[i] = L.dst[done + i];
+      b.chain[i] = L.chain[done + i];
+    }
+    if (pass == Pass::Both) launch_ntt(c, b, inverse, s);
+    else if (pass == Pass::Rows) launch_ntt_rows(c, b, inverse, s);
+    else launch_ntt_cols(c, b, s);
+    done += m;
+  }
+}
+}  // namespace
+
+void ntt_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) { run_list(c, L, inverse, Pass::Both, s); }
+void rows_list(hy_ctx* c, const LimbList& L, bool inverse, cudaStream_t s) { run_list(c, L, inverse, Pass::Rows, s); }
+void ntt_cols_list(hy_ctx* c, const LimbList& L, cudaStream_t s) { run_list(c, L, false, Pass::Cols, s); }
+
 void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* chain, uint32_t n, bool inverse,
                 cudaStream_t s) {
   LimbBatch b;

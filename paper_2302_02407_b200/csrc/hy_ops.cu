@@ -1,6 +1,7 @@
 // hy_ops.cu -- MulPt / MulFilter&Sum / AddCt / Rescale and the
 // client-side key generation, encryption and decryption (
 // DESIGN R-SK, R-EVK, R-ENC, R-PRNG), all as device kernels.
+#include <algorithm>
 #include <vector>
 
 #include "hy_arith.cuh"
@@ -13,11 +14,67 @@ namespace {
 constexpr int kT = 256;
 constexpr int kMaxTerms = 64;
 
+constexpr int kPbJ = 64, kPbM = 8;
+struct PBlock {
+  const uint64_t* ct[kPbJ];
+  uint64_t* out[kPbM];
+  const uint64_t* pt_base;        // stored weight plaintexts [..][l+1][N]
+  uint32_t pt_idx[kPbM][kPbJ];    // plaintext index of term (m, j)
+  uint32_t prot[kPbM][kPbJ];      // Galois element of its PRot (1 = none)
+};
+
 struct TermPtrs {
   const uint64_t* ct[kMaxTerms];
   const uint64_t* pt[kMaxTerms];
   uint64_t prot[kMaxTerms];  // Galois element of a PRot applied to pt (1 = none), fused as a gather
 };
+
+// Blocked MulFilter&Sum: M outputs x J ciphertext operands, dense,
+//   out_m[p][i][x] (+)= sum_j ct_j[p][i][x] * PRot_{k_mj}(pt_{mj})[i][x]
+// Each thread owns (x, limb i) for both polys and all M outputs: ct_j is read once per block of M outputs
+// (instead of once per term) and each gathered weight word serves both polys.  Products on the FP64 pipe
+// (fmulmod, |r| <= 1.5 q for canonical operands), summed exactly in a double and re-centred with fred
+// every 4 operands (|acc| < 6.5 q), canonicalised once per output word.  grid (N/256, l+1)
+template <int M>
+__global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBlock b, int J, DevTables dt, int level,
+                                                     int logN, int accumulate) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const size_t n = level + 1;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  double acc[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double c0 = u2d(b.ct[j][(size_t)i * N + x]), c1 = u2d(b.ct[j][(n + i) * N + x]);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t xs = k != 1 ? aut_index(x, k, logN) : x;
+      const double w = u2d(b.pt_base[((size_t)b.pt_idx[m][j] * n + i) * N + xs]);
+      acc[m][0] += fmulmod(c0, w, q, qinv);
+      acc[m][1] += fmulmod(c1, w, q, qinv);
+    }
+    if ((j & 3) == 3) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        acc[m][0] = fred(acc[m][0], q, qinv);
+        acc[m][1] = fred(acc[m][1], q, qinv);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      uint64_t* o = b.out[m] + ((size_t)p * n + i) * N + x;
+      double v = acc[m][p];
+      if (accumulate) v += u2d(*o);
+      *o = d2u(fcanon(v, q, qinv));
+    }
+}
 
 // out[p][i][x] (+)= sum_m ct_m[p][i][x] * pt_m[i][x] mod q_i.  grid (N/256, l+1, 2)
 __global__ void k_pmult_acc(const __grid_constant__ TermPtrs tp, int nterm, uint64_t* __restrict__ out, DevTables dt, int level, int logN,
@@ -46,34 +103,48 @@ __global__ void k_add(const uint64_t* __restrict__ a, const uint64_t* __restrict
   out[o] = add_mod(a[o], b[o], dt.pc[blockIdx.y % nlimb].q);
 }
 
-// Rescale step 2: w[p][i][x] = [centre(v[p][x])]_{q_i}, v = iNTT(c_p on q_l).  grid (N/256, l, 2)
-__global__ void k_rescale_lift(const uint64_t* __restrict__ v, uint64_t* __restrict__ w, DevTables dt, int level,
-                               int logN) {
+// Batched rescale / mask product over up to kG items (pointer arrays as __grid_constant__ parameters).
+struct ItemPtrs {
+  const uint64_t* in[kG];
+  uint64_t* out[kG];
+  uint64_t* v[kG];  // rescale scratch: iNTT of the dropped limb [2][N]
+  uint64_t* w[kG];  // rescale scratch: its lift [2][l][N]
+};
+// w_g[p][i] = [centre(v_g[p])]_{q_i}.  grid (N/256, l, 2 G), blockIdx.z = 2 g + p
+__global__ void k_rescale_lift_multi(const __grid_constant__ ItemPtrs a, DevTables dt, int level, int logN) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y, p = blockIdx.z;
+  const int i = blockIdx.y, g = blockIdx.z >> 1, p = blockIdx.z & 1;
   const uint64_t ql = dt.pc[level].q, qi = dt.pc[i].q;
-  uint64_t val = v[(size_t)p * N + x];
+  const uint64_t val = a.v[g][(size_t)p * N + x];
   uint64_t r;
   if (val > (ql - 1) / 2) {  // negative representative val - ql
-    uint64_t m = reduce64(ql - val, dt.pc[i]);
+    const uint64_t m = reduce64(ql - val, dt.pc[i]);
     r = m ? qi - m : 0;
   } else {
     r = reduce64(val, dt.pc[i]);
   }
-  w[((size_t)p * level + i) * N + x] = r;
+  a.w[g][((size_t)p * level + i) * N + x] = r;
 }
-
-// Rescale step 4: out[p][i] = (c[p][i] - w[p][i]) * q_l^{-1}.  grid (N/256, l, 2)
-__global__ void k_rescale_final(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
-                                const RescaleConst* rc, DevTables dt, int level, uint64_t* __restrict__ out,
-                                int logN) {
+// out_g[p][i] = (in_g[p][i] - w_g[p][i]) q_l^{-1}.  grid (N/256, l, 2 G)
+__global__ void k_rescale_final_multi(const __grid_constant__ ItemPtrs a, const RescaleConst* rc, DevTables dt,
+                                      int level, int logN) {
   const size_t N = (size_t)1 << logN;
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y, p = blockIdx.z;
+  const int i = blockIdx.y, g = blockIdx.z >> 1, p = blockIdx.z & 1;
   const uint64_t q = dt.pc[i].q;
-  uint64_t v = sub_mod(ct[((size_t)p * (level + 1) + i) * N + x], w[((size_t)p * level + i) * N + x], q);
-  out[((size_t)p * level + i) * N + x] = shoup(v, rc->ql_inv[i], rc->ql_inv_sh[i], q);
+  const uint64_t v = sub_mod(a.in[g][((size_t)p * (level + 1) + i) * N + x], a.w[g][((size_t)p * level + i) * N + x], q);
+  a.out[g][((size_t)p * level + i) * N + x] = shoup(v, rc->ql_inv[i], rc->ql_inv_sh[i], q);
+}
+// out_g = in_g (.) pt (one plaintext for every item; the IR_g mask).  grid (N/256, l+1, 2 G)
+__global__ void k_pmult_many(const __grid_constant__ ItemPtrs a, const uint64_t* __restrict__ pt, DevTables dt,
+                             int level, int logN) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, g = blockIdx.z >> 1, p = blockIdx.z & 1;
+  const PrimeConst& pc = dt.pc[i];
+  const size_t o = ((size_t)p * (level + 1) + i) * N + x;
+  a.out[g][o] = d2u(fcanon(fmulmod(u2d(a.in[g][o]), u2d(pt[(size_t)i * N + x]), pc.qd, pc.qinv), pc.qd, pc.qinv));
 }
 
 // small signed values (int8 or int32 source) to residues on chain limbs [0, nlimb).  grid (N/256, nlimb)
@@ -207,6 +278,46 @@ hy_status pmult_acc_prot(hy_ctx* c, const uint64_t* const* cts, const uint64_t* 
   }
   return cuda_check("hy_pmult_acc");
 }
+
+// Dense block: out_m (+)= sum_j ct_j (.) PRot_{gal[m*J+j]}(pt_base[pt_idx[m*J+j]]), m < M, j < J
+hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_t* const* outs, uint32_t M,
+                      const uint64_t* pt_base, const uint32_t* pt_idx, const uint64_t* gal, uint32_t level,
+                      int accumulate, void* stream) {
+  if (!c || !cts || !outs || !pt_base || !pt_idx || !gal) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  if (M == 0 || M > (uint32_t)kPbM || J == 0) return fail(HY_E_ARG, "block shape");
+  cudaStream_t s = st(stream);
+  for (uint32_t done = 0; done < J;) {
+    const uint32_t jn = std::min<uint32_t>(J - done, kPbJ);
+    PBlock b;
+    b.pt_base = pt_base;
+    for (uint32_t j = 0; j < jn; ++j) b.ct[j] = cts[done + j];
+    for (uint32_t m = 0; m < M; ++m) {
+      b.out[m] = outs[m];
+      for (uint32_t j = 0; j < jn; ++j) {
+        b.pt_idx[m][j] = pt_idx[(size_t)m * J + done + j];
+        b.prot[m][j] = (uint32_t)gal[(size_t)m * J + done + j];
+      }
+    }
+    const int acc = (accumulate || done > 0) ? 1 : 0;
+    dim3 g(c->N / kT, level + 1);
+    KTimer kt(c, FAM_ELEM, s);
+    // cts (2 polys) once, every term's weight limb once, outputs written (and read when accumulating)
+    kt.bytes = ((uint64_t)jn * 2 + (uint64_t)M * jn + (uint64_t)M * 2 * (acc ? 2 : 1)) * (level + 1) * c->N * 8;
+    switch (M) {
+      case 1: k_pmult_block<1><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 2: k_pmult_block<2><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 3: k_pmult_block<3><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 4: k_pmult_block<4><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 5: k_pmult_block<5><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 6: k_pmult_block<6><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      case 7: k_pmult_block<7><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      default: k_pmult_block<8><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+    }
+    done += jn;
+  }
+  return cuda_check("pmult_block");
+}
 }  // namespace hy
 
 extern "C" hy_status hy_pmult_acc(hy_ctx* c, const uint64_t* const* cts, const uint64_t* const* pts, uint32_t n,
@@ -232,45 +343,86 @@ extern "C" hy_status hy_add(hy_ctx* c, const uint64_t* a, const uint64_t* b, uin
   return cuda_check("hy_add");
 }
 
-extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, uint64_t* out, void* stream) {
-  if (!c || !ct || !out) return fail(HY_E_ARG, "null");
+namespace hy {
+// Rescale of n ciphertexts at `level` (DESIGN R-RESCALE), batched kG per launch set:
+// iNTT of every dropped limb, centred lift, NTT of the lifts, (c - w) q_l^{-1}.  out_g must not alias in_g.
+hy_status rescale_multi(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint32_t level, uint64_t* const* outs,
+                        cudaStream_t s) {
+  if (!c || (n && (!cts || !outs))) return fail(HY_E_ARG, "null");
   if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
   if (level == 0) return fail(HY_E_LEVEL_EXHAUSTED, "rescale at level 0");
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
-  cudaStream_t s = st(stream);
-  const size_t N = c->N, n = level + 1;
-  Ws ws{c->ws, c->ws_bytes};
-  uint64_t* v = ws.take<uint64_t>(2 * N);
-  uint64_t* w = ws.take<uint64_t>(2 * level * N);
-  if (!w) return fail(HY_E_WORKSPACE, "workspace too small");
-  LimbBatch b;
-  b.n = 2;
-  for (int p = 0; p < 2; ++p) {
-    b.src[p] = ct + ((size_t)p * n + level) * N;
-    b.dst[p] = v + (size_t)p * N;
-    b.chain[p] = (uint8_t)level;
-  }
-  launch_ntt(c, b, true, s);
-  dim3 g(c->N / kT, level, 2);
-  {
-    KTimer kt(c, FAM_RESCALE, s);
-    k_rescale_lift<<<g, kT, 0, s>>>(v, w, c->dt, level, c->log_n);
-  }
-  b.n = 0;
-  for (int p = 0; p < 2; ++p)
-    for (uint32_t i = 0; i < level; ++i) {
-      uint64_t* q = w + ((size_t)p * level + i) * N;
-      b.src[b.n] = q;
-      b.dst[b.n] = q;
-      b.chain[b.n] = (uint8_t)i;
-      ++b.n;
+  const size_t N = c->N, nl = level + 1;
+  for (uint32_t done = 0; done < n;) {
+    const int G = (int)std::min<uint32_t>(n - done, kG);
+    Ws ws{c->ws, c->ws_bytes};
+    ItemPtrs a{};
+    LimbBatch b;
+    b.n = 0;
+    for (int g = 0; g < G; ++g) {
+      a.in[g] = cts[done + g];
+      a.out[g] = outs[done + g];
+      if (!a.in[g] || !a.out[g]) return fail(HY_E_ARG, "null ciphertext");
+      if (a.in[g] == a.out[g]) return fail(HY_E_ARG, "rescale cannot run in place");
+      a.v[g] = ws.take<uint64_t>(2 * N);
+      a.w[g] = ws.take<uint64_t>(2 * level * N);
+      if (!a.w[g]) return fail(HY_E_WORKSPACE, "workspace too small");
+      for (int p = 0; p < 2; ++p) {
+        b.src[b.n] = a.in[g] + ((size_t)p * nl + level) * N;
+        b.dst[b.n] = a.v[g] + (size_t)p * N;
+        b.chain[b.n++] = (uint8_t)level;
+      }
     }
-  launch_ntt(c, b, false, s);
-  {
-    KTimer kt(c, FAM_RESCALE, s);
-    k_rescale_final<<<g, kT, 0, s>>>(ct, w, c->d_rescale[level], c->dt, level, out, c->log_n);
+    launch_ntt(c, b, true, s);
+    dim3 g3(c->N / kT, level, 2 * G);
+    {
+      KTimer kt(c, FAM_RESCALE, s);
+      kt.bytes = (uint64_t)G * (2 + 2 * level) * N * 8;
+      k_rescale_lift_multi<<<g3, kT, 0, s>>>(a, c->dt, level, c->log_n);
+    }
+    LimbList L;
+    for (int g = 0; g < G; ++g)
+      for (int p = 0; p < 2; ++p)
+        for (uint32_t i = 0; i < level; ++i) {
+          uint64_t* q = a.w[g] + ((size_t)p * level + i) * N;
+          L.add(q, q, i);
+        }
+    ntt_list(c, L, false, s);
+    {
+      KTimer kt(c, FAM_RESCALE, s);
+      kt.bytes = (uint64_t)G * 2 * (nl + 2 * level) * N * 8;
+      k_rescale_final_multi<<<g3, kT, 0, s>>>(a, c->d_rescale[level], c->dt, level, c->log_n);
+    }
+    done += G;
   }
-  return cuda_check("hy_rescale");
+  return cuda_check("rescale");
+}
+
+// out_g = ct_g (.) pt for n ciphertexts (one plaintext), batched kG per launch
+hy_status pmult_many(hy_ctx* c, const uint64_t* const* cts, uint32_t n, const uint64_t* pt, uint32_t level,
+                     uint64_t* const* outs, cudaStream_t s) {
+  if (!c || !pt || (n && (!cts || !outs))) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  for (uint32_t done = 0; done < n;) {
+    const int G = (int)std::min<uint32_t>(n - done, kG);
+    ItemPtrs a{};
+    for (int g = 0; g < G; ++g) {
+      a.in[g] = cts[done + g];
+      a.out[g] = outs[done + g];
+    }
+    dim3 g3(c->N / kT, level + 1, 2 * G);
+    KTimer kt(c, FAM_ELEM, s);
+    kt.bytes = (uint64_t)(level + 1) * c->N * 8 * (4 * G + 1);
+    k_pmult_many<<<g3, kT, 0, s>>>(a, pt, c->dt, level, c->log_n);
+    done += G;
+  }
+  return cuda_check("pmult_many");
+}
+}  // namespace hy
+
+extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, uint64_t* out, void* stream) {
+  if (!c || !ct || !out) return fail(HY_E_ARG, "null");
+  return rescale_multi(c, &ct, 1, level, &out, st(stream));
 }
 
 extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* evk,
