@@ -148,7 +148,8 @@ class Context:
         self._pb = (C.c_uint32 * len(p_bits))(*p_bits)
         prm = _Params(log_n, len(q_bits), len(p_bits), dnum, h, self._qb, self._pb)
         h_ = C.c_void_p()
-        _check(lib().hy_ctx_create(C.byref(prm), device, C.byref(h_)))
+        self._lib = lib()
+        _check(self._lib.hy_ctx_create(C.byref(prm), device, C.byref(h_)))
         self._c = h_
         mods = (C.c_uint64 * (self.n_q + self.n_p))()
         _check(lib().hy_ctx_moduli(self._c, mods))
@@ -162,8 +163,9 @@ class Context:
         _check(lib().hy_ctx_set_workspace(self._c, self.ws.data_ptr(), self.ws.numel() * 8))
 
     def __del__(self):
-        if getattr(self, "_c", None):
-            lib().hy_ctx_destroy(self._c)
+        # the library handle is held by the object: module globals may be gone at interpreter exit
+        if getattr(self, "_c", None) and getattr(self, "_lib", None) is not None:
+            self._lib.hy_ctx_destroy(self._c)
             self._c = None
 
     # -- helpers ---------------------------------------------------------
@@ -328,7 +330,8 @@ class ConvPlan:
         self.algo = {"CA": 0, "RA": 1}.get(algo, algo)
         spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo, S)
         h = C.c_void_p()
-        _check(lib().hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
+        self._lib = lib()
+        _check(self._lib.hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
         self._p = h
         ni, no, npt, hm, nr = (C.c_uint32() for _ in range(5))
         counts = (C.c_uint32 * 5)()
@@ -342,8 +345,8 @@ class ConvPlan:
         self.f = f
 
     def __del__(self):
-        if getattr(self, "_p", None):
-            lib().hy_conv_plan_destroy(self._p)
+        if getattr(self, "_p", None) and getattr(self, "_lib", None) is not None:
+            self._lib.hy_conv_plan_destroy(self._p)
             self._p = None
 
     def weight_slots(self, K, idx):
