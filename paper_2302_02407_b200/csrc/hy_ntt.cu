@@ -87,6 +87,19 @@ __device__ __forceinline__ void load_twiddles(double* T, const double* __restric
     T[li] = __ldg(W + ((hb - 1) << m) + (uint32_t)li);
   }
 }
+// One warp fills a row's heap: all 8 loads are issued before the first shared-memory store, so the
+// warp waits for one L2 round trip instead of eight.
+__device__ __forceinline__ void load_twiddles_warp(double* T, const double* __restrict__ W, uint32_t hb, int l) {
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int li = l + 32 * k;
+    const int m = 31 - __clz(li | 1);
+    v[k] = li ? __ldg(W + ((hb - 1) << m) + (uint32_t)li) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) T[l + 32 * k] = v[k];
+}
 
 __device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
 
@@ -111,7 +124,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
   double x[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = FWD ? raw2d(src[elem<1>(l, k)]) : u2d(src[elem<1>(l, k)]);
-  load_twiddles(T, W, (uint32_t)(N >> 8) + (uint32_t)row, l, 32);
+  load_twiddles_warp(T, W, (uint32_t)(N >> 8) + (uint32_t)row, l);
   __syncwarp();
   if (FWD) {
     run_stages<1, true>(x, l, 7, 5, T, q, qinv);
@@ -352,7 +365,7 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
   const int own_digit = u <= level ? u / alpha : -1;
   double* S = sm[w];
   double* T = tws[w];
-  load_twiddles(T, dt.tw + (size_t)t * N, (uint32_t)R + (uint32_t)row, l, 32);
+  load_twiddles_warp(T, dt.tw + (size_t)t * N, (uint32_t)R + (uint32_t)row, l);
   __syncwarp();
   const size_t roff = (size_t)row * 256;
   double s0[8], s1[8];
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
   const double q = pc.qd, qinv = pc.qinv;
   double* S = sm[w];
   double* T = tws[w];
-  load_twiddles(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l, 32);
+  load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
   const size_t roff = (size_t)row * 256;
   const uint64_t* src = a.w[g] + ((size_t)c * (level + 1) + i) * N + roff;
   double x[8];
