@@ -53,7 +53,7 @@ def peaks():
 # --------------------------------------------------------------------------- ncu traffic
 def ncu_traffic(fam_name):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the family's kernel, from the committed
-    `ncu --set full` capture summary (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    `ncu --set full` capture summary (profiles/ncu_traffic.json, written by tools/ncu_round.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
@@ -408,6 +408,18 @@ def run_ours(args, ws, rank, local):
             limbs = breakdown[f]["alg_bytes_per_launch"] / (2 * N * 8)
             roofs[f] = alu_roof(f, limbs * pass_ops, "NTT pass: 8 stages x N/2 butterflies x 8 ops per limb")
     roof = roofs.get(dominant) or hbm_roof(dominant)
+    # whole-HRot HBM fraction (the metric's "HBM GB/s vs peak"): the bytes a rotation must move -- input ct,
+    # its evaluation key, output ct -- over the measured time per rotation (north_star target >= 60 %)
+    ct_bytes = 2 * n_l * N * 8
+    evk_bytes = 2 * len(digits) * E * N * 8
+    hrot_hbm = {}
+    for name_, t_ms, moved in (("plain", ms, 2 * ct_bytes + evk_bytes), ("hoisted", ms_h, ct_bytes + evk_bytes)):
+        gbs = moved * BATCH / (t_ms * 1e-3) / 1e9
+        hrot_hbm[name_] = {"alg_bytes_per_rotation": moved, "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                           "frac": gbs / pk["hbm_gbs"]}
+    hrot_hbm["note"] = ("plain: ct in + evk + ct out per rotation; hoisted: the shared input is read once per batch, "
+                        "so evk + ct out; the FP64-pipe NTT/BConv work bounds plain HRot below the HBM roofline "
+                        "(DESIGN.md section 5)")
     ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
 
     # e2e through the public API with host buffers: pinned H2D of the 64 input cts, D2H of the outputs
@@ -457,6 +469,7 @@ def run_ours(args, ws, rank, local):
                        "l2": "inputs larger than L2 (64 x 168 MiB evaluation keys streamed per step)"},
             "roofline": roof,
             "roofline_families": roofs,
+            "hrot_hbm": hrot_hbm,
             "resnet20_conv": conv,
             "resnet18_conv": conv18,
             "cpu_baseline": cpu,
@@ -479,7 +492,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-rotations", type=int, default=2)
+    ap.add_argument("--cpu-rotations", type=int, default=60)
     ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 / ResNet-18 conv-layer timings")
     ap.add_argument("--no-r18", action="store_true", help="skip the ResNet-18 (PRCR) conv-layer timings")
     args = ap.parse_args()
