@@ -143,8 +143,31 @@ struct RowsIpArgs {
   const uint64_t* evk[kG];
   uint64_t* u[kG];
 };
+// u0: first extended limb produced (0: all of Q_l u P; l+1: the P limbs only, for the split ModDown)
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s);
+                        cudaStream_t s, int u0 = 0);
+
+// Key-switch inner product on the Q_l limbs fused with the ModDown epilogue (hy_ntt.cu), per item g,
+// limb i <= level, poly c:
+//   out_g[c][i] = (sum_j D_j(ext_g, own_g)[i] (.) evk_g[j][c][i] - NTT_rows(w_g[c][i])) P^{-1}
+//                 (+ add0_g[i][kappa_k0(x)] for c = 0) (+ add1_g[i] for c = 1) (+ addct_g[c][i])
+// where D_j is the digit's limb i in the NTT domain: plain -- the row pass of the column-pass output
+// ext_g[j][i] (own digit: own_g[i] as is); hoisted -- ext_g[j][i] / own_g[i] read through the Galois
+// permutation kx_g (Halevi-Shoup).  w_g is the column-pass output of the P -> Q_l conversion of the
+// P limbs of the same inner product, so the Q limbs of u are never stored.  out_g may alias addct_g.
+struct IpFinalArgs {
+  const uint64_t* ext[kG];
+  const uint64_t* own[kG];
+  const uint64_t* evk[kG];
+  const uint64_t* w[kG];
+  const uint64_t* add0[kG];
+  const uint64_t* add1[kG];
+  const uint64_t* addct[kG];
+  uint64_t* out[kG];
+  uint64_t k0[kG];
+  uint64_t kx[kG];
+};
+void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level, bool hoisted, cudaStream_t s);
 
 // Fused ModDown NTT row pass + epilogue (hy_ntt.cu), per item g and poly c < npoly:
 //   out_g[c][i] = (u_g[c][i] - NTT_rows(w_g[c][i])) P^{-1} (+ add0_g[i][kappa_k0(x)] for c = 0)

@@ -121,10 +121,12 @@ __global__ void __launch_bounds__(256) k_modup_bconv(const __grid_constant__ Arr
 // u_g[c][u][x] (+)= sum_j src_g,j[u][perm_g(x)] * evk_g[j][c][chain(u)][x], where src_g,j[u] is the
 // digit's own limb of own_g (the NTT-domain c1 the digits were cut from) when u belongs to digit j,
 // else ext_g[j][u].
-//   default: grid (N/256, E, G), one item per z-slice;
-//   SHARED : grid (N/256, E), each thread loops over the items with evk_0 held in registers, so the
-//            key is streamed from HBM once for the whole batch;
-//   SUM    : grid (N/256, E), all items accumulate into u_0 (the lazy HRotSum), race-free because
+//   default: grid (G, N/256, E), one item per x-slice: the item index is the fastest grid dimension,
+//            so when the items share their digits (hoisted: one ModUp, G Galois permutations) every
+//            digit limb is fetched from HBM once per batch and then served from L2;
+//   SHARED : grid (1, N/256, E), each thread loops over the items with evk_0 held in registers, so
+//            the key is streamed from HBM once for the whole batch;
+//   SUM    : grid (1, N/256, E), all items accumulate into u_0 (the lazy HRotSum), race-free because
 //            one thread owns (u, x).
 // Products reduced on the FP64 pipe and summed exactly (|sum| <= 1.5 B t < 2^53), canonicalised once
 // per item (SUM: each item's sum is re-centred with fred before the cross-item sum).
@@ -135,10 +137,10 @@ __global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const
                                                const __grid_constant__ Arr<uint64_t*> uo,
                                                const __grid_constant__ Arr<uint64_t> kperm, int G, DevTables dt,
                                                int level, int n_q, int L1, int E, int alpha, int logN,
-                                               int accumulate) {
+                                               int accumulate, int u0) {
   const size_t N = (size_t)1 << logN;
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int u = blockIdx.y;
+  const uint32_t x = blockIdx.y * blockDim.x + threadIdx.x;
+  const int u = u0 + (int)blockIdx.z;
   const int t = u <= level ? u : n_q + (u - level - 1);
   const PrimeConst& p = dt.pc[t];
   const double q = p.qd, qinv = p.qinv;
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const
     }
   }
   double s0 = 0.0, s1 = 0.0;
-  const int g0 = (SHARED || SUM) ? 0 : (int)blockIdx.z;
+  const int g0 = (SHARED || SUM) ? 0 : (int)blockIdx.x;
   const int g1 = (SHARED || SUM) ? G : g0 + 1;
   for (int g = g0; g < g1; ++g) {
     const uint32_t xs = kperm.p[g] != 1 ? aut_index(x, kperm.p[g], logN) : x;
@@ -400,7 +402,7 @@ void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* ou
 // row pass / IP (hy_ntt.cu)
 void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
-                    cudaStream_t s) {
+                    cudaStream_t s, int u0 = 0) {
   if (modup_cols_ok(c)) {
     LimbList L;
     for (int g = 0; g < G; ++g)
@@ -423,7 +425,7 @@ void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64
     ra.evk[g] = evk[g];
     ra.u[g] = u[sum ? 0 : g];
   }
-  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s);
+  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0);
 }
 
 // HY_FUSE_IP=0 / HY_FUSE_MD=0 run the unfused ModUp NTT + IP / ModDown NTT + epilogue (A/B measurements)
@@ -435,12 +437,18 @@ bool fuse_moddown() {
   static const bool on = env_int("HY_FUSE_MD", 1) != 0;
   return on;
 }
+// HY_SPLIT_MD=0: store every limb of the inner product and run ModDown afterwards (A/B measurements)
+bool split_moddown() {
+  static const bool on = env_int("HY_SPLIT_MD", 1) != 0 && env_int("HY_FUSE_IP", 1) != 0;
+  return on;
+}
 
-// IP of G items.  shared: all items use evk[0]; sum: all items accumulate into u[0].
+// IP of G items.  shared: all items use evk[0]; sum: all items accumulate into u[0].  u0: first
+// extended limb produced (l+1: the P limbs only, for the split ModDown).
 void ip_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* ext, const uint64_t* const* own,
               const uint64_t* const* evk, uint64_t* const* u, const uint64_t* kperm, bool acc, bool shared, bool sum,
-              cudaStream_t s) {
-  const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level);
+              cudaStream_t s, int u0 = 0) {
+  const int n = level + 1, E = n + c->n_p, beta = n_digits(c, level), nu = E - u0;
   Arr<const uint64_t*> ae{}, ao{}, ak{};
   Arr<uint64_t*> au{};
   Arr<uint64_t> ap{};
@@ -451,12 +459,12 @@ void ip_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* ext, cons
     au.p[g] = u[sum ? 0 : g];
     ap.p[g] = kperm ? kperm[g] : 1;
   }
-  dim3 g(c->N / kT, E, (shared || sum) ? 1 : G);
+  dim3 g((shared || sum) ? 1 : G, c->N / kT, nu);
   KTimer kt(c, FAM_IP, s);
   const uint64_t keys = shared ? 1 : G, outs = sum ? 1 : G;
-  kt.bytes = ((uint64_t)G * beta * E + keys * 2ull * beta * E + outs * 2ull * E * (acc ? 2 : 1)) * c->N * 8;
+  kt.bytes = ((uint64_t)G * beta * nu + keys * 2ull * beta * nu + outs * 2ull * nu * (acc ? 2 : 1)) * c->N * 8;
 #define ARGS ae, ao, ak, au, ap, G, c->dt, (int)level, (int)c->n_q, (int)(c->n_q + c->n_p), E, (int)c->alpha, \
-             (int)c->log_n, acc ? 1 : 0
+             (int)c->log_n, acc ? 1 : 0, u0
   if (shared && !sum) {
     HY_DISPATCH_IP(true, false)
   } else if (!shared && sum) {
@@ -541,6 +549,41 @@ void moddown_batch(hy_ctx* c, uint32_t level, int npoly, int G, const DownItem* 
   k_moddown_final<<<g2, kT, 0, s>>>(a, npoly, E, c->d_moddown[level], c->dt, (int)level, (int)c->log_n);
 }
 
+// Split ModDown, first half: the P limbs of u_g (computed first) -> iNTT -> P -> Q_l conversion -> forward
+// column pass into w_g [2][l+1][N]; the second half is launch_rows_ip_final, which computes the Q limbs
+// of the inner product and finishes (u - w) P^{-1} without storing them.
+void moddown_p(hy_ctx* c, uint32_t level, int G, uint64_t* const* u, uint64_t* const* v, uint64_t* const* w,
+               cudaStream_t s) {
+  const int n = level + 1, E = n + c->n_p, K = c->n_p;
+  LimbList L;
+  for (int g = 0; g < G; ++g)
+    for (int cc = 0; cc < 2; ++cc)
+      for (int k = 0; k < K; ++k)
+        L.add(u[g] + ((size_t)cc * E + n + k) * c->N, v[g] + ((size_t)cc * K + k) * c->N, c->n_q + k);
+  ntt_list(c, L, true, s);
+  Arr<const uint64_t*> av{};
+  Arr<uint64_t*> aw{};
+  for (int g = 0; g < G; ++g) {
+    av.p[g] = v[g];
+    aw.p[g] = w[g];
+  }
+  dim3 grid(c->N / kT, 2, G);
+  {
+    KTimer kt(c, FAM_MODDOWN, s);
+    kt.bytes = (uint64_t)G * ((uint64_t)2 * K + (uint64_t)2 * n) * c->N * 8;
+    HY_DISPATCH_1_8(k_moddown_bconv, K, grid, kT, s, av, aw, c->d_moddown[level], c->dt, (int)level, (int)c->n_q,
+                    (int)c->log_n);
+  }
+  LimbList L2;
+  for (int g = 0; g < G; ++g)
+    for (int cc = 0; cc < 2; ++cc)
+      for (int i = 0; i < n; ++i) {
+        uint64_t* p = w[g] + ((size_t)cc * n + i) * c->N;
+        L2.add(p, p, i);
+      }
+  ntt_cols_list(c, L2, s);
+}
+
 void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* out, uint32_t level, cudaStream_t s) {
   LimbList L;
   for (int g = 0; g < G; ++g)
@@ -617,6 +660,29 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
     }
     if (alias) automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
     else automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
+    if (split_moddown()) {
+      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s, (int)n);
+      uint64_t* v[kG];
+      uint64_t* w[kG];
+      IpFinalArgs fa{};
+      for (int g = 0; g < G; ++g) {
+        v[g] = it[g].v;
+        w[g] = it[g].w;
+        fa.ext[g] = ext[g];
+        fa.own[g] = rc1[g];
+        fa.evk[g] = keys[g];
+        fa.w[g] = w[g];
+        fa.add0[g] = di[g].add0;
+        fa.k0[g] = di[g].k0;
+        fa.addct[g] = di[g].addct;
+        fa.out[g] = di[g].out;
+        fa.kx[g] = 1;
+      }
+      moddown_p(c, level, G, u, v, w, s);
+      launch_rows_ip_final(c, fa, G, level, false, s);
+      done += G;
+      continue;
+    }
     if (fuse_ip()) {
       modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s);
     } else {
@@ -758,6 +824,28 @@ extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, con
       u[g] = it[g].u;
       kk[g] = hy_galois_elt(c, r[i]);
       di[g] = DownItem{it[g].u, outs[i], ct, kk[g], nullptr, nullptr, it[g].v, it[g].w};
+    }
+    if (split_moddown()) {  // P limbs of the IP, their conversion, then the Q limbs fused with the epilogue
+      uint64_t* v[kG];
+      uint64_t* w[kG];
+      IpFinalArgs fa{};
+      for (int g = 0; g < G; ++g) {
+        v[g] = it[g].v;
+        w[g] = it[g].w;
+        fa.ext[g] = it[0].ext;
+        fa.own[g] = c1;
+        fa.evk[g] = keys[g];
+        fa.w[g] = w[g];
+        fa.add0[g] = ct;
+        fa.k0[g] = kk[g];
+        fa.out[g] = outs[ks[done + g]];
+        fa.kx[g] = kk[g];
+      }
+      ip_batch(c, level, G, ext, own, keys, u, kk, false, false, false, s, (int)nl);
+      moddown_p(c, level, G, u, v, w, s);
+      launch_rows_ip_final(c, fa, G, level, true, s);
+      done += G;
+      continue;
     }
     ip_batch(c, level, G, ext, own, keys, u, kk, false, false, false, s);
     moddown_batch(c, level, 2, G, di, s);

@@ -351,13 +351,13 @@ __device__ __forceinline__ void store_l3(uint64_t* p, int l, const double (&x)[8
 template <int B, bool SUM>
 __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ RowsIpArgs a, int G, DevTables dt,
                                                         int level, int n_q, int L1, int E, int alpha, int logN,
-                                                        int accumulate) {
+                                                        int accumulate, int u0) {
   __shared__ double sm[8][272];
   __shared__ double tws[8][256];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const size_t N = (size_t)1 << logN;
   const int R = (int)(N >> 8);
-  const int row = blockIdx.y * 8 + w, u = blockIdx.z;
+  const int row = blockIdx.y * 8 + w, u = u0 + (int)blockIdx.z;
   if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
   const int t = u <= level ? u : n_q + (u - level - 1);
   const PrimeConst& pc = dt.pc[t];
@@ -471,6 +471,108 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
     for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
   }
   store_l3(o, l, x, q, qinv, false);
+}
+
+// ---------------------------------------------------------------- Q-limb IP fused with the ModDown epilogue
+// One warp per (item g, limb i <= level, row), both polys: the inner product of the digits' row i with the
+// evk rows (plain: row pass of the column-pass output; hoisted: NTT-domain digits gathered through kx_g),
+// kept in registers; then for c = 0, 1 the row pass of the conversion w_g[c][i] and
+// out = (fred(acc_c) - w) P^{-1} (+ addends), canonicalised once.  |fred(acc) - w| < q/2 + 1 + 13 q.
+// grid (G, R/8, l+1): the item index is the fastest grid dimension (hoisted items share their digits).
+template <int B, bool HOIST>
+__global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant__ IpFinalArgs a, DevTables dt,
+                                                          const ModDownConst* md, int level, int L1, int E,
+                                                          int alpha, int logN) {
+  __shared__ double sm[8][272];
+  __shared__ double tws[8][256];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t N = (size_t)1 << logN;
+  const int R = (int)(N >> 8);
+  const int g = blockIdx.x, row = blockIdx.y * 8 + w, i = blockIdx.z;
+  if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  const int own_digit = i / alpha;
+  double* S = sm[w];
+  double* T = tws[w];
+  load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
+  __syncwarp();
+  const size_t roff = (size_t)row * 256;
+  uint32_t gi[8];
+  if (HOIST) {
+    const uint64_t kx = a.kx[g];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+      gi[k] = kx != 1 ? aut_index(xi, kx, logN) : xi;
+    }
+  }
+  double a0[8], a1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < B; ++j) {
+    const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
+    ulonglong2 k0[4], k1[4];
+    load_l3(e0, l, k0, true);
+    load_l3(e0 + (size_t)L1 * N, l, k1, true);
+    double x[8];
+    if (HOIST) {
+      const uint64_t* src = j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = u2d(src[gi[k]]);
+    } else if (j == own_digit) {
+      ulonglong2 v[4];
+      load_l3(a.own[g] + (size_t)i * N + roff, l, v, false);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = l3_word(v, k);
+    } else {
+      const uint64_t* src = a.ext[g] + ((size_t)j * E + i) * N + roff;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = raw2d(src[elem<1>(l, k)]);
+      rows_forward_l3(x, l, S, T, q, qinv);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a0[k] += fmulmod(x[k], l3_word(k0, k), q, qinv);
+      a1[k] += fmulmod(x[k], l3_word(k1, k), q, qinv);
+    }
+  }
+  const double pinv = (double)md->p_inv[i];
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    const uint64_t* src = a.w[g] + ((size_t)c * (level + 1) + i) * N + roff;
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = raw2d(src[elem<1>(l, k)]);
+    __syncwarp();
+    rows_forward_l3(x, l, S, T, q, qinv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fmulmod(fred(c ? a1[k] : a0[k], q, qinv) - x[k], pinv, q, qinv);
+    if (c == 0 && a.add0[g]) {
+      const uint64_t* p0 = a.add0[g] + (size_t)i * N;
+      const uint64_t k0 = a.k0[g];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+        x[k] += u2d(p0[k0 != 1 ? aut_index(xi, k0, logN) : xi]);
+      }
+    }
+    if (c == 1 && a.add1[g]) {
+      ulonglong2 v[4];
+      load_l3(a.add1[g] + (size_t)i * N + roff, l, v, false);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+    }
+    const size_t o = ((size_t)c * (level + 1) + i) * N + roff;
+    if (a.addct[g]) {
+      ulonglong2 v[4];
+      load_l3(a.addct[g] + o, l, v, false);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+    }
+    store_l3(a.out[g] + o, l, x, q, qinv, false);
+  }
 }
 
 // ---------------------------------------------------------------- ModUp: iNTT column pass + BConv + NTT column pass
@@ -643,30 +745,31 @@ void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
 }
 
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s) {
+                        cudaStream_t s, int u0) {
   if (G <= 0) return;
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
+  const int nu = E - u0;  // extended limbs produced
   int keys = 0;
   for (int g = 0; g < G; ++g) {
     bool seen = false;
     for (int h = 0; h < g; ++h) seen |= a.evk[h] == a.evk[g];
     keys += seen ? 0 : 1;
   }
-  dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, E);
+  dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, nu);
   KTimer kt(c, FAM_NTT_IP, s);
   // algorithmic bytes: every digit limb in once, each distinct key once, the outputs (read back too
   // when accumulating)
   const uint64_t outs = sum ? 1 : G;
-  kt.bytes = ((uint64_t)G * beta * E + (uint64_t)keys * 2 * beta * E + outs * 2 * E * (accumulate ? 2 : 1)) * c->N * 8;
+  kt.bytes = ((uint64_t)G * beta * nu + (uint64_t)keys * 2 * beta * nu + outs * 2 * nu * (accumulate ? 2 : 1)) * c->N * 8;
   const int L1 = (int)(c->n_q + c->n_p);
 #define HY_RIP(BB)                                                                                             \
   case BB:                                                                                                     \
     if (sum)                                                                                                   \
       k_ntt_rows_ip<BB, true><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E, (int)c->alpha, \
-                                                   (int)c->log_n, accumulate ? 1 : 0);                         \
+                                                   (int)c->log_n, accumulate ? 1 : 0, u0);                     \
     else                                                                                                       \
       k_ntt_rows_ip<BB, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,              \
-                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0);         \
+                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0);     \
     break;
   switch (beta) {
     HY_RIP(1)
@@ -680,6 +783,44 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
       HY_RIP(8)
   }
 #undef HY_RIP
+}
+
+void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level, bool hoisted, cudaStream_t s) {
+  if (G <= 0) return;
+  const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
+  int keys = 0;
+  for (int g = 0; g < G; ++g) {
+    bool seen = false;
+    for (int h = 0; h < g; ++h) seen |= a.evk[h] == a.evk[g];
+    keys += seen ? 0 : 1;
+  }
+  uint64_t extra = 0;
+  for (int g = 0; g < G; ++g) extra += (a.add0[g] ? n : 0) + (a.add1[g] ? n : 0) + (a.addct[g] ? 2 * n : 0);
+  dim3 grid(G, R / 8 > 0 ? R / 8 : 1, n);
+  KTimer kt(c, FAM_NTT_IP, s);
+  // algorithmic bytes: the digits' Q limbs in (hoisted: shared, once), each distinct key's Q rows once,
+  // the conversion w in, the output written, the addends
+  const uint64_t digits = (hoisted ? 1 : (uint64_t)G) * beta * n;
+  kt.bytes = (digits + (uint64_t)keys * 2 * beta * n + (uint64_t)G * 4 * n + extra) * c->N * 8;
+  const int L1 = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
+  const ModDownConst* md = c->d_moddown[level];
+#define HY_RIF(BB)                                                                                     \
+  case BB:                                                                                             \
+    if (hoisted) k_rows_ip_final<BB, true><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);      \
+    else k_rows_ip_final<BB, false><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);             \
+    break;
+  switch (beta) {
+    HY_RIF(1)
+    HY_RIF(2)
+    HY_RIF(3)
+    HY_RIF(4)
+    HY_RIF(5)
+    HY_RIF(6)
+    HY_RIF(7)
+    default:
+      HY_RIF(8)
+  }
+#undef HY_RIF
 }
 
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
