@@ -223,6 +223,14 @@ R18_LAYERS = [
     ("L3_ra", (256, 256, 14, 3, 1, 64, 4, 4, 4, "RA", 8), 2),
     ("L4_ca", (512, 512, 7, 3, 1, 64, 8, 8, 8, "CA", 8), 1),
     ("L4_ra", (512, 512, 7, 3, 1, 64, 8, 8, 8, "RA", 8), 2),
+    # downsampling blocks: stride-2 dsconv and the 1x1 stride-2 shortcut (pconv), full (non-PRCR) weights
+    # (PRCR needs stride 1, DESIGN R-PRCR); output RA(2d, 2m) at gap 2g feeds the next stage (R-DSCONV)
+    ("L2_ds", (64, 128, 56, 3, 2, 64, 1, 1, 1, "CA", 1), 1),
+    ("L2_pconv", (64, 128, 56, 1, 2, 64, 1, 1, 1, "CA", 1), 1),
+    ("L3_ds", (128, 256, 28, 3, 2, 64, 2, 2, 2, "CA", 1), 1),
+    ("L3_pconv", (128, 256, 28, 1, 2, 64, 2, 2, 2, "CA", 1), 1),
+    ("L4_ds", (256, 512, 14, 3, 2, 64, 4, 4, 4, "CA", 1), 1),
+    ("L4_pconv", (256, 512, 14, 1, 2, 64, 4, 4, 4, "CA", 1), 1),
 ]
 
 
@@ -287,9 +295,9 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
                 "fresh encryption at its scheduled level; bootstrapping/activation excluded (P:1095-1101 conv "
                 "columns: 0.52 s on A100, context only)")
     else:
-        note = ("sum over the 14 stride-1 3x3 convs (PRCR |S|=8) of per-layer device time; the 3 dsconv and 3 pconv "
-                "layers are not included (stride-2 weights are not PRCR-compressible in our design, DESIGN R-PRCR); "
-                "context: ResNet-18 conv 7.59 s on A100 (P:1095-1096)")
+        note = ("sum over the 19 convs after the stem (13 stride-1 3x3 convs with PRCR |S|=8, 3 stride-2 dsconv and "
+                "3 pconv shortcuts with full weights) of per-layer device time, each layer on a fresh encryption at "
+                "its scheduled level; context: ResNet-18 conv 7.59 s on A100 (P:1095-1096)")
     return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note}
 
 
@@ -363,6 +371,18 @@ def run_ours(args, ws, rank, local):
         if n:
             breakdown[name] = {"ms_per_step": t / args.steps, "launches_per_step": n // args.steps,
                                "alg_bytes_per_launch": by // n, "avg_us": 1000.0 * t / n}
+    ctx.time_kernels(0)
+    # the same for the hoisted batch
+    ctx.time_kernels(sum(fam.values()))
+    for _ in range(args.steps):
+        step_hoisted()
+    torch.cuda.synchronize()
+    breakdown_h = {}
+    for name, m in fam.items():
+        t, n, by = ctx.kernel_times(m)
+        if n:
+            breakdown_h[name] = {"ms_per_step": t / args.steps, "launches_per_step": n // args.steps,
+                                 "alg_bytes_per_launch": by // n, "avg_us": 1000.0 * t / n}
     ctx.time_kernels(0)
     dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
     pk = peaks()
@@ -477,7 +497,8 @@ def run_ours(args, ws, rank, local):
             "gpu_launches": launches,
             "clocks": clocks,
             "hoisted": {"value": BATCH * ws * 1000.0 / ms_h, "unit": UNIT, "ms_per_step": ms_h,
-                        "note": "ct_0 rotated by 1..64 with one shared ModUp (Slide_f pattern, P:369-375)"},
+                        "note": "ct_0 rotated by 1..64 with one shared ModUp (Slide_f pattern, P:369-375)",
+                        "kernel_breakdown": breakdown_h},
             "kernel_breakdown": breakdown,
             "ntt_ms_per_step": ntt_ms,
         }

@@ -84,12 +84,15 @@ def test_toy_layers_bit_exact(ctx_toy, orc_toy, spec):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10
 
 
-R18_PRCR = {"r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8)}
+R18 = {"r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8),
+       # ResNet-18 stage-4 shortcut: 1x1 stride-2 pconv from plan (4,4) at gap 4 to RA(8,8) at gap 8
+       "r18_L4_pconv": H.ConvSpec(256, 512, 14, 1, 2, 64, 4, 4, 4, "CA")}
 
 
-@pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1]), ("r18_L1_ca_S8", [5])])
+@pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1]), ("r18_L1_ca_S8", [5]),
+                                          ("r18_L4_pconv", [1])])
 def test_resnet_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
-    spec = R20[name] if name in R20 else R18_PRCR[name]
+    spec = R20[name] if name in R20 else R18[name]
     level = 9 if spec.algo == "CA" else 6      # l+1 = 10 for CAConv, 7 for RAConv (DESIGN R-LEVELS)
     X = synth.image(21, spec.ci, spec.w)
     K = synth.conv_weight(22, spec.co, spec.ci, spec.f)

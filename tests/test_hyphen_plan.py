@@ -142,3 +142,14 @@ def test_prcr_plan_equals_conv2d(name):
         assert len(plan.weights) * spec.S == n_pt_plain
         assert plan.counts == p0.counts
     assert plan.mask is not None
+
+
+def test_simulated_r18_pconv_equals_conv2d():
+    """ResNet-18 stage-4 shortcut (1x1, stride 2, 256 -> 512 at 14x14, plan (4,4) -> RA(8,8) at gap 8;
+    W_p = 64 with the 14 -> 16 padding of R-LAYOUT): simulator = conv2d on every output replica."""
+    spec = H.ConvSpec(256, 512, 14, 1, 2, 64, 4, 4, 4, "CA")
+    X, K, plan, ys = _run(spec, 3)
+    want = H.conv2d(X, K, spec.s)
+    for rep in range(plan.fout.d):
+        got = H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo, rep)
+        assert np.max(np.abs(got - want)) < 1e-9

@@ -20,6 +20,9 @@ CASES = dict(R20)
 CASES["C1_raconv"] = H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048)
 CASES["toy_dsconv"] = H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048)
 CASES["r18_L4_ra"] = H.ConvSpec(512, 512, 7, 3, 1, 64, 8, 8, 8, "RA")
+# ResNet-18 downsampling blocks (full weights): dsconv from plan (1,1) and the stage-4 pconv from (4,4)
+CASES["r18_L2_ds"] = H.ConvSpec(64, 128, 56, 3, 2, 64, 1, 1, 1, "CA")
+CASES["r18_L4_pconv"] = H.ConvSpec(256, 512, 14, 1, 2, 64, 4, 4, 4, "CA")
 CASES.update(PRCR)
 
 
