@@ -101,7 +101,13 @@ __device__ __forceinline__ void load_twiddles_warp(double* T, const double* __re
   for (int k = 0; k < 8; ++k) T[l + 32 * k] = v[k];
 }
 
-__device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
+// Shared-memory word of element e in a warp's 256-word transpose buffer: an XOR swizzle (a bijection
+// on [0, 256)) under which every layout access of a half-warp (S[pidx(elem<L>(l, k))], L = 1, 2, 3)
+// touches 16 distinct 8-byte banks (checked by brute force over all l, k, L).
+__device__ __forceinline__ int pidx(int e) { return e ^ ((e >> 2) & 1) ^ (((e >> 4) & 7) << 1); }
+// The same for an 8-column strip [256][8] (thread column c = tid & 7, lane l = tid >> 3): word of
+// (element e, column c); rows e and e^1 / e^4 met by one half-warp land in opposite bank halves.
+__device__ __forceinline__ int sidx8(int e, int c) { return 8 * (e ^ ((e >> 2) & 1)) + c; }
 
 // ---------------------------------------------------------------- pass B (rows)
 // CTA = 8 warps, one 256-word row per warp.  grid = (N/256/8, n_limbs)
@@ -589,7 +595,7 @@ template <int A>
 __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ ModUpColsArgs a,
                                                        const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
                                                        int logN) {
-  __shared__ double sm[8 * 273];
+  __shared__ double sm[8 * 256];
   __shared__ double T[2][256];
   __shared__ double s_hat[kMaxExt][A];
   const int c = threadIdx.x & 7, l = threadIdx.x >> 3, tid = threadIdx.x;
@@ -612,7 +618,6 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
     return dt.tw + (size_t)(u <= level ? u : n_q + (u - level - 1)) * N;
   };
   if (tid > 0 && tid < 256) T[0][tid] = table(0)[tid];
-  double* S = sm + c * 273;
   double y[A][8];
 #pragma unroll
   for (int i = 0; i < A; ++i)
@@ -631,17 +636,17 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
       for (int k = 0; k < 8; ++k) x[k] = raw2d(src[(size_t)elem<3>(l, k) * 256]);
       run_stages<3, false>(x, l, 1, 0, Tp, q, qinv);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) S[elem<3>(l, k)] = x[k];
+      for (int k = 0; k < 8; ++k) sm[sidx8(elem<3>(l, k), c)] = x[k];
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+      for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<2>(l, k), c)];
       run_stages<2, false>(x, l, 4, 2, Tp, q, qinv);
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+      for (int k = 0; k < 8; ++k) sm[sidx8(elem<2>(l, k), c)] = x[k];
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = S[elem<1>(l, k)];
+      for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<1>(l, k), c)];
       run_stages<1, false>(x, l, 7, 5, Tp, q, qinv);
       const double cst = fcanon(fmulmod(pc.n_inv_d, (double)m.hat_inv[p], q, qinv), q, qinv);
 #pragma unroll
@@ -666,17 +671,17 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
       }
       run_stages<1, true>(x, l, 7, 5, Tp, q, qinv);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) S[elem<1>(l, k)] = x[k];
+      for (int k = 0; k < 8; ++k) sm[sidx8(elem<1>(l, k), c)] = x[k];
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = S[elem<2>(l, k)];
+      for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<2>(l, k), c)];
       run_stages<2, true>(x, l, 4, 2, Tp, q, qinv);
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) S[elem<2>(l, k)] = x[k];
+      for (int k = 0; k < 8; ++k) sm[sidx8(elem<2>(l, k), c)] = x[k];
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = S[elem<3>(l, k)];
+      for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<3>(l, k), c)];
       run_stages<3, true>(x, l, 1, 0, Tp, q, qinv);
       uint64_t* dst = a.ext[g] + ((size_t)j * E + u) * N + col;
 #pragma unroll
