@@ -142,10 +142,12 @@ struct RowsIpArgs {
   const uint64_t* own[kG];
   const uint64_t* evk[kG];
   uint64_t* u[kG];
+  uint64_t* v[kG];  // inv_p: [2][K][N] P limbs after the inverse row pass (between-pass format)
 };
 // u0: first extended limb produced (0: all of Q_l u P; l+1: the P limbs only, for the split ModDown)
+// inv_p (with u0 = l+1): store the P limbs after their inverse row pass into v instead (split ModDown)
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0 = 0);
+                        cudaStream_t s, int u0 = 0, bool inv_p = false);
 
 // Key-switch inner product on the Q_l limbs fused with the ModDown epilogue (hy_ntt.cu), per item g,
 // limb i <= level, poly c:
@@ -194,6 +196,11 @@ struct ModUpColsArgs {
 };
 void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
 bool modup_cols_ok(const hy_ctx* c);  // N = 2^16 and alpha <= 4
+// The same fused column kernel for ModDown, per item g and poly c: inverse column pass of the K P limbs
+// src_g[c][k] (after their inverse row pass), z_k = [v_k (P/p_k)^{-1}]_{p_k}, and for every q_i <= level
+// ext_g[c][i] = forward column pass of [sum_k z_k ((P/p_k) mod q_i)] (between-pass format).
+void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
+bool moddown_cols_ok(const hy_ctx* c);  // N = 2^16 and K <= 4
 // one NTT row pass (forward: reads the between-pass format; inverse: writes it)
 void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices

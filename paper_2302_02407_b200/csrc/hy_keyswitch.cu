@@ -402,7 +402,7 @@ void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* ou
 // row pass / IP (hy_ntt.cu)
 void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
-                    cudaStream_t s, int u0 = 0) {
+                    cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr) {
   if (modup_cols_ok(c)) {
     LimbList L;
     for (int g = 0; g < G; ++g)
@@ -424,8 +424,9 @@ void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64
     ra.own[g] = own[g];
     ra.evk[g] = evk[g];
     ra.u[g] = u[sum ? 0 : g];
+    ra.v[g] = v ? v[g] : nullptr;
   }
-  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0);
+  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0, v != nullptr);
 }
 
 // HY_FUSE_IP=0 / HY_FUSE_MD=0 run the unfused ModUp NTT + IP / ModDown NTT + epilogue (A/B measurements)
@@ -552,9 +553,27 @@ void moddown_batch(hy_ctx* c, uint32_t level, int npoly, int G, const DownItem* 
 // Split ModDown, first half: the P limbs of u_g (computed first) -> iNTT -> P -> Q_l conversion -> forward
 // column pass into w_g [2][l+1][N]; the second half is launch_rows_ip_final, which computes the Q limbs
 // of the inner product and finishes (u - w) P^{-1} without storing them.
+// v_ready: v already holds the P limbs after their inverse row pass (fused into the P-limb IP).
 void moddown_p(hy_ctx* c, uint32_t level, int G, uint64_t* const* u, uint64_t* const* v, uint64_t* const* w,
-               cudaStream_t s) {
+               cudaStream_t s, bool v_ready = false) {
   const int n = level + 1, E = n + c->n_p, K = c->n_p;
+  if (moddown_cols_ok(c)) {  // inverse row pass (unless fused upstream), then one fused column kernel
+    if (!v_ready) {
+      LimbList L;
+      for (int g = 0; g < G; ++g)
+        for (int cc = 0; cc < 2; ++cc)
+          for (int k = 0; k < K; ++k)
+            L.add(u[g] + ((size_t)cc * E + n + k) * c->N, v[g] + ((size_t)cc * K + k) * c->N, c->n_q + k);
+      rows_list(c, L, true, s);
+    }
+    ModUpColsArgs ma{};
+    for (int g = 0; g < G; ++g) {
+      ma.src[g] = v[g];
+      ma.ext[g] = w[g];
+    }
+    launch_moddown_cols(c, ma, G, level, s);
+    return;
+  }
   LimbList L;
   for (int g = 0; g < G; ++g)
     for (int cc = 0; cc < 2; ++cc)
@@ -661,13 +680,16 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
     if (alias) automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
     else automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
     if (split_moddown()) {
-      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s, (int)n);
       uint64_t* v[kG];
       uint64_t* w[kG];
-      IpFinalArgs fa{};
       for (int g = 0; g < G; ++g) {
         v[g] = it[g].v;
         w[g] = it[g].w;
+      }
+      const bool vr = moddown_cols_ok(c);  // P-limb IP with the inverse row pass fused
+      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s, (int)n, vr ? v : nullptr);
+      IpFinalArgs fa{};
+      for (int g = 0; g < G; ++g) {
         fa.ext[g] = ext[g];
         fa.own[g] = rc1[g];
         fa.evk[g] = keys[g];
@@ -678,7 +700,7 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
         fa.out[g] = di[g].out;
         fa.kx[g] = 1;
       }
-      moddown_p(c, level, G, u, v, w, s);
+      moddown_p(c, level, G, u, v, w, s, vr);
       launch_rows_ip_final(c, fa, G, level, false, s);
       done += G;
       continue;

@@ -314,6 +314,26 @@ __device__ __forceinline__ void rows_forward_l3(double (&x)[8], int l, double* S
   __syncwarp();
 }
 
+// The inverse row stages of one 256-word row from layout L3 (|v| <= q/2 + 1) to layout L1 (between-pass
+// format, as k_ntt_rows<false> leaves it), S = the warp's transpose buffer, T = the row's inverse heap.
+__device__ __forceinline__ void rows_inverse_from_l3(double (&x)[8], int l, double* S, const double* T, double q,
+                                                     double qinv) {
+  run_stages<3, false>(x, l, 1, 0, T, q, qinv);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[pidx(elem<3>(l, k))] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
+  run_stages<2, false>(x, l, 4, 2, T, q, qinv);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<1>(l, k))];
+  run_stages<1, false>(x, l, 7, 5, T, q, qinv);
+}
+
 // Layout L3 holds words 4(l + 32h) + m (m < 4) in x[4h + m]: two 32-byte runs per lane.
 __device__ __forceinline__ void load_l3(const uint64_t* __restrict__ p, int l, ulonglong2 (&v)[4], bool stream) {
 #pragma unroll
@@ -357,7 +377,7 @@ __device__ __forceinline__ void store_l3(uint64_t* p, int l, const double (&x)[8
 template <int B, bool SUM>
 __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ RowsIpArgs a, int G, DevTables dt,
                                                         int level, int n_q, int L1, int E, int alpha, int logN,
-                                                        int accumulate, int u0) {
+                                                        int accumulate, int u0, int inv_p) {
   __shared__ double sm[8][272];
   __shared__ double tws[8][256];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -411,6 +431,22 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
       for (int k = 0; k < 8; ++k) {
         s0[k] += fred(a0[k], q, qinv);
         s1[k] += fred(a1[k], q, qinv);
+      }
+    } else if (inv_p) {
+      // split ModDown: the P limb's inverse row pass straight from registers (layout L3), stored in the
+      // between-pass format for the ModDown column kernel: v_g[c][u - (l+1)]
+      __syncwarp();
+      load_twiddles_warp(T, dt.itw + (size_t)t * N, (uint32_t)R + (uint32_t)row, l);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fred(c ? a1[k] : a0[k], q, qinv);
+        __syncwarp();
+        rows_inverse_from_l3(x, l, S, T, q, qinv);
+        uint64_t* dst = a.v[g] + ((size_t)c * (E - level - 1) + (u - level - 1)) * N + roff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2raw(x[k]);
       }
     } else {
       store_l3(a.u[g] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
@@ -581,41 +617,54 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
   }
 }
 
-// ---------------------------------------------------------------- ModUp: iNTT column pass + BConv + NTT column pass
+// ---------------------------------------------------------------- iNTT column pass + fast BConv + NTT column pass
 // CTA = 256 threads on one 8-column strip (thread: column c = tid & 7, lane l = tid >> 3; the
 // k_ntt_cols256 scheme at half width, so that two CTAs of 126-register threads share an SM and one
-// CTA's barriers are covered by the other's work) of item g = blockIdx.z, digit j = blockIdx.y.  Phase i < A: inverse column stages of
-// source limb lo + i, ending in layout L1 with y_i = [d_i (D_j/q_i)^{-1}]_{q_i} (canonical: the fast
-// BConv lifts y_i as an integer in [0, q_i)) kept in registers; N^{-1} is folded into that constant.
-// Then one phase per non-own limb u: x = fred(sum_i fmulmod(y_i, (D_j/q_i) mod t_u)) (|x| <= t/2 + 1)
-// goes straight into the forward column stages and is stored fred-reduced (between-pass format).
-// The coefficient-domain digit and the un-transformed BConv output never reach HBM.  The next phase's
+// CTA's barriers are covered by the other's work) of item g = blockIdx.z and group blockIdx.y.
+//   ModUp (DOWN = false), group = digit j: sources = the digit's A limbs of c1 (after the inverse row
+//     pass), y_i = [d_i (D_j/q_i)^{-1}]_{q_i}; targets = every limb u of Q_l u P outside the digit,
+//     x = [sum_i y_i ((D_j/q_i) mod t_u)]; out = ext_g[j][u].
+//   ModDown (DOWN = true), group = poly c: sources = the K P-limbs of the inner product u_g[c] (after the
+//     inverse row pass), z_k = [v_k (P/p_k)^{-1}]_{p_k}; targets = the l+1 limbs q_i,
+//     x = [sum_k z_k ((P/p_k) mod q_i)]; out = w_g[c][i].
+// Phase i < A: inverse column stages of source i, ending in layout L1 with the source word (canonical:
+// the fast BConv lifts it as an integer) kept in registers; N^{-1} is folded into its constant.  Then one
+// phase per target: x = fred(sum_i fmulmod(y_i, hat_i)) (|x| <= t/2 + 1) goes straight into the forward
+// column stages and is stored fred-reduced (between-pass format, for the fused row kernels).  The
+// coefficient-domain sources and the un-transformed conversion never reach HBM.  The next phase's
 // twiddle heap is fetched into a register during the current phase (double-buffered T).
-template <int A>
-__global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ ModUpColsArgs a,
-                                                       const ModUpConst* mc, DevTables dt, int level, int n_q, int E,
-                                                       int logN) {
+template <int A, bool DOWN>
+__global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ ModUpColsArgs a,
+                                                       const ModUpConst* mc, const ModDownConst* md, DevTables dt,
+                                                       int level, int n_q, int E, int logN) {
   __shared__ double sm[8 * 256];
   __shared__ double T[2][256];
   __shared__ double s_hat[kMaxExt][A];
   const int c = threadIdx.x & 7, l = threadIdx.x >> 3, tid = threadIdx.x;
   const int col = blockIdx.x * 8 + c, j = blockIdx.y, g = blockIdx.z;
   const size_t N = (size_t)1 << logN;
-  const ModUpConst& m = mc[j];
-  const int lo = m.lo, nsrc = m.hi - m.lo, nph = E;  // nsrc inverse phases + (E - nsrc) targets
-  for (int i = tid; i < E * A; i += blockDim.x) {
-    const int u = i / A, ii = i % A;
-    s_hat[u][ii] = ii < nsrc ? (double)m.hat_mod[u][ii] : 0.0;
+  const int n = level + 1;
+  int lo = 0, nsrc = A, nph = A + n;  // DOWN: K sources, l+1 targets
+  if constexpr (!DOWN) {
+    lo = mc[j].lo;
+    nsrc = mc[j].hi - mc[j].lo;
+    nph = E;  // nsrc inverse phases + (E - nsrc) targets
   }
-  // phase p -> (chain index, twiddle table); phases [0, nsrc) inverse, then the targets in order
-  auto target = [&](int p) {  // p >= nsrc: the (p - nsrc)-th ext limb outside [lo, hi)
+  for (int i = tid; i < (DOWN ? n : E) * A; i += blockDim.x) {
+    const int u = i / A, ii = i % A;
+    if constexpr (DOWN) s_hat[u][ii] = (double)md->phat_mod[u][ii];
+    else s_hat[u][ii] = ii < nsrc ? (double)mc[j].hat_mod[u][ii] : 0.0;
+  }
+  // target phase p >= nsrc -> target index (ModUp: the (p - nsrc)-th ext limb outside [lo, hi))
+  auto target = [&](int p) {
     const int k = p - nsrc;
-    return k < lo ? k : k + nsrc;
+    return (DOWN || k < lo) ? k : k + nsrc;
   };
+  auto src_chain = [&](int p) { return DOWN ? n_q + p : lo + p; };
+  auto tgt_chain = [&](int u) { return (DOWN || u <= level) ? u : n_q + (u - level - 1); };
   auto table = [&](int p) -> const double* {
-    if (p < nsrc) return dt.itw + (size_t)(lo + p) * N;
-    const int u = target(p);
-    return dt.tw + (size_t)(u <= level ? u : n_q + (u - level - 1)) * N;
+    if (p < nsrc) return dt.itw + (size_t)src_chain(p) * N;
+    return dt.tw + (size_t)tgt_chain(target(p)) * N;
   };
   if (tid > 0 && tid < 256) T[0][tid] = table(0)[tid];
   double y[A][8];
@@ -628,10 +677,10 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
     const double tw_next = (p + 1 < nph && tid > 0 && tid < 256) ? table(p + 1)[tid] : 0.0;
     const double* Tp = T[p & 1];
     double x[8];
-    if (p < nsrc) {  // inverse column pass of source limb lo + p
-      const PrimeConst& pc = dt.pc[lo + p];
+    if (p < nsrc) {  // inverse column pass of source p
+      const PrimeConst& pc = dt.pc[src_chain(p)];
       const double q = pc.qd, qinv = pc.qinv;
-      const uint64_t* src = a.src[g] + (size_t)(lo + p) * N + col;
+      const uint64_t* src = a.src[g] + (size_t)(DOWN ? j * A + p : lo + p) * N + col;
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = raw2d(src[(size_t)elem<3>(l, k) * 256]);
       run_stages<3, false>(x, l, 1, 0, Tp, q, qinv);
@@ -648,16 +697,17 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<1>(l, k), c)];
       run_stages<1, false>(x, l, 7, 5, Tp, q, qinv);
-      const double cst = fcanon(fmulmod(pc.n_inv_d, (double)m.hat_inv[p], q, qinv), q, qinv);
+      const double hinv = DOWN ? (double)md->phat_inv[p] : (double)mc[j].hat_inv[p];
+      const double cst = fcanon(fmulmod(pc.n_inv_d, hinv, q, qinv), q, qinv);
 #pragma unroll
       for (int i = 0; i < A; ++i)
         if (i == p) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) y[i][k] = fcanon(fmulmod(x[k], cst, q, qinv), q, qinv);
         }
-    } else {  // BConv to limb u, then the forward column pass
+    } else {  // BConv to target u, then the forward column pass
       const int u = target(p);
-      const PrimeConst& pc = dt.pc[u <= level ? u : n_q + (u - level - 1)];
+      const PrimeConst& pc = dt.pc[tgt_chain(u)];
       const double q = pc.qd, qinv = pc.qinv;
       double h[A];
 #pragma unroll
@@ -683,7 +733,7 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<3>(l, k), c)];
       run_stages<3, true>(x, l, 1, 0, Tp, q, qinv);
-      uint64_t* dst = a.ext[g] + ((size_t)j * E + u) * N + col;
+      uint64_t* dst = a.ext[g] + (size_t)(DOWN ? j * n + u : j * E + u) * N + col;
 #pragma unroll
       for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256] = d2raw(fred(x[k], q, qinv));
     }
@@ -695,6 +745,7 @@ __global__ void __launch_bounds__(256, 2) k_modup_cols(const __grid_constant__ M
 }  // namespace
 
 bool modup_cols_ok(const hy_ctx* c) { return c->N == 65536 && c->alpha <= 4; }
+bool moddown_cols_ok(const hy_ctx* c) { return c->N == 65536 && c->n_p <= 4; }
 
 void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
   if (b.n == 0) return;
@@ -718,11 +769,29 @@ void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level,
   const ModUpConst* mc = c->d_modup[level];
   const int nq = (int)c->n_q, lg = (int)c->log_n, lv = (int)level;
   switch (c->alpha) {
-    case 1: k_modup_cols<1><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 2: k_modup_cols<2><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 3: k_modup_cols<3><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
-    case 4: k_modup_cols<4><<<grid, 256, 0, s>>>(a, mc, c->dt, lv, nq, E, lg); break;
+    case 1: k_bconv_cols<1, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
+    case 2: k_bconv_cols<2, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
+    case 3: k_bconv_cols<3, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
+    case 4: k_bconv_cols<4, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
     default: break;  // callers check modup_cols_ok
+  }
+}
+
+void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  const int n = (int)level + 1, E = n + (int)c->n_p;
+  dim3 grid(32, 2, G);
+  KTimer kt(c, FAM_MODDOWN, s);
+  // algorithmic bytes: the 2K P limbs in, the 2(l+1) conversion limbs out
+  kt.bytes = (uint64_t)G * 2 * (c->n_p + n) * c->N * 8;
+  const ModDownConst* md = c->d_moddown[level];
+  const int nq = (int)c->n_q, lg = (int)c->log_n, lv = (int)level;
+  switch (c->n_p) {
+    case 1: k_bconv_cols<1, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
+    case 2: k_bconv_cols<2, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
+    case 3: k_bconv_cols<3, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
+    case 4: k_bconv_cols<4, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
+    default: break;  // callers check moddown_cols_ok
   }
 }
 
@@ -750,7 +819,7 @@ void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
 }
 
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0) {
+                        cudaStream_t s, int u0, bool inv_p) {
   if (G <= 0) return;
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
   const int nu = E - u0;  // extended limbs produced
@@ -771,10 +840,11 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
   case BB:                                                                                                     \
     if (sum)                                                                                                   \
       k_ntt_rows_ip<BB, true><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E, (int)c->alpha, \
-                                                   (int)c->log_n, accumulate ? 1 : 0, u0);                     \
+                                                   (int)c->log_n, accumulate ? 1 : 0, u0, inv_p);             \
     else                                                                                                       \
       k_ntt_rows_ip<BB, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,              \
-                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0);     \
+                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0,      \
+                                                    inv_p);                                                    \
     break;
   switch (beta) {
     HY_RIP(1)
