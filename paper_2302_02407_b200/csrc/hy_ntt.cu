@@ -617,6 +617,173 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
   }
 }
 
+// ---------------------------------------------------------------- the same, rows staged by bulk async copies
+// (TMA bulk engine, cp.async.bulk + mbarrier): every 2 KB row a warp consumes -- the two evk rows and the
+// digit row of each digit, then the two conversion rows w_g[0][i], w_g[1][i] and the c0 row of the gather --
+// is copied global -> shared by one lane one step ahead (two stages per warp), so the row loads of digit
+// j + 1 are in flight while digit j is transformed and multiplied, without staging registers.  The digit
+// row's stage buffer doubles as the warp's transpose buffer once it is in registers.  Hoisted: the Galois
+// permutation maps a 256-word row onto one row (the high index bits of kappa depend only on high bits), so
+// the source row is copied whole and gathered from shared memory.
+namespace tma {
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint64_t* b) {  // 2048 bytes
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 2048, [%2];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(saddr(b))
+               : "memory");
+}
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+}  // namespace tma
+
+constexpr int kRowWarpWords = 256 * 7;  // per warp: twiddle heap + 2 stages x (e0, e1, x) rows
+constexpr size_t kRowsTmaSmem = 8 * (kRowWarpWords * 8 + 16);
+
+template <int B, bool HOIST>
+__global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
+                                                              const ModDownConst* md, int level, int L1, int E,
+                                                              int alpha, int logN) {
+  extern __shared__ __align__(128) double dsm[];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t N = (size_t)1 << logN;
+  const int R = (int)(N >> 8);
+  const int g = blockIdx.x, row = blockIdx.y * 8 + w, i = blockIdx.z;
+  if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
+  double* T = dsm + (size_t)w * kRowWarpWords;  // stage s at T + 256 + 768 s: e0 row, e1 row, digit (x) row
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * kRowWarpWords) + 2 * w;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  const int own_digit = i / alpha;
+  const size_t roff = (size_t)row * 256;
+  // source rows of the permuted reads (hoisted digits; the c0 gather)
+  const uint32_t rowx = HOIST && a.kx[g] != 1 ? aut_index((uint32_t)roff, a.kx[g], logN) >> 8 : (uint32_t)row;
+  const uint64_t k0 = a.add0[g] ? a.k0[g] : 1;
+  const uint32_t row0 = k0 != 1 ? aut_index((uint32_t)roff, k0, logN) >> 8 : (uint32_t)row;
+  // iteration j < B: digit j; j == B: the ModDown epilogue (w rows and the c0 row)
+  auto issue = [&](int j) {
+    double* b = T + 256 + 768 * (j & 1);
+    uint64_t* mb = mbar + (j & 1);
+    if (j < B) {
+      const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
+      const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N) +
+                           (HOIST ? (size_t)rowx * 256 : roff);
+      tma::mbar_expect(mb, 3 * 2048);
+      tma::bulk_row(b, e0, mb);
+      tma::bulk_row(b + 256, e0 + (size_t)L1 * N, mb);
+      tma::bulk_row(b + 512, xs, mb);
+    } else {
+      const bool c0 = a.add0[g] != nullptr;
+      tma::mbar_expect(mb, (c0 ? 3 : 2) * 2048);
+      tma::bulk_row(b, a.w[g] + (size_t)i * N + roff, mb);
+      tma::bulk_row(b + 256, a.w[g] + ((size_t)(level + 1) + i) * N + roff, mb);
+      if (c0) tma::bulk_row(b + 512, a.add0[g] + (size_t)i * N + (size_t)row0 * 256, mb);
+    }
+  };
+  // hoisted: in-row positions of the 8 gathered words, packed 4 per register
+  uint32_t gpk[2] = {0, 0};
+  if (HOIST) {
+    const uint64_t kx = a.kx[g];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+      gpk[k >> 2] |= ((kx != 1 ? aut_index(xi, kx, logN) : xi) & 255u) << (8 * (k & 3));
+    }
+  }
+  if (l == 0) {
+    tma::mbar_init(mbar);
+    tma::mbar_init(mbar + 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    issue(0);
+  }
+  load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
+  __syncwarp();
+  double a0[8], a1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j <= B; ++j) {
+    if (l == 0 && j < B) issue(j + 1);  // the stage it fills was released at the end of iteration j - 1
+    double* b = T + 256 + 768 * (j & 1);
+    tma::mbar_wait(mbar + (j & 1), (uint32_t)(j >> 1) & 1);
+    if (j < B) {
+      double x[8];
+      const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
+      if (HOIST) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = u2d(xb[(gpk[k >> 2] >> (8 * (k & 3))) & 255]);
+      } else if (j == own_digit) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = u2d(xb[elem<3>(l, k)]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = raw2d(xb[elem<1>(l, k)]);
+        __syncwarp();
+        rows_forward_l3(x, l, b + 512, T, q, qinv);  // the row buffer is now the transpose buffer
+      }
+      const uint64_t* e0 = reinterpret_cast<const uint64_t*>(b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a0[k] += fmulmod(x[k], u2d(e0[elem<3>(l, k)]), q, qinv);
+        a1[k] += fmulmod(x[k], u2d(e0[256 + elem<3>(l, k)]), q, qinv);
+      }
+    } else {
+      const double pinv = (double)md->p_inv[i];
+      const uint64_t* c0b = reinterpret_cast<const uint64_t*>(b + 512);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const uint64_t* wb = reinterpret_cast<const uint64_t*>(b + 256 * c);
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = raw2d(wb[elem<1>(l, k)]);
+        __syncwarp();
+        rows_forward_l3(x, l, b + 256 * c, T, q, qinv);  // w_c's own buffer as the transpose buffer
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fmulmod(fred(c ? a1[k] : a0[k], q, qinv) - x[k], pinv, q, qinv);
+        if (c == 0 && a.add0[g]) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+            x[k] += u2d(c0b[(k0 != 1 ? aut_index(xi, k0, logN) : xi) & 255]);
+          }
+        }
+        if (c == 1 && a.add1[g]) {
+          ulonglong2 v[4];
+          load_l3(a.add1[g] + (size_t)i * N + roff, l, v, false);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+        }
+        const size_t o = ((size_t)c * (level + 1) + i) * N + roff;
+        if (a.addct[g]) {
+          ulonglong2 v[4];
+          load_l3(a.addct[g] + o, l, v, false);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] += l3_word(v, k);
+        }
+        store_l3(a.out[g] + o, l, x, q, qinv, false);
+      }
+    }
+    // release the stage: every lane's generic accesses before the next bulk write into it
+    tma::proxy_fence();
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- iNTT column pass + fast BConv + NTT column pass
 // CTA = 256 threads on one 8-column strip (thread: column c = tid & 7, lane l = tid >> 3; the
 // k_ntt_cols256 scheme at half width, so that two CTAs of 126-register threads share an SM and one
@@ -879,10 +1046,26 @@ void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level
   kt.bytes = (digits + (uint64_t)keys * 2 * beta * n + (uint64_t)G * 4 * n + extra) * c->N * 8;
   const int L1 = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
   const ModDownConst* md = c->d_moddown[level];
-#define HY_RIF(BB)                                                                                     \
-  case BB:                                                                                             \
-    if (hoisted) k_rows_ip_final<BB, true><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);      \
-    else k_rows_ip_final<BB, false><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);             \
+  // HY_TMA=0: register loads instead of the bulk-copy staged rows (A/B; staged: +0.2 % plain, +3 % hoisted)
+  static const bool use_tma = getenv("HY_TMA") == nullptr || atoi(getenv("HY_TMA")) != 0;
+#define HY_RIF(BB)                                                                                            \
+  case BB:                                                                                                    \
+    if (use_tma) {                                                                                            \
+      static bool attr = false;                                                                               \
+      if (!attr) {                                                                                            \
+        cudaFuncSetAttribute(k_rows_ip_final_tma<BB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                             (int)kRowsTmaSmem);                                                              \
+        cudaFuncSetAttribute(k_rows_ip_final_tma<BB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             (int)kRowsTmaSmem);                                                              \
+        attr = true;                                                                                          \
+      }                                                                                                       \
+      if (hoisted) k_rows_ip_final_tma<BB, true><<<grid, 256, kRowsTmaSmem, s>>>(a, c->dt, md, lv, L1, E, al, lg); \
+      else k_rows_ip_final_tma<BB, false><<<grid, 256, kRowsTmaSmem, s>>>(a, c->dt, md, lv, L1, E, al, lg);       \
+    } else if (hoisted) {                                                                                     \
+      k_rows_ip_final<BB, true><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);                        \
+    } else {                                                                                                  \
+      k_rows_ip_final<BB, false><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);                       \
+    }                                                                                                         \
     break;
   switch (beta) {
     HY_RIF(1)
