@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBl
   double acc[M][2];
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  // unrolled so that the loads of several operands are in flight together (the stream is HBM-bound)
+#pragma unroll 4
   for (int j = 0; j < J; ++j) {
     const double c0 = u2d(b.ct[j][(size_t)i * N + x]), c1 = u2d(b.ct[j][(n + i) * N + x]);
 #pragma unroll
