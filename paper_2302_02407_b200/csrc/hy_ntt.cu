@@ -652,10 +652,11 @@ __device__ __forceinline__ void bulk_row(void* dst, const void* src, uint64_t* b
 __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 }  // namespace tma
 
-constexpr int kRowWarpWords = 256 * 7;  // per warp: twiddle heap + 2 stages x (e0, e1, x) rows
-constexpr size_t kRowsTmaSmem = 8 * (kRowWarpWords * 8 + 16);
+// per warp: twiddle heap + NST stages x (e0, e1, x) rows, and NST mbarriers
+__host__ __device__ constexpr int rows_warp_words(int nst) { return 256 * (1 + 3 * nst); }
+constexpr size_t rows_tma_smem(int nst) { return 8 * ((size_t)rows_warp_words(nst) * 8 + 8 * nst); }
 
-template <int B, bool HOIST>
+template <int B, bool HOIST, int NST>
 __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
                                                               const ModDownConst* md, int level, int L1, int E,
                                                               int alpha, int logN) {
@@ -665,8 +666,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   const int R = (int)(N >> 8);
   const int g = blockIdx.x, row = blockIdx.y * 8 + w, i = blockIdx.z;
   if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
-  double* T = dsm + (size_t)w * kRowWarpWords;  // stage s at T + 256 + 768 s: e0 row, e1 row, digit (x) row
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * kRowWarpWords) + 2 * w;
+  double* T = dsm + (size_t)w * rows_warp_words(NST);  // stage s at T + 256 + 768 s: e0, e1, digit (x) rows
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * rows_warp_words(NST)) + NST * w;
   const PrimeConst& pc = dt.pc[i];
   const double q = pc.qd, qinv = pc.qinv;
   const int own_digit = i / alpha;
@@ -677,8 +678,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   const uint32_t row0 = k0 != 1 ? aut_index((uint32_t)roff, k0, logN) >> 8 : (uint32_t)row;
   // iteration j < B: digit j; j == B: the ModDown epilogue (w rows and the c0 row)
   auto issue = [&](int j) {
-    double* b = T + 256 + 768 * (j & 1);
-    uint64_t* mb = mbar + (j & 1);
+    double* b = T + 256 + 768 * (j % NST);
+    uint64_t* mb = mbar + j % NST;
     if (j < B) {
       const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
       const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N) +
@@ -706,10 +707,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
     }
   }
   if (l == 0) {
-    tma::mbar_init(mbar);
-    tma::mbar_init(mbar + 1);
+    for (int t = 0; t < NST; ++t) tma::mbar_init(mbar + t);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    issue(0);
+    for (int t = 0; t < NST - 1 && t <= B; ++t) issue(t);
   }
   load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
   __syncwarp();
@@ -718,9 +718,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
 #pragma unroll 1
   for (int j = 0; j <= B; ++j) {
-    if (l == 0 && j < B) issue(j + 1);  // the stage it fills was released at the end of iteration j - 1
-    double* b = T + 256 + 768 * (j & 1);
-    tma::mbar_wait(mbar + (j & 1), (uint32_t)(j >> 1) & 1);
+    if (l == 0 && j + NST - 1 <= B) issue(j + NST - 1);  // its stage was released at the end of j - 1
+    double* b = T + 256 + 768 * (j % NST);
+    tma::mbar_wait(mbar + j % NST, (uint32_t)(j / NST) & 1);
     if (j < B) {
       double x[8];
       const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
@@ -1048,19 +1048,27 @@ void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level
   const ModDownConst* md = c->d_moddown[level];
   // HY_TMA=0: register loads instead of the bulk-copy staged rows (A/B; staged: +0.2 % plain, +3 % hoisted)
   static const bool use_tma = getenv("HY_TMA") == nullptr || atoi(getenv("HY_TMA")) != 0;
+  // HY_TMA_STAGES: depth of the per-warp bulk-copy ring (2: two CTAs per SM; 3 or 4: one CTA per SM)
+  static const int nst = getenv("HY_TMA_STAGES") ? atoi(getenv("HY_TMA_STAGES")) : 2;
+#define HY_TMA_LAUNCH(BB, HH, NS)                                                                             \
+  {                                                                                                           \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      cudaFuncSetAttribute(k_rows_ip_final_tma<BB, HH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           (int)rows_tma_smem(NS));                                                           \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    k_rows_ip_final_tma<BB, HH, NS><<<grid, 256, rows_tma_smem(NS), s>>>(a, c->dt, md, lv, L1, E, al, lg);    \
+  }
+#define HY_TMA_NST(BB, HH)                   \
+  if (nst <= 2) HY_TMA_LAUNCH(BB, HH, 2)     \
+  else if (nst == 3) HY_TMA_LAUNCH(BB, HH, 3) \
+  else HY_TMA_LAUNCH(BB, HH, 4)
 #define HY_RIF(BB)                                                                                            \
   case BB:                                                                                                    \
     if (use_tma) {                                                                                            \
-      static bool attr = false;                                                                               \
-      if (!attr) {                                                                                            \
-        cudaFuncSetAttribute(k_rows_ip_final_tma<BB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                             (int)kRowsTmaSmem);                                                              \
-        cudaFuncSetAttribute(k_rows_ip_final_tma<BB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                             (int)kRowsTmaSmem);                                                              \
-        attr = true;                                                                                          \
-      }                                                                                                       \
-      if (hoisted) k_rows_ip_final_tma<BB, true><<<grid, 256, kRowsTmaSmem, s>>>(a, c->dt, md, lv, L1, E, al, lg); \
-      else k_rows_ip_final_tma<BB, false><<<grid, 256, kRowsTmaSmem, s>>>(a, c->dt, md, lv, L1, E, al, lg);       \
+      if (hoisted) HY_TMA_NST(BB, true)                                                                       \
+      else HY_TMA_NST(BB, false)                                                                              \
     } else if (hoisted) {                                                                                     \
       k_rows_ip_final<BB, true><<<grid, 256, 0, s>>>(a, c->dt, md, lv, L1, E, al, lg);                        \
     } else {                                                                                                  \
@@ -1079,6 +1087,8 @@ void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level
       HY_RIF(8)
   }
 #undef HY_RIF
+#undef HY_TMA_NST
+#undef HY_TMA_LAUNCH
 }
 
 void launch_ntt(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s) {
