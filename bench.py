@@ -241,7 +241,7 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
     import torch
 
     import paper_2302_02407_b200 as hy
-    from paper_2302_02407_b200.dist import all_gather_cts, shard
+    from paper_2302_02407_b200.dist import all_gather_cts, raconv_tap_sharded, shard
 
     sk, ek = synth.SEED_SK, synth.SEED_EVK
     keys = {}
@@ -268,7 +268,13 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
         like = ctx.empty(*ctx.ct_shape(lo))
         evks = [keys[r] for r in p.rots]
 
+        tap_shard = algo == "RA" and ws > 1 and p.n_out < ws  # ResNet-20 RAConv: one output, shard the taps
+
         def step():
+            if tap_shard:  # every rank ends with every output: no gather
+                for o in range(p.n_out):
+                    raconv_tap_sharded(p, evks, cts, level, pts, o, scratch)
+                return
             if e > b:
                 p.run(evks, cts, level, pts, scratch, b, e, outs)
             if ws > 1:
@@ -286,6 +292,7 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
                 fams[fn] = round(t, 3)
         ctx.time_kernels(0)
         layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
+                        "sharding": "taps (all-reduce)" if tap_shard else ("outputs (all-gather)" if ws > 1 else None),
                         "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S,
                         "family_ms": fams}
         total += mult * ms

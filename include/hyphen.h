@@ -227,6 +227,27 @@ hy_status hy_caconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const
 hy_status hy_raconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
                     const uint64_t* const* d_in, uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch,
                     uint32_t out_begin, uint32_t out_end, uint64_t* const* d_out, void* stream);
+/* RAConv tap sharding: the multi-GPU exchange step for layers with fewer outputs than GPUs (ResNet-20
+ * RAConv has one output ciphertext).  An output of RAConv_Reorder is
+ * sum_t HRot_{r_t}(acc_t) over the f^2 taps with ONE ModDown (Alg. P:727-733).  hy_raconv_partial
+ * computes, for output out_index and taps [tap_begin, tap_end), the state before that ModDown into
+ * d_state (hy_raconv_partial_words words, caller-allocated):
+ *   [2][l+1+K][N]  sum of the taps' key-switch inner products over Q_l u P (NTT domain, canonical),
+ *   [2][l+1][N]    (sum_t kappa_t(c0_t), the centre tap's c1) -- canonical.
+ * States of disjoint tap ranges may be added as unsigned 64-bit integers (e.g. an int64 all-reduce SUM
+ * over ranks; every word stays below ranks * 2^48); hy_raconv_finish reduces the sum mod q, runs the
+ * ModDown, rescale, RaS_g and IR_g (in place on d_state and d_scratch) and writes output out_index at
+ * level l - 1 - has_mask, bit-identical to hy_raconv.  An empty tap range yields an all-zero state.
+ * Errors: HY_E_PLAN (not an RAConv plan, index or tap range outside the plan), HY_E_LEVEL_EXHAUSTED,
+ * HY_E_MISSING_KEY, HY_E_WORKSPACE. */
+size_t hy_raconv_partial_words(const hy_ctx* ctx, uint32_t level);
+hy_status hy_raconv_partial(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
+                            const uint64_t* const* d_in, uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch,
+                            uint32_t out_index, uint32_t tap_begin, uint32_t tap_end, uint64_t* d_state,
+                            void* stream);
+hy_status hy_raconv_finish(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks, uint32_t level,
+                           const uint64_t* d_pts, uint64_t* d_state, uint64_t* d_scratch, uint32_t out_index,
+                           uint64_t* d_out, void* stream);
 
 /* ---- client side: keys, encode, encrypt, decrypt (untimed) ------- */
 /* Rotation key for Galois element of a left rotation by r (DESIGN R-EVK, R-PRNG):

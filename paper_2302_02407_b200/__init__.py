@@ -90,6 +90,9 @@ SIGNATURES = {
     "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), _U32, _P, _P]),
     "hy_caconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
     "hy_raconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
+    "hy_raconv_partial_words": (C.c_size_t, [_P, _U32]),
+    "hy_raconv_partial": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _U32, _P, _P]),
+    "hy_raconv_finish": (C.c_int, [_P, _P, _PP, _U32, _P, _P, _P, _U32, _P, _P]),
 }
 
 
@@ -382,3 +385,26 @@ class ConvPlan:
         _check(fn(self.ctx._c, self._p, _ptr_array(evks), _ptr_array(cts), level, _ptr(pts), _ptr(scratch),
                   out_begin, out_end, _ptr_array(outs), self.ctx._stream()))
         return outs
+
+    # ---- RAConv tap sharding (include/hyphen.h hy_raconv_partial / hy_raconv_finish)
+    def partial_state(self, level):
+        """An int64 device buffer for the lazy-sum state of one output (summable across ranks)."""
+        return self.ctx.zeros(int(lib().hy_raconv_partial_words(self.ctx._c, level)))
+
+    def raconv_partial(self, evks, cts, level, pts, out_index, tap_begin, tap_end, state, scratch=None):
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        scratch = self.scratch(level) if scratch is None else scratch
+        _check(lib().hy_raconv_partial(self.ctx._c, self._p, _ptr_array(evks), _ptr_array(cts), level, _ptr(pts),
+                                       _ptr(scratch), out_index, tap_begin, tap_end, _ptr(state),
+                                       self.ctx._stream()))
+        return state
+
+    def raconv_finish(self, evks, level, pts, state, out_index, out=None, scratch=None):
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        out = self.ctx.empty(*self.ctx.ct_shape(self.out_level(level))) if out is None else out
+        scratch = self.scratch(level) if scratch is None else scratch
+        _check(lib().hy_raconv_finish(self.ctx._c, self._p, _ptr_array(evks), level, _ptr(pts), _ptr(state),
+                                      _ptr(scratch), out_index, _ptr(out), self.ctx._stream()))
+        return out

@@ -400,6 +400,43 @@ extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, co
 
 namespace {
 
+// RAConv after its lazy Slide_1&Sum_f: rescale, RaS_g, then (with a mask) the IR_g mask product + rescale
+// and the IR_g rotations, batched over the outputs.  dst: per output, a ciphertext buffer at level - 1
+// (the output itself without a mask); tmp: up to 8 temporaries of ct_l words.
+hy_status ra_tail(const Ctx& x, std::vector<const uint64_t*>& sums, std::vector<uint64_t*>& dst, uint32_t level,
+                  const uint64_t* mask, uint64_t* tmp, size_t ct_l, uint64_t* const* out) {
+  const hy_conv_plan* p = x.p;
+  const size_t no = sums.size();
+  hy_status stt = rescale_multi(x.c, sums.data(), (uint32_t)no, level, dst.data(), x.s);
+  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g);
+  if (stt == HY_OK && p->has_mask) {
+    std::vector<uint64_t*> fin(out, out + no);
+    stt = mask_rescale(x, dst, mask, level - 1, tmp, ct_l, fin);
+    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g);
+  }
+  return stt;
+}
+
+// RAConv tap accumulators of output o for taps [tb, te): acc_t = sum_j x_j (.) W'_{o,j,t} (MulFilter&Sum_{c_i})
+hy_status ra_taps(const Ctx& x, const uint64_t* const* in, uint32_t level, const uint64_t* wpt, uint32_t o,
+                  size_t tb, size_t te, uint64_t* const* accs) {
+  const hy_conv_plan* p = x.p;
+  const size_t J = (size_t)p->n_in;
+  std::vector<uint32_t> bidx(J);
+  std::vector<uint64_t> bgal(J);
+  for (size_t t = tb; t < te; ++t) {
+    for (size_t i = 0; i < J; ++i) {
+      const auto tm = p->term(o, (int64_t)i, (int64_t)t);
+      bidx[i] = (uint32_t)tm.first;
+      bgal[i] = hy_galois_elt(x.c, tm.second);
+    }
+    uint64_t* dst = accs[t - tb];
+    hy_status st = pmult_block(x.c, in, (uint32_t)J, &dst, 1, wpt, bidx.data(), bgal.data(), level, 0, x.s);
+    if (st != HY_OK) return st;
+  }
+  return HY_OK;
+}
+
 hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
                    uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
                    uint64_t* const* out, void* stream) {
@@ -554,13 +591,7 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
     sums[o - ob] = sum;
     dst[o - ob] = p->has_mask ? oacc : out[o - ob];  // the output's consumed tap accumulators
   }
-  stt = rescale_multi(c, sums.data(), (uint32_t)no, level, dst.data(), x.s);
-  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g);
-  if (stt == HY_OK && p->has_mask) {
-    std::vector<uint64_t*> fin(out, out + no);
-    stt = mask_rescale(x, dst, mask, level - 1, tmp, ct_l, fin);
-    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g);
-  }
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, out);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv");
 }
@@ -579,4 +610,79 @@ extern "C" hy_status hy_raconv(hy_ctx* c, const hy_conv_plan* p, const uint64_t*
                                uint32_t out_begin, uint32_t out_end, uint64_t* const* out, void* stream) {
   if (p && p->s.algo != HY_CONV_RA) return fail(HY_E_PLAN, "plan is not an RAConv plan");
   return conv_run(c, p, evks, in, level, pts, scratch, out_begin, out_end, out, stream);
+}
+
+extern "C" size_t hy_raconv_partial_words(const hy_ctx* c, uint32_t level) {
+  if (!c) return 0;
+  return (2ull * (level + 1 + c->n_p) + 2ull * (level + 1)) * c->N;
+}
+
+namespace {
+hy_status ra_check(hy_ctx* c, const hy_conv_plan* p, uint32_t level, uint32_t o) {
+  if (!c || !p) return fail(HY_E_ARG, "null");
+  if (p->s.algo != HY_CONV_RA) return fail(HY_E_PLAN, "plan is not an RAConv plan");
+  if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
+  if (o >= p->n_out) return fail(HY_E_PLAN, "output index outside the plan");
+  return HY_OK;
+}
+}  // namespace
+
+extern "C" hy_status hy_raconv_partial(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
+                                       const uint64_t* const* in, uint32_t level, const uint64_t* pts,
+                                       uint64_t* scratch, uint32_t out_index, uint32_t tap_begin, uint32_t tap_end,
+                                       uint64_t* state, void* stream) {
+  hy_status stt = ra_check(c, p, level, out_index);
+  if (stt != HY_OK) return stt;
+  const size_t f2 = (size_t)p->s.f * p->s.f;
+  if (!evks || !in || !pts || !scratch || !state) return fail(HY_E_ARG, "null");
+  if (tap_begin > tap_end || tap_end > f2) return fail(HY_E_PLAN, "tap range outside the filter");
+  for (int64_t i = 0; i < p->n_in; ++i)
+    if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
+  Ctx x{c, p, evks, st(stream)};
+  const size_t N = c->N, nl = level + 1, ct_l = 2 * nl * N, nt = tap_end - tap_begin;
+  uint64_t* u = state;
+  uint64_t* acc = state + 2 * (nl + c->n_p) * N;
+  if (nt == 0) {  // an empty shard contributes zero
+    cudaMemsetAsync(state, 0, hy_raconv_partial_words(c, level) * 8, x.s);
+    return cuda_check("hy_raconv_partial");
+  }
+  std::vector<uint64_t*> accs(nt);
+  std::vector<const uint64_t*> accc(nt), keys(nt);
+  std::vector<int32_t> rs(nt);
+  for (size_t k = 0; k < nt; ++k) {
+    const size_t t = tap_begin + k;
+    accs[k] = scratch + k * ct_l;
+    accc[k] = accs[k];
+    rs[k] = (int32_t)p->taps[t];
+    keys[k] = (p->taps[t] % p->n) ? x.key(p->taps[t]) : nullptr;
+  }
+  stt = ra_taps(x, in, level, pts, out_index, tap_begin, tap_end, accs.data());
+  if (stt == HY_OK)
+    stt = hrot_sum_partial(c, keys.data(), accc.data(), level, rs.data(), (uint32_t)nt, u, acc, x.s);
+  if (stt != HY_OK) return stt;
+  return cuda_check("hy_raconv_partial");
+}
+
+extern "C" hy_status hy_raconv_finish(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, uint32_t level,
+                                      const uint64_t* pts, uint64_t* state, uint64_t* scratch, uint32_t out_index,
+                                      uint64_t* out, void* stream) {
+  hy_status stt = ra_check(c, p, level, out_index);
+  if (stt != HY_OK) return stt;
+  if (!evks || !pts || !state || !scratch || !out) return fail(HY_E_ARG, "null");
+  Ctx x{c, p, evks, st(stream)};
+  const size_t N = c->N, nl = level + 1, ct_l = 2 * nl * N;
+  uint64_t* u = state;
+  uint64_t* acc = state + 2 * (nl + c->n_p) * N;
+  const uint64_t* mask = pts + (size_t)p->n_pt() * nl * N;
+  stt = mod_reduce_ext(c, level, u, acc, x.s);  // the partials were summed as integers
+  uint64_t* sum = scratch;
+  uint64_t* dstb = scratch + ct_l;
+  uint64_t* tmp = scratch + 2 * ct_l;
+  if (stt == HY_OK) stt = hrot_sum_finish(c, level, u, acc, sum, x.s);
+  if (stt != HY_OK) return stt;
+  std::vector<const uint64_t*> sums{sum};
+  std::vector<uint64_t*> dst{p->has_mask ? dstb : out};
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out);
+  if (stt != HY_OK) return stt;
+  return cuda_check("hy_raconv_finish");
 }

@@ -215,6 +215,16 @@ hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_
 hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* const* ct, uint32_t level,
                      const int32_t* r, uint32_t n_items, uint64_t* const* out, const uint64_t* const* addct,
                      cudaStream_t s);
+// Lazy HRotSum split at its ModDown (RAConv tap sharding, hy_conv.cu):
+//   hrot_sum_partial: u [2][l+1+K][N] = sum of the terms' key-switch inner products (NTT, canonical; zero if no
+//                     term is switched), acc [2][l+1][N] = (sum kappa_t(c0_t), sum of the r = 0 terms' c1)
+//   mod_reduce_ext:   u, acc mod q in place (after an integer sum of partials over ranks)
+//   hrot_sum_finish:  out = ModDown(u) + acc
+hy_status hrot_sum_partial(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                           const int32_t* r, uint32_t n, uint64_t* u, uint64_t* acc, cudaStream_t s);
+hy_status mod_reduce_ext(hy_ctx* c, uint32_t level, uint64_t* u, uint64_t* acc, cudaStream_t s);
+hy_status hrot_sum_finish(hy_ctx* c, uint32_t level, const uint64_t* u, const uint64_t* acc, uint64_t* out,
+                          cudaStream_t s);
 // workspace bytes of one batched key-switch item at `level`
 size_t ks_item_bytes(const hy_ctx* c, uint32_t level);
 // out (+)= sum_i ct_i (.) PRot_{k_i}(pt_i), k_i Galois elements (1 = none), PRot fused as a gather (hy_ops.cu)

@@ -876,16 +876,19 @@ extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, con
   return cuda_check("hy_hrot_hoisted");
 }
 
-extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
-                                 const int32_t* r, uint32_t n, uint64_t* out, void* stream) {
-  hy_status s0 = check_level(c, level);
-  if (s0 != HY_OK) return s0;
-  if (!evks || !cts || !r || !out || n == 0) return fail(HY_E_ARG, "null / empty");
-  cudaStream_t s = st(stream);
-  const size_t nl = level + 1, N = c->N;
+namespace hy {
+
+// The lazy HRotSum state of n terms (hy_hrot_sum before its ModDown, DESIGN R-HROT):
+//   u   [2][l+1+K][N]  sum_t of the key-switch inner products IP_t(kappa_t(c1_t)) over Q_l u P (NTT, canonical;
+//                      zero when no term needs a key switch)
+//   acc [2][l+1][N]    (sum_t kappa_t(c0_t) incl. the r = 0 terms' c0, sum of the r = 0 terms' c1)
+// it: cap carved key-switch items (their u / v / w are not used).  *any_ks: some term was key-switched.
+hy_status hrot_sum_state(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                         const int32_t* r, uint32_t n, uint64_t* u, uint64_t* acc, KsItem* it, int cap, bool* any_ks,
+                         cudaStream_t s) {
+  const size_t nl = level + 1, N = c->N, E = nl + c->n_p;
   std::vector<uint32_t> ks, zero;
   for (uint32_t t = 0; t < n; ++t) {
-    if (cts[t] == out) return fail(HY_E_ARG, "output aliases an input");
     if (hy_galois_elt(c, r[t]) == 1) {
       zero.push_back(t);
     } else {
@@ -893,12 +896,6 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
       ks.push_back(t);
     }
   }
-  const int cap = max_items(c, level);
-  if (cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
-  KsItem it[kG];
-  uint64_t* acc = nullptr;
-  s0 = carve(c, level, cap, it, &acc);
-  if (s0 != HY_OK) return s0;
   uint64_t* acc0 = acc;           // sum of kappa(c0_t) (and unrotated c0_t)
   uint64_t* acc1 = acc + nl * N;  // sum of unrotated c1_t
   cudaMemsetAsync(acc, 0, 2 * nl * N * 8, s);
@@ -943,21 +940,106 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
       k_automorph_sum<<<grid, kT, 0, s>>>(ai, ak, G, acc0, c->log_n, (int)nl, c->dt);
     }
     automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
-    uint64_t* u0 = it[0].u;
     if (fuse_ip()) {
-      modup_ip_fused(c, level, G, d, ext, rc1c, keys, &u0, !first, true, s);
+      modup_ip_fused(c, level, G, d, ext, rc1c, keys, &u, !first, true, s);
     } else {
       intt_polys(c, G, rc1c, d, level, s);
       modup_batch(c, level, G, d, ext, s);
-      ip_batch(c, level, G, ext, rc1c, keys, &u0, nullptr, !first, false, true, s);
+      ip_batch(c, level, G, ext, rc1c, keys, &u, nullptr, !first, false, true, s);
     }
     first = false;
     done += G;
   }
-  if (first) {  // no key switching at all: out = accumulated sum
+  if (first) cudaMemsetAsync(u, 0, 2 * E * N * 8, s);
+  *any_ks = !first;
+  return HY_OK;
+}
+
+// hrot_sum_state into caller buffers (carves its own key-switch items)
+hy_status hrot_sum_partial(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                           const int32_t* r, uint32_t n, uint64_t* u, uint64_t* acc, cudaStream_t s) {
+  const int cap = max_items(c, level);
+  if (cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  hy_status s0 = carve(c, level, cap, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  bool any = false;
+  return hrot_sum_state(c, evks, cts, level, r, n, u, acc, it, cap, &any, s);
+}
+
+// out = ModDown(u) + acc (the lazy HRotSum's one ModDown); u, acc canonical.
+hy_status hrot_sum_finish(hy_ctx* c, uint32_t level, const uint64_t* u, const uint64_t* acc, uint64_t* out,
+                          cudaStream_t s) {
+  if (max_items(c, level) == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[1];
+  hy_status s0 = carve(c, level, 1, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  const size_t nl = level + 1, N = c->N;
+  DownItem di{u, out, acc, 1, acc + nl * N, nullptr, it[0].v, it[0].w};
+  moddown_batch(c, level, 2, 1, &di, s);
+  return HY_OK;
+}
+
+// x mod q_t in place for words < 2^64 (sums of canonical residues over ranks): [npoly][nlimb][N], limb i of
+// every poly on chain index chain0[i]
+__global__ void k_mod_reduce(uint64_t* __restrict__ x, const __grid_constant__ Arr<uint64_t> chain, int nlimb,
+                             int logN, DevTables dt) {
+  const size_t N = (size_t)1 << logN;
+  const int i = blockIdx.y % nlimb;
+  const size_t o = (size_t)blockIdx.y * N + blockIdx.x * blockDim.x + threadIdx.x;
+  x[o] = reduce64(x[o], dt.pc[chain.p[i]]);
+}
+
+hy_status mod_reduce_ext(hy_ctx* c, uint32_t level, uint64_t* u, uint64_t* acc, cudaStream_t s) {
+  const int nl = level + 1, E = nl + c->n_p;
+  Arr<uint64_t> ch{};  // kG chain indices per launch: limbs are reduced in slices of at most kG
+  for (int lo = 0; lo < E; lo += kG) {
+    const int m = std::min(kG, E - lo);
+    for (int i = 0; i < m; ++i) ch.p[i] = ext_chain(c, level, lo + i);
+    for (int p = 0; p < 2; ++p) {
+      dim3 g(c->N / kT, m);
+      KTimer kt(c, FAM_ELEM, s);
+      kt.bytes = 2ull * m * c->N * 8;
+      k_mod_reduce<<<g, kT, 0, s>>>(u + ((size_t)p * E + lo) * c->N, ch, m, c->log_n, c->dt);
+    }
+  }
+  for (int lo = 0; lo < nl; lo += kG) {
+    const int m = std::min(kG, nl - lo);
+    for (int i = 0; i < m; ++i) ch.p[i] = lo + i;
+    for (int p = 0; p < 2; ++p) {
+      dim3 g(c->N / kT, m);
+      KTimer kt(c, FAM_ELEM, s);
+      kt.bytes = 2ull * m * c->N * 8;
+      k_mod_reduce<<<g, kT, 0, s>>>(acc + ((size_t)p * nl + lo) * c->N, ch, m, c->log_n, c->dt);
+    }
+  }
+  return HY_OK;
+}
+
+}  // namespace hy
+
+extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                                 const int32_t* r, uint32_t n, uint64_t* out, void* stream) {
+  hy_status s0 = check_level(c, level);
+  if (s0 != HY_OK) return s0;
+  if (!evks || !cts || !r || !out || n == 0) return fail(HY_E_ARG, "null / empty");
+  for (uint32_t t = 0; t < n; ++t)
+    if (cts[t] == out) return fail(HY_E_ARG, "output aliases an input");
+  cudaStream_t s = st(stream);
+  const size_t nl = level + 1, N = c->N;
+  const int cap = max_items(c, level);
+  if (cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  uint64_t* acc = nullptr;
+  s0 = carve(c, level, cap, it, &acc);
+  if (s0 != HY_OK) return s0;
+  bool any_ks = false;
+  s0 = hrot_sum_state(c, evks, cts, level, r, n, it[0].u, acc, it, cap, &any_ks, s);
+  if (s0 != HY_OK) return s0;
+  if (!any_ks) {  // no key switching at all: out = accumulated sum
     cudaMemcpyAsync(out, acc, 2 * nl * N * 8, cudaMemcpyDeviceToDevice, s);
   } else {
-    DownItem di{it[0].u, out, acc0, 1, zero.empty() ? nullptr : acc1, nullptr, it[0].v, it[0].w};
+    DownItem di{it[0].u, out, acc, 1, acc + nl * N, nullptr, it[0].v, it[0].w};
     moddown_batch(c, level, 2, 1, &di, s);
   }
   return cuda_check("hy_hrot_sum");

@@ -39,3 +39,34 @@ def all_gather_cts(local: list, n_total: int, like, group=None) -> list:
     for r, (b, e) in enumerate(sizes):
         out.extend(recv[r][i] for i in range(e - b))
     return out
+
+
+def tap_sharded(partial, finish, n_taps: int, group=None):
+    """The exchange step of a tap-sharded RAConv output: this rank computes the lazy-sum
+    state of its contiguous tap range, `partial(tap_begin, tap_end) -> int64 tensor`, the states are summed with
+    one all-reduce, and `finish(state)` turns the sum into the output on every rank (modular sums are exact and
+    order-free, so the result is bit-identical to the single-GPU one)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    b, e = shard(n_taps, rank, world)
+    state = partial(b, e)
+    dist.all_reduce(state, op=dist.ReduceOp.SUM, group=group)
+    return finish(state)
+
+
+def raconv_tap_sharded(plan, evks, cts, level, pts, out_index: int, scratch=None, group=None):
+    """One output of an RAConv layer with its f^2 taps sharded over the ranks (include/hyphen.h
+    hy_raconv_partial / hy_raconv_finish): for layers with fewer output ciphertexts than GPUs (ResNet-20
+    RAConv: one output)."""
+    scratch = plan.scratch(level) if scratch is None else scratch
+    state = plan.partial_state(level)
+
+    def partial(b, e):
+        return plan.raconv_partial(evks, cts, level, pts, out_index, b, e, state, scratch)
+
+    def finish(st):
+        return plan.raconv_finish(evks, level, pts, st, out_index, scratch=scratch)
+
+    return tap_sharded(partial, finish, plan.f * plan.f, group)

@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2302_02407_b200.dist import all_gather_cts, shard
+from paper_2302_02407_b200.dist import all_gather_cts, shard, tap_sharded
 
 
 def test_shard_partitions():
@@ -62,3 +62,44 @@ def test_all_gather_world2(n_total):
         assert p.exitcode == 0
     res = dict(q.get() for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+Q = 281474976710597  # a 48-bit prime (residues < 2^48, as in the product's chain)
+
+
+def _tap_value(t):  # the lazy-sum state contributed by tap t alone (deterministic residues)
+    g = torch.Generator().manual_seed(500 + t)
+    return torch.randint(0, Q, (2, 3, 16), generator=g, dtype=torch.int64)
+
+
+def _partial(b, e):  # the state of taps [b, e): canonical sum mod Q (what hy_raconv_partial returns)
+    st = torch.zeros((2, 3, 16), dtype=torch.int64)
+    for t in range(b, e):
+        st = (st + _tap_value(t)) % Q
+    return st
+
+
+def _tap_worker(rank, world, port, n_taps, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    got = tap_sharded(_partial, lambda st: st % Q, n_taps)  # finish: reduce the integer sum mod Q
+    q.put((rank, bool(torch.equal(got, _partial(0, n_taps)))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_taps", [(2, 9), (2, 1), (3, 9)])
+def test_tap_sharded_allreduce(world, n_taps):
+    """RAConv tap sharding: per-rank partial states summed by one all-reduce and reduced mod q equal the
+    single-rank state for every rank (including a rank with an empty tap range)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tap_worker, args=(r, world, port, n_taps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict(q.get() for _ in range(world))
+    assert res == {r: True for r in range(world)}

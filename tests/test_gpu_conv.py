@@ -100,3 +100,38 @@ def test_resnet_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
     p, outs = gpu_layer(ctx_hyp, spec, X, K, level, 2 ** 42, j, j + 1)
     plan, ref = oracle_layer(orc_hyp, spec, X, K, level, 2 ** 42, outputs)
     assert np.array_equal(to_np(outs[0]), ref[0].data)
+
+
+def _tap_split_equals_raconv(ctx, spec, level, scale, j, shards):
+    """hy_raconv_partial over disjoint tap ranges, states added as integers (what the all-reduce of
+    dist.raconv_tap_sharded does across ranks), then hy_raconv_finish: bit-identical to hy_raconv."""
+    import paper_2302_02407_b200 as hy
+    p = hy.ConvPlan(ctx, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo,
+                    S=spec.S)
+    fin = H.Fmt("RA", spec.n, spec.wp, spec.g, spec.m, spec.d, spec.S)
+    X = synth.image(31, spec.ci, spec.w)
+    K = synth.conv_weight(32, spec.co, spec.ci, spec.f)
+    cts = [ctx.encrypt(SK, 901, i, ctx.encode(v, scale, level), level) for i, v in enumerate(H.pack(X, fin))]
+    evks = {r: ctx.keygen_rot(SK, EK, r) for r in p.rots}
+    pts = p.encode_weights(K, level)
+    want = p.run(evks, cts, level, pts, out_begin=j, out_end=j + 1)[0]
+    total = p.partial_state(level)
+    for b, e in shards:
+        st = p.partial_state(level)
+        p.raconv_partial(evks, cts, level, pts, j, b, e, st)
+        total += st  # int64 sum, as the all-reduce
+    got = p.raconv_finish(evks, level, pts, total, j)
+    assert np.array_equal(to_np(got), to_np(want))
+
+
+@pytest.mark.parametrize("shards", [[(0, 9)], [(0, 5), (5, 9)], [(0, 2), (2, 4), (4, 6), (6, 8), (8, 9), (9, 9)]])
+def test_raconv_tap_sharding_toy(ctx_toy, shards):
+    # config 1 (BASELINE configs[0]) and an R_g = 2 layer (IR_g mask step)
+    _tap_split_equals_raconv(ctx_toy, TOY[0], 2, 2 ** 40, 0, shards)
+    _tap_split_equals_raconv(ctx_toy, TOY[3], 2, 2 ** 40, 0, shards)
+
+
+def test_raconv_tap_sharding_resnet20(ctx_hyp):
+    # ResNet-20 stage-3 RAConv (one output ciphertext) at l+1 = 7, taps over 8 "ranks"
+    shards = [(0, 2)] + [(t, t + 1) for t in range(2, 9)]
+    _tap_split_equals_raconv(ctx_hyp, R20["L3_ra"], 6, 2 ** 42, 0, shards)
