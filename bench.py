@@ -128,8 +128,15 @@ def dist_setup():
     if ws > 1:
         import torch
         import torch.distributed as dist
+        # HY_DIST_BACKEND=gloo: a functional check of the multi-rank paths with several ranks sharing one
+        # GPU (NCCL needs one GPU per rank); timings of such a run are not bench numbers
+        backend = os.environ.get("HY_DIST_BACKEND", "nccl")
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
 
 
