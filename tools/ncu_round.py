@@ -20,7 +20,8 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 # kernel-name prefix -> bench.py family (hy_internal.h Family)
-FAMILY = [("k_rows_ip_final", "ntt_ip"), ("k_modup_cols", "modup"), ("k_modup_bconv", "modup"), ("k_ntt_rows_ip", "ntt_ip"),
+FAMILY = [("k_rows_ip_final_tma<6, 1", "ntt_ip_hoisted"), ("k_rows_ip_final", "ntt_ip"),
+          ("k_bconv_cols<4, 1", "moddown"), ("k_bconv_cols", "modup"), ("k_modup_cols", "modup"), ("k_modup_bconv", "modup"), ("k_ntt_rows_ip", "ntt_ip"),
           ("k_ntt_rows_final", "moddown"), ("k_moddown_bconv", "moddown"), ("k_moddown_final", "moddown"),
           ("k_ks_ip", "ip"), ("k_ntt_cols", "ntt_a"), ("k_ntt_rows", "ntt_b"), ("k_automorph", "aut")]
 KEYS = ["Grid Size", "Block Size", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
