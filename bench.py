@@ -325,7 +325,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     prm = synth.PARAMS["hyp"]
-    ctx = hy.Context(**prm, device=local)
+    ctx = hy.Context(**prm, device=local, max_batch=32)  # 32 key switches per batched launch
     sk, ek = synth.SEED_SK, synth.SEED_EVK
     rs = [i + 1 for i in range(BATCH)]
     # keys (server state) and inputs (client output), resident in HBM before timing

@@ -140,7 +140,7 @@ def encode_coeffs(log_n: int, slots, scale: int) -> np.ndarray:
 class Context:
     """One RNS-CKKS context on one CUDA device (see include/hyphen.h)."""
 
-    def __init__(self, log_n, q_bits, p_bits, dnum, h=192, device=0, max_level=None, max_batch=16, **_):
+    def __init__(self, log_n, q_bits, p_bits, dnum, h=192, device=0, max_level=None, max_batch=None, **_):
         import torch
 
         self.torch = torch
@@ -160,7 +160,9 @@ class Context:
         self.q, self.p = self.moduli[: self.n_q], self.moduli[self.n_q:]
         self.alpha = int(lib().hy_ctx_alpha(self._c))
         self.max_level = self.n_q - 1 if max_level is None else max_level
-        # workspace for up to `max_batch` key switches per batched launch (library cap: 16)
+        # workspace for up to `max_batch` key switches per batched launch (library cap: 32; HY_MAX_BATCH)
+        if max_batch is None:
+            max_batch = int(os.environ.get("HY_MAX_BATCH", "16"))
         nbytes = int(lib().hy_workspace_bytes(self._c, self.max_level, max_batch))
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.int64, device=self.device)
         _check(lib().hy_ctx_set_workspace(self._c, self.ws.data_ptr(), self.ws.numel() * 8))

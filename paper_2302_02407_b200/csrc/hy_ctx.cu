@@ -296,9 +296,9 @@ extern "C" uint64_t hy_galois_elt(const hy_ctx* c, int64_t r) {
 extern "C" size_t hy_workspace_bytes(const hy_ctx* c, uint32_t max_level, uint32_t max_terms) {
   if (!c) return 0;
   if (max_level >= c->n_q) max_level = c->n_q - 1;
-  // max_terms key switches per batched launch (capped at 16), plus one accumulator ciphertext;
+  // max_terms key switches per batched launch (capped at kG), plus one accumulator ciphertext;
   // at least enough for key generation (3 (n_q + n_p) limbs + small buffers)
-  const size_t items = std::max<uint32_t>(1, std::min<uint32_t>(max_terms, 16));
+  const size_t items = std::max<uint32_t>(1, std::min<uint32_t>(max_terms, (uint32_t)hy::kG));
   const size_t n = max_level + 1;
   const size_t ks = items * hy::ks_item_bytes(c, max_level) + 2 * n * (size_t)c->N * 8 + 4096;
   const size_t keygen = (3 * (size_t)(c->n_q + c->n_p) + 2) * c->N * 8 + 65536;

@@ -736,11 +736,17 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
         __syncwarp();
         rows_forward_l3(x, l, b + 512, T, q, qinv);  // the row buffer is now the transpose buffer
       }
-      const uint64_t* e0 = reinterpret_cast<const uint64_t*>(b);
+      // the evk rows in layout L3 as 16-byte words (x[2h], x[2h+1] are adjacent): 2-way instead of the
+      // 4-way bank conflicts of 8-byte reads at a 32-byte lane stride
+      const ulonglong2* e0 = reinterpret_cast<const ulonglong2*>(b);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        a0[k] += fmulmod(x[k], u2d(e0[elem<3>(l, k)]), q, qinv);
-        a1[k] += fmulmod(x[k], u2d(e0[256 + elem<3>(l, k)]), q, qinv);
+      for (int h = 0; h < 4; ++h) {
+        const int w2 = (elem<3>(l, 2 * h)) >> 1;  // 16-byte word of elements 2h, 2h + 1
+        const ulonglong2 v0 = e0[w2], v1 = e0[128 + w2];
+        a0[2 * h] += fmulmod(x[2 * h], u2d(v0.x), q, qinv);
+        a0[2 * h + 1] += fmulmod(x[2 * h + 1], u2d(v0.y), q, qinv);
+        a1[2 * h] += fmulmod(x[2 * h], u2d(v1.x), q, qinv);
+        a1[2 * h + 1] += fmulmod(x[2 * h + 1], u2d(v1.y), q, qinv);
       }
     } else {
       const double pinv = (double)md->p_inv[i];
