@@ -77,6 +77,8 @@ def lib():
             "orc_pmult": (None, [P, C.c_int, u64p, u64p, u64p]),
             "orc_add": (None, [P, C.c_int, C.c_int, u64p, u64p, u64p]),
             "orc_rescale": (None, [P, C.c_int, u64p, u64p]),
+            "orc_keygen_relin": (None, [P, C.c_uint64, C.c_int, C.c_uint64, u64p]),
+            "orc_mulct": (None, [P, C.c_int, u64p, u64p, u64p, u64p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -193,6 +195,12 @@ class Oracle:
     def keygen_galois(self, sk_seed, ek_seed, k: int):
         evk = np.zeros((self.dnum, 2, self.nq + self.np_, self.N), np.uint64)
         lib().orc_keygen_rot(self._c, sk_seed, self.h, ek_seed, k, evk)
+        return evk
+
+    def keygen_relin(self, sk_seed, ek_seed):
+        """relinearization key s^2 -> s (DESIGN R-RELIN); [dnum][2][nq+np][N]."""
+        evk = np.zeros((self.dnum, 2, self.nq + self.np_, self.N), np.uint64)
+        lib().orc_keygen_relin(self._c, sk_seed, self.h, ek_seed, evk)
         return evk
 
     # -- encode / encrypt ------------------------------------------------
@@ -330,6 +338,19 @@ class Oracle:
         out = np.zeros((2, ct.level, self.N), np.uint64)
         lib().orc_rescale(self._c, ct.level, np.ascontiguousarray(ct.data), out)
         return Ct(out, ct.level - 1, ct.scale / self.q[ct.level])
+
+    def mulct(self, a: Ct, b: Ct, rlk) -> Ct:
+        """MulCt + relinearization, no rescale; scale a.scale * b.scale."""
+        assert a.level == b.level
+        out = np.zeros_like(a.data)
+        lib().orc_mulct(self._c, a.level, np.ascontiguousarray(a.data), np.ascontiguousarray(b.data),
+                        np.ascontiguousarray(rlk), out)
+        return Ct(out, a.level, a.scale * b.scale)
+
+    def square(self, a: Ct, rlk) -> Ct:
+        """AESPA activation after its coefficients are fused into the neighbouring layers: x^2,
+        MulCt(a, a) + relinearization + rescale."""
+        return self.rescale(self.mulct(a, a, rlk))
 
     def level_down(self, ct: Ct, level: int) -> Ct:
         assert level <= ct.level

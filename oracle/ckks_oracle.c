@@ -756,3 +756,73 @@ void orc_rescale(const orc_ctx* c, int level, const uint64_t* ct, uint64_t* out)
     free(v);
   }
 }
+
+/* ------------------------------------------------------------------ */
+/* MulCt with relinearization (key switching P:1238-1241)    */
+/* ------------------------------------------------------------------ */
+/* Relinearization key (DESIGN R-RELIN): the hybrid key-switching key from s^2 to s,
+ * b_j = -a_j*s + e_j + g_j*s^2 with the g_j of R-EVK, object id (0 << 8) | j (Galois element 0,
+ * which no rotation uses).  Layout as orc_keygen_rot. */
+void orc_keygen_relin(const orc_ctx* c, uint64_t sk_seed, int h, uint64_t ek_seed, uint64_t* evk) {
+  const int N = c->N, L1 = c->nq + c->np;
+  int8_t* s = (int8_t*)malloc(N);
+  orc_sample_secret(c, sk_seed, h, s);
+#pragma omp parallel for schedule(dynamic)
+  for (int jt = 0; jt < c->dnum * L1; ++jt) {
+    int j = jt / L1, t = jt % L1;
+    uint64_t q = c->mod[t];
+    uint64_t obj = (uint64_t)j;
+    uint64_t* b = evk + ((size_t)(j * 2 + 0) * L1 + t) * N;
+    uint64_t* a = evk + ((size_t)(j * 2 + 1) * L1 + t) * N;
+    uint64_t* s_ntt = (uint64_t*)malloc(sizeof(uint64_t) * N);
+    uint64_t* e_ntt = (uint64_t*)malloc(sizeof(uint64_t) * N);
+    int32_t* e = (int32_t*)malloc(sizeof(int32_t) * N);
+    small_to_ntt_i8(c, s, t, s_ntt);
+    orc_sample_cbd(ek_seed, DOM_EVK_E, obj, N, e);
+    small_to_ntt_i32(c, e, t, e_ntt);
+    uint64_t g = 0;
+    if (t < c->nq && t >= j * c->alpha && t < (j + 1) * c->alpha) {
+      g = 1;
+      for (int kk = 0; kk < c->np; ++kk) g = mulmod(g, c->mod[c->nq + kk] % q, q);
+    }
+    for (int i = 0; i < N; ++i) {
+      a[i] = draw_uniform(ek_seed, DOM_EVK_A, obj, (uint32_t)t, (uint32_t)i, q);
+      uint64_t v = submod(e_ntt[i], mulmod(a[i], s_ntt[i], q), q);
+      /* s^2 in the NTT domain is the pointwise square (NTT multiplication = negacyclic product) */
+      b[i] = addmod(v, mulmod(g, mulmod(s_ntt[i], s_ntt[i], q), q), q);
+    }
+    free(s_ntt); free(e_ntt); free(e);
+  }
+  free(s);
+}
+
+/* MulCt: the tensor product of a = (a0, a1) and b = (b0, b1) at level l,
+ *   d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1            (NTT domain, limbwise mod q_i),
+ * so that d0 + d1 s + d2 s^2 = (a0 + a1 s)(b0 + b1 s); then d2 is key-switched from s^2 to s with the
+ * relinearization key exactly as HRot's plain path switches kappa(c1) (iNTT, ModUp, IP, ModDown; no
+ * automorphism):  out = (d0 + KS_0(d2), d1 + KS_1(d2)).  No rescale (the caller rescales). */
+void orc_mulct(const orc_ctx* c, int level, const uint64_t* a, const uint64_t* b, const uint64_t* rlk, uint64_t* out) {
+  const int N = c->N, n = level + 1, E = n + c->np, beta = n_digits(c, level);
+  size_t pl = (size_t)n * N;
+  uint64_t* d2 = (uint64_t*)malloc(sizeof(uint64_t) * pl);
+  for (int i = 0; i < n; ++i) {
+    uint64_t q = c->mod[i];
+    for (int x = 0; x < N; ++x) {
+      size_t o = (size_t)i * N + x;
+      out[o] = mulmod(a[o], b[o], q);
+      out[pl + o] = addmod(mulmod(a[o], b[pl + o], q), mulmod(a[pl + o], b[o], q), q);
+      d2[o] = mulmod(a[pl + o], b[pl + o], q);
+    }
+  }
+  int* ch = q_chain(n);
+  intt_limbs(c, d2, ch, n);
+  uint64_t* ext = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)beta * E * N);
+  orc_modup_coeff(c, level, d2, ext);
+  uint64_t* u = (uint64_t*)malloc(sizeof(uint64_t) * 2 * (size_t)E * N);
+  orc_ks_inner_product(c, level, ext, rlk, u);
+  uint64_t* ks = (uint64_t*)malloc(sizeof(uint64_t) * 2 * pl);
+  orc_moddown(c, level, u, ks);
+  orc_moddown(c, level, u + (size_t)E * N, ks + pl);
+  for (size_t o = 0; o < 2 * pl; ++o) out[o] = addmod(out[o], ks[o], c->mod[(o % pl) / N]);
+  free(ch); free(d2); free(ext); free(u); free(ks);
+}

@@ -429,3 +429,64 @@ def test_set_hyp_sizes(orc_hyp):
     assert o.dnum * 2 * (o.nq + o.np_) * limb == int(g["evk_mib"]) * 2**20
     # P:1243 multiplies the MiB-exact key size by 66 in decimal units: 66 x 168 MB = 11.09 GB
     assert abs(int(g["n_evk_resnet18"]) * int(g["evk_mib"]) / 1000 - float(g["evk_gb_resnet18"])) < 0.05
+
+
+# ---------------------------------------------------------------- MulCt + relinearization
+def _negacyclic_square(s):
+    """s^2 in Z[X]/(X^N + 1) by schoolbook over the nonzero coefficients (plain integers)."""
+    N = len(s)
+    nz = [(i, v) for i, v in enumerate(s) if v]
+    out = [0] * N
+    for i, a in nz:
+        for j, b in nz:
+            k = i + j
+            if k < N:
+                out[k] += a * b
+            else:
+                out[k - N] -= a * b
+    return out
+
+
+def test_relin_key_structure(orc_mini):
+    """Relinearization key (DESIGN R-RELIN): b_j + a_j s == e_j + g_j s^2 (mod every prime), s^2 by schoolbook,
+    g_j = P on digit j's q-limbs (R-EVK), e_j drawn with object id j (Galois element 0)."""
+    o = orc_mini
+    rlk = o.keygen_relin(synth.SEED_SK, synth.SEED_EVK)
+    s = [int(x) for x in o.secret(synth.SEED_SK)]
+    s2 = _negacyclic_square(s)
+    P = math.prod(o.p)
+    for j in range(o.dnum):
+        e = [int(x) for x in o.cbd(synth.SEED_EVK, oracle.DOM_EVK_E, j)]
+        for t in range(o.nq + o.np_):
+            q = int(o.moduli[t])
+            b = o.intt(rlk[j, 0, t], t)
+            s_ntt = o.ntt(np.array([x % q for x in s], np.uint64), t)
+            a_s = o.intt((rlk[j, 1, t].astype(object) * s_ntt.astype(object) % q).astype(np.uint64), t)
+            g = P % q if (t < o.nq and j * o.alpha <= t < (j + 1) * o.alpha) else 0
+            for x in range(0, o.N, 37):
+                assert (int(b[x]) + int(a_s[x])) % q == (e[x] + g * s2[x]) % q
+
+
+def test_mulct_decrypts_to_product(orc_mini):
+    """dec(MulCt(a, b)) = dec(a) * dec(b) (negacyclic, mod Q) up to the key-switch error of relinearizing
+    d2 (R-KSBOUND); the rescaled square decodes to the slot-wise square (AESPA x^2)."""
+    o = orc_mini
+    level = o.nq - 1
+    Q = math.prod(o.q[: level + 1])
+    rlk = o.keygen_relin(synth.SEED_SK, synth.SEED_EVK)
+    za, zb = synth.slots_uniform(40, o.n), synth.slots_uniform(41, o.n)
+    a = o.encrypt(synth.SEED_SK, 42, 0, o.encode(za, 2**40, level))
+    b = o.encrypt(synth.SEED_SK, 42, 1, o.encode(zb, 2**40, level))
+    ab = o.mulct(a, b, rlk)
+    # dec(a) * dec(b): product of the decrypted plaintexts in the NTT domain (NTT product = schoolbook,
+    # pinned above), back to centred integer coefficients by CRT
+    ma, mb = o.decrypt(synth.SEED_SK, a), o.decrypt(synth.SEED_SK, b)
+    prod = np.array([[int(x) * int(y) % o.q[i] for x, y in zip(ma.data[i], mb.data[i])] for i in range(level + 1)],
+                    dtype=object).astype(np.uint64)
+    want = o.crt_coeffs(prod, level)
+    got = _dec_coeffs(o, ab)
+    err = max(abs(_centre(x - y, Q)) for x, y in zip(got, want))
+    assert err <= _ks_bound(o, level), err
+    sq = o.square(a, rlk)
+    assert sq.level == level - 1
+    assert np.max(np.abs(np.real(o.decode(o.decrypt(synth.SEED_SK, sq))) - za * za)) < 2**-20
