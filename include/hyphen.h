@@ -153,6 +153,18 @@ hy_status hy_hrot_hoisted(hy_ctx* ctx, const uint64_t* const* d_evks, const uint
 hy_status hy_hrot_sum(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* const* d_cts, uint32_t level,
                       const int32_t* r, uint32_t n, uint64_t* d_out, void* stream);
 
+/* ---- MulCt with relinearization (AESPA square activation P:1013-1015) ---- */
+/* out = MulCt(a, b) at level l: the tensor product (a0 b0, a0 b1 + a1 b0, a1 b1), whose last part is
+ * key-switched from s^2 to s with the relinearization key d_rlk (hy_keygen_relin) through the same
+ * hybrid key switch as HRot (ModUp, inner product, ModDown; DESIGN R-RELIN).  No rescale (the caller
+ * rescales); the scale is scale_a * scale_b.  Layouts as hy_hrot; out_i may alias a_i or b_i (the
+ * square is hy_mulct(a, a)) but not another item's inputs.  Batched: the key streams once per batch. */
+hy_status hy_mulct(hy_ctx* ctx, const uint64_t* d_rlk, const uint64_t* d_a, const uint64_t* d_b, uint32_t level,
+                   uint64_t* d_out, void* stream);
+hy_status hy_mulct_batch(hy_ctx* ctx, const uint64_t* d_rlk, const uint64_t* const* d_as,
+                         const uint64_t* const* d_bs, uint32_t level, uint32_t n, uint64_t* const* d_outs,
+                         void* stream);
+
 /* ---- MulPt / AddCt / Rescale -------------------------------- */
 /* out = ct (.) pt limbwise; no auto-rescale (scale bookkeeping is the caller's). */
 hy_status hy_pmult(hy_ctx* ctx, const uint64_t* d_ct, const uint64_t* d_pt, uint32_t level, uint64_t* d_out,
@@ -254,6 +266,9 @@ hy_status hy_raconv_finish(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t
  * secret from sk_seed, randomness from ek_seed.  d_evk: [dnum][2][n_q+n_p][N]. */
 hy_status hy_keygen_rot(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, int32_t r, uint64_t* d_evk, void* stream);
 hy_status hy_keygen_galois(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* d_evk, void* stream);
+/* Relinearization key s^2 -> s (DESIGN R-RELIN): b_j = -a_j s + e_j + g_j s^2, object ids j (Galois
+ * element 0, used by no rotation); layout as a rotation key. */
+hy_status hy_keygen_relin(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, uint64_t* d_rlk, void* stream);
 /* Secret-key encryption of an NTT-domain plaintext at level l (DESIGN R-ENC). */
 hy_status hy_encrypt(hy_ctx* ctx, uint64_t sk_seed, uint64_t enc_seed, uint64_t ct_id, const uint64_t* d_pt,
                      uint32_t level, uint64_t* d_ct, void* stream);

@@ -75,6 +75,9 @@ SIGNATURES = {
     "hy_rescale": (C.c_int, [_P, _P, _U32, _P, _P]),
     "hy_keygen_rot": (C.c_int, [_P, _U64, _U64, C.c_int32, _P, _P]),
     "hy_keygen_galois": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
+    "hy_keygen_relin": (C.c_int, [_P, _U64, _U64, _P, _P]),
+    "hy_mulct": (C.c_int, [_P, _P, _P, _P, _U32, _P, _P]),
+    "hy_mulct_batch": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _PP, _P]),
     "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
     "hy_decrypt": (C.c_int, [_P, _U64, _P, _U32, _P, _P]),
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
@@ -292,6 +295,24 @@ class Context:
         out = self.empty(*self.evk_shape()) if out is None else out
         _check(lib().hy_keygen_rot(self._c, sk_seed, ek_seed, int(r), _ptr(out), self._stream()))
         return out
+
+    def keygen_relin(self, sk_seed, ek_seed, out=None):
+        out = self.empty(*self.evk_shape()) if out is None else out
+        _check(lib().hy_keygen_relin(self._c, sk_seed, ek_seed, _ptr(out), self._stream()))
+        return out
+
+    def mulct(self, rlk, a, b, level, out=None):
+        """MulCt + relinearization, no rescale (include/hyphen.h hy_mulct)."""
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_mulct(self._c, _ptr(rlk), _ptr(a), _ptr(b), level, _ptr(out), self._stream()))
+        return out
+
+    def square_batch(self, rlk, cts, level, outs=None):
+        """x^2 of every ciphertext (AESPA after fusion), MulCt + relinearization, no rescale."""
+        outs = [self.empty(*self.ct_shape(level)) for _ in cts] if outs is None else outs
+        _check(lib().hy_mulct_batch(self._c, _ptr(rlk), _ptr_array(cts), _ptr_array(cts), level, len(cts),
+                                    _ptr_array(outs), self._stream()))
+        return outs
 
     def keygen_galois(self, sk_seed, ek_seed, k, out=None):
         out = self.empty(*self.evk_shape()) if out is None else out

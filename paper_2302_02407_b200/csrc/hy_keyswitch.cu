@@ -60,6 +60,26 @@ __global__ void k_automorph_sum(const __grid_constant__ Arr<const uint64_t*> in,
   out[off + x] = v;
 }
 
+// MulCt tensor product of item g = blockIdx.z at limb i = blockIdx.y:
+//   d0 = a0 b0 -> out[0], d1 = a0 b1 + a1 b0 -> out[1], d2 = a1 b1 -> d2 (all canonical, NTT domain).
+// Every input word is read before the thread writes, so out may alias a or b.  grid (N/256, l+1, G)
+__global__ void k_tensor(const __grid_constant__ Arr<const uint64_t*> a, const __grid_constant__ Arr<const uint64_t*> b,
+                         const __grid_constant__ Arr<uint64_t*> out, const __grid_constant__ Arr<uint64_t*> d2,
+                         int level, int logN, DevTables dt) {
+  const size_t N = (size_t)1 << logN, pl = (size_t)(level + 1) * N;
+  const int g = blockIdx.z, i = blockIdx.y;
+  const size_t o = (size_t)i * N + blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  const double a0 = u2d(a.p[g][o]), a1 = u2d(a.p[g][pl + o]), b0 = u2d(b.p[g][o]), b1 = u2d(b.p[g][pl + o]);
+  const double d0 = fmulmod(a0, b0, q, qinv);
+  const double d1 = fmulmod(a0, b1, q, qinv) + fmulmod(a1, b0, q, qinv);
+  const double dd = fmulmod(a1, b1, q, qinv);
+  out.p[g][o] = d2u(fcanon(d0, q, qinv));
+  out.p[g][pl + o] = d2u(fcanon(d1, q, qinv));
+  d2.p[g][o] = d2u(fcanon(dd, q, qinv));
+}
+
 // FP64 constants of one prime, staged in shared memory.
 struct FConst {
   double q, qinv;
@@ -718,6 +738,67 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
   return HY_OK;
 }
 
+// MulCt + relinearization of G pairs: the tensor product, then d2 is key-switched from s^2 to
+// s with the relinearization key through the split-ModDown engine of plain HRot (no automorphism): the
+// P-limb IP, the ModDown column kernel, and the Q-limb IP fused with the epilogue, which adds (d0, d1)
+// (held in out itself).  One key for every item: its rows stream from HBM once per batch.
+hy_status mulct_multi(hy_ctx* c, const uint64_t* rlk, const uint64_t* const* a, const uint64_t* const* b,
+                      uint32_t level, uint32_t n_items, uint64_t* const* out, cudaStream_t s) {
+  const size_t n = level + 1, N = c->N;
+  const int cap = max_items(c, level);
+  if (n_items && cap == 0) return fail(HY_E_WORKSPACE, "workspace too small for this level");
+  KsItem it[kG];
+  for (size_t done = 0; done < n_items;) {
+    const int G = (int)std::min<size_t>(n_items - done, cap);
+    hy_status st0 = carve(c, level, G, it, nullptr);
+    if (st0 != HY_OK) return st0;
+    Arr<const uint64_t*> aa{}, bb{};
+    Arr<uint64_t*> oo{}, dd{};
+    uint64_t* d[kG];
+    uint64_t* ext[kG];
+    uint64_t* u[kG];
+    uint64_t* v[kG];
+    uint64_t* w[kG];
+    const uint64_t* own[kG];
+    const uint64_t* keys[kG];
+    IpFinalArgs fa{};
+    for (int g = 0; g < G; ++g) {
+      aa.p[g] = a[done + g];
+      bb.p[g] = b[done + g];
+      oo.p[g] = out[done + g];
+      dd.p[g] = it[g].rc + n * N;  // d2 takes the place of kappa(c1)
+      own[g] = dd.p[g];
+      d[g] = it[g].d;
+      ext[g] = it[g].ext;
+      u[g] = it[g].u;
+      v[g] = it[g].v;
+      w[g] = it[g].w;
+      keys[g] = rlk;
+      fa.ext[g] = ext[g];
+      fa.own[g] = own[g];
+      fa.evk[g] = rlk;
+      fa.w[g] = w[g];
+      fa.add0[g] = out[done + g];  // d0
+      fa.k0[g] = 1;
+      fa.add1[g] = out[done + g] + n * N;  // d1
+      fa.out[g] = out[done + g];
+      fa.kx[g] = 1;
+    }
+    {
+      dim3 grid(c->N / kT, n, G);
+      KTimer kt(c, FAM_ELEM, s);
+      kt.bytes = (uint64_t)G * 7 * n * N * 8;
+      k_tensor<<<grid, kT, 0, s>>>(aa, bb, oo, dd, (int)level, c->log_n, c->dt);
+    }
+    const bool vr = moddown_cols_ok(c);
+    modup_ip_fused(c, level, G, d, ext, own, keys, u, false, false, s, (int)n, vr ? v : nullptr);
+    moddown_p(c, level, G, u, v, w, s, vr);
+    launch_rows_ip_final(c, fa, G, level, false, s);
+    done += G;
+  }
+  return HY_OK;
+}
+
 hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
                      cudaStream_t s, const uint64_t* addct) {
   return hrot_multi(c, &evk, &ct, level, &r, 1, &out, addct ? &addct : nullptr, s);
@@ -1043,4 +1124,24 @@ extern "C" hy_status hy_hrot_sum(hy_ctx* c, const uint64_t* const* evks, const u
     moddown_batch(c, level, 2, 1, &di, s);
   }
   return cuda_check("hy_hrot_sum");
+}
+
+extern "C" hy_status hy_mulct_batch(hy_ctx* c, const uint64_t* rlk, const uint64_t* const* a, const uint64_t* const* b,
+                                    uint32_t level, uint32_t n, uint64_t* const* outs, void* stream) {
+  hy_status s0 = check_level(c, level);
+  if (s0 != HY_OK) return s0;
+  if (!rlk || !a || !b || !outs) return fail(HY_E_ARG, "null");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!a[i] || !b[i] || !outs[i]) return fail(HY_E_ARG, "null ciphertext");
+    for (uint32_t j = 0; j < n; ++j)  // an output may alias its own inputs only
+      if (j != i && (outs[i] == a[j] || outs[i] == b[j])) return fail(HY_E_ARG, "output aliases another item's input");
+  }
+  s0 = mulct_multi(c, rlk, a, b, level, n, outs, st(stream));
+  if (s0 != HY_OK) return s0;
+  return cuda_check("hy_mulct_batch");
+}
+
+extern "C" hy_status hy_mulct(hy_ctx* c, const uint64_t* rlk, const uint64_t* a, const uint64_t* b, uint32_t level,
+                              uint64_t* out, void* stream) {
+  return hy_mulct_batch(c, rlk, &a, &b, level, 1, &out, stream);
 }

@@ -427,10 +427,21 @@ extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, u
   return rescale_multi(c, &ct, 1, level, &out, st(stream));
 }
 
-extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* evk,
-                                      void* stream) {
+namespace hy {
+namespace {
+// s^2 in the NTT domain: the pointwise square of NTT(s) (NTT multiplication = negacyclic product)
+__global__ void k_square_limbs(const uint64_t* __restrict__ s_ntt, uint64_t* __restrict__ out, DevTables dt,
+                               int logN) {
+  const size_t N = (size_t)1 << logN;
+  const size_t o = (size_t)blockIdx.y * N + blockIdx.x * blockDim.x + threadIdx.x;
+  out[o] = mul_mod(s_ntt[o], s_ntt[o], dt.pc[blockIdx.y]);
+}
+
+// Key-switching key to the secret s from kappa_k(s) (k odd: rotation key, DESIGN R-EVK) or from s^2 (k = 0:
+// relinearization key, DESIGN R-RELIN); object ids (k << 8) | j.
+hy_status keygen_ks(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* evk, void* stream) {
   if (!c || !evk) return fail(HY_E_ARG, "null");
-  if (!(k & 1) || k >= 2ull * c->N) return fail(HY_E_ARG, "bad Galois element");
+  if (k != 0 && (!(k & 1) || k >= 2ull * c->N)) return fail(HY_E_ARG, "bad Galois element");
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
   cudaStream_t s = st(stream);
   const uint32_t L1 = c->n_q + c->n_p;
@@ -444,7 +455,12 @@ extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_s
   uint64_t* gm = ws.take<uint64_t>(kMaxChain);
   if (!gm) return fail(HY_E_WORKSPACE, "workspace too small for key generation");
   secret_ntt(c, sk_seed, L1, s_ntt, d_s, s);
-  launch_automorph(c, s_ntt, sk_ntt, L1, k, s);  // kappa_k(s): NTT-domain permutation
+  if (k == 0) {
+    KTimer kt(c, FAM_CLIENT, s);
+    k_square_limbs<<<dim3(c->N / kT, L1), kT, 0, s>>>(s_ntt, sk_ntt, c->dt, c->log_n);
+  } else {
+    launch_automorph(c, s_ntt, sk_ntt, L1, k, s);  // kappa_k(s): NTT-domain permutation
+  }
   std::vector<uint32_t> chain(L1);
   for (uint32_t i = 0; i < L1; ++i) chain[i] = i;
   std::vector<uint64_t> g(L1);
@@ -474,7 +490,19 @@ extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_s
     }
     cudaStreamSynchronize(s);  // g is reused on the host
   }
-  return cuda_check("hy_keygen_galois");
+  return cuda_check("hy_keygen");
+}
+}  // namespace
+}  // namespace hy
+
+extern "C" hy_status hy_keygen_galois(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* evk,
+                                      void* stream) {
+  if (k == 0) return fail(HY_E_ARG, "bad Galois element");
+  return keygen_ks(c, sk_seed, ek_seed, k, evk, stream);
+}
+
+extern "C" hy_status hy_keygen_relin(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, uint64_t* rlk, void* stream) {
+  return keygen_ks(c, sk_seed, ek_seed, 0, rlk, stream);
 }
 
 extern "C" hy_status hy_keygen_rot(hy_ctx* c, uint64_t sk_seed, uint64_t ek_seed, int32_t r, uint64_t* evk,

@@ -171,3 +171,29 @@ def test_pmult_add_rescale(pair):
                  o.pmult(A, oracle.Pt(pts[2], level, 1.0)))
     assert np.array_equal(to_np(acc), want.data)
     assert np.array_equal(to_np(ctx.rescale(da, level)), o.rescale(A).data)
+
+
+def test_relin_key_and_mulct(pair):
+    """Relinearization key and MulCt (+ relinearization, no rescale) bit-exact vs the oracle, including the
+    square (a = b, output aliasing the input) and a batch sharing the key; the rescaled square decodes to z^2."""
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    rlk = ctx.keygen_relin(SK, EK)
+    orlk = o.keygen_relin(SK, EK)
+    assert np.array_equal(to_np(rlk), orlk)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    za, zb = synth.slots_uniform(60, o.n), synth.slots_uniform(61, o.n)
+    pa, pb = o.encode(za, scale, level), o.encode(zb, scale, level)
+    oa, ob = o.encrypt(SK, 62, 0, pa), o.encrypt(SK, 62, 1, pb)
+    a, b = to_dev(oa.data, ctx), to_dev(ob.data, ctx)
+    want = o.mulct(oa, ob, orlk)
+    assert np.array_equal(to_np(ctx.mulct(rlk, a, b, level)), want.data)
+    # batch of squares, in place
+    cts = [a.clone(), b.clone(), a.clone()]
+    outs = ctx.square_batch(rlk, cts, level, outs=cts)
+    wsq = [o.mulct(x, x, orlk) for x in (oa, ob, oa)]
+    for g, w in zip(outs, wsq):
+        assert np.array_equal(to_np(g), w.data)
+    sq = o.rescale(wsq[0])
+    zs = np.real(o.decode(o.decrypt(SK, sq)))
+    assert np.max(np.abs(zs - za * za)) < 2**-15
