@@ -552,3 +552,20 @@ def rotation_amounts(plan: Plan, n: int) -> list[int]:
         rs.add(plan.combine % n)
     rs.discard(0)
     return sorted(rs)
+
+
+# --------------------------------------------------------------------------- fused CA -> x^2 -> RA block
+def simulate_block(ca: Plan, ra: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
+    """Alg. 3 on cleartext slot vectors: CAConv, the AESPA activation after its coefficients are
+    fused into the neighbouring layers -- a plain square x^2 -- then RAConv."""
+    return simulate(ra, [v * v for v in simulate(ca, xs)])
+
+
+def run_block_encrypted(o, ca: Plan, ra: Plan, ca_evks: dict, ra_evks: dict, rlk, cts):
+    """Alg. 3 on ciphertexts: CAConv (all outputs), Square = MulCt + relinearization + rescale
+    (one level), RAConv on the squared ciphertexts.  The paper interleaves the loops to bound the
+    live ciphertexts (ct_4[l] += MulFilter&Sum(ct_3[j]) as each ct_3[j] is produced); modular sums do not
+    depend on that order, so the composition computes the same limbs."""
+    mid = EncConv(o, ca, ca_evks).run(cts)
+    sq = [o.square(c, rlk) for c in mid]
+    return EncConv(o, ra, ra_evks).run(sq)

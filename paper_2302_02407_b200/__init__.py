@@ -431,3 +431,28 @@ class ConvPlan:
         _check(lib().hy_raconv_finish(self.ctx._c, self._p, _ptr_array(evks), level, _ptr(pts), _ptr(state),
                                       _ptr(scratch), out_index, _ptr(out), self.ctx._stream()))
         return out
+
+
+class ConvBlock:
+    """The conv half of a ResNet basic block as HyPHEN fuses it (Alg. 3): CAConv, the AESPA activation
+    with its coefficients fused into the neighbouring layers -- x^2, MulCt + relinearization +
+    rescale, one level -- then RAConv.  Every step is a C-ABI call (hy_caconv, hy_mulct_batch, hy_rescale,
+    hy_raconv); the paper interleaves the loops only to bound the live ciphertexts, which 180 GB of HBM does
+    not need, and modular sums do not depend on that order (identical limbs)."""
+
+    def __init__(self, ctx, ca: "ConvPlan", ra: "ConvPlan"):
+        assert ca.algo == ConvPlan.CA and ra.algo == ConvPlan.RA
+        assert ca.n_out == ra.n_in, "CAConv outputs must be the RAConv inputs"
+        self.ctx, self.ca, self.ra = ctx, ca, ra
+
+    def levels(self, level):
+        """(CAConv output, RAConv input, block output) levels for a block input at `level`."""
+        mid = self.ca.out_level(level)
+        return mid, mid - 1, self.ra.out_level(mid - 1)
+
+    def run(self, ca_evks, ra_evks, rlk, cts, level, ca_pts, ra_pts, ca_scratch=None, ra_scratch=None):
+        mid, ra_level, _ = self.levels(level)
+        x = self.ca.run(ca_evks, cts, level, ca_pts, ca_scratch)
+        x = self.ctx.square_batch(rlk, x, mid, outs=x)
+        x = [self.ctx.rescale(c, mid) for c in x]
+        return self.ra.run(ra_evks, x, ra_level, ra_pts, ra_scratch)

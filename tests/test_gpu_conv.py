@@ -135,3 +135,38 @@ def test_raconv_tap_sharding_resnet20(ctx_hyp):
     # ResNet-20 stage-3 RAConv (one output ciphertext) at l+1 = 7, taps over 8 "ranks"
     shards = [(0, 2)] + [(t, t + 1) for t in range(2, 9)]
     _tap_split_equals_raconv(ctx_hyp, R20["L3_ra"], 6, 2 ** 42, 0, shards)
+
+
+def test_block_mini_bit_exact():
+    """Alg. 3 block (CAConv -> x^2 -> RAConv) through the C ABI, bit-exact vs the oracle's composition, and its
+    decryption = conv2d(conv2d(X, K1)^2, K2) within 2^-10."""
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS["mini"]
+    ctx, o = hy.Context(**prm), oracle.Oracle(**prm)
+    n = o.n
+    ca_s = H.ConvSpec(4, 4, 4, 3, 1, 4, 1, 1, 2, "CA", n=n)
+    ra_s = H.ConvSpec(4, 4, 4, 3, 1, 4, 1, 2, 1, "RA", n=n)
+    X = synth.image(70, 4, 4)
+    K1, K2 = synth.conv_weight(71, 4, 4, 3), synth.conv_weight(72, 4, 4, 3)
+    ca, ra = H.plan_caconv(ca_s, K1), H.plan_raconv(ra_s, K2)
+    level = o.nq - 1
+    octs = [o.encrypt(SK, 73, i, o.encode(v, 2**40, level)) for i, v in enumerate(H.pack(X, ca.fin))]
+    ek = {r: o.keygen_rot(SK, EK, r) for r in H.rotation_amounts(ca, n)}
+    rk = {r: o.keygen_rot(SK, EK, r) for r in H.rotation_amounts(ra, n)}
+    want = H.run_block_encrypted(o, ca, ra, ek, rk, o.keygen_relin(SK, EK), octs)
+    g_ca = hy.ConvPlan(ctx, *[getattr(ca_s, k) for k in ("ci", "co", "w", "f", "s", "wp", "g", "m", "d", "algo")])
+    g_ra = hy.ConvPlan(ctx, *[getattr(ra_s, k) for k in ("ci", "co", "w", "f", "s", "wp", "g", "m", "d", "algo")])
+    blk = hy.ConvBlock(ctx, g_ca, g_ra)
+    mid, ra_level, out_level = blk.levels(level)
+    import torch
+    cts = [torch.from_numpy(c.data.view(np.int64)).to(ctx.device) for c in octs]
+    got = blk.run({r: ctx.keygen_rot(SK, EK, r) for r in g_ca.rots}, {r: ctx.keygen_rot(SK, EK, r) for r in g_ra.rots},
+                  ctx.keygen_relin(SK, EK), cts, level, g_ca.encode_weights(K1, level),
+                  g_ra.encode_weights(K2, ra_level))
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        assert b.level == out_level and np.array_equal(to_np(a), b.data)
+    dec = [np.real(o.decode(o.decrypt(SK, b))) for b in want]
+    res = H.unpack(dec, ra.fout, 4, 4, 4)
+    ref = H.conv2d(H.conv2d(X, K1) ** 2, K2)
+    assert np.max(np.abs(res - ref)) / np.max(np.abs(ref)) < 2**-10

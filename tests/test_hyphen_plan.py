@@ -153,3 +153,18 @@ def test_simulated_r18_pconv_equals_conv2d():
     for rep in range(plan.fout.d):
         got = H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo, rep)
         assert np.max(np.abs(got - want)) < 1e-9
+
+
+def test_simulated_block_equals_conv_square_conv():
+    """The fused block (Alg. 3) on cleartext slots: CAConv (1,2) -> x^2 -> RAConv (2,1) equals
+    conv2d(conv2d(X, K1)^2, K2) (AESPA activation fused to x^2), ResNet-20 stage 1 shapes."""
+    ca_s, ra_s = R20["L1_ca"], R20["L1_ra"]
+    X = synth.image(5, ca_s.ci, ca_s.w)
+    K1 = synth.conv_weight(6, ca_s.co, ca_s.ci, 3)
+    K2 = synth.conv_weight(7, ra_s.co, ra_s.ci, 3)
+    ca, ra = H.plan_caconv(ca_s, K1), H.plan_raconv(ra_s, K2)
+    assert (ca.fout.m, ca.fout.d, ca.fout.g) == (ra.fin.m, ra.fin.d, ra.fin.g)
+    ys = H.simulate_block(ca, ra, H.pack(X, ca.fin))
+    want = H.conv2d(H.conv2d(X, K1) ** 2, K2)
+    got = H.unpack(ys, ra.fout, ra_s.co, ra_s.wo, ra_s.wo)
+    assert np.max(np.abs(got - want)) < 1e-9

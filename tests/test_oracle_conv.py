@@ -42,3 +42,26 @@ def test_encrypted_conv_matches_conv2d(orc_toy, spec):
     used = 1 + (1 if plan.mask is not None else 0)
     assert outs[0].level == o.nq - 1 - used
     assert all(abs(c.scale - 2 ** 40) < 1e-6 * 2 ** 40 for c in outs)
+
+
+def test_encrypted_block_mini():
+    """Alg. 3 block (CAConv -> MulCt square + relinearization + rescale -> RAConv) on encrypted data at the mini
+    parameter set: decrypts to conv2d(conv2d(X, K1)^2, K2) within 2^-10 relative (north star)."""
+    o = oracle.Oracle(**synth.PARAMS["mini"])
+    n = o.n
+    ca_s = H.ConvSpec(4, 4, 4, 3, 1, 4, 1, 1, 2, "CA", n=n)
+    ra_s = H.ConvSpec(4, 4, 4, 3, 1, 4, 1, 2, 1, "RA", n=n)
+    X = synth.image(70, 4, 4)
+    K1 = synth.conv_weight(71, 4, 4, 3)
+    K2 = synth.conv_weight(72, 4, 4, 3)
+    ca, ra = H.plan_caconv(ca_s, K1), H.plan_raconv(ra_s, K2)
+    level = o.nq - 1
+    cts = [o.encrypt(synth.SEED_SK, 73, i, o.encode(v, 2**40, level)) for i, v in enumerate(H.pack(X, ca.fin))]
+    ek = {r: o.keygen_rot(synth.SEED_SK, synth.SEED_EVK, r) for r in H.rotation_amounts(ca, n)}
+    rk = {r: o.keygen_rot(synth.SEED_SK, synth.SEED_EVK, r) for r in H.rotation_amounts(ra, n)}
+    rlk = o.keygen_relin(synth.SEED_SK, synth.SEED_EVK)
+    outs = H.run_block_encrypted(o, ca, ra, ek, rk, rlk, cts)
+    dec = [np.real(o.decode(o.decrypt(synth.SEED_SK, c))) for c in outs]
+    got = H.unpack(dec, ra.fout, 4, 4, 4)
+    want = H.conv2d(H.conv2d(X, K1) ** 2, K2)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2**-10
