@@ -316,6 +316,56 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
     return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note}
 
 
+def bench_blocks(ctx, ws, rank, steps, warmup, timed):
+    """ResNet-20 basic-block conv halves (Alg. 3): stride-1 CAConv -> x^2 (MulCt + relinearization
+    + rescale) -> RAConv, device-timed as one step per stage (CAConv input at l+1 = 10).  Every rank
+    runs the whole block (weak scaling is the HRot microbenchmark's; the layer tables shard)."""
+    import torch
+
+    import paper_2302_02407_b200 as hy
+
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    rlk = ctx.keygen_relin(sk, ek)
+    scale = 2 ** synth.PARAMS["hyp"]["log_scale"]
+    spec = {name: sp for name, sp, _ in R20_LAYERS}
+    out = {}
+    for stage, (ca_n, ra_n) in enumerate([("L1_ca", "L1_ra"), ("L2_ca", "L2_ra"), ("L3_ca", "L3_ra")]):
+        plans = []
+        for nm in (ca_n, ra_n):
+            ci, co, w, f, s_, wp, g, m, d, algo = spec[nm][:10]
+            plans.append(hy.ConvPlan(ctx, ci, co, w, f, s_, wp, g, m, d, algo))
+        blk = hy.ConvBlock(ctx, *plans)
+        mid, ra_level, out_level = blk.levels(CA_LEVEL)
+        keys = [{r: ctx.keygen_rot(sk, ek, r) for r in p.rots} for p in plans]
+        K1 = synth.conv_weight(5000 + stage, spec[ca_n][1], spec[ca_n][0], 3)
+        K2 = synth.conv_weight(5100 + stage, spec[ra_n][1], spec[ra_n][0], 3)
+        pts = [plans[0].encode_weights(K1, CA_LEVEL), plans[1].encode_weights(K2, ra_level)]
+        cts = [ctx.encrypt(sk, synth.SEED_ENC, 20_000 + 100 * stage + i,
+                           ctx.encode(synth.slots_uniform(6000 + 100 * stage + i, ctx.n), scale, CA_LEVEL), CA_LEVEL)
+               for i in range(plans[0].n_in)]
+        scr = [plans[0].scratch(CA_LEVEL), plans[1].scratch(ra_level)]
+
+        def step():
+            blk.run(keys[0], keys[1], rlk, cts, CA_LEVEL, pts[0], pts[1], scr[0], scr[1])
+
+        ms, launches = timed(step, steps, warmup)
+        mids = [ctx.empty(*ctx.ct_shape(mid)) for _ in range(plans[0].n_out)]
+
+        def sq_step():
+            x = ctx.square_batch(rlk, mids, mid, outs=mids)
+            for c in x:
+                ctx.rescale(c, mid)
+
+        ms_sq, _ = timed(sq_step, steps, warmup)
+        out[f"stage{stage + 1}"] = {"ms": ms, "square_ms": ms_sq, "ca": ca_n, "ra": ra_n, "level_in": CA_LEVEL,
+                                    "level_ra": ra_level, "level_out": out_level, "n_square": plans[0].n_out,
+                                    "gpu_launches": launches}
+        del pts, cts, scr, keys, mids
+        torch.cuda.empty_cache()
+    return {"blocks": out, "note": "CAConv -> x^2 -> RAConv per stage (Alg. 3, P:739-765), device time; the "
+                                   "square is MulCt + relinearization + rescale of the n_o CAConv outputs"}
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, ws, rank, local):
     import torch
@@ -507,12 +557,13 @@ def run_ours(args, ws, rank, local):
                        f"chunks of {E2E_CHUNK} with the copies on two side streams (overlapped with the key "
                        "switching); evaluation keys are server state, resident before timing (P:1030)"}
 
-    conv = conv18 = None
+    conv = conv18 = blocks = None
     if not args.no_conv:
         del evks, cts, outs, houts
         torch.cuda.empty_cache()
         conv = bench_conv(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
         conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18")
+        blocks = bench_blocks(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -534,6 +585,7 @@ def run_ours(args, ws, rank, local):
             "hrot_hbm": hrot_hbm,
             "resnet20_conv": conv,
             "resnet18_conv": conv18,
+            "resnet20_blocks": blocks,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
