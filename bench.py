@@ -313,7 +313,12 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
         note = ("sum over the 19 convs after the stem (13 stride-1 3x3 convs with PRCR |S|=8, 3 stride-2 dsconv and "
                 "3 pconv shortcuts with full weights) of per-layer device time, each layer on a fresh encryption at "
                 "its scheduled level; context: ResNet-18 conv 7.59 s on A100 (P:1095-1096)")
-    return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note}
+    # the evaluation keys the network's conv layers use (every non-Slide amount is +-2^i, i.e. in a bootstrapping
+    # key set, so no rotation has to be decomposed into loaded keys; P:1242-1245 loads 66 keys for ResNet-18)
+    n_keys = len(keys)
+    key_info = {"distinct_rotation_keys": n_keys, "gib_at_full_level": n_keys * ctx.evk_bytes() / 2**30,
+                "non_slide_amounts_all_power_of_two": True}
+    return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note, "keys": key_info}
 
 
 def bench_blocks(ctx, ws, rank, steps, warmup, timed):

@@ -192,6 +192,10 @@ class Context:
     def evk_shape(self):
         return (self.dnum, 2, self.n_q + self.n_p, self.N)
 
+    def evk_bytes(self):
+        """bytes of one evaluation key at full level (168 MiB at Set_hyp)"""
+        return int(np.prod(self.evk_shape())) * 8
+
     def n_digits(self, level):
         return int(lib().hy_ctx_n_digits(self._c, level))
 

@@ -168,3 +168,24 @@ def test_simulated_block_equals_conv_square_conv():
     want = H.conv2d(H.conv2d(X, K1) ** 2, K2)
     got = H.unpack(ys, ra.fout, ra_s.co, ra_s.wo, ra_s.wo)
     assert np.max(np.abs(got - want)) < 1e-9
+
+
+def test_key_set_needs_no_decomposition():
+    """P:1242-1245 loads the frequent Slide keys and synthesizes irregular IR rotations from loaded keys.  In this
+    layout (R-LAYOUT, R-DSCONV) every rotation other than a Slide tap is +-2^i -- RaS over blocks, RaS_g / IR_g
+    over cell strides, the dsconv merge -- so a power-of-two key set (as bootstrapping loads) covers them and no
+    rotation is decomposed: the conv rotation counts are the effective counts.  Distinct keys: ResNet-20 30,
+    ResNet-18 35 (vs 66 loaded incl. 48 bootstrapping keys in the paper)."""
+    import bench
+    for layers, want in ((bench.R20_LAYERS, 30), (bench.R18_LAYERS, 35)):
+        allr = set()
+        for _, sp, _ in layers:
+            ci, co, w, f, s, wp, g, m, d, algo = sp[:10]
+            spec = H.ConvSpec(ci, co, w, f, s, wp, g, m, d, algo, S=sp[10] if len(sp) > 10 else 1)
+            p = (H.plan_caconv if algo == "CA" else H.plan_raconv)(spec, None, with_weights=False)
+            rs = set(H.rotation_amounts(p, N_SLOTS))
+            taps = {t % N_SLOTS for t in p.taps if t % N_SLOTS}
+            for r in rs - taps:
+                assert r & (r - 1) == 0 or (N_SLOTS - r) & (N_SLOTS - r - 1) == 0, r
+            allr |= rs
+        assert len(allr) == want
