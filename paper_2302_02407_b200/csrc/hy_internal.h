@@ -201,6 +201,14 @@ bool modup_cols_ok(const hy_ctx* c);  // N = 2^16 and alpha <= 4
 // ext_g[c][i] = forward column pass of [sum_k z_k ((P/p_k) mod q_i)] (between-pass format).
 void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
 bool moddown_cols_ok(const hy_ctx* c);  // N = 2^16 and K <= 4
+// Inverse row pass of kappa_{k_g}(c1_g) read straight from c1_g (the automorphism fused as a row gather),
+// [l+1][N] each, into dst_g in the between-pass format (for launch_modup_cols)
+struct RowsAutArgs {
+  const uint64_t* src[kG];
+  uint64_t* dst[kG];
+  uint64_t k[kG];
+};
+void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t level, cudaStream_t s);
 // one NTT row pass (forward: reads the between-pass format; inverse: writes it)
 void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices

@@ -422,12 +422,14 @@ void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* ou
 // row pass / IP (hy_ntt.cu)
 void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
-                    cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr) {
+                    cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr, bool rows_done = false) {
   if (modup_cols_ok(c)) {
-    LimbList L;
-    for (int g = 0; g < G; ++g)
-      for (uint32_t i = 0; i <= level; ++i) L.add(own[g] + (size_t)i * c->N, d[g] + (size_t)i * c->N, i);
-    rows_list(c, L, true, s);
+    if (!rows_done) {  // rows_done: d already holds the inverse row pass (launch_ntt_rows_inv_aut)
+      LimbList L;
+      for (int g = 0; g < G; ++g)
+        for (uint32_t i = 0; i <= level; ++i) L.add(own[g] + (size_t)i * c->N, d[g] + (size_t)i * c->N, i);
+      rows_list(c, L, true, s);
+    }
     ModUpColsArgs ma{};
     for (int g = 0; g < G; ++g) {
       ma.src[g] = d[g];
@@ -697,8 +699,23 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
                     : DownItem{it[g].u, out[i], ct[i], kk[g], nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w};
       if (!alias) cin[g] = ct[i] + n * N;
     }
-    if (alias) automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
-    else automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
+    // kappa fused into the inverse row pass and the own-digit reads (N = 2^16, no aliasing): kappa(c1) is never
+    // stored; otherwise kappa(c1) (or the whole ct when an output aliases an input) is permuted into rc
+    const bool fuse_aut = split_moddown() && !alias && modup_cols_ok(c);
+    if (fuse_aut) {
+      RowsAutArgs ra{};
+      for (int g = 0; g < G; ++g) {
+        ra.src[g] = ct[ks[done + g]] + n * N;
+        ra.dst[g] = d[g];
+        ra.k[g] = kk[g];
+        rc1[g] = ct[ks[done + g]] + n * N;  // the own digits are read from c1 through kappa
+      }
+      launch_ntt_rows_inv_aut(c, ra, G, level, s);
+    } else if (alias) {
+      automorph_batch(c, G, cin, rc, kk, 2 * n, n, false, s);
+    } else {
+      automorph_batch(c, G, cin, rc1w, kk, n, n, false, s);
+    }
     if (split_moddown()) {
       uint64_t* v[kG];
       uint64_t* w[kG];
@@ -707,7 +724,7 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
         w[g] = it[g].w;
       }
       const bool vr = moddown_cols_ok(c);  // P-limb IP with the inverse row pass fused
-      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s, (int)n, vr ? v : nullptr);
+      modup_ip_fused(c, level, G, d, ext, rc1, keys, u, false, false, s, (int)n, vr ? v : nullptr, fuse_aut);
       IpFinalArgs fa{};
       for (int g = 0; g < G; ++g) {
         fa.ext[g] = ext[g];
@@ -718,7 +735,7 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
         fa.k0[g] = di[g].k0;
         fa.addct[g] = di[g].addct;
         fa.out[g] = di[g].out;
-        fa.kx[g] = 1;
+        fa.kx[g] = fuse_aut ? kk[g] : 1;  // own digits gathered from c1 through kappa
       }
       moddown_p(c, level, G, u, v, w, s, vr);
       launch_rows_ip_final(c, fa, G, level, false, s);

@@ -179,6 +179,58 @@ __global__ void __launch_bounds__(256) k_ntt_rows(LimbBatch b, DevTables dt, int
   }
 }
 
+// ---------------------------------------------------------------- pass B (rows), inverse, with the automorphism
+// The inverse row pass of kappa_k(c1) read straight from c1 (plain HRot): the NTT-domain Galois permutation maps
+// every 256-word row onto one source row (the high index bits of kappa depend only on high bits), so each warp
+// gathers its row from one 2 KB source row (L1-resident) and kappa(c1) is never stored.  Item g = blockIdx.z,
+// limb i = blockIdx.y (chain index i), grid (R/8, l+1, G).
+__global__ void __launch_bounds__(256) k_ntt_rows_inv_aut(const __grid_constant__ RowsAutArgs a, DevTables dt,
+                                                          int logN) {
+  __shared__ double sm[8][272];
+  __shared__ double tws[8][256];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + w, i = blockIdx.y, g = blockIdx.z;
+  const size_t N = (size_t)1 << logN;
+  if (row >= (int)(N >> 8)) return;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  const uint64_t* src = a.src[g] + (size_t)i * N;
+  uint64_t* dst = a.dst[g] + (size_t)i * N + (size_t)row * 256;
+  const uint64_t k = a.k[g];
+  double* S = sm[w];
+  double* T = tws[w];
+  double x[8];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint32_t xi = (uint32_t)row * 256 + elem<1>(l, kk);
+    x[kk] = u2d(src[k != 1 ? aut_index(xi, k, logN) : xi]);
+  }
+  load_twiddles_warp(T, dt.itw + (size_t)i * N, (uint32_t)(N >> 8) + (uint32_t)row, l);
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) S[pidx(elem<1>(l, kk))] = x[kk];
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) x[kk] = S[pidx(elem<3>(l, kk))];
+  run_stages<3, false>(x, l, 1, 0, T, q, qinv);
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) S[pidx(elem<3>(l, kk))] = x[kk];
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) x[kk] = S[pidx(elem<2>(l, kk))];
+  run_stages<2, false>(x, l, 4, 2, T, q, qinv);
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) S[pidx(elem<2>(l, kk))] = x[kk];
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) x[kk] = S[pidx(elem<1>(l, kk))];
+  run_stages<1, false>(x, l, 7, 5, T, q, qinv);
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) dst[elem<1>(l, kk)] = d2raw(x[kk]);
+}
+
 // ---------------------------------------------------------------- pass A (columns), R = 256
 // CTA = 512 threads: column c = tid & 15 of a 16-column strip, virtual lane l = tid >> 4.
 // grid = (256/16, n_limbs)
@@ -540,14 +592,13 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
   load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
   __syncwarp();
   const size_t roff = (size_t)row * 256;
+  // gathered positions: hoisted -- every digit; plain -- the own digit, read from c1 through kappa_kx
   uint32_t gi[8];
-  if (HOIST) {
-    const uint64_t kx = a.kx[g];
+  const uint64_t kx = a.kx[g];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
-      gi[k] = kx != 1 ? aut_index(xi, kx, logN) : xi;
-    }
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+    gi[k] = kx != 1 ? aut_index(xi, kx, logN) : xi;
   }
   double a0[8], a1[8];
 #pragma unroll
@@ -564,10 +615,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = u2d(src[gi[k]]);
     } else if (j == own_digit) {
-      ulonglong2 v[4];
-      load_l3(a.own[g] + (size_t)i * N + roff, l, v, false);
+      const uint64_t* src = a.own[g] + (size_t)i * N;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = l3_word(v, k);
+      for (int k = 0; k < 8; ++k) x[k] = u2d(src[gi[k]]);
     } else {
       const uint64_t* src = a.ext[g] + ((size_t)j * E + i) * N + roff;
 #pragma unroll
@@ -673,7 +723,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   const int own_digit = i / alpha;
   const size_t roff = (size_t)row * 256;
   // source rows of the permuted reads (hoisted digits; the c0 gather)
-  const uint32_t rowx = HOIST && a.kx[g] != 1 ? aut_index((uint32_t)roff, a.kx[g], logN) >> 8 : (uint32_t)row;
+  // kx: hoisted -- every digit is read through kappa_kx; plain -- the own digit (c1 itself, kappa fused here)
+  const uint32_t rowx = a.kx[g] != 1 ? aut_index((uint32_t)roff, a.kx[g], logN) >> 8 : (uint32_t)row;
   const uint64_t k0 = a.add0[g] ? a.k0[g] : 1;
   const uint32_t row0 = k0 != 1 ? aut_index((uint32_t)roff, k0, logN) >> 8 : (uint32_t)row;
   // iteration j < B: digit j; j == B: the ModDown epilogue (w rows and the c0 row)
@@ -683,7 +734,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
     if (j < B) {
       const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
       const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N) +
-                           (HOIST ? (size_t)rowx * 256 : roff);
+                           ((HOIST || j == own_digit) ? (size_t)rowx * 256 : roff);
       tma::mbar_expect(mb, 3 * 2048);
       tma::bulk_row(b, e0, mb);
       tma::bulk_row(b + 256, e0 + (size_t)L1 * N, mb);
@@ -698,7 +749,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   };
   // hoisted: in-row positions of the 8 gathered words, packed 4 per register
   uint32_t gpk[2] = {0, 0};
-  if (HOIST) {
+  {
     const uint64_t kx = a.kx[g];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -724,12 +775,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
     if (j < B) {
       double x[8];
       const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
-      if (HOIST) {
+      if (HOIST || j == own_digit) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) x[k] = u2d(xb[(gpk[k >> 2] >> (8 * (k & 3))) & 255]);
-      } else if (j == own_digit) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = u2d(xb[elem<3>(l, k)]);
       } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) x[k] = raw2d(xb[elem<1>(l, k)]);
@@ -928,6 +976,15 @@ void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s
   kt.bytes = 2ull * b.n * c->N * 8;
   if (inverse) k_ntt_rows<false><<<gB, 256, 0, s>>>(b, c->dt, (int)c->log_n);
   else k_ntt_rows<true><<<gB, 256, 0, s>>>(b, c->dt, (int)c->log_n);
+}
+
+void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  const int R = (int)c->N / 256;
+  dim3 grid(R / 8 > 0 ? R / 8 : 1, level + 1, G);
+  KTimer kt(c, FAM_NTT_B, s);
+  kt.bytes = 2ull * G * (level + 1) * c->N * 8;
+  k_ntt_rows_inv_aut<<<grid, 256, 0, s>>>(a, c->dt, (int)c->log_n);
 }
 
 void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
