@@ -189,3 +189,42 @@ def test_key_set_needs_no_decomposition():
                 assert r & (r - 1) == 0 or (N_SLOTS - r) & (N_SLOTS - r - 1) == 0, r
             allr |= rs
         assert len(allr) == want
+
+
+def _ca_slide(ci, w, wp, g, m, d, n=N_SLOTS):
+    """Slide rotations of a CAConv: f^2 - 1 per input ciphertext (Alg. 1), n_in from the layout."""
+    return H.Fmt("CA", n, wp, g, m, d).n_ct(ci) * 8
+
+
+def _stride1(ci, w, wp, g, m, d, algo):
+    spec = H.ConvSpec(ci, ci, w, 3, 1, wp, g, m, d, algo)
+    return (H.plan_caconv if algo == "CA" else H.plan_raconv)(spec, None, with_weights=False).counts["Slide"]
+
+
+def test_siso_counts_of_the_other_plans():
+    """tb:Rot and Boot lists SISO counts for three more (m, d) plans; the layout reading
+    (R-LAYOUT: CA(m, d) -> RA(d, m), c_n from the padded width) reproduces them too:
+      ResNet-20 Min Rot (1,2)/(1,8)/(2,16): 240;  ResNet-18 Min Boot (1,1)/(4,1)/(16,1)/(64,1): 536.
+    Stride-1 convs come from the full plans; a downsampling conv's Slide count depends only on its input format
+    (its IR is our own design, R-DSCONV, and needs m = g)."""
+    # ResNet-20: stem + 3 CA + 3 RA in stage 1, then per stage dsconv + 2 CA + 3 RA (tb:resnet 20 parameter)
+    plan = [(1, 2), (1, 8), (2, 16)]
+    gaps, chans, widths = [1, 2, 4], [16, 32, 64], [32, 16, 8]
+    siso = _ca_slide(3, 32, 32, 1, *plan[0])
+    for st, ((m, d), g, c, w) in enumerate(zip(plan, gaps, chans, widths)):
+        n_ca = 3 if st == 0 else 2
+        siso += n_ca * _stride1(c, w, 32, g, m, d, "CA") + 3 * _stride1(c, w, 32, g, d, m, "RA")
+        if st:
+            pm, pd = plan[st - 1]
+            siso += _ca_slide(chans[st - 1], widths[st - 1], 32, gaps[st - 1], pm, pd)
+    assert siso == 240
+    # ResNet-18 (stem out of scope): stage 1 2 CA + 2 RA, then per stage dsconv + 1 CA + 2 RA, widths padded to 64
+    plan = [(1, 1), (4, 1), (16, 1), (64, 1)]
+    gaps, chans, widths = [1, 2, 4, 8], [64, 128, 256, 512], [56, 28, 14, 7]
+    siso = 0
+    for st, ((m, d), g, c, w) in enumerate(zip(plan, gaps, chans, widths)):
+        siso += (2 if st == 0 else 1) * _stride1(c, w, 64, g, m, d, "CA") + 2 * _stride1(c, w, 64, g, d, m, "RA")
+        if st:
+            pm, pd = plan[st - 1]
+            siso += _ca_slide(chans[st - 1], widths[st - 1], 64, gaps[st - 1], pm, pd)
+    assert siso == 536
