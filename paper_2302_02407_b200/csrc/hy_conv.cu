@@ -200,15 +200,25 @@ struct Ctx {
 
 // x_g += HRot_r(x_g) for every r in rs, in order, for all ciphertexts x_g at once: each step is one
 // batched HRot whose evaluation key is shared by every item (RaS / RaS_g / IR_g)
-hy_status ras_all(const Ctx& x, const std::vector<uint64_t*>& v, uint32_t level, const std::vector<int64_t>& rs) {
-  if (v.empty()) return HY_OK;
+// tmp (optional): v.size() scratch ciphertexts (stride tmp_stride words): the steps ping-pong between v and tmp
+// (out = in + HRot(in) never aliases its input, so the key switch reads c1 / c0 through kappa without first
+// copying the permuted ciphertext), and an odd final position is copied back into v.
+hy_status ras_all(const Ctx& x, const std::vector<uint64_t*>& v, uint32_t level, const std::vector<int64_t>& rs,
+                  uint64_t* tmp = nullptr, size_t tmp_stride = 0) {
+  if (v.empty() || rs.empty()) return HY_OK;
+  const size_t G = v.size(), bytes = 2ull * (level + 1) * x.c->N * 8;
+  std::vector<uint64_t*> cur(v.begin(), v.end()), nxt(G);
+  for (size_t g = 0; g < G; ++g) nxt[g] = tmp ? tmp + g * tmp_stride : v[g];
   for (int64_t r : rs) {
-    std::vector<const uint64_t*> keys(v.size(), x.key(r)), in_c(v.begin(), v.end());
-    std::vector<int32_t> rr(v.size(), (int32_t)r);
-    hy_status st = hy::hrot_multi(x.c, keys.data(), in_c.data(), level, rr.data(), (uint32_t)v.size(), v.data(),
-                              in_c.data(), x.s);
+    std::vector<const uint64_t*> keys(G, x.key(r)), in_c(cur.begin(), cur.end());
+    std::vector<int32_t> rr(G, (int32_t)r);
+    hy_status st = hy::hrot_multi(x.c, keys.data(), in_c.data(), level, rr.data(), (uint32_t)G, nxt.data(),
+                                  in_c.data(), x.s);
     if (st != HY_OK) return st;
+    if (tmp) std::swap(cur, nxt);
   }
+  if (tmp && cur[0] != v[0])
+    for (size_t g = 0; g < G; ++g) cudaMemcpyAsync(v[g], cur[g], bytes, cudaMemcpyDeviceToDevice, x.s);
   return HY_OK;
 }
 
@@ -364,7 +374,8 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   const size_t f2 = (size_t)p->s.f * p->s.f;
   // CA: slid inputs + acc + (up to) two ciphertexts per SISO group (group sums, masked groups)
   // (8 = one block of MulFilter&Sum accumulators)
-  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + 2 * p->n_groups) * ct;
+  // (+ n_groups ping-pong ciphertexts for the RaS / RaS_g / IR_g steps)
+  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + 3 * p->n_groups) * ct;
   return (p->n_out * (f2 + 1) + 8) * ct;                          // tap accumulators + one sum per output
 }
 
@@ -403,16 +414,18 @@ namespace {
 // RAConv after its lazy Slide_1&Sum_f: rescale, RaS_g, then (with a mask) the IR_g mask product + rescale
 // and the IR_g rotations, batched over the outputs.  dst: per output, a ciphertext buffer at level - 1
 // (the output itself without a mask); tmp: up to 8 temporaries of ct_l words.
+// pp / pp_stride: no ping-pong ciphertexts for the RaS_g / IR_g steps (nullptr: in place).
 hy_status ra_tail(const Ctx& x, std::vector<const uint64_t*>& sums, std::vector<uint64_t*>& dst, uint32_t level,
-                  const uint64_t* mask, uint64_t* tmp, size_t ct_l, uint64_t* const* out) {
+                  const uint64_t* mask, uint64_t* tmp, size_t ct_l, uint64_t* const* out, uint64_t* pp = nullptr,
+                  size_t pp_stride = 0) {
   const hy_conv_plan* p = x.p;
   const size_t no = sums.size();
   hy_status stt = rescale_multi(x.c, sums.data(), (uint32_t)no, level, dst.data(), x.s);
-  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g);
+  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g, pp, pp_stride);
   if (stt == HY_OK && p->has_mask) {
     std::vector<uint64_t*> fin(out, out + no);
     stt = mask_rescale(x, dst, mask, level - 1, tmp, ct_l, fin);
-    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g);
+    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g, pp, pp_stride);
   }
   return stt;
 }
@@ -527,8 +540,9 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
       }
       if (stt != HY_OK) return stt;
     }
-    stt = ras_all(x, gp, level - 1, p->ras);                        // RaS over C_a
-    if (stt == HY_OK) stt = ras_all(x, gp, level - 1, p->ras_g);    // RaS_g over C_g
+    uint64_t* pp = gbuf + 2 * G * ct_m;  // G ping-pong ciphertexts (hy_conv_scratch_words)
+    stt = ras_all(x, gp, level - 1, p->ras, pp, ct_m);                        // RaS over C_a
+    if (stt == HY_OK) stt = ras_all(x, gp, level - 1, p->ras_g, pp, ct_m);    // RaS_g over C_g
     if (stt != HY_OK || (!p->has_mask && !ds)) return stt == HY_OK ? cuda_check("hy_caconv") : stt;
     // IR_g: mask (one level) ...
     std::vector<uint64_t*> masked(G);
@@ -547,7 +561,7 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
       stt = hrot_multi(c, keys.data(), b.data(), level - 2, rr.data(), (uint32_t)J, fin.data(), a.data(), x.s);
       if (stt != HY_OK) return stt;
     }
-    stt = ras_all(x, fin, level - 2, p->ir_g);                     // ... and replicate
+    stt = ras_all(x, fin, level - 2, p->ir_g, pp, ct_m);           // ... and replicate
     if (stt != HY_OK) return stt;
     return cuda_check("hy_caconv");
   }
@@ -591,7 +605,9 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
     sums[o - ob] = sum;
     dst[o - ob] = p->has_mask ? oacc : out[o - ob];  // the output's consumed tap accumulators
   }
-  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, out);
+  // ping-pong buffers: the second tap accumulator of every output (consumed by its HRotSum; f^2 >= 2)
+  const bool ppok = f2 >= 2;
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, out, ppok ? accs + ct_l : nullptr, f2 * ct_l);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv");
 }
@@ -682,7 +698,7 @@ extern "C" hy_status hy_raconv_finish(hy_ctx* c, const hy_conv_plan* p, const ui
   if (stt != HY_OK) return stt;
   std::vector<const uint64_t*> sums{sum};
   std::vector<uint64_t*> dst{p->has_mask ? dstb : out};
-  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out);
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out, scratch + 3 * ct_l, ct_l);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv_finish");
 }
