@@ -142,12 +142,14 @@ struct RowsIpArgs {
   const uint64_t* own[kG];
   const uint64_t* evk[kG];
   uint64_t* u[kG];
-  uint64_t* v[kG];  // inv_p: [2][K][N] P limbs after the inverse row pass (between-pass format)
+  uint64_t* v[kG];   // inv_p: [2][K][N] P limbs after the inverse row pass (between-pass format)
+  uint64_t kx[kG];   // hoist: Galois element each item reads the shared NTT-domain digits through
 };
 // u0: first extended limb produced (0: all of Q_l u P; l+1: the P limbs only, for the split ModDown)
 // inv_p (with u0 = l+1): store the P limbs after their inverse row pass into v instead (split ModDown)
+// hoist: ext holds the NTT-domain digits of one shared ModUp, read through kx_g (hoisted batch)
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0 = 0, bool inv_p = false);
+                        cudaStream_t s, int u0 = 0, bool inv_p = false, bool hoist = false);
 
 // Key-switch inner product on the Q_l limbs fused with the ModDown epilogue (hy_ntt.cu), per item g,
 // limb i <= level, poly c:

@@ -961,8 +961,22 @@ extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, con
         fa.out[g] = outs[ks[done + g]];
         fa.kx[g] = kk[g];
       }
-      ip_batch(c, level, G, ext, own, keys, u, kk, false, false, false, s, (int)nl);
-      moddown_p(c, level, G, u, v, w, s);
+      const bool vr = moddown_cols_ok(c);
+      if (vr) {  // P-limb IP as a row kernel with the inverse row pass fused (v in the between-pass format)
+        RowsIpArgs ra{};
+        for (int g = 0; g < G; ++g) {
+          ra.ext[g] = ext[g];
+          ra.own[g] = c1;
+          ra.evk[g] = keys[g];
+          ra.u[g] = u[g];
+          ra.v[g] = v[g];
+          ra.kx[g] = kk[g];
+        }
+        launch_ntt_rows_ip(c, ra, G, level, false, false, s, (int)nl, true, true);
+      } else {
+        ip_batch(c, level, G, ext, own, keys, u, kk, false, false, false, s, (int)nl);
+      }
+      moddown_p(c, level, G, u, v, w, s, vr);
       launch_rows_ip_final(c, fa, G, level, true, s);
       done += G;
       continue;

@@ -426,7 +426,9 @@ __device__ __forceinline__ void store_l3(uint64_t* p, int l, const double (&x)[8
 // item index is the fastest grid dimension so that items sharing a key hit its rows in L2.
 // SUM: one warp loops over all G items and accumulates into u[0] (each item's sum re-centred with
 // fred first), race-free because one warp owns (u, row).
-template <int B, bool SUM>
+// HOIST: the digits are the NTT-domain extended digits of one shared ModUp, read through the Galois permutation
+// kx_g of each item (Halevi-Shoup; used for the P limbs of the hoisted batch, with inv_p).
+template <int B, bool SUM, bool HOIST>
 __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ RowsIpArgs a, int G, DevTables dt,
                                                         int level, int n_q, int L1, int E, int alpha, int logN,
                                                         int accumulate, int u0, int inv_p) {
@@ -461,7 +463,15 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
       load_l3(e0, l, k0, true);
       load_l3(e0 + (size_t)L1 * N, l, k1, true);
       double x[8];
-      if (j == own_digit) {
+      if (HOIST) {
+        const uint64_t kx = a.kx[g];
+        const uint64_t* src = j == own_digit ? a.own[g] + (size_t)u * N : a.ext[g] + ((size_t)j * E + u) * N;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+          x[k] = u2d(src[kx != 1 ? aut_index(xi, kx, logN) : xi]);
+        }
+      } else if (j == own_digit) {
         ulonglong2 v[4];
         load_l3(a.own[g] + (size_t)u * N + roff, l, v, false);
 #pragma unroll
@@ -1049,7 +1059,7 @@ void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
 }
 
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0, bool inv_p) {
+                        cudaStream_t s, int u0, bool inv_p, bool hoist) {
   if (G <= 0) return;
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
   const int nu = E - u0;  // extended limbs produced
@@ -1069,12 +1079,17 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
 #define HY_RIP(BB)                                                                                             \
   case BB:                                                                                                     \
     if (sum)                                                                                                   \
-      k_ntt_rows_ip<BB, true><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E, (int)c->alpha, \
-                                                   (int)c->log_n, accumulate ? 1 : 0, u0, inv_p);             \
+      k_ntt_rows_ip<BB, true, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,         \
+                                                          (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0, \
+                                                          inv_p);                                              \
+    else if (hoist)                                                                                            \
+      k_ntt_rows_ip<BB, false, true><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,         \
+                                                          (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0, \
+                                                          inv_p);                                              \
     else                                                                                                       \
-      k_ntt_rows_ip<BB, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,              \
-                                                    (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0, u0,      \
-                                                    inv_p);                                                    \
+      k_ntt_rows_ip<BB, false, false><<<grid, 256, 0, s>>>(a, G, c->dt, (int)level, (int)c->n_q, L1, E,        \
+                                                           (int)c->alpha, (int)c->log_n, accumulate ? 1 : 0,    \
+                                                           u0, inv_p);                                         \
     break;
   switch (beta) {
     HY_RIP(1)
