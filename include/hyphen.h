@@ -285,6 +285,17 @@ hy_status hy_encode_coeffs(uint32_t log_n, const double* h_slots, uint32_t n_slo
                            int64_t* h_coeffs);
 /* Signed integer coefficients (host, N words) -> NTT-domain plaintext on q_0..q_l. */
 hy_status hy_pt_from_coeffs(hy_ctx* ctx, const int64_t* h_coeffs, uint32_t level, uint64_t* d_pt, void* stream);
+/* CKKS decode (client side, the inverse of R-ENCODE; P:98-100 canonical embedding):
+ * z_j = m(zeta^{5^j}) / scale for j < n_slots, zeta = exp(i pi / N), where m is the centred CRT lift of the
+ * NTT-domain plaintext d_pt [l+1][N] (as hy_decrypt returns it) to (-Q_l/2, Q_l/2].  h_re / h_im: host,
+ * n_slots doubles each (h_im may be NULL).  Synchronous (one device iNTT, then host CRT + special FFT).
+ * A floating-point result: its contract is a tolerance, not bit-exactness.
+ * Errors: HY_E_ARG (null, level, scale <= 0), HY_E_CAPACITY (n_slots > N/2), HY_E_WORKSPACE. */
+hy_status hy_decode(hy_ctx* ctx, const uint64_t* d_pt, uint32_t level, double scale, uint32_t n_slots,
+                    double* h_re, double* h_im, void* stream);
+/* Host-only part of hy_decode: real coefficients (host, N doubles) -> slots. */
+hy_status hy_decode_coeffs(uint32_t log_n, const double* h_coeffs, double scale, uint32_t n_slots, double* h_re,
+                           double* h_im);
 
 #ifdef __cplusplus
 }

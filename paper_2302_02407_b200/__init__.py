@@ -83,6 +83,9 @@ SIGNATURES = {
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
     "hy_encode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), _U32, _U64, C.POINTER(C.c_int64)]),
     "hy_pt_from_coeffs": (C.c_int, [_P, C.POINTER(C.c_int64), _U32, _P, _P]),
+    "hy_decode": (C.c_int, [_P, _P, _U32, C.c_double, _U32, C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
+    "hy_decode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), C.c_double, _U32, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double)]),
     "hy_conv_plan_create": (C.c_int, [_U32, C.POINTER(_ConvSpec), C.POINTER(_P)]),
     "hy_conv_plan_destroy": (None, [_P]),
     "hy_conv_plan_query": (C.c_int, [_P, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
@@ -138,6 +141,16 @@ def encode_coeffs(log_n: int, slots, scale: int) -> np.ndarray:
     _check(lib().hy_encode_coeffs(log_n, z.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale),
                                   out.ctypes.data_as(C.POINTER(C.c_int64))))
     return out
+
+
+def decode_coeffs(log_n: int, coeffs, scale: float, n_slots=None) -> np.ndarray:
+    """Host-side CKKS decoding of real coefficients: complex slots z_j = m(zeta^{5^j}) / scale."""
+    m = np.ascontiguousarray(coeffs, np.float64)
+    n_slots = (1 << log_n) // 2 if n_slots is None else n_slots
+    re, im = np.zeros(n_slots), np.zeros(n_slots)
+    _check(lib().hy_decode_coeffs(log_n, m.ctypes.data_as(C.POINTER(C.c_double)), float(scale), n_slots,
+                                  re.ctypes.data_as(C.POINTER(C.c_double)), im.ctypes.data_as(C.POINTER(C.c_double))))
+    return re + 1j * im
 
 
 class Context:
@@ -339,6 +352,15 @@ class Context:
         _check(lib().hy_encode(self._c, z.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale), level,
                                _ptr(out), self._stream()))
         return out
+
+    def decode(self, pt, level, scale, n_slots=None):
+        """Complex slots of an NTT-domain plaintext (hy_decode; synchronous)."""
+        n_slots = self.N // 2 if n_slots is None else n_slots
+        re, im = np.zeros(n_slots), np.zeros(n_slots)
+        _check(lib().hy_decode(self._c, _ptr(pt), level, float(scale), n_slots,
+                               re.ctypes.data_as(C.POINTER(C.c_double)), im.ctypes.data_as(C.POINTER(C.c_double)),
+                               self._stream()))
+        return re + 1j * im
 
     def pt_from_coeffs(self, coeffs, level, out=None):
         out = self.empty(level + 1, self.N) if out is None else out

@@ -151,3 +151,96 @@ extern "C" hy_status hy_encode_coeffs(uint32_t log_n, const double* slots, uint3
   }
   return HY_OK;
 }
+
+// CKKS decode (client side, untimed): the inverse of R-ENCODE.  The N real coefficients m_i
+// form the complex vector v_i = (m_i + i m_{i+n}) / scale; the "special" forward FFT over <5> evaluates
+// it at zeta^{5^j}, i.e. z_j = m(zeta^{5^j}) / scale (canonical embedding, slot j <-> zeta^{5^j}).
+// Decode is a floating-point result (a tolerance, not bit-exactness, is its contract), so plain
+// double arithmetic over the double-double tables' high parts is used.
+extern "C" hy_status hy_decode_coeffs(uint32_t log_n, const double* coeffs, double scale, uint32_t n_slots,
+                                      double* re, double* im) {
+  if (!coeffs || !re || log_n < 2 || log_n > 17 || !(scale > 0)) return HY_E_ARG;
+  const uint64_t N = 1ull << log_n, n = N / 2, M = 2 * N;
+  if (n_slots > n) return HY_E_CAPACITY;
+  auto T = tables(log_n);
+  std::vector<double> vr(n), vi(n);
+  const double inv = 1.0 / scale;
+  for (uint64_t i = 0; i < n; ++i) {
+    vr[i] = coeffs[i] * inv;
+    vi[i] = coeffs[i + n] * inv;
+  }
+  int bits = 0;
+  while ((1ull << bits) < n) ++bits;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1ull) << (bits - 1 - b);
+    if (r > i) {
+      std::swap(vr[i], vr[r]);
+      std::swap(vi[i], vi[r]);
+    }
+  }
+  for (uint64_t len = 2; len <= n; len <<= 1) {
+    const uint64_t lenh = len >> 1, lenq = len << 2, gap = M / lenq;
+    for (uint64_t i = 0; i < n; i += len) {
+      for (uint64_t j = 0; j < lenh; ++j) {
+        const CDD& w = T->ksi[(T->rot[j] % lenq) * gap];
+        const double wr = w.re.hi, wi = w.im.hi;
+        const double ar = vr[i + j + lenh], ai = vi[i + j + lenh];
+        const double br = ar * wr - ai * wi, bi = ar * wi + ai * wr;
+        const double ur = vr[i + j], ui = vi[i + j];
+        vr[i + j] = ur + br;
+        vi[i + j] = ui + bi;
+        vr[i + j + lenh] = ur - br;
+        vi[i + j + lenh] = ui - bi;
+      }
+    }
+  }
+  for (uint32_t j = 0; j < n_slots; ++j) {
+    re[j] = vr[j];
+    if (im) im[j] = vi[j];
+  }
+  return HY_OK;
+}
+
+namespace hy {
+// Centred CRT of the n coefficient-domain limbs limbs[u][N] (moduli mods[0..n)) to doubles: the unique
+// representative of x mod Q in (-Q/2, Q/2], found by Garner's mixed-radix algorithm with centred digits
+// a_k in [-(q_k-1)/2, (q_k-1)/2] (the symmetric digit set covers exactly Q consecutive integers around 0),
+// then evaluated in binary128 by Horner from the top digit and rounded to double.
+void crt_centered_to_double(const uint64_t* limbs, uint32_t n, uint64_t N, const uint64_t* mods, double* out) {
+  using u128 = unsigned __int128;
+  // Mmod[k][j] = (q_0 ... q_{j-1}) mod q_k for j < k; inv[k] = (q_0 ... q_{k-1})^{-1} mod q_k
+  std::vector<uint64_t> Mmod((size_t)n * n, 0), inv(n, 1);
+  auto powmod = [](uint64_t b, uint64_t e, uint64_t q) {
+    uint64_t r = 1;
+    for (; e; e >>= 1, b = (uint64_t)((u128)b * b % q))
+      if (e & 1) r = (uint64_t)((u128)r * b % q);
+    return r;
+  };
+  for (uint32_t k = 0; k < n; ++k) {
+    uint64_t m = 1 % mods[k];
+    for (uint32_t j = 0; j < k; ++j) {
+      Mmod[(size_t)k * n + j] = m;
+      m = (uint64_t)((u128)m * (mods[j] % mods[k]) % mods[k]);
+    }
+    inv[k] = powmod(m, mods[k] - 2, mods[k]);
+  }
+  std::vector<int64_t> a(n);
+  for (uint64_t x = 0; x < N; ++x) {
+    for (uint32_t k = 0; k < n; ++k) {
+      const uint64_t q = mods[k];
+      u128 s = 0;
+      for (uint32_t j = 0; j < k; ++j) {
+        const uint64_t aj = a[j] < 0 ? q - (uint64_t)(-a[j]) % q : (uint64_t)a[j] % q;
+        s = (s + (u128)aj * Mmod[(size_t)k * n + j]) % q;
+      }
+      const uint64_t xk = limbs[(size_t)k * N + x] % q;
+      const uint64_t d = (uint64_t)(((u128)(xk + q - (uint64_t)s) % q) * inv[k] % q);
+      a[k] = d > (q - 1) / 2 ? (int64_t)d - (int64_t)q : (int64_t)d;
+    }
+    __float128 v = 0;
+    for (int k = (int)n - 1; k >= 0; --k) v = v * (__float128)mods[k] + (__float128)a[k];
+    out[x] = (double)v;
+  }
+}
+}  // namespace hy

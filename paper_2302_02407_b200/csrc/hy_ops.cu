@@ -588,3 +588,33 @@ extern "C" hy_status hy_encode(hy_ctx* c, const double* h_slots, uint32_t n_slot
   if (s0 != HY_OK) return s0;
   return hy_pt_from_coeffs(c, coeffs.data(), level, pt, stream);
 }
+
+namespace hy {
+void crt_centered_to_double(const uint64_t* limbs, uint32_t n, uint64_t N, const uint64_t* mods, double* out);
+}
+
+extern "C" hy_status hy_decode(hy_ctx* c, const uint64_t* pt, uint32_t level, double scale, uint32_t n_slots,
+                               double* h_re, double* h_im, void* stream) {
+  if (!c || !pt || !h_re) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  if (n_slots > c->N / 2) return fail(HY_E_CAPACITY, "more slots than N/2");
+  if (!(scale > 0)) return fail(HY_E_ARG, "scale must be positive");
+  if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
+  cudaStream_t s = st(stream);
+  const uint32_t n = level + 1;
+  Ws ws{c->ws, c->ws_bytes};
+  uint64_t* coeff = ws.take<uint64_t>((size_t)n * c->N);
+  if (!coeff) return fail(HY_E_WORKSPACE, "workspace too small");
+  std::vector<uint32_t> chain(n);
+  for (uint32_t i = 0; i < n; ++i) chain[i] = i;
+  ntt_contig(c, pt, coeff, chain.data(), n, true, s);
+  std::vector<uint64_t> h((size_t)n * c->N);
+  cudaMemcpyAsync(h.data(), coeff, h.size() * 8, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  hy_status e = cuda_check("hy_decode");
+  if (e != HY_OK) return e;
+  std::vector<double> m(c->N);
+  crt_centered_to_double(h.data(), n, c->N, c->mod.data(), m.data());
+  e = hy_decode_coeffs(c->log_n, m.data(), scale, n_slots, h_re, h_im);
+  return e == HY_OK ? HY_OK : fail(e, "hy_decode_coeffs");
+}

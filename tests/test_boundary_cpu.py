@@ -69,3 +69,20 @@ def test_encode_tie_rule(hy):
     for c, scale, want in [(0.5, 1, 1), (-0.5, 1, -1), (1.5, 1, 2), (-2.5, 1, -3)]:
         m = hy.encode_coeffs(10, np.full(512, c), scale)
         assert int(m[0]) == want and not np.any(m[1:])
+
+
+@pytest.mark.parametrize("pset", ["toy", "hyp"])
+def test_decode_coeffs_matches_oracle(hy, pset):
+    """Host decode (hy_decode_coeffs) = the oracle's canonical embedding m(zeta^{5^j}) / scale (its own
+    pinned eval_slots, an independent 2N-point FFT) for random integer coefficients, and it inverts encode."""
+    prm = synth.PARAMS[pset]
+    o = oracle.Oracle(**prm)
+    scale = 2.0 ** prm["log_scale"]
+    m = np.random.default_rng(5).integers(-2**50, 2**50, o.N).astype(np.float64)
+    got = hy.decode_coeffs(prm["log_n"], m, scale)
+    want = o.eval_slots(m) / scale
+    assert np.max(np.abs(got - want)) < 1e-9 * np.max(np.abs(want))
+    z = synth.slots_uniform(9, o.n)
+    back = hy.decode_coeffs(prm["log_n"], hy.encode_coeffs(prm["log_n"], z, int(scale)).astype(np.float64), scale)
+    assert np.max(np.abs(back - z)) < 2**-25
+    assert hy.decode_coeffs(prm["log_n"], m, scale, n_slots=7).shape == (7,)

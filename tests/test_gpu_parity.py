@@ -88,6 +88,22 @@ def test_encode_encrypt_decrypt(pair):
     assert np.array_equal(to_np(dec), o.decrypt(SK, oct_).data)
 
 
+def test_decode(pair):
+    """hy_decode (device iNTT + centred CRT + special FFT) vs the oracle's big-int CRT + FFT decode of the same
+    limbs (a float result: tolerance), and decode(decrypt(encrypt(encode z))) = z within the encryption noise."""
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 3
+    z = synth.slots_uniform(31, o.n)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    ct = ctx.encrypt(SK, 41, 8, ctx.encode(z, scale, level), level)
+    dec = ctx.decrypt(SK, ct, level)
+    got = ctx.decode(dec, level, scale)
+    want = o.decode(oracle.Pt(to_np(dec), level, float(scale)))
+    assert np.max(np.abs(got - want)) < 1e-9
+    assert np.max(np.abs(got - z)) < 2**-20
+    assert np.array_equal(ctx.decode(dec, level, scale, n_slots=5), got[:5])
+
+
 def test_modup_ip_moddown(pair):
     name, ctx, o = pair
     for level in sorted({o.nq - 1, 0, min(5, o.nq - 1)}):
@@ -197,3 +213,7 @@ def test_relin_key_and_mulct(pair):
     sq = o.rescale(wsq[0])
     zs = np.real(o.decode(o.decrypt(SK, sq)))
     assert np.max(np.abs(zs - za * za)) < 2**-15
+    # hy_decode of the unrescaled square: coefficients ~ scale^2, far beyond q_0 (multi-limb centred CRT)
+    sq_dec = ctx.decrypt(SK, outs[0], level)
+    zq = ctx.decode(sq_dec, level, float(scale) ** 2)
+    assert np.max(np.abs(np.real(zq) - za * za)) < 2**-15

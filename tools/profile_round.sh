@@ -1,21 +1,36 @@
 #!/bin/bash
-# Round evidence: launch list of the bench's timed regions + ncu --set full of the hot kernels.
+# Round evidence: launch list of the bench's timed regions + ncu --set full of every distinct kernel in it.
 # usage: tools/profile_round.sh <tag>   (run from the repo root under gpurun; then tools/ncu_round.py <tag>)
 TAG=${1:-r01}
 export HY_NCU_TIMED=1
 B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-conv"
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_${TAG}.csv $B > /dev/null 2>&1
-# (kernel regex, launches to skip) in the timed region's launch order: per 16-item chunk of the plain step
-# k_bconv_cols runs ModUp (<4, 0>) then ModDown (<4, 1>); the plain Q-limb kernels (<6, 0, 2>) precede the
-# hoisted ones (<6, 1, 2>) of the second timed step
+    --kernel-name-base demangled --log-file gpurun_out/launches_${TAG}.csv $B > /dev/null 2>&1
+# one full capture per distinct kernel (first launch in the timed region, which is the plain step's chunk 0
+# for the kernels both steps share; the hoisted-only instantiations are captured from the hoisted step)
+python - "$TAG" > gpurun_out/kernels_${TAG}.txt << 'PY'
+import csv, re, sys
+tag = sys.argv[1]
+rows = list(csv.reader(l for l in open(f"gpurun_out/launches_{tag}.csv") if not l.startswith("==")))
+h = rows[0]; ki = h.index("Kernel Name")
+names = []
+for x in rows[1:]:
+    if len(x) != len(h) or x[h.index("Metric Name")] != "gpu__time_duration.sum":
+        continue
+    names.append(x[ki].replace("(anonymous namespace)::", "").split("(")[0].replace("void ", "").strip().split("::")[-1])
+seen = []
+for n in names:
+    if n not in seen:
+        seen.append(n)
+for n in seen:  # ncu -k regex:<base>[<(] counts only matching launches for --launch-skip
+    base = n.split("<")[0]
+    same = [m for m in names if m.split("<")[0] == base]
+    print(base, same.index(n))
+PY
 i=0
-for ks in "k_bconv_cols:2" "k_bconv_cols:3" "k_rows_ip_final_tma:2" "k_rows_ip_final_tma:5" "k_ntt_rows_ip:2" \
-          "k_ntt_rows:2" "k_automorph:2" "k_ks_ip:1" "k_modup_bconv:0"; do
+while read -r k skip; do
   i=$((i+1))
-  k=${ks%%:*}; skip=${ks##*:}
   ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k regex:"${k}[<(]" -s $skip -c 1 \
-      -o gpurun_out/prof_${TAG}_k$i $B > /dev/null 2>&1
-done
+      -k "regex:${k}[<(]" -s $skip -c 1 -o gpurun_out/prof_${TAG}_k$i $B > /dev/null 2>&1
+done < gpurun_out/kernels_${TAG}.txt
 ls gpurun_out | grep $TAG
