@@ -716,15 +716,15 @@ __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.
 __host__ __device__ constexpr int rows_warp_words(int nst) { return 256 * (1 + 3 * nst); }
 constexpr size_t rows_tma_smem(int nst) { return 8 * ((size_t)rows_warp_words(nst) * 8 + 8 * nst); }
 
+// (item g, row block by, Q limb i) of the Q-limb kernel; dsm = rows_tma_smem(NST) bytes of dynamic smem
 template <int B, bool HOIST, int NST>
-__global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
-                                                              const ModDownConst* md, int level, int L1, int E,
-                                                              int alpha, int logN) {
-  extern __shared__ __align__(128) double dsm[];
+__device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, const DevTables& dt,
+                                                       const ModDownConst* md, int level, int L1, int E, int alpha,
+                                                       int logN, double* dsm, int g, int by, int i) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const size_t N = (size_t)1 << logN;
   const int R = (int)(N >> 8);
-  const int g = blockIdx.x, row = blockIdx.y * 8 + w, i = blockIdx.z;
+  const int row = by * 8 + w;
   if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
   double* T = dsm + (size_t)w * rows_warp_words(NST);  // stage s at T + 256 + 768 s: e0, e1, digit (x) rows
   uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * rows_warp_words(NST)) + NST * w;
@@ -848,6 +848,15 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   }
 }
 
+template <int B, bool HOIST, int NST>
+__global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
+                                                              const ModDownConst* md, int level, int L1, int E,
+                                                              int alpha, int logN) {
+  extern __shared__ __align__(128) double dsm[];
+  rows_ip_final_tma_body<B, HOIST, NST>(a, dt, md, level, L1, E, alpha, logN, dsm, blockIdx.x, blockIdx.y,
+                                        blockIdx.z);
+}
+
 // ---------------------------------------------------------------- iNTT column pass + fast BConv + NTT column pass
 // CTA = 256 threads on one 8-column strip (thread: column c = tid & 7, lane l = tid >> 3; the
 // k_ntt_cols256 scheme at half width, so that two CTAs of 126-register threads share an SM and one
@@ -864,15 +873,19 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
 // column stages and is stored fred-reduced (between-pass format, for the fused row kernels).  The
 // coefficient-domain sources and the un-transformed conversion never reach HBM.  The next phase's
 // twiddle heap is fetched into a register during the current phase (double-buffered T).
+// shared memory of one column CTA: the 8-column strip, the double-buffered twiddle heap, the BConv constants
+template <int A>
+__host__ __device__ constexpr int cols_smem_words() { return 8 * 256 + 2 * 256 + kMaxExt * A; }
+
+// (strip bx, group j, item g); sm = cols_smem_words<A>() doubles of shared memory
 template <int A, bool DOWN>
-__global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ ModUpColsArgs a,
-                                                       const ModUpConst* mc, const ModDownConst* md, DevTables dt,
-                                                       int level, int n_q, int E, int logN) {
-  __shared__ double sm[8 * 256];
-  __shared__ double T[2][256];
-  __shared__ double s_hat[kMaxExt][A];
+__device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const ModUpConst* mc, const ModDownConst* md,
+                                                const DevTables& dt, int level, int n_q, int E, int logN,
+                                                double* sm, int bx, int j, int g) {
+  double* T = sm + 8 * 256;       // [2][256]
+  double* s_hat = T + 2 * 256;    // [kMaxExt][A]
   const int c = threadIdx.x & 7, l = threadIdx.x >> 3, tid = threadIdx.x;
-  const int col = blockIdx.x * 8 + c, j = blockIdx.y, g = blockIdx.z;
+  const int col = bx * 8 + c;
   const size_t N = (size_t)1 << logN;
   const int n = level + 1;
   int lo = 0, nsrc = A, nph = A + n;  // DOWN: K sources, l+1 targets
@@ -883,8 +896,8 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
   }
   for (int i = tid; i < (DOWN ? n : E) * A; i += blockDim.x) {
     const int u = i / A, ii = i % A;
-    if constexpr (DOWN) s_hat[u][ii] = (double)md->phat_mod[u][ii];
-    else s_hat[u][ii] = ii < nsrc ? (double)mc[j].hat_mod[u][ii] : 0.0;
+    if constexpr (DOWN) s_hat[u * A + ii] = (double)md->phat_mod[u][ii];
+    else s_hat[u * A + ii] = ii < nsrc ? (double)mc[j].hat_mod[u][ii] : 0.0;
   }
   // target phase p >= nsrc -> target index (ModUp: the (p - nsrc)-th ext limb outside [lo, hi))
   auto target = [&](int p) {
@@ -897,7 +910,7 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
     if (p < nsrc) return dt.itw + (size_t)src_chain(p) * N;
     return dt.tw + (size_t)tgt_chain(target(p)) * N;
   };
-  if (tid > 0 && tid < 256) T[0][tid] = table(0)[tid];
+  if (tid > 0 && tid < 256) T[tid] = table(0)[tid];
   double y[A][8];
 #pragma unroll
   for (int i = 0; i < A; ++i)
@@ -906,7 +919,7 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
   __syncthreads();
   for (int p = 0; p < nph; ++p) {
     const double tw_next = (p + 1 < nph && tid > 0 && tid < 256) ? table(p + 1)[tid] : 0.0;
-    const double* Tp = T[p & 1];
+    const double* Tp = T + 256 * (p & 1);
     double x[8];
     if (p < nsrc) {  // inverse column pass of source p
       const PrimeConst& pc = dt.pc[src_chain(p)];
@@ -942,7 +955,7 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
       const double q = pc.qd, qinv = pc.qinv;
       double h[A];
 #pragma unroll
-      for (int i = 0; i < A; ++i) h[i] = s_hat[u][i];
+      for (int i = 0; i < A; ++i) h[i] = s_hat[u * A + i];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         double acc = 0.0;
@@ -968,9 +981,17 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
 #pragma unroll
       for (int k = 0; k < 8; ++k) dst[(size_t)elem<3>(l, k) * 256] = d2raw(fred(x[k], q, qinv));
     }
-    if (tid > 0 && tid < 256) T[(p + 1) & 1][tid] = tw_next;
+    if (tid > 0 && tid < 256) T[256 * ((p + 1) & 1) + tid] = tw_next;
     __syncthreads();
   }
+}
+
+template <int A, bool DOWN>
+__global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ ModUpColsArgs a,
+                                                       const ModUpConst* mc, const ModDownConst* md, DevTables dt,
+                                                       int level, int n_q, int E, int logN) {
+  __shared__ double sm[cols_smem_words<A>()];
+  bconv_cols_body<A, DOWN>(a, mc, md, dt, level, n_q, E, logN, sm, blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
 }  // namespace

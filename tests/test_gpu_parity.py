@@ -217,3 +217,19 @@ def test_relin_key_and_mulct(pair):
     sq_dec = ctx.decrypt(SK, outs[0], level)
     zq = ctx.decode(sq_dec, level, float(scale) ** 2)
     assert np.max(np.abs(np.real(zq) - za * za)) < 2**-15
+
+
+@pytest.mark.parametrize("level", [23, 9])
+def test_hrot_hoisted_chunked(level):
+    """Hoisted batch longer than the workspace's key-switch batch (4 -> chunks of 4 and 1 sharing one ModUp):
+    bit-exact vs the oracle at both conv and full level."""
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS["hyp"]
+    ctx, o = hy.Context(**prm, max_batch=4), oracle.Oracle(**prm)
+    rs = [1, 2, -3, 7, 100]
+    evks = [o.keygen_rot(SK, EK, r) for r in rs]
+    dct, oct_ = _fresh_ct(ctx, o, "hyp", level, 71)
+    outs = ctx.hrot_hoisted([to_dev(e, ctx) for e in evks], dct, level, rs)
+    oo = o.hrot_hoisted(oct_, evks, rs)
+    for a, b in zip(outs, oo):
+        assert np.array_equal(to_np(a), b.data)
