@@ -4,8 +4,9 @@
 Workload (BASELINE.json configs[1]): HRot / key-switch microbenchmark at
 N = 2^16 over the full limb chain of Set_hyp (L+1 = 24, dnum = 6, K = 4;
 P:1207-1208): one step = a batch of 64 non-hoisted rotations, ct_i rotated by
-r_i = i + 1 with its own evaluation key (64 x 168 MiB of keys resident in HBM,
-larger than L2, so no flush is needed).  The hoisted batch (ct_0 rotated by
+r_i = i + 1 with its own evaluation key (64 x 126 MiB of 6-byte-packed keys,
+168 MB each unpacked as in P:1208, resident in HBM and larger than L2, so no
+flush is needed).  The hoisted batch (ct_0 rotated by
 1..64 with one shared ModUp) is reported alongside.
 
 Metric: key switches per second (whole job, all ranks).  Multi-GPU: every rank
@@ -172,6 +173,47 @@ def oracle_keyswitch_rate(n_rot: int, level: int = LEVEL, seed: int = 0):
         o.hrot(c, evk, i + 1)
     dt = time.perf_counter() - t0
     return n_rot / dt, dt
+
+
+def oracle_conv_layers(names=("L1_ca", "L1_ra")):
+    """Time the CPU oracle's encrypted execution (oracle/hyphen.py EncConv, the plain C RNS-CKKS underneath) of
+    whole ResNet-20 layers at the bench's levels, all outputs, on the host cores.  The oracle's work is
+    data-independent, so keys, input ciphertexts and weight plaintexts are seeded uniform residues (one key
+    serves every rotation amount; encoding is untimed in the paper, and is skipped)."""
+    import oracle
+    from oracle import hyphen as H
+    o = oracle.Oracle(**synth.PARAMS["hyp"])
+    chain_all = list(range(o.nq + o.np_))
+    evk = synth.residues(7, (o.dnum * 2, len(chain_all), o.N), [int(o.moduli[t]) for t in chain_all]) \
+        .reshape(o.dnum, 2, len(chain_all), o.N)
+
+    class AnyKey(dict):
+        def __missing__(self, r):
+            return evk
+
+    spec_of = {nm: sp for nm, sp, _ in R20_LAYERS}
+    out = {}
+    for li, nm in enumerate(names):
+        sp = H.ConvSpec(*spec_of[nm][:10])
+        K = synth.conv_weight(2000 + li, sp.co, sp.ci, sp.f)
+        plan = H.plan_caconv(sp, K) if sp.algo == "CA" else H.plan_raconv(sp, K)
+        level = CA_LEVEL if sp.algo == "CA" else RA_LEVEL
+        enc = H.EncConv(o, plan, AnyKey())
+        pts = {}
+
+        def encode(v, lv, pts=pts):
+            if lv not in pts:
+                pts[lv] = oracle.Pt(synth.residues(8 + lv, (lv + 1, o.N), o.q[: lv + 1]), lv, float(o.q[lv]))
+            return pts[lv]
+
+        enc.encode = encode
+        cts = [oracle.Ct(synth.residues(100 + i, (2, level + 1, o.N), o.q[: level + 1]), level, 2.0**42)
+               for i in range(plan.n_in)]
+        t0 = time.perf_counter()
+        enc.run(cts)
+        out[nm] = {"oracle_ms": 1000.0 * (time.perf_counter() - t0), "level_in": level, "n_out": plan.n_out,
+                   "rotations": dict(plan.counts)}
+    return out
 
 
 def run_reference(args, ws, rank):
@@ -507,13 +549,13 @@ def run_ours(args, ws, rank, local):
     # whole-HRot HBM fraction (the metric's "HBM GB/s vs peak"): the bytes a rotation must move -- input ct,
     # its evaluation key, output ct -- over the measured time per rotation (north_star target >= 60 %)
     ct_bytes = 2 * n_l * N * 8
-    evk_bytes = 2 * len(digits) * E * N * 8
+    evk_bytes = 2 * len(digits) * E * N * 6  # the key slice a rotation reads, 6-byte packed words
     hrot_hbm = {}
     for name_, t_ms, moved in (("plain", ms, 2 * ct_bytes + evk_bytes), ("hoisted", ms_h, ct_bytes + evk_bytes)):
         gbs = moved * BATCH / (t_ms * 1e-3) / 1e9
         hrot_hbm[name_] = {"alg_bytes_per_rotation": moved, "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                            "frac": gbs / pk["hbm_gbs"]}
-    hrot_hbm["note"] = ("plain: ct in + evk + ct out per rotation; hoisted: the shared input is read once per batch, "
+    hrot_hbm["note"] = ("plain: ct in + evk (6-byte packed words) + ct out per rotation; hoisted: the shared input is read once per batch, "
                         "so evk + ct out; the FP64-pipe NTT/BConv work bounds plain HRot below the HBM roofline "
                         "(DESIGN.md section 5)")
     ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
@@ -575,6 +617,13 @@ def run_ours(args, ws, rank, local):
         rate, dt = oracle_keyswitch_rate(args.cpu_rotations)
         cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                "sample": f"{args.cpu_rotations} plain HRot(s) at full level (Set_hyp, N=2^16), {dt:.1f} s"}
+        if conv is not None:  # the same ResNet-20 layers, whole, through the oracle beside the GPU times
+            lay = oracle_conv_layers()
+            for nm, x in lay.items():
+                x["gpu_ms"] = conv["layers"][nm]["ms"]
+                x["oracle_over_gpu"] = x["oracle_ms"] / x["gpu_ms"]
+            cpu["resnet20_layers"] = {"layers": lay, "cores": os.cpu_count(),
+                                      "sample": "whole layers (every output ct), oracle EncConv on the host cores"}
 
     if rank == 0:
         line = {
@@ -584,7 +633,7 @@ def run_ours(args, ws, rank, local):
             "config": {"workload": "C2 HRot keyswitch microbenchmark, N=2^16, Set_hyp L+1=24 dnum=6 K=4, "
                                    "batch of 64 plain (non-hoisted) rotations per step per GPU",
                        "global_batch": BATCH * ws, "level": LEVEL, "parallelism": f"independent batches x{ws}",
-                       "l2": "inputs larger than L2 (64 x 168 MiB evaluation keys streamed per step)"},
+                       "l2": "inputs larger than L2 (64 x 126 MiB packed evaluation keys streamed per step)"},
             "roofline": roof,
             "roofline_families": roofs,
             "hrot_hbm": hrot_hbm,

@@ -22,9 +22,14 @@
  *    a(psi^(2*br(k)+1)) (DESIGN R-NTT), unless a function says otherwise.
  *  - Ciphertext at level l: device array [2][l+1][N] (c0 then c1), limb i on q_i.
  *    Plaintext at level l: device array [l+1][N].
- *    Evaluation (rotation) key: device array [dnum][2][n_q+n_p][N]
+ *    Evaluation (rotation / relinearization) key: [dnum][2][n_q+n_p] limbs
  *    ([.][0] = b, [.][1] = a), generated at the full level and used at any
  *    level l by reading q-limbs 0..l and the n_p p-limbs (DESIGN R-EVK).
+ *    PACKED: every residue is < 2^48 (R-PRIMES), so key words take 6 bytes:
+ *    word x of a limb at bytes [6x, 6x+6) little-endian, a limb = 6N bytes,
+ *    the key = hy_evk_words() uint64 (3/4 of the unpacked size; 126 MiB at
+ *    Set_hyp instead of the paper's 168 MB).  hy_evk_pack/unpack
+ *    convert from/to one uint64 per word.
  *  - Ownership: every ciphertext/plaintext/key/workspace buffer is caller-
  *    allocated device memory (in practice torch uint64/int64 tensors).  The
  *    library never frees caller memory.  The context owns its read-only
@@ -265,6 +270,12 @@ hy_status hy_raconv_finish(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t
 /* Rotation key for Galois element of a left rotation by r (DESIGN R-EVK, R-PRNG):
  * secret from sk_seed, randomness from ek_seed.  d_evk: [dnum][2][n_q+n_p][N]. */
 hy_status hy_keygen_rot(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, int32_t r, uint64_t* d_evk, void* stream);
+/* uint64 words of one packed key (see Conventions): dnum * 2 * (n_q+n_p) * 3N/4. */
+size_t hy_evk_words(const hy_ctx* ctx);
+/* d_in [dnum][2][n_q+n_p][N] (one uint64 per word, each < 2^48) -> packed d_out (hy_evk_words), and back.
+ * Device buffers, must not alias; stream-ordered. */
+hy_status hy_evk_pack(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, void* stream);
+hy_status hy_evk_unpack(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, void* stream);
 hy_status hy_keygen_galois(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* d_evk, void* stream);
 /* Relinearization key s^2 -> s (DESIGN R-RELIN): b_j = -a_j s + e_j + g_j s^2, object ids j (Galois
  * element 0, used by no rotation); layout as a rotation key. */

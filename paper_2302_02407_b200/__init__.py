@@ -76,6 +76,9 @@ SIGNATURES = {
     "hy_keygen_rot": (C.c_int, [_P, _U64, _U64, C.c_int32, _P, _P]),
     "hy_keygen_galois": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "hy_keygen_relin": (C.c_int, [_P, _U64, _U64, _P, _P]),
+    "hy_evk_words": (C.c_size_t, [_P]),
+    "hy_evk_pack": (C.c_int, [_P, _P, _P, _P]),
+    "hy_evk_unpack": (C.c_int, [_P, _P, _P, _P]),
     "hy_mulct": (C.c_int, [_P, _P, _P, _P, _U32, _P, _P]),
     "hy_mulct_batch": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _PP, _P]),
     "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
@@ -203,11 +206,23 @@ class Context:
         return (2, level + 1, self.N)
 
     def evk_shape(self):
-        return (self.dnum, 2, self.n_q + self.n_p, self.N)
+        """packed key (include/hyphen.h Conventions): 6 bytes per word, 3N/4 uint64 per limb"""
+        return (self.dnum, 2, self.n_q + self.n_p, self.N // 4 * 3)
 
     def evk_bytes(self):
-        """bytes of one evaluation key at full level (168 MiB at Set_hyp)"""
-        return int(np.prod(self.evk_shape())) * 8
+        """bytes of one packed evaluation key at full level (126 MiB at Set_hyp; 168 MB unpacked)"""
+        return int(lib().hy_evk_words(self._c)) * 8
+
+    def evk_pack(self, evk_u64, out=None):
+        """[dnum][2][n_q+n_p][N] one word per uint64 (e.g. the oracle's key) -> packed device key"""
+        out = self.empty(*self.evk_shape()) if out is None else out
+        _check(lib().hy_evk_pack(self._c, _ptr(evk_u64), _ptr(out), self._stream()))
+        return out
+
+    def evk_unpack(self, evk, out=None):
+        out = self.empty(self.dnum, 2, self.n_q + self.n_p, self.N) if out is None else out
+        _check(lib().hy_evk_unpack(self._c, _ptr(evk), _ptr(out), self._stream()))
+        return out
 
     def n_digits(self, level):
         return int(lib().hy_ctx_n_digits(self._c, level))

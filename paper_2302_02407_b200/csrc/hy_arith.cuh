@@ -100,4 +100,35 @@ __device__ __forceinline__ double fcanon(double v, double q, double qinv) {
   return r >= q ? r - q : r;
 }
 
+// ---- packed evaluation keys (DESIGN "Evk layout"): every residue is < 2^48 (R-PRIMES), so a key word takes
+// 6 bytes: word x of a limb at bytes [6x, 6x+6) little-endian, a limb is 6N bytes = 3N/4 uint64 (N >= 4),
+// a 256-word row 1536 bytes.  Limb li of a key [dnum][2][n_q+n_p] starts at evk + li * 3N/4.
+constexpr uint64_t kM48 = (1ull << 48) - 1;
+__host__ __device__ __forceinline__ size_t evk_limb_words(size_t N) { return N / 4 * 3; }
+__device__ __forceinline__ const uint64_t* evk_limb(const uint64_t* evk, size_t li, size_t N) {
+  return evk + li * evk_limb_words(N);
+}
+// word x of a packed limb (streaming loads; the second only when the word straddles two uint64)
+__device__ __forceinline__ uint64_t evk_word(const uint64_t* limb, uint32_t x) {
+  const uint32_t o = 6 * x, a = o >> 3, sh = (o & 7) * 8;
+  uint64_t w = __ldcs(limb + a) >> sh;
+  if (sh > 16) w |= __ldcs(limb + a + 1) << (64 - sh);
+  return w & kM48;
+}
+// words 4m..4m+3 from the three uint64 (24 bytes) that hold them
+__device__ __forceinline__ void evk_unpack4(uint64_t p0, uint64_t p1, uint64_t p2, uint64_t& w0, uint64_t& w1,
+                                            uint64_t& w2, uint64_t& w3) {
+  w0 = p0 & kM48;
+  w1 = (p0 >> 48) | ((p1 & 0xFFFFFFFFull) << 16);
+  w2 = (p1 >> 32) | ((p2 & 0xFFFFull) << 32);
+  w3 = p2 >> 16;
+}
+// store word x (three 2-byte stores: threads of neighbouring words never share a store address)
+__device__ __forceinline__ void evk_store(uint64_t* limb, uint32_t x, uint64_t w) {
+  uint16_t* p = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(limb) + 6ull * x);
+  p[0] = (uint16_t)w;
+  p[1] = (uint16_t)(w >> 16);
+  p[2] = (uint16_t)(w >> 32);
+}
+
 }  // namespace hy

@@ -12,7 +12,7 @@
 // and items that share an evaluation key (RaS of all output groups of a conv
 // layer) stream that key from HBM once for the whole batch.
 //
-// Data layout (HBM): ct [2][l+1][N], ext [beta][l+1+K][N], u [2][l+1+K][N], evk
+// Data layout (HBM): ct [2][l+1][N], ext [beta][l+1+K][N], u [2][l+1+K][N], evk (6-byte packed words)
 // [dnum][2][n_q+n_p][N]; every limb is N contiguous uint64 (coalesced rows).
 #include <algorithm>
 #include <vector>
@@ -169,9 +169,8 @@ __global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const
   if (SHARED) {
 #pragma unroll
     for (int j = 0; j < B; ++j) {
-      const uint64_t* e = evk.p[0] + ((size_t)(j * 2) * L1 + t) * N + x;
-      e0[j] = u2d(__ldcs(e));
-      e1[j] = u2d(__ldcs(e + (size_t)L1 * N));
+      e0[j] = u2d(evk_word(evk_limb(evk.p[0], (size_t)(j * 2) * L1 + t, N), x));
+      e1[j] = u2d(evk_word(evk_limb(evk.p[0], (size_t)(j * 2 + 1) * L1 + t, N), x));
     }
   }
   double s0 = 0.0, s1 = 0.0;
@@ -189,9 +188,8 @@ __global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const
     if (!SHARED) {
 #pragma unroll
       for (int j = 0; j < B; ++j) {
-        const uint64_t* e = evk.p[g] + ((size_t)(j * 2) * L1 + t) * N + x;
-        e0[j] = u2d(__ldcs(e));
-        e1[j] = u2d(__ldcs(e + (size_t)L1 * N));
+        e0[j] = u2d(evk_word(evk_limb(evk.p[g], (size_t)(j * 2) * L1 + t, N), x));
+        e1[j] = u2d(evk_word(evk_limb(evk.p[g], (size_t)(j * 2 + 1) * L1 + t, N), x));
       }
     }
     double a0 = 0.0, a1 = 0.0;
@@ -485,7 +483,7 @@ void ip_batch(hy_ctx* c, uint32_t level, int G, const uint64_t* const* ext, cons
   dim3 g((shared || sum) ? 1 : G, c->N / kT, nu);
   KTimer kt(c, FAM_IP, s);
   const uint64_t keys = shared ? 1 : G, outs = sum ? 1 : G;
-  kt.bytes = ((uint64_t)G * beta * nu + keys * 2ull * beta * nu + outs * 2ull * nu * (acc ? 2 : 1)) * c->N * 8;
+  kt.bytes = ((uint64_t)G * beta * nu * 8 + keys * 2ull * beta * nu * 6 + outs * 2ull * nu * (acc ? 2 : 1) * 8) * c->N;
 #define ARGS ae, ao, ak, au, ap, G, c->dt, (int)level, (int)c->n_q, (int)(c->n_q + c->n_p), E, (int)c->alpha, \
              (int)c->log_n, acc ? 1 : 0, u0
   if (shared && !sum) {

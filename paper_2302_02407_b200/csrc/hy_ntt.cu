@@ -396,6 +396,20 @@ __device__ __forceinline__ void load_l3(const uint64_t* __restrict__ p, int l, u
       v[2 * h + i] = stream ? __ldcs(a) : *a;
     }
 }
+// The same layout from a packed key limb (hy_arith.cuh): the 4 words 4(l + 32h)..+3 of row `roff` are the
+// 24 bytes at uint64 3(l + 32h) of the 192-uint64 packed row (streaming loads).
+__device__ __forceinline__ void load_l3_evk(const uint64_t* __restrict__ limb, size_t roff, int l,
+                                            ulonglong2 (&v)[4]) {
+  const uint64_t* r = limb + roff / 4 * 3;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint64_t* p = r + 3 * (l + 32 * h);
+    uint64_t w0, w1, w2, w3;
+    evk_unpack4(__ldcs(p), __ldcs(p + 1), __ldcs(p + 2), w0, w1, w2, w3);
+    v[2 * h] = make_ulonglong2(w0, w1);
+    v[2 * h + 1] = make_ulonglong2(w2, w3);
+  }
+}
 __device__ __forceinline__ double l3_word(const ulonglong2 (&v)[4], int k) {
   const ulonglong2 w = v[k >> 1];
   return u2d((k & 1) ? w.y : w.x);
@@ -458,10 +472,9 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
     for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
 #pragma unroll 1
     for (int j = 0; j < B; ++j) {
-      const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + t) * N + roff;
       ulonglong2 k0[4], k1[4];
-      load_l3(e0, l, k0, true);
-      load_l3(e0 + (size_t)L1 * N, l, k1, true);
+      load_l3_evk(evk_limb(a.evk[g], (size_t)(j * 2) * L1 + t, N), roff, l, k0);
+      load_l3_evk(evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + t, N), roff, l, k1);
       double x[8];
       if (HOIST) {
         const uint64_t kx = a.kx[g];
@@ -615,10 +628,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
   for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
 #pragma unroll 1
   for (int j = 0; j < B; ++j) {
-    const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
     ulonglong2 k0[4], k1[4];
-    load_l3(e0, l, k0, true);
-    load_l3(e0 + (size_t)L1 * N, l, k1, true);
+    load_l3_evk(evk_limb(a.evk[g], (size_t)(j * 2) * L1 + i, N), roff, l, k0);
+    load_l3_evk(evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + i, N), roff, l, k1);
     double x[8];
     if (HOIST) {
       const uint64_t* src = j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N;
@@ -703,10 +715,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint64_t* b) {  // 2048 bytes
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 2048, [%2];" ::"r"(
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint64_t* b, uint32_t bytes = 2048) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    saddr(dst)),
-               "l"(src), "r"(saddr(b))
+               "l"(src), "r"(bytes), "r"(saddr(b))
                : "memory");
 }
 __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -742,12 +754,14 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
     double* b = T + 256 + 768 * (j % NST);
     uint64_t* mb = mbar + j % NST;
     if (j < B) {
-      const uint64_t* e0 = a.evk[g] + ((size_t)(j * 2) * L1 + i) * N + roff;
+      // packed key rows: 1536 bytes each (hy_arith.cuh), at the start of their 2048-byte stage slots
+      const uint64_t* e0 = evk_limb(a.evk[g], (size_t)(j * 2) * L1 + i, N) + roff / 4 * 3;
+      const uint64_t* e1 = evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + i, N) + roff / 4 * 3;
       const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N) +
                            ((HOIST || j == own_digit) ? (size_t)rowx * 256 : roff);
-      tma::mbar_expect(mb, 3 * 2048);
-      tma::bulk_row(b, e0, mb);
-      tma::bulk_row(b + 256, e0 + (size_t)L1 * N, mb);
+      tma::mbar_expect(mb, 2 * 1536 + 2048);
+      tma::bulk_row(b, e0, mb, 1536);
+      tma::bulk_row(b + 256, e1, mb, 1536);
       tma::bulk_row(b + 512, xs, mb);
     } else {
       const bool c0 = a.add0[g] != nullptr;
@@ -794,17 +808,21 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
         __syncwarp();
         rows_forward_l3(x, l, b + 512, T, q, qinv);  // the row buffer is now the transpose buffer
       }
-      // the evk rows in layout L3 as 16-byte words (x[2h], x[2h+1] are adjacent): 2-way instead of the
-      // 4-way bank conflicts of 8-byte reads at a 32-byte lane stride
-      const ulonglong2* e0 = reinterpret_cast<const ulonglong2*>(b);
+      // the packed evk rows in layout L3: elements 4h..4h+3 = words 4(l + 32h)..+3 = the 24 bytes at
+      // uint64 3(l + 32h) (8-byte reads at a 24-byte lane stride: conflict-free per half-warp)
+      const uint64_t* e0 = reinterpret_cast<const uint64_t*>(b);
+      const uint64_t* e1 = reinterpret_cast<const uint64_t*>(b + 256);
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int w2 = (elem<3>(l, 2 * h)) >> 1;  // 16-byte word of elements 2h, 2h + 1
-        const ulonglong2 v0 = e0[w2], v1 = e0[128 + w2];
-        a0[2 * h] += fmulmod(x[2 * h], u2d(v0.x), q, qinv);
-        a0[2 * h + 1] += fmulmod(x[2 * h + 1], u2d(v0.y), q, qinv);
-        a1[2 * h] += fmulmod(x[2 * h], u2d(v1.x), q, qinv);
-        a1[2 * h + 1] += fmulmod(x[2 * h + 1], u2d(v1.y), q, qinv);
+      for (int h = 0; h < 2; ++h) {
+        const int o = 3 * (l + 32 * h);
+        uint64_t v0[4], v1[4];
+        evk_unpack4(e0[o], e0[o + 1], e0[o + 2], v0[0], v0[1], v0[2], v0[3]);
+        evk_unpack4(e1[o], e1[o + 1], e1[o + 2], v1[0], v1[1], v1[2], v1[3]);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          a0[4 * h + m] += fmulmod(x[4 * h + m], u2d(v0[m]), q, qinv);
+          a1[4 * h + m] += fmulmod(x[4 * h + m], u2d(v1[m]), q, qinv);
+        }
       }
     } else {
       const double pinv = (double)md->p_inv[i];
@@ -1095,7 +1113,8 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
   // algorithmic bytes: every digit limb in once, each distinct key once, the outputs (read back too
   // when accumulating)
   const uint64_t outs = sum ? 1 : G;
-  kt.bytes = ((uint64_t)G * beta * nu + (uint64_t)keys * 2 * beta * nu + outs * 2 * nu * (accumulate ? 2 : 1)) * c->N * 8;
+  kt.bytes = ((uint64_t)G * beta * nu * 8 + (uint64_t)keys * 2 * beta * nu * 6 + outs * 2 * nu * (accumulate ? 2 : 1) * 8) *
+             c->N;  // key words packed in 6 bytes
   const int L1 = (int)(c->n_q + c->n_p);
 #define HY_RIP(BB)                                                                                             \
   case BB:                                                                                                     \
@@ -1142,7 +1161,7 @@ void launch_rows_ip_final(hy_ctx* c, const IpFinalArgs& a, int G, uint32_t level
   // algorithmic bytes: the digits' Q limbs in (hoisted: shared, once), each distinct key's Q rows once,
   // the conversion w in, the output written, the addends
   const uint64_t digits = (hoisted ? 1 : (uint64_t)G) * beta * n;
-  kt.bytes = (digits + (uint64_t)keys * 2 * beta * n + (uint64_t)G * 4 * n + extra) * c->N * 8;
+  kt.bytes = ((digits + (uint64_t)G * 4 * n + extra) * 8 + (uint64_t)keys * 2 * beta * n * 6) * c->N;  // packed key
   const int L1 = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
   const ModDownConst* md = c->d_moddown[level];
   // HY_TMA=0: register loads instead of the bulk-copy staged rows (A/B; staged: +0.2 % plain, +3 % hoisted)

@@ -187,8 +187,20 @@ __global__ void k_evk_digit(uint64_t* __restrict__ evk, const uint64_t* __restri
   const uint64_t a = uniform_mod(draw(seed, kDomEvkA, obj, (uint32_t)t, x), pc.q);
   uint64_t b = sub_mod(e_ntt[o], mul_mod(a, s_ntt[o], pc), pc.q);
   if (gmod[t]) b = add_mod(b, mul_mod(gmod[t], sk_ntt[o], pc), pc.q);
-  evk[((size_t)(j * 2 + 1) * L1 + t) * N + x] = a;
-  evk[((size_t)(j * 2 + 0) * L1 + t) * N + x] = b;
+  evk_store(evk + ((size_t)(j * 2 + 1) * L1 + t) * evk_limb_words(N), x, a);  // packed (hy_arith.cuh)
+  evk_store(evk + ((size_t)(j * 2 + 0) * L1 + t) * evk_limb_words(N), x, b);
+}
+
+// Packed key <-> one uint64 per word (hy_evk_pack / hy_evk_unpack).  grid (N/256, n_limbs)
+__global__ void k_evk_pack(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int logN) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  evk_store(out + blockIdx.y * evk_limb_words(N), x, in[blockIdx.y * N + x]);
+}
+__global__ void k_evk_unpack(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int logN) {
+  const size_t N = (size_t)1 << logN;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  out[blockIdx.y * N + x] = evk_word(in + blockIdx.y * evk_limb_words(N), x);
 }
 
 // Encryption: c1 = a (uniform, NTT domain), c0 = -a*s + e + m.  grid (N/256, l+1)
@@ -617,4 +629,24 @@ extern "C" hy_status hy_decode(hy_ctx* c, const uint64_t* pt, uint32_t level, do
   crt_centered_to_double(h.data(), n, c->N, c->mod.data(), m.data());
   e = hy_decode_coeffs(c->log_n, m.data(), scale, n_slots, h_re, h_im);
   return e == HY_OK ? HY_OK : fail(e, "hy_decode_coeffs");
+}
+
+extern "C" size_t hy_evk_words(const hy_ctx* c) {
+  return c ? (size_t)c->dnum * 2 * (c->n_q + c->n_p) * evk_limb_words(c->N) : 0;
+}
+
+extern "C" hy_status hy_evk_pack(hy_ctx* c, const uint64_t* d_in, uint64_t* d_out, void* stream) {
+  if (!c || !d_in || !d_out) return fail(HY_E_ARG, "null");
+  const uint32_t L = c->dnum * 2 * (c->n_q + c->n_p);
+  KTimer kt(c, FAM_CLIENT, st(stream));
+  k_evk_pack<<<dim3(c->N / kT, L), kT, 0, st(stream)>>>(d_in, d_out, (int)c->log_n);
+  return cuda_check("hy_evk_pack");
+}
+
+extern "C" hy_status hy_evk_unpack(hy_ctx* c, const uint64_t* d_in, uint64_t* d_out, void* stream) {
+  if (!c || !d_in || !d_out) return fail(HY_E_ARG, "null");
+  const uint32_t L = c->dnum * 2 * (c->n_q + c->n_p);
+  KTimer kt(c, FAM_CLIENT, st(stream));
+  k_evk_unpack<<<dim3(c->N / kT, L), kT, 0, st(stream)>>>(d_in, d_out, (int)c->log_n);
+  return cuda_check("hy_evk_unpack");
 }

@@ -21,6 +21,11 @@ def to_dev(a, ctx):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(ctx.device)
 
 
+def evk_dev(e, ctx):
+    """an oracle key (one uint64 per word) -> the library's packed device key"""
+    return ctx.evk_pack(to_dev(e, ctx))
+
+
 @pytest.fixture(scope="module", params=["toy", "mini", "hyp"])
 def pair(request):
     import paper_2302_02407_b200 as hy
@@ -70,7 +75,12 @@ def test_automorph(pair):
 def test_keygen(pair):
     name, ctx, o = pair
     for r in ([1, -7] if name != "hyp" else [3]):
-        assert np.array_equal(to_np(ctx.keygen_rot(SK, EK, r)), o.keygen_rot(SK, EK, r))
+        k = ctx.keygen_rot(SK, EK, r)
+        want = o.keygen_rot(SK, EK, r)
+        assert np.array_equal(to_np(ctx.evk_unpack(k)), want)
+        # packed layout: 6 bytes per word, 3/4 of the unpacked size, equal to packing the oracle's key
+        assert k.numel() * 8 == want.nbytes // 4 * 3 == ctx.evk_bytes()
+        assert np.array_equal(to_np(k), to_np(evk_dev(want, ctx)))
 
 
 def test_encode_encrypt_decrypt(pair):
@@ -113,7 +123,7 @@ def test_modup_ip_moddown(pair):
         assert np.array_equal(to_np(ext), oext)
         evk = o.keygen_rot(SK, EK, 1) if name != "hyp" else None
         if evk is not None:
-            u = ctx.ks_inner_product(level, ext, to_dev(evk, ctx))
+            u = ctx.ks_inner_product(level, ext, evk_dev(evk, ctx))
             ou = o.ks_inner_product(level, oext, evk)
             assert np.array_equal(to_np(u), ou)
         chain = o.ext_chain(level)
@@ -134,7 +144,7 @@ def test_hrot_plain_and_batch(pair):
     level = o.nq - 1
     rs = [1, -1, 9] if name != "hyp" else [5]
     evks = [o.keygen_rot(SK, EK, r) for r in rs]
-    d_evks = [to_dev(e, ctx) for e in evks]
+    d_evks = [evk_dev(e, ctx) for e in evks]
     cts = [_fresh_ct(ctx, o, name, level, 60 + i) for i in range(len(rs))]
     for (dct, oct_), r, e, de in zip(cts, rs, evks, d_evks):
         got = to_np(ctx.hrot(de, dct, level, r))
@@ -153,7 +163,7 @@ def test_hrot_hoisted(pair):
     rs = [1, 0, -1, 8] if name != "hyp" else [1, 32, -64]
     evks = [o.keygen_rot(SK, EK, r) if o.galois_elt(r) != 1 else None for r in rs]
     dct, oct_ = _fresh_ct(ctx, o, name, level, 70)
-    d_evks = [to_dev(e, ctx) if e is not None else None for e in evks]
+    d_evks = [evk_dev(e, ctx) if e is not None else None for e in evks]
     outs = ctx.hrot_hoisted(d_evks, dct, level, rs)
     oo = o.hrot_hoisted(oct_, [e if e is not None else np.zeros(1, np.uint64) for e in evks], rs)
     for a, b in zip(outs, oo):
@@ -166,7 +176,7 @@ def test_hrot_sum(pair):
     rs = [1, 0, -1, 7] if name != "hyp" else [1, 0, -9]
     evks = [o.keygen_rot(SK, EK, r) if o.galois_elt(r) != 1 else None for r in rs]
     cts = [_fresh_ct(ctx, o, name, level, 80 + i) for i in range(len(rs))]
-    got = ctx.hrot_sum([to_dev(e, ctx) if e is not None else None for e in evks], [c[0] for c in cts], level, rs)
+    got = ctx.hrot_sum([evk_dev(e, ctx) if e is not None else None for e in evks], [c[0] for c in cts], level, rs)
     want = o.hrot_sum([c[1] for c in cts], evks, rs)
     assert np.array_equal(to_np(got), want.data)
 
@@ -196,7 +206,7 @@ def test_relin_key_and_mulct(pair):
     level = o.nq - 1 if name != "hyp" else 9
     rlk = ctx.keygen_relin(SK, EK)
     orlk = o.keygen_relin(SK, EK)
-    assert np.array_equal(to_np(rlk), orlk)
+    assert np.array_equal(to_np(ctx.evk_unpack(rlk)), orlk)
     scale = 2 ** synth.PARAMS[name]["log_scale"]
     za, zb = synth.slots_uniform(60, o.n), synth.slots_uniform(61, o.n)
     pa, pb = o.encode(za, scale, level), o.encode(zb, scale, level)
@@ -229,7 +239,7 @@ def test_hrot_hoisted_chunked(level):
     rs = [1, 2, -3, 7, 100]
     evks = [o.keygen_rot(SK, EK, r) for r in rs]
     dct, oct_ = _fresh_ct(ctx, o, "hyp", level, 71)
-    outs = ctx.hrot_hoisted([to_dev(e, ctx) for e in evks], dct, level, rs)
+    outs = ctx.hrot_hoisted([evk_dev(e, ctx) for e in evks], dct, level, rs)
     oo = o.hrot_hoisted(oct_, evks, rs)
     for a, b in zip(outs, oo):
         assert np.array_equal(to_np(a), b.data)
