@@ -35,6 +35,13 @@ KEYS = ["Grid Size", "Block Size", "gpu__time_duration.sum", "dram__bytes_read.s
 
 def family(name):
     short = name.split("(")[0].split("::")[-1]
+    if short.startswith("k_ntt_rows_ip") and short.endswith(", 1>"):  # <B, SUM, HOIST=1>: hoisted P-limb IP
+        return "ntt_ip_hoisted", short
+    # the hoisted step's one shared ModUp (separate NTT passes + BConv): not part of the plain step's families
+    for pre, fam in (("k_modup_bconv", "modup_hoisted"), ("k_ntt_rows<", "ntt_b_hoisted"),
+                     ("k_ntt_cols256", "ntt_a_hoisted")):
+        if short.startswith(pre):
+            return fam, short
     for pre, fam in FAMILY:
         if short.startswith(pre):
             return fam, short
