@@ -291,6 +291,12 @@ hy_status hy_decrypt(hy_ctx* ctx, uint64_t sk_seed, const uint64_t* d_ct, uint32
  * then reduced mod q_0..q_l and NTT'd into d_pt [l+1][N].  Synchronous w.r.t. the host buffer. */
 hy_status hy_encode(hy_ctx* ctx, const double* h_slots, uint32_t n_slots, uint64_t scale, uint32_t level,
                     uint64_t* d_pt, void* stream);
+/* Batched device CKKS encoding (same rounding as hy_encode, DESIGN R-ENCODE; the bulk weight path of
+ * hy_conv_encode_weights): P real slot vectors h_slots [P][N/2] (host) at integer scale -> NTT-domain
+ * plaintexts d_pts [P][l+1][N].  Double-double special FFT on the device; synchronous w.r.t. the host buffer.
+ * Errors: HY_E_ARG, HY_E_WORKSPACE, HY_E_CAPACITY (a coefficient >= 2^62). */
+hy_status hy_encode_batch(hy_ctx* ctx, const double* h_slots, uint32_t P, uint64_t scale, uint32_t level,
+                          uint64_t* d_pts, void* stream);
 /* Host-only part of hy_encode: the N integer coefficients (no device needed). */
 hy_status hy_encode_coeffs(uint32_t log_n, const double* h_slots, uint32_t n_slots, uint64_t scale,
                            int64_t* h_coeffs);

@@ -86,6 +86,7 @@ SIGNATURES = {
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
     "hy_encode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), _U32, _U64, C.POINTER(C.c_int64)]),
     "hy_pt_from_coeffs": (C.c_int, [_P, C.POINTER(C.c_int64), _U32, _P, _P]),
+    "hy_encode_batch": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
     "hy_decode": (C.c_int, [_P, _P, _U32, C.c_double, _U32, C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
     "hy_decode_coeffs": (C.c_int, [_U32, C.POINTER(C.c_double), C.c_double, _U32, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
@@ -366,6 +367,14 @@ class Context:
         z = np.ascontiguousarray(slots, np.float64)
         _check(lib().hy_encode(self._c, z.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale), level,
                                _ptr(out), self._stream()))
+        return out
+
+    def encode_batch(self, slots, scale, level, out=None):
+        """P real slot vectors [P][N/2] -> [P][level+1][N] plaintexts, encoded on the device (hy_encode_batch)"""
+        z = np.ascontiguousarray(slots, np.float64).reshape(-1, self.n)
+        out = self.empty(z.shape[0], level + 1, self.N) if out is None else out
+        _check(lib().hy_encode_batch(self._c, z.ctypes.data_as(C.POINTER(C.c_double)), z.shape[0], int(scale),
+                                     level, _ptr(out), self._stream()))
         return out
 
     def decode(self, pt, level, scale, n_slots=None):

@@ -383,29 +383,37 @@ extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, co
                                             uint64_t* d_pts, void* stream) {
   if (!c || !p || !K || !d_pts) return fail(HY_E_ARG, "null");
   if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
+  if (p->n != (int64_t)c->N / 2) return fail(HY_E_PLAN, "plan ring size differs from the context's");
+  if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
+  // Slot vectors are built on the host (the plan's weight placement, OpenMP), uploaded in batches and
+  // encoded on the device (hy_encode_dev.cu; the same rounding as hy_encode_coeffs, DESIGN R-ENCODE).
+  // Weights at scale q_level, the mask at q_{level-1}: each rescale restores the ciphertext scale.
+  cudaStream_t s = st(stream);
   const int64_t npt = p->n_pt() + (p->has_mask ? 1 : 0);
-  std::vector<std::vector<int64_t>> coeffs(npt, std::vector<int64_t>(c->N));
+  const size_t n = (size_t)p->n, per = n * 8 + n * 32 + (size_t)c->N * 8 + 64;
+  const int64_t B = std::min<int64_t>({64, npt, (int64_t)((c->ws_bytes - 4096) / per)});
+  if (B < 1) return fail(HY_E_WORKSPACE, "workspace too small for weight encoding");
+  double* h_slots = nullptr;
+  if (cudaMallocHost(&h_slots, (size_t)B * n * 8) != cudaSuccess) return fail(HY_E_CUDA, "pinned slot buffer");
+  double* d_slots = reinterpret_cast<double*>(c->ws);
+  uint8_t* ws_rest = c->ws + (((size_t)B * n * 8 + 255) & ~(size_t)255);
+  const size_t rest_bytes = c->ws_bytes - (size_t)(ws_rest - c->ws);
+  const size_t stride = (size_t)(level + 1) * c->N;
   hy_status err = HY_OK;
+  for (int64_t k0 = 0; k0 < npt && err == HY_OK;) {
+    // a batch never mixes the mask (level - 1 limbs, scale q_{level-1}) with the weights
+    const bool mask = p->has_mask && k0 == p->n_pt();
+    const int64_t cnt = mask ? 1 : std::min<int64_t>(B, p->n_pt() - k0);
 #pragma omp parallel for schedule(dynamic)
-  for (int64_t k = 0; k < npt; ++k) {
-    std::vector<double> v(p->n);
-    weight_slots(*p, K, k, v.data());
-    const bool mask = k == p->n_pt();
-    // weights at scale q_level, the mask at q_{level-1}: each rescale restores the ciphertext scale
-    const uint64_t scale = mask ? c->mod[level - 1] : c->mod[level];
-    hy_status st = hy_encode_coeffs(c->log_n, v.data(), (uint32_t)p->n, scale, coeffs[k].data());
-    if (st != HY_OK) {
-#pragma omp critical
-      err = st;
-    }
+    for (int64_t k = 0; k < cnt; ++k) weight_slots(*p, K, k0 + k, h_slots + (size_t)k * n);
+    cudaMemcpyAsync(d_slots, h_slots, (size_t)cnt * n * 8, cudaMemcpyHostToDevice, s);
+    std::vector<uint64_t> sc((size_t)cnt, mask ? c->mod[level - 1] : c->mod[level]);
+    err = encode_batch_device(c, d_slots, sc.data(), (uint32_t)cnt, mask ? level : level + 1,
+                              d_pts + (size_t)k0 * stride, stride, ws_rest, rest_bytes, s);
+    k0 += cnt;
   }
-  if (err != HY_OK) return fail(err, "weight encoding failed");
-  for (int64_t k = 0; k < npt; ++k) {
-    const bool mask = k == p->n_pt();
-    uint64_t* dst = d_pts + (size_t)k * (level + 1) * c->N;
-    hy_status st = hy_pt_from_coeffs(c, coeffs[k].data(), mask ? level - 1 : level, dst, stream);
-    if (st != HY_OK) return st;
-  }
+  cudaFreeHost(h_slots);
+  if (err != HY_OK) return err;
   return cuda_check("hy_conv_encode_weights");
 }
 

@@ -271,6 +271,7 @@ extern "C" void hy_ctx_destroy(hy_ctx* c) {
   cudaSetDevice(c->device);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   cudaFree(c->d_tables);
+  if (c->d_enc) cudaFree(c->d_enc);
   for (auto p : c->d_modup) cudaFree(p);
   for (auto p : c->d_moddown) cudaFree(p);
   for (auto p : c->d_rescale) cudaFree(p);

@@ -92,6 +92,26 @@ std::shared_ptr<Tables> tables(uint32_t log_n) {
   return t;
 }
 
+}  // namespace
+
+namespace hy {
+// the encoder's tables for the device path (hy_encode_dev.cu): ksi^k, k in [0, 2N], as (re.hi, re.lo, im.hi,
+// im.lo), and the rotation group 5^j mod 2N, j < N/2
+void encode_tables(uint32_t log_n, std::vector<double>& ksi4, std::vector<uint32_t>& rot) {
+  auto T = tables(log_n);
+  ksi4.resize(4 * T->ksi.size());
+  for (size_t k = 0; k < T->ksi.size(); ++k) {
+    ksi4[4 * k] = T->ksi[k].re.hi;
+    ksi4[4 * k + 1] = T->ksi[k].re.lo;
+    ksi4[4 * k + 2] = T->ksi[k].im.hi;
+    ksi4[4 * k + 3] = T->ksi[k].im.lo;
+  }
+  rot.assign(T->rot.begin(), T->rot.end());
+}
+}  // namespace hy
+
+namespace {
+
 int64_t round_dd(DD x) {
   double fl = std::floor(x.hi);
   DD r = dd_add({x.hi - fl, 0.0}, {x.lo, 0.0});

@@ -85,6 +85,9 @@ struct hy_ctx {
     uint64_t bytes;  // algorithmic bytes of the bracketed launch(es)
   };
   std::vector<TimedPair> timed;
+  // device CKKS-encoding tables (hy_encode_dev.cu): ksi^k as complex double-double, then 5^j mod 2N (uint32)
+  void* d_enc = nullptr;
+  size_t enc_rot_off = 0;
 };
 
 namespace hy {
@@ -197,6 +200,11 @@ struct ModUpColsArgs {
   uint64_t* ext[kG];
 };
 void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
+// Device CKKS encoding (DESIGN R-ENCODE, same rounding as hy_encode_coeffs) of P real slot vectors d_slots
+// [P][N/2] at integer scales h_scales[P] into NTT-domain plaintexts out + p*stride on q_0..q_{nl-1}.
+// Uses ws (P * 40 * N bytes + 256); synchronous.
+hy_status encode_batch_device(hy_ctx* c, const double* d_slots, const uint64_t* h_scales, uint32_t P, uint32_t nl,
+                              uint64_t* out, size_t stride, uint8_t* ws, size_t ws_bytes, cudaStream_t s);
 bool modup_cols_ok(const hy_ctx* c);  // N = 2^16 and alpha <= 4
 // The same fused column kernel for ModDown, per item g and poly c: inverse column pass of the K P limbs
 // src_g[c][k] (after their inverse row pass), z_k = [v_k (P/p_k)^{-1}]_{p_k}, and for every q_i <= level

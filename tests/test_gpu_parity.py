@@ -243,3 +243,21 @@ def test_hrot_hoisted_chunked(level):
     oo = o.hrot_hoisted(oct_, evks, rs)
     for a, b in zip(outs, oo):
         assert np.array_equal(to_np(a), b.data)
+
+
+def test_encode_batch_device(pair):
+    """Batched device encoding (hy_encode_batch: double-double special FFT on the GPU) = the oracle's encoder
+    (binary128 DFT), bit-exact, for random, sparse weight-like, 0/1-mask and zero slot vectors, at a power-of-two
+    and a prime scale."""
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    g = np.random.default_rng(77)
+    z = np.zeros((5, o.n))
+    z[0] = synth.slots_uniform(32, o.n)
+    z[1, g.choice(o.n, o.n // 16, replace=False)] = g.normal(0, 0.1, o.n // 16)  # sparse, weight-like
+    z[2, ::4] = 1.0                                                               # mask
+    z[3, : o.n // 3] = synth.slots_uniform(33, o.n // 3)
+    for scale in (2 ** synth.PARAMS[name]["log_scale"], o.q[level]):
+        got = to_np(ctx.encode_batch(z, scale, level))
+        for i in range(len(z)):
+            assert np.array_equal(got[i], o.encode(z[i], scale, level).data), (scale, i)
