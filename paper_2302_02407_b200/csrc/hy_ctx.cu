@@ -238,6 +238,8 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
       md.p_inv[i] = inv_h(P, qi);
       md.p_inv_sh[i] = shoup_pre(md.p_inv[i], qi);
     }
+    md.src0 = c->n_q;
+    md.center = 0;
     RescaleConst& rc = c->h_rescale[lvl];
     memset(&rc, 0, sizeof(rc));
     for (uint32_t i = 0; i < lvl; ++i) {
@@ -248,6 +250,21 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
   c->d_modup.resize(c->n_q);
   c->d_moddown.resize(c->n_q);
   c->d_rescale.resize(c->n_q);
+  c->d_rescale_md.assign(c->n_q, nullptr);
+  for (uint32_t lvl = 1; lvl < c->n_q; ++lvl) {  // rescale = ModDown by P = q_lvl (K = 1), centred
+    ModDownConst md;
+    memset(&md, 0, sizeof(md));
+    md.phat_inv[0] = 1;  // P / p_0 = 1
+    for (uint32_t i = 0; i < lvl; ++i) {
+      md.phat_mod[i][0] = 1 % c->mod[i];
+      md.p_inv[i] = c->h_rescale[lvl].ql_inv[i];
+      md.p_inv_sh[i] = c->h_rescale[lvl].ql_inv_sh[i];
+    }
+    md.src0 = lvl;
+    md.center = 1;
+    cudaMalloc(&c->d_rescale_md[lvl], sizeof(ModDownConst));
+    cudaMemcpy(c->d_rescale_md[lvl], &md, sizeof(ModDownConst), cudaMemcpyHostToDevice);
+  }
   for (uint32_t lvl = 0; lvl < c->n_q; ++lvl) {
     size_t b1 = sizeof(ModUpConst) * c->h_modup[lvl].size();
     cudaMalloc(&c->d_modup[lvl], b1);
@@ -275,6 +292,7 @@ extern "C" void hy_ctx_destroy(hy_ctx* c) {
   for (auto p : c->d_modup) cudaFree(p);
   for (auto p : c->d_moddown) cudaFree(p);
   for (auto p : c->d_rescale) cudaFree(p);
+  for (auto p : c->d_rescale_md) cudaFree(p);
   delete c;
 }
 

@@ -42,6 +42,10 @@ struct ModDownConst {
   uint64_t phat_inv[8], phat_inv_sh[8];    // (P/p_k)^{-1} mod p_k
   uint64_t phat_mod[kMaxChain][8];         // (P/p_k) mod q_i
   uint64_t p_inv[kMaxChain], p_inv_sh[kMaxChain];  // P^{-1} mod q_i
+  // chain index of the first source limb (ModDown: n_q, the first special prime); center: lift the source
+  // residue to (-p/2, p/2] before converting it (the fused rescale, a ModDown by P = q_l with the centred
+  // remainder of R-RESCALE)
+  uint32_t src0, center;
 };
 
 struct RescaleConst {  // for dropping q_l
@@ -67,6 +71,7 @@ struct hy_ctx {
   std::vector<hy::ModUpConst*> d_modup;      // [level] -> device array [beta]
   std::vector<hy::ModDownConst*> d_moddown;  // [level]
   std::vector<hy::RescaleConst*> d_rescale;  // [level] (drop q_level)
+  std::vector<hy::ModDownConst*> d_rescale_md;  // [level >= 1]: rescale as a centred ModDown by q_level
   // host copies (used to fill launch parameters)
   std::vector<std::vector<hy::ModUpConst>> h_modup;
   std::vector<hy::ModDownConst> h_moddown;
@@ -210,6 +215,11 @@ bool modup_cols_ok(const hy_ctx* c);  // N = 2^16 and alpha <= 4
 // src_g[c][k] (after their inverse row pass), z_k = [v_k (P/p_k)^{-1}]_{p_k}, and for every q_i <= level
 // ext_g[c][i] = forward column pass of [sum_k z_k ((P/p_k) mod q_i)] (between-pass format).
 void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
+// Fused rescale of G ciphertexts at `level` (N = 2^16): src_g = the two last limbs after their inverse row pass
+// (between-pass format, [2][N]) -> w_g [2][level][N] (column kernel, centred lift to q_0..q_{level-1}); then
+// out_g[c][i] = (ct_g[c][i] - NTT(w_g[c][i])) q_level^{-1} (row kernel).
+void launch_rescale_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s);
+void launch_rescale_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, uint32_t level, cudaStream_t s);
 bool moddown_cols_ok(const hy_ctx* c);  // N = 2^16 and K <= 4
 // Inverse row pass of kappa_{k_g}(c1_g) read straight from c1_g (the automorphism fused as a row gather),
 // [l+1][N] each, into dst_g in the between-pass format (for launch_modup_cols)

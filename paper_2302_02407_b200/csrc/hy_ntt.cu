@@ -922,7 +922,7 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
     const int k = p - nsrc;
     return (DOWN || k < lo) ? k : k + nsrc;
   };
-  auto src_chain = [&](int p) { return DOWN ? n_q + p : lo + p; };
+  auto src_chain = [&](int p) { return DOWN ? (int)md->src0 + p : lo + p; };
   auto tgt_chain = [&](int u) { return (DOWN || u <= level) ? u : n_q + (u - level - 1); };
   auto table = [&](int p) -> const double* {
     if (p < nsrc) return dt.itw + (size_t)src_chain(p) * N;
@@ -961,11 +961,16 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
       run_stages<1, false>(x, l, 7, 5, Tp, q, qinv);
       const double hinv = DOWN ? (double)md->phat_inv[p] : (double)mc[j].hat_inv[p];
       const double cst = fcanon(fmulmod(pc.n_inv_d, hinv, q, qinv), q, qinv);
+      const bool center = DOWN && md->center;  // rescale: the centred remainder in (-q/2, q/2] (R-RESCALE)
+      const double half = 0.5 * (q - 1.0);
 #pragma unroll
       for (int i = 0; i < A; ++i)
         if (i == p) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) y[i][k] = fcanon(fmulmod(x[k], cst, q, qinv), q, qinv);
+          for (int k = 0; k < 8; ++k) {
+            const double v = fcanon(fmulmod(x[k], cst, q, qinv), q, qinv);
+            y[i][k] = center && v > half ? v - q : v;
+          }
         }
     } else {  // BConv to target u, then the forward column pass
       const int u = target(p);
@@ -1072,6 +1077,28 @@ void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t leve
     case 4: k_bconv_cols<4, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
     default: break;  // callers check moddown_cols_ok
   }
+}
+
+void launch_rescale_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  dim3 grid(32, 2, G);
+  KTimer kt(c, FAM_RESCALE, s);
+  // algorithmic bytes: the 2 dropped limbs in, the 2 level conversion limbs out
+  kt.bytes = (uint64_t)G * 2 * (1 + level) * c->N * 8;
+  // a ModDown by P = q_level: one source (chain level), targets q_0..q_{level-1}, i.e. the DOWN kernel at level-1
+  k_bconv_cols<1, true><<<grid, 256, 0, s>>>(a, nullptr, c->d_rescale_md[level], c->dt, (int)level - 1,
+                                              (int)c->n_q, (int)level + 1, (int)c->log_n);
+}
+
+void launch_rescale_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, uint32_t level, cudaStream_t s) {
+  if (G <= 0) return;
+  const int R = (int)(c->N / 256);
+  dim3 grid(R / 8 > 0 ? R / 8 : 1, level, 2 * G);
+  KTimer kt(c, FAM_RESCALE, s);
+  // the input ciphertext's first level limbs and w in, the output written
+  kt.bytes = (uint64_t)G * 2 * 3 * level * c->N * 8;
+  k_ntt_rows_final<<<grid, 256, 0, s>>>(a, 2, (int)level + 1, c->d_rescale_md[level], c->dt, (int)level - 1,
+                                        (int)c->log_n);
 }
 
 void launch_ntt_rows_final(hy_ctx* c, const RowsFinalArgs& a, int G, int npoly, uint32_t level, cudaStream_t s) {

@@ -2,6 +2,7 @@
 // client-side key generation, encryption and decryption (
 // DESIGN R-SK, R-EVK, R-ENC, R-PRNG), all as device kernels.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "hy_arith.cuh"
@@ -367,6 +368,40 @@ hy_status rescale_multi(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint3
   if (level == 0) return fail(HY_E_LEVEL_EXHAUSTED, "rescale at level 0");
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
   const size_t N = c->N, nl = level + 1;
+  static const bool fused = getenv("HY_FUSE_RESCALE") == nullptr || atoi(getenv("HY_FUSE_RESCALE")) != 0;
+  if (fused && moddown_cols_ok(c)) {
+    // a ModDown by P = q_level with the centred remainder: inverse row pass of the two dropped limbs, one
+    // column kernel (inverse column pass, centred lift, forward column pass of the level targets), one row
+    // kernel ((c_i - t_i) q_level^{-1}); the lifted limbs never make an HBM round trip through separate passes
+    for (uint32_t done = 0; done < n;) {
+      const int G = (int)std::min<uint32_t>(n - done, kG);
+      Ws ws{c->ws, c->ws_bytes};
+      LimbList L;
+      ModUpColsArgs ma{};
+      RowsFinalArgs fa{};
+      for (int g = 0; g < G; ++g) {
+        const uint64_t* in = cts[done + g];
+        uint64_t* out = outs[done + g];
+        if (!in || !out) return fail(HY_E_ARG, "null ciphertext");
+        if (in == out) return fail(HY_E_ARG, "rescale cannot run in place");
+        uint64_t* v = ws.take<uint64_t>(2 * N);
+        uint64_t* w = ws.take<uint64_t>(2 * level * N);
+        if (!w) return fail(HY_E_WORKSPACE, "workspace too small");
+        for (int p = 0; p < 2; ++p) L.add(in + ((size_t)p * nl + level) * N, v + (size_t)p * N, level);
+        ma.src[g] = v;
+        ma.ext[g] = w;
+        fa.u[g] = in;
+        fa.w[g] = w;
+        fa.out[g] = out;
+        fa.k0[g] = 1;
+      }
+      rows_list(c, L, true, s);
+      launch_rescale_cols(c, ma, G, level, s);
+      launch_rescale_rows_final(c, fa, G, level, s);
+      done += G;
+    }
+    return cuda_check("rescale");
+  }
   for (uint32_t done = 0; done < n;) {
     const int G = (int)std::min<uint32_t>(n - done, kG);
     Ws ws{c->ws, c->ws_bytes};

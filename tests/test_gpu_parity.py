@@ -261,3 +261,26 @@ def test_encode_batch_device(pair):
         got = to_np(ctx.encode_batch(z, scale, level))
         for i in range(len(z)):
             assert np.array_equal(got[i], o.encode(z[i], scale, level).data), (scale, i)
+
+
+@pytest.mark.parametrize("level", [1, 2, 9, 23])
+def test_rescale_fused_levels(level):
+    """Rescale at N = 2^16 runs as a centred ModDown by q_l (inverse row pass, fused column kernel, row kernel with
+    the epilogue): bit-exact vs the oracle's big-int-pinned rescale at the lowest, conv and full levels, on random
+    residues (both centring branches taken); the conv-layer tests cover the batched calls."""
+    ctx, o = _hyp_pair()
+    cts = [rand_limbs(o, 300 + level * 10 + k, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+           for k in range(3)]
+    for a in cts:
+        assert np.array_equal(to_np(ctx.rescale(to_dev(a, ctx), level)), o.rescale(oracle.Ct(a, level, 1.0)).data)
+
+
+_HYP = {}
+
+
+def _hyp_pair():
+    if not _HYP:
+        import paper_2302_02407_b200 as hy
+        prm = synth.PARAMS["hyp"]
+        _HYP["p"] = (hy.Context(**prm), oracle.Oracle(**prm))
+    return _HYP["p"]
