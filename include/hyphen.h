@@ -276,6 +276,12 @@ size_t hy_evk_words(const hy_ctx* ctx);
  * Device buffers, must not alias; stream-ordered. */
 hy_status hy_evk_pack(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, void* stream);
 hy_status hy_evk_unpack(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, void* stream);
+/* 48-bit wire format for any residue array (ciphertexts, plaintexts; every residue < 2^48): n_words words
+ * (a multiple of 4) <-> 6 bytes per word, word x at bytes [6x, 6x+6) little-endian (3 n_words / 4 uint64),
+ * the layout of the packed keys.  A client that keeps ciphertexts in this form moves 25 % fewer bytes over
+ * PCIe.  Device buffers, must not alias; stream-ordered.  Errors: HY_E_ARG (null, n_words % 4 != 0). */
+hy_status hy_pack48(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, size_t n_words, void* stream);
+hy_status hy_unpack48(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, size_t n_words, void* stream);
 hy_status hy_keygen_galois(hy_ctx* ctx, uint64_t sk_seed, uint64_t ek_seed, uint64_t k, uint64_t* d_evk, void* stream);
 /* Relinearization key s^2 -> s (DESIGN R-RELIN): b_j = -a_j s + e_j + g_j s^2, object ids j (Galois
  * element 0, used by no rotation); layout as a rotation key. */

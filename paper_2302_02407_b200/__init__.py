@@ -79,6 +79,8 @@ SIGNATURES = {
     "hy_evk_words": (C.c_size_t, [_P]),
     "hy_evk_pack": (C.c_int, [_P, _P, _P, _P]),
     "hy_evk_unpack": (C.c_int, [_P, _P, _P, _P]),
+    "hy_pack48": (C.c_int, [_P, _P, _P, C.c_size_t, _P]),
+    "hy_unpack48": (C.c_int, [_P, _P, _P, C.c_size_t, _P]),
     "hy_mulct": (C.c_int, [_P, _P, _P, _P, _U32, _P, _P]),
     "hy_mulct_batch": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _PP, _P]),
     "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
@@ -218,6 +220,17 @@ class Context:
         """[dnum][2][n_q+n_p][N] one word per uint64 (e.g. the oracle's key) -> packed device key"""
         out = self.empty(*self.evk_shape()) if out is None else out
         _check(lib().hy_evk_pack(self._c, _ptr(evk_u64), _ptr(out), self._stream()))
+        return out
+
+    def pack48(self, t, out=None):
+        """residue tensor (numel % 4 == 0) -> 48-bit wire format, 3 numel / 4 int64 words (hy_pack48)"""
+        out = self.empty(t.numel() // 4 * 3) if out is None else out
+        _check(lib().hy_pack48(self._c, _ptr(t), _ptr(out), t.numel(), self._stream()))
+        return out
+
+    def unpack48(self, packed, out):
+        """48-bit wire format -> residues into `out` (its numel words, hy_unpack48)"""
+        _check(lib().hy_unpack48(self._c, _ptr(packed), _ptr(out), out.numel(), self._stream()))
         return out
 
     def evk_unpack(self, evk, out=None):

@@ -192,6 +192,26 @@ __global__ void k_evk_digit(uint64_t* __restrict__ evk, const uint64_t* __restri
   evk_store(evk + ((size_t)(j * 2 + 0) * L1 + t) * evk_limb_words(N), x, b);
 }
 
+// Generic 48-bit packing of n4 groups of 4 words (hy_pack48 / hy_unpack48): group m = words 4m..4m+3 <->
+// the 3 uint64 (24 bytes) at 3m, the layout of the packed keys.  One thread per group.
+__global__ void k_pack48(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n4) {
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n4) return;
+  const ulonglong2 a = reinterpret_cast<const ulonglong2*>(in)[2 * m];
+  const ulonglong2 b = reinterpret_cast<const ulonglong2*>(in)[2 * m + 1];
+  out[3 * m] = (a.x & kM48) | (a.y << 48);
+  out[3 * m + 1] = ((a.y & kM48) >> 16) | (b.x << 32);
+  out[3 * m + 2] = ((b.x & kM48) >> 32) | (b.y << 16);
+}
+__global__ void k_unpack48(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n4) {
+  const size_t m = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n4) return;
+  uint64_t w0, w1, w2, w3;
+  evk_unpack4(in[3 * m], in[3 * m + 1], in[3 * m + 2], w0, w1, w2, w3);
+  reinterpret_cast<ulonglong2*>(out)[2 * m] = make_ulonglong2(w0, w1);
+  reinterpret_cast<ulonglong2*>(out)[2 * m + 1] = make_ulonglong2(w2, w3);
+}
+
 // Packed key <-> one uint64 per word (hy_evk_pack / hy_evk_unpack).  grid (N/256, n_limbs)
 __global__ void k_evk_pack(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int logN) {
   const size_t N = (size_t)1 << logN;
@@ -684,4 +704,26 @@ extern "C" hy_status hy_evk_unpack(hy_ctx* c, const uint64_t* d_in, uint64_t* d_
   KTimer kt(c, FAM_CLIENT, st(stream));
   k_evk_unpack<<<dim3(c->N / kT, L), kT, 0, st(stream)>>>(d_in, d_out, (int)c->log_n);
   return cuda_check("hy_evk_unpack");
+}
+
+extern "C" hy_status hy_pack48(hy_ctx* c, const uint64_t* d_in, uint64_t* d_out, size_t n_words, void* stream) {
+  if (!c || !d_in || !d_out) return fail(HY_E_ARG, "null");
+  if (n_words % 4) return fail(HY_E_ARG, "n_words must be a multiple of 4");
+  const size_t n4 = n_words / 4;
+  if (!n4) return HY_OK;
+  KTimer kt(c, FAM_ELEM, st(stream));
+  kt.bytes = n_words * 14;
+  k_pack48<<<(unsigned)((n4 + 255) / 256), 256, 0, st(stream)>>>(d_in, d_out, n4);
+  return cuda_check("hy_pack48");
+}
+
+extern "C" hy_status hy_unpack48(hy_ctx* c, const uint64_t* d_in, uint64_t* d_out, size_t n_words, void* stream) {
+  if (!c || !d_in || !d_out) return fail(HY_E_ARG, "null");
+  if (n_words % 4) return fail(HY_E_ARG, "n_words must be a multiple of 4");
+  const size_t n4 = n_words / 4;
+  if (!n4) return HY_OK;
+  KTimer kt(c, FAM_ELEM, st(stream));
+  kt.bytes = n_words * 14;
+  k_unpack48<<<(unsigned)((n4 + 255) / 256), 256, 0, st(stream)>>>(d_in, d_out, n4);
+  return cuda_check("hy_unpack48");
 }

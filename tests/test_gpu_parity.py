@@ -284,3 +284,19 @@ def _hyp_pair():
         prm = synth.PARAMS["hyp"]
         _HYP["p"] = (hy.Context(**prm), oracle.Oracle(**prm))
     return _HYP["p"]
+
+
+def test_pack48_wire_format():
+    """hy_pack48 / hy_unpack48: word x at bytes [6x, 6x+6) little-endian (checked against a numpy byte view),
+    round trip exact, and the packed keys use the same layout."""
+    ctx, o = _hyp_pair()
+    level = 3
+    a = rand_limbs(o, 5, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+    d = to_dev(a, ctx)
+    packed = to_np(ctx.pack48(d))
+    want = a.reshape(-1).view(np.uint8).reshape(-1, 8)[:, :6].reshape(-1)
+    assert np.array_equal(packed.view(np.uint8), want)
+    back = ctx.unpack48(ctx.pack48(d), ctx.empty(*d.shape))
+    assert np.array_equal(to_np(back), a)
+    k = ctx.keygen_rot(SK, EK, 3)
+    assert np.array_equal(to_np(ctx.pack48(ctx.evk_unpack(k))), to_np(k).reshape(-1))
