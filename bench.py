@@ -471,6 +471,32 @@ def run_ours(args, ws, rank, local):
 
     ms_h, _ = timed(step_hoisted, args.steps, max(1, args.warmup // 2))
 
+    # the three HRot variants at the full level and the two conv levels: the same 64 keys
+    # and ciphertexts (level l = the first l+1 limbs, a level-down), keyswitch/s and the whole-rotation HBM
+    # fraction in algorithmic bytes (ct in once per distinct input, the key slice read, 6-byte packed, ct out)
+    variants = None
+    if not args.no_variants and os.environ.get("HY_NCU_TIMED") != "1":
+        variants = {}
+        pk_hbm = peaks()["hbm_gbs"]
+        E_ = lambda lv: lv + 1 + len(prm["p_bits"])  # noqa: E731
+        for lv in (LEVEL, CA_LEVEL, RA_LEVEL):
+            cl = [c[:, : lv + 1].contiguous() for c in cts]
+            ol = [ctx.empty(*ctx.ct_shape(lv)) for _ in range(BATCH)]
+            o1 = ctx.empty(*ctx.ct_shape(lv))
+            ct_b = 2 * (lv + 1) * ctx.N * 8
+            key_b = 2 * ctx.n_digits(lv) * E_(lv) * ctx.N * 6
+            row = {}
+            for vname, fn, moved in (
+                    ("plain", lambda: ctx.hrot_batch(evks, cl, lv, rs, ol), BATCH * (2 * ct_b + key_b)),
+                    ("hoisted", lambda: ctx.hrot_hoisted(evks, cl[0], lv, rs, ol), ct_b + BATCH * (ct_b + key_b)),
+                    ("lazy_sum", lambda: ctx.hrot_sum(evks, cl, lv, rs, o1), BATCH * (ct_b + key_b) + ct_b)):
+                t_ms, _ = timed(fn, max(2, args.steps // 2), 2)
+                gbs = moved / (t_ms * 1e-3) / 1e9
+                row[vname] = {"keyswitch_per_s": BATCH * ws * 1000.0 / t_ms, "ms_per_64": t_ms,
+                              "hbm_gbs": gbs, "hbm_frac": gbs / pk_hbm}
+            variants[f"l+1={lv + 1}"] = row
+            del cl, ol, o1
+
     # live per-family kernel timing over K instrumented steps (same stream, CUDA events)
     fam = ctx.FAMILIES
     ctx.time_kernels(sum(fam.values()))
@@ -670,6 +696,7 @@ def run_ours(args, ws, rank, local):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
+            "hrot_variants": variants,
             "hoisted": {"value": BATCH * ws * 1000.0 / ms_h, "unit": UNIT, "ms_per_step": ms_h,
                         "note": "ct_0 rotated by 1..64 with one shared ModUp (Slide_f pattern, P:369-375)",
                         "kernel_breakdown": breakdown_h},
@@ -690,6 +717,7 @@ def main():
     ap.add_argument("--cpu-rotations", type=int, default=60)
     ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 / ResNet-18 conv-layer timings")
     ap.add_argument("--no-r18", action="store_true", help="skip the ResNet-18 (PRCR) conv-layer timings")
+    ap.add_argument("--no-variants", action="store_true", help="skip the HRot variant x level table")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
