@@ -300,3 +300,30 @@ def test_pack48_wire_format():
     assert np.array_equal(to_np(back), a)
     k = ctx.keygen_rot(SK, EK, 3)
     assert np.array_equal(to_np(ctx.pack48(ctx.evk_unpack(k))), to_np(k).reshape(-1))
+
+
+def test_bench_configuration_sampled():
+    """The C2 bench workload in the bench's launch configuration (workspace for 32 key switches per launch, level
+    23): 34 plain rotations r_i = i + 1 (a full chunk of 32 and a ragged chunk of 2) and 40 hoisted rotations of one
+    ciphertext; sampled outputs bit-exact vs the oracle (device keys, themselves bit-exact with the oracle's)."""
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS["hyp"]
+    _, o = _hyp_pair()
+    ctx = hy.Context(**prm, max_batch=32)
+    level = 23
+    n_rot = 34
+    rs = [i + 1 for i in range(n_rot)]
+    keys = [ctx.keygen_rot(SK, EK, r) for r in rs]
+    cts = [_fresh_ct(ctx, o, "hyp", level, 400 + i) for i in range(n_rot)]
+    outs = ctx.hrot_batch(keys, [c[0] for c in cts], level, rs)
+    for i in (0, 17, 31, 33):
+        okey = to_np(ctx.evk_unpack(keys[i])).reshape(o.dnum, 2, o.nq + o.np_, o.N)
+        assert np.array_equal(to_np(outs[i]), o.hrot(cts[i][1], okey, rs[i]).data), i
+    hrs = [i + 1 for i in range(40)]
+    hkeys = keys + [ctx.keygen_rot(SK, EK, r) for r in hrs[n_rot:]]
+    hout = ctx.hrot_hoisted(hkeys, cts[0][0], level, hrs)
+    sample = (0, 31, 39)
+    okeys = [to_np(ctx.evk_unpack(hkeys[i])).reshape(o.dnum, 2, o.nq + o.np_, o.N) for i in sample]
+    want = o.hrot_hoisted(cts[0][1], okeys, [hrs[i] for i in sample])
+    for i, w in zip(sample, want):
+        assert np.array_equal(to_np(hout[i]), w.data), i
