@@ -136,7 +136,7 @@ uint64_t hy_galois_elt(const hy_ctx* ctx, int64_t r);
  * d_ext out [beta][l+1+K][N] NTT domain; limbs of digit j's own primes are
  * NTT(d) (fast basis conversion without correction elsewhere). */
 hy_status hy_modup(hy_ctx* ctx, uint32_t level, const uint64_t* d_coeff, uint64_t* d_ext, void* stream);
-/* u[c][t] = sum_j ext[j][t] * evk[j][c][chain(t)]  ([2][l+1+K][N] out). */
+/* u[c][t] = sum_j ext[j][t] * evk[j][c][chain(t)]  ([2][l+1+K][N] out; d_evk packed, see Conventions). */
 hy_status hy_ks_inner_product(hy_ctx* ctx, uint32_t level, const uint64_t* d_ext, const uint64_t* d_evk,
                               uint64_t* d_u, void* stream);
 /* ModDown of one polynomial [l+1+K][N] -> [l+1][N] (both NTT domain). */
