@@ -181,6 +181,11 @@ hy_status hy_pmult_acc(hy_ctx* ctx, const uint64_t* const* d_cts, const uint64_t
 /* out = a + b over npoly polynomials ([npoly][l+1][N]); in-place allowed. */
 hy_status hy_add(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t npoly, uint32_t level,
                  uint64_t* d_out, void* stream);
+/* Level alignment (SPEC level_down; P:102-112 levels): [2][l+1][N] -> [2][l'+1][N], l' <= l, by dropping the
+ * limbs above l' (reduction mod Q_l'); scale unchanged, no rounding.  out must not alias ct unless l' == l.
+ * Errors: HY_E_ARG, HY_E_LEVEL_MISMATCH (l' > l). */
+hy_status hy_level_down(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint32_t new_level, uint64_t* d_out,
+                        void* stream);
 /* Rescale (DESIGN R-RESCALE): [2][l+1][N] -> [2][l][N], exact round(c/q_l). */
 hy_status hy_rescale(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint64_t* d_out, void* stream);
 

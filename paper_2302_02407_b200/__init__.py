@@ -73,6 +73,7 @@ SIGNATURES = {
     "hy_pmult_acc": (C.c_int, [_P, _PP, _PP, _U32, _U32, _P, C.c_int, _P]),
     "hy_add": (C.c_int, [_P, _P, _P, _U32, _U32, _P, _P]),
     "hy_rescale": (C.c_int, [_P, _P, _U32, _P, _P]),
+    "hy_level_down": (C.c_int, [_P, _P, _U32, _U32, _P, _P]),
     "hy_keygen_rot": (C.c_int, [_P, _U64, _U64, C.c_int32, _P, _P]),
     "hy_keygen_galois": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "hy_keygen_relin": (C.c_int, [_P, _U64, _U64, _P, _P]),
@@ -329,6 +330,11 @@ class Context:
     def add(self, a, b, level, out=None, npoly=2):
         out = self.empty(*a.shape) if out is None else out
         _check(lib().hy_add(self._c, _ptr(a), _ptr(b), npoly, level, _ptr(out), self._stream()))
+        return out
+
+    def level_down(self, ct, level, new_level, out=None):
+        out = self.empty(*self.ct_shape(new_level)) if out is None else out
+        _check(lib().hy_level_down(self._c, _ptr(ct), level, new_level, _ptr(out), self._stream()))
         return out
 
     def rescale(self, ct, level, out=None):

@@ -378,6 +378,21 @@ extern "C" hy_status hy_add(hy_ctx* c, const uint64_t* a, const uint64_t* b, uin
   return cuda_check("hy_add");
 }
 
+extern "C" hy_status hy_level_down(hy_ctx* c, const uint64_t* ct, uint32_t level, uint32_t new_level,
+                                   uint64_t* out, void* stream) {
+  if (!c || !ct || !out) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  if (new_level > level) return fail(HY_E_LEVEL_MISMATCH, "level_down cannot raise the level");
+  if (ct == out && new_level != level) return fail(HY_E_ARG, "level_down cannot run in place");
+  if (ct == out) return HY_OK;
+  const size_t N = c->N;
+  // the first new_level+1 limbs of each polynomial: Q_l -> Q_l' is a reduction of every coefficient, which in
+  // the RNS is dropping the limbs above new_level (scale unchanged)
+  cudaMemcpy2DAsync(out, (new_level + 1) * N * 8, ct, (size_t)(level + 1) * N * 8, (new_level + 1) * N * 8, 2,
+                    cudaMemcpyDeviceToDevice, st(stream));
+  return cuda_check("hy_level_down");
+}
+
 namespace hy {
 // Rescale of n ciphertexts at `level` (DESIGN R-RESCALE), batched kG per launch set:
 // iNTT of every dropped limb, centred lift, NTT of the lifts, (c - w) q_l^{-1}.  out_g must not alias in_g.

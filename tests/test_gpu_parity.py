@@ -327,3 +327,22 @@ def test_bench_configuration_sampled():
     want = o.hrot_hoisted(cts[0][1], okeys, [hrs[i] for i in sample])
     for i, w in zip(sample, want):
         assert np.array_equal(to_np(hout[i]), w.data), i
+
+
+def test_level_down(pair):
+    """level_down keeps the first l'+1 limbs of both polynomials (reduction mod Q_l'), decrypts to the same
+    message, and refuses to raise the level."""
+    import paper_2302_02407_b200 as hy
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 9
+    a = rand_limbs(o, 95, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+    for nl in (level, level - 1, 0):
+        got = to_np(ctx.level_down(to_dev(a, ctx), level, nl))
+        assert np.array_equal(got, a[:, : nl + 1])
+    z = synth.slots_uniform(34, o.n)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    ct = ctx.encrypt(SK, 41, 9, ctx.encode(z, scale, level), level)
+    low = ctx.level_down(ct, level, 1)
+    assert np.max(np.abs(np.real(ctx.decode(ctx.decrypt(SK, low, 1), 1, scale)) - z)) < 2**-20
+    with pytest.raises(hy.HyError):
+        ctx.level_down(low, 1, 2)
