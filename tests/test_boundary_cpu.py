@@ -86,3 +86,31 @@ def test_decode_coeffs_matches_oracle(hy, pset):
     back = hy.decode_coeffs(prm["log_n"], hy.encode_coeffs(prm["log_n"], z, int(scale)).astype(np.float64), scale)
     assert np.max(np.abs(back - z)) < 2**-25
     assert hy.decode_coeffs(prm["log_n"], m, scale, n_slots=7).shape == (7,)
+
+
+@pytest.mark.parametrize("spec,code", [
+    ((4, 4, 8, 3, 1, 8, 1, 3, 1, "RA"), 6),    # m not a power of two: HY_E_FORMAT
+    ((4, 4, 8, 2, 1, 8, 1, 1, 1, "RA"), 4),    # even filter: HY_E_SHAPE
+    ((4, 4, 8, 3, 3, 8, 1, 1, 1, "CA"), 4),    # stride 3: HY_E_SHAPE
+    ((4, 4, 16, 3, 1, 8, 1, 1, 1, "CA"), 5),   # image wider than the physical width: HY_E_CAPACITY
+    ((4, 4, 8, 3, 2, 8, 1, 1, 1, "RA"), 6),    # stride-2 RAConv: HY_E_FORMAT (downsampling is in CAConv)
+    ((4, 4, 8, 3, 1, 8, 2, 1, 1, "CA"), 6),    # m d not a multiple of g^2: HY_E_FORMAT
+])
+def test_conv_plan_errors(hy, spec, code):
+    """hy_conv_plan_create checks the spec on the host (no device) and returns the documented status."""
+    with pytest.raises(hy.HyError) as e:
+        hy.ConvPlan(None, *spec, log_n=12)
+    assert e.value.code == code, hy.lib().hy_last_error()
+
+
+def test_host_entry_errors(hy):
+    """host-only entry points: more slots than N/2 is HY_E_CAPACITY, log_n out of range is HY_E_ARG."""
+    with pytest.raises(hy.HyError) as e:
+        hy.encode_coeffs(10, np.zeros(513), 2**20)
+    assert e.value.code == 5
+    with pytest.raises(hy.HyError) as e:
+        hy.decode_coeffs(10, np.zeros(1024), 2.0**20, n_slots=513)
+    assert e.value.code == 5
+    with pytest.raises(hy.HyError) as e:
+        hy.decode_coeffs(1, np.zeros(2), 1.0)
+    assert e.value.code == 1

@@ -346,3 +346,38 @@ def test_level_down(pair):
     assert np.max(np.abs(np.real(ctx.decode(ctx.decrypt(SK, low, 1), 1, scale)) - z)) < 2**-20
     with pytest.raises(hy.HyError):
         ctx.level_down(low, 1, 2)
+
+
+def test_error_paths():
+    """Status codes at the C ABI (include/hyphen.h): checked on the host before any launch."""
+    import ctypes as C
+
+    import paper_2302_02407_b200 as hy
+    ctx, o = _hyp_pair()
+    L = hy.lib()
+    level = 3
+    ct = ctx.empty(*ctx.ct_shape(level))
+    ct.zero_()
+    key = ctx.keygen_rot(SK, EK, 1)
+
+    def code(fn):
+        with pytest.raises(hy.HyError) as e:
+            fn()
+        return e.value.code
+
+    assert code(lambda: ctx.rescale(ctx.empty(*ctx.ct_shape(0)), 0, out=ctx.empty(*ctx.ct_shape(0)))) == 3  # EXHAUSTED
+    assert code(lambda: ctx.hrot(key, ct, level, 1, out=ct)) == 1                       # in place: ARG
+    assert code(lambda: ctx.hrot(key, ct, o.nq, 1)) == 1                                # level out of range: ARG
+    assert code(lambda: ctx.decode(ct[0], level, 2.0**42, n_slots=o.N)) == 5            # > N/2 slots: CAPACITY
+    assert code(lambda: ctx.pack48(ctx.empty(6))) == 1                                  # not a multiple of 4: ARG
+    assert code(lambda: ctx.level_down(ct, level, level + 1)) == 2                      # raise: LEVEL_MISMATCH
+    # a rotation without its key: MISSING_KEY
+    outs = (C.c_void_p * 1)(ctx.empty(*ctx.ct_shape(level)).data_ptr())
+    keys = (C.c_void_p * 1)(0)
+    cts = (C.c_void_p * 1)(ct.data_ptr())
+    rs = (C.c_int32 * 1)(5)
+    rc = L.hy_hrot_batch(ctx._c, keys, cts, level, rs, 1, outs, ctx._stream())
+    assert rc == 8, L.hy_last_error()
+    # r = 0 needs no key; an empty batch is a no-op
+    assert L.hy_hrot_batch(ctx._c, keys, cts, level, (C.c_int32 * 1)(0), 1, outs, ctx._stream()) == 0
+    assert L.hy_hrot_batch(ctx._c, keys, cts, level, rs, 0, outs, ctx._stream()) == 0
