@@ -729,10 +729,13 @@ __host__ __device__ constexpr int rows_warp_words(int nst) { return 256 * (1 + 3
 constexpr size_t rows_tma_smem(int nst) { return 8 * ((size_t)rows_warp_words(nst) * 8 + 8 * nst); }
 
 // (item g, row block by, Q limb i) of the Q-limb kernel; dsm = rows_tma_smem(NST) bytes of dynamic smem
-template <int B, bool HOIST, int NST>
+// PL (P-limb mode, split ModDown): i = the special prime k; the B digit iterations only (no own digit), then the
+// inverse row pass of the two products stored into a.out[g] + (c K + k) N in the between-pass format (the input
+// of the ModDown column kernel).  Otherwise i = the Q limb and the ModDown epilogue follows.
+template <int B, bool HOIST, int NST, bool PL = false>
 __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, const DevTables& dt,
                                                        const ModDownConst* md, int level, int L1, int E, int alpha,
-                                                       int logN, double* dsm, int g, int by, int i) {
+                                                       int logN, double* dsm, int g, int by, int ii) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const size_t N = (size_t)1 << logN;
   const int R = (int)(N >> 8);
@@ -740,9 +743,13 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
   if (row >= R) return;  // N = 2^10: 4 rows in an 8-warp CTA (warp-level sync only below)
   double* T = dsm + (size_t)w * rows_warp_words(NST);  // stage s at T + 256 + 768 s: e0, e1, digit (x) rows
   uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * rows_warp_words(NST)) + NST * w;
+  const int K = E - level - 1;
+  const int i = PL ? L1 - K + ii : ii;      // chain index of the limb (Q: the limb itself)
+  const int ui = PL ? level + 1 + ii : ii;  // its index among the extended limbs
+  constexpr int LAST = PL ? B - 1 : B;      // last iteration (Q: the epilogue)
   const PrimeConst& pc = dt.pc[i];
   const double q = pc.qd, qinv = pc.qinv;
-  const int own_digit = i / alpha;
+  const int own_digit = PL ? -1 : i / alpha;
   const size_t roff = (size_t)row * 256;
   // source rows of the permuted reads (hoisted digits; the c0 gather)
   // kx: hoisted -- every digit is read through kappa_kx; plain -- the own digit (c1 itself, kappa fused here)
@@ -757,7 +764,7 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
       // packed key rows: 1536 bytes each (hy_arith.cuh), at the start of their 2048-byte stage slots
       const uint64_t* e0 = evk_limb(a.evk[g], (size_t)(j * 2) * L1 + i, N) + roff / 4 * 3;
       const uint64_t* e1 = evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + i, N) + roff / 4 * 3;
-      const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + i) * N) +
+      const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)i * N : a.ext[g] + ((size_t)j * E + ui) * N) +
                            ((HOIST || j == own_digit) ? (size_t)rowx * 256 : roff);
       tma::mbar_expect(mb, 2 * 1536 + 2048);
       tma::bulk_row(b, e0, mb, 1536);
@@ -784,7 +791,7 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
   if (l == 0) {
     for (int t = 0; t < NST; ++t) tma::mbar_init(mbar + t);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int t = 0; t < NST - 1 && t <= B; ++t) issue(t);
+    for (int t = 0; t < NST - 1 && t <= LAST; ++t) issue(t);
   }
   load_twiddles_warp(T, dt.tw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
   __syncwarp();
@@ -792,8 +799,8 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
 #pragma unroll
   for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
 #pragma unroll 1
-  for (int j = 0; j <= B; ++j) {
-    if (l == 0 && j + NST - 1 <= B) issue(j + NST - 1);  // its stage was released at the end of j - 1
+  for (int j = 0; j <= LAST; ++j) {
+    if (l == 0 && j + NST - 1 <= LAST) issue(j + NST - 1);  // its stage was released at the end of j - 1
     double* b = T + 256 + 768 * (j % NST);
     tma::mbar_wait(mbar + j % NST, (uint32_t)(j / NST) & 1);
     if (j < B) {
@@ -864,6 +871,24 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
     tma::proxy_fence();
     __syncwarp();
   }
+  if constexpr (PL) {
+    // the P limb's inverse row pass straight from registers (layout L3), stage 0's buffer as transpose space
+    __syncwarp();
+    load_twiddles_warp(T, dt.itw + (size_t)i * N, (uint32_t)R + (uint32_t)row, l);
+    __syncwarp();
+    double* S = T + 256;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fred(c ? a1[k] : a0[k], q, qinv);
+      __syncwarp();
+      rows_inverse_from_l3(x, l, S, T, q, qinv);
+      uint64_t* dst = a.out[g] + ((size_t)c * K + ii) * N + roff;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dst[elem<1>(l, k)] = d2raw(x[k]);
+    }
+  }
 }
 
 template <int B, bool HOIST, int NST>
@@ -873,6 +898,15 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
   extern __shared__ __align__(128) double dsm[];
   rows_ip_final_tma_body<B, HOIST, NST>(a, dt, md, level, L1, E, alpha, logN, dsm, blockIdx.x, blockIdx.y,
                                         blockIdx.z);
+}
+
+// P limbs of the IP (split ModDown) on the same bulk-copy ring: grid (G, R/8, K); a.out[g] = v_g [2][K][N]
+template <int B, bool HOIST>
+__global__ void __launch_bounds__(256, 2) k_rows_ip_p_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
+                                                          int level, int L1, int E, int alpha, int logN) {
+  extern __shared__ __align__(128) double dsm[];
+  rows_ip_final_tma_body<B, HOIST, 2, true>(a, dt, nullptr, level, L1, E, alpha, logN, dsm, blockIdx.x, blockIdx.y,
+                                            blockIdx.z);
 }
 
 // ---------------------------------------------------------------- iNTT column pass + fast BConv + NTT column pass
@@ -1137,6 +1171,55 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
   }
   dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, nu);
   KTimer kt(c, FAM_NTT_IP, s);
+  // HY_PTMA (default on): the split-ModDown P limbs on the bulk-copy ring of the Q-limb kernel
+  static const bool ptma = getenv("HY_PTMA") == nullptr || atoi(getenv("HY_PTMA")) != 0;
+  if (ptma && !sum && !accumulate && inv_p && u0 == n) {
+    IpFinalArgs fa{};
+    for (int g = 0; g < G; ++g) {
+      fa.ext[g] = a.ext[g];
+      fa.own[g] = a.own[g];
+      fa.evk[g] = a.evk[g];
+      fa.out[g] = a.v[g];
+      fa.k0[g] = 1;
+      fa.kx[g] = hoist ? a.kx[g] : 1;
+    }
+    const size_t smem = rows_tma_smem(2);
+    const int L1p = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
+    kt.bytes = ((uint64_t)(hoist ? 1 : G) * beta * nu * 8 + (uint64_t)keys * 2 * beta * nu * 6 +
+                (uint64_t)G * 2 * nu * 8) * c->N;
+#define HY_PT(BB)                                                                                              \
+  case BB:                                                                                                     \
+    if (hoist) {                                                                                               \
+      static bool at = false;                                                                                  \
+      if (!at) {                                                                                               \
+        cudaFuncSetAttribute(k_rows_ip_p_tma<BB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        at = true;                                                                                             \
+      }                                                                                                        \
+      k_rows_ip_p_tma<BB, true><<<grid, 256, smem, s>>>(fa, c->dt, lv, L1p, E, al, lg);                        \
+    } else {                                                                                                   \
+      static bool at = false;                                                                                  \
+      if (!at) {                                                                                               \
+        cudaFuncSetAttribute(k_rows_ip_p_tma<BB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                             (int)smem);                                                                       \
+        at = true;                                                                                             \
+      }                                                                                                        \
+      k_rows_ip_p_tma<BB, false><<<grid, 256, smem, s>>>(fa, c->dt, lv, L1p, E, al, lg);                       \
+    }                                                                                                          \
+    break;
+    switch (beta) {
+      HY_PT(1)
+      HY_PT(2)
+      HY_PT(3)
+      HY_PT(4)
+      HY_PT(5)
+      HY_PT(6)
+      HY_PT(7)
+      default:
+        HY_PT(8)
+    }
+#undef HY_PT
+    return;
+  }
   // algorithmic bytes: every digit limb in once, each distinct key once, the outputs (read back too
   // when accumulating)
   const uint64_t outs = sum ? 1 : G;
