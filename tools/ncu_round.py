@@ -37,6 +37,8 @@ def family(name):
     short = name.split("(")[0].split("::")[-1]
     if short.startswith("k_ntt_rows_ip") and short.endswith(", 1>"):  # <B, SUM, HOIST=1>: hoisted P-limb IP
         return "ntt_ip_hoisted", short
+    if short.startswith("k_rows_ip_p_tma"):  # <B, HOIST>: the P-limb IP on the bulk-copy ring
+        return ("ntt_ip_hoisted" if short.endswith(", 1>") or short.endswith(", true>") else "ntt_ip"), short
     # the hoisted step's one shared ModUp (separate NTT passes + BConv): not part of the plain step's families
     for pre, fam in (("k_modup_bconv", "modup_hoisted"), ("k_ntt_rows<", "ntt_b_hoisted"),
                      ("k_ntt_cols256", "ntt_a_hoisted")):
