@@ -66,6 +66,12 @@ def ncu_traffic(fam_name):
                                    "items_per_launch": e.get("items"), "source": t.get("source")}
 
 
+def traffic_fields(fam_name):
+    """roofline.traffic = dram read + write bytes per launch (a number, or None) and where it comes from."""
+    t = ncu_traffic(fam_name)
+    return {"traffic": None if t is None else t["bytes_per_launch"], "traffic_detail": t}
+
+
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -529,7 +535,7 @@ def run_ours(args, ws, rank, local):
         d = breakdown[fam_name]
         achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
         return {"bound": "hbm", "kernel_family": fam_name, "achieved": achieved, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(fam_name),
+                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], **traffic_fields(fam_name),
                 "share_of_step": d["ms_per_step"] / ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
 
@@ -539,7 +545,7 @@ def run_ours(args, ws, rank, local):
         d = breakdown[fam_name]
         achieved = ops_per_launch / (d["avg_us"] * 1e-6) / 1e12
         return {"bound": "alu", "kernel_family": fam_name, "achieved": achieved, "peak": fp64_peak,
-                "unit": "TFP64op/s", "frac": achieved / fp64_peak, "traffic": ncu_traffic(fam_name),
+                "unit": "TFP64op/s", "frac": achieved / fp64_peak, **traffic_fields(fam_name),
                 "share_of_step": d["ms_per_step"] / ms, "work": what,
                 "peak_source": "148 SM x 64 FP64 lanes x 1.965 GHz (DESIGN.md section 5); one DFMA/DMUL/DADD = 1 op"}
 
