@@ -428,7 +428,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     prm = synth.PARAMS["hyp"]
-    ctx = hy.Context(**prm, device=local, max_batch=32)  # 32 key switches per batched launch
+    ctx = hy.Context(**prm, device=local, max_batch=int(os.environ.get("HY_BENCH_BATCH", "64")))  # key switches per launch
     sk, ek = synth.SEED_SK, synth.SEED_EVK
     rs = [i + 1 for i in range(BATCH)]
     # keys (server state) and inputs (client output), resident in HBM before timing

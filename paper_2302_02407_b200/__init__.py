@@ -183,7 +183,7 @@ class Context:
         self.q, self.p = self.moduli[: self.n_q], self.moduli[self.n_q:]
         self.alpha = int(lib().hy_ctx_alpha(self._c))
         self.max_level = self.n_q - 1 if max_level is None else max_level
-        # workspace for up to `max_batch` key switches per batched launch (library cap: 32; HY_MAX_BATCH)
+        # workspace for up to `max_batch` key switches per batched launch (library cap: 64; HY_MAX_BATCH)
         if max_batch is None:
             max_batch = int(os.environ.get("HY_MAX_BATCH", "16"))
         nbytes = int(lib().hy_workspace_bytes(self._c, self.max_level, max_batch))

@@ -139,7 +139,7 @@ hy_status pmult_many(hy_ctx* c, const uint64_t* const* cts, uint32_t n, const ui
 // forward pass A only (the column stages); the row stages are then run by launch_ntt_rows_ip
 void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s);
 
-constexpr int kG = 32;  // key switches per batched launch (upper bound; HY_KS_BATCH and the workspace set the size)
+constexpr int kG = 64;  // key switches per batched launch (upper bound; HY_KS_BATCH and the workspace set the size)
 
 // Fused ModUp NTT row pass + key-switch inner product (hy_ntt.cu), per item g:
 //   u_g[c][u] (+)= sum_j NTT_rows(ext_g[j][u]) (.) evk_g[j][c][chain(u)]   (own digit: own_g[u] as is)

@@ -303,26 +303,26 @@ def test_pack48_wire_format():
 
 
 def test_bench_configuration_sampled():
-    """The C2 bench workload in the bench's launch configuration (workspace for 32 key switches per launch, level
-    23): 34 plain rotations r_i = i + 1 (a full chunk of 32 and a ragged chunk of 2) and 40 hoisted rotations of one
+    """The C2 bench workload in the bench's launch configuration (workspace for 64 key switches per launch, level
+    23): 66 plain rotations r_i = i + 1 (a full chunk of 64 and a ragged chunk of 2) and 70 hoisted rotations of one
     ciphertext; sampled outputs bit-exact vs the oracle (device keys, themselves bit-exact with the oracle's)."""
     import paper_2302_02407_b200 as hy
     prm = synth.PARAMS["hyp"]
     _, o = _hyp_pair()
-    ctx = hy.Context(**prm, max_batch=32)
+    ctx = hy.Context(**prm, max_batch=64)
     level = 23
-    n_rot = 34
+    n_rot = 66
     rs = [i + 1 for i in range(n_rot)]
     keys = [ctx.keygen_rot(SK, EK, r) for r in rs]
     cts = [_fresh_ct(ctx, o, "hyp", level, 400 + i) for i in range(n_rot)]
     outs = ctx.hrot_batch(keys, [c[0] for c in cts], level, rs)
-    for i in (0, 17, 31, 33):
+    for i in (0, 33, 63, 65):
         okey = to_np(ctx.evk_unpack(keys[i])).reshape(o.dnum, 2, o.nq + o.np_, o.N)
         assert np.array_equal(to_np(outs[i]), o.hrot(cts[i][1], okey, rs[i]).data), i
-    hrs = [i + 1 for i in range(40)]
+    hrs = [i + 1 for i in range(70)]
     hkeys = keys + [ctx.keygen_rot(SK, EK, r) for r in hrs[n_rot:]]
     hout = ctx.hrot_hoisted(hkeys, cts[0][0], level, hrs)
-    sample = (0, 31, 39)
+    sample = (0, 63, 69)
     okeys = [to_np(ctx.evk_unpack(hkeys[i])).reshape(o.dnum, 2, o.nq + o.np_, o.N) for i in sample]
     want = o.hrot_hoisted(cts[0][1], okeys, [hrs[i] for i in sample])
     for i, w in zip(sample, want):

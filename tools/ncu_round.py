@@ -81,7 +81,7 @@ def main():
           "Launch list: `ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none` over",
           "bench.py's timed regions (`HY_NCU_TIMED=1`, 1 plain step of 64 HRots + 1 hoisted step); the per-launch",
           "times are cold-cache and serialised, so compare shares, not absolutes.  Full captures: one launch per",
-          "kernel, `--set full --clock-control none --import-source on` (32 key switches per launch, L+1 = 24).", ""]
+          "kernel, `--set full --clock-control none --import-source on` (64 key switches per launch, L+1 = 24).", ""]
     lpath = os.path.join(OUT, f"launches_{tag}.csv")
     if os.path.exists(lpath):
         shutil.copy(lpath, os.path.join(PROF, f"{tag}_launches.csv"))
@@ -118,7 +118,7 @@ def main():
             fam_acc[fam].append((short, rd + wr))
     for fam, lst in fam_acc.items():
         traffic["families"][fam] = {"kernel": " + ".join(k for k, _ in lst),
-                                    "dram_bytes": sum(b for _, b in lst) / len(lst), "items": int(os.environ.get("HY_ITEMS", "32"))}
+                                    "dram_bytes": sum(b for _, b in lst) / len(lst), "items": int(os.environ.get("HY_ITEMS", "64"))}
     with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as fh:
         fh.write("\n".join(md) + "\n")
     with open(os.path.join(PROF, "ncu_traffic.json"), "w") as fh:

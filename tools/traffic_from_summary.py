@@ -22,6 +22,6 @@ for sec in re.split(r"^### ", md, flags=re.M)[1:]:
 t = {"source": f"profiles/{tag}_ncu_summary.md (ncu --set full, one launch per kernel)", "families": {}}
 for fam, lst in acc.items():
     t["families"][fam] = {"kernel": " + ".join(k for k, _ in lst), "dram_bytes": sum(b for _, b in lst) / len(lst),
-                          "items": int(os.environ.get("HY_ITEMS", "32"))}
+                          "items": int(os.environ.get("HY_ITEMS", "64"))}
 json.dump(t, open(os.path.join(nr.PROF, "ncu_traffic.json"), "w"), indent=1)
 print(json.dumps(t, indent=1))
