@@ -202,6 +202,10 @@ __global__ void __launch_bounds__(256) k_ks_ip(const __grid_constant__ Arr<const
     if (SUM) {
       s0 += fred(a0, q, qinv);
       s1 += fred(a1, q, qinv);
+      if ((g & 31) == 31) {  // keep the running sum below 2^52 (exact) for batches of up to kG = 64
+        s0 = fred(s0, q, qinv);
+        s1 = fred(s1, q, qinv);
+      }
       continue;
     }
     uint64_t* o0 = uo.p[g] + (size_t)u * N + x;

@@ -502,10 +502,16 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
       }
     }
     if (SUM) {
+      // |fred| <= q/2 + 1 < 2^47: re-centre every 32 items so the running sum stays below 2^52 (exact)
+      const bool wrap = (g & 31) == 31;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         s0[k] += fred(a0[k], q, qinv);
         s1[k] += fred(a1[k], q, qinv);
+        if (wrap) {
+          s0[k] = fred(s0[k], q, qinv);
+          s1[k] = fred(s1[k], q, qinv);
+        }
       }
     } else if (inv_p) {
       // split ModDown: the P limb's inverse row pass straight from registers (layout L3), stored in the

@@ -381,3 +381,20 @@ def test_error_paths():
     # r = 0 needs no key; an empty batch is a no-op
     assert L.hy_hrot_batch(ctx._c, keys, cts, level, (C.c_int32 * 1)(0), 1, outs, ctx._stream()) == 0
     assert L.hy_hrot_batch(ctx._c, keys, cts, level, rs, 0, outs, ctx._stream()) == 0
+
+
+def test_hrot_sum_long_batch():
+    """Lazy HRotSum over 66 ciphertexts with a 64-item workspace (one full SUM launch of 64 items, whose running
+    FP64 sums are re-centred every 32 items, and a ragged chunk of 2): bit-exact vs the oracle."""
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS["hyp"]
+    _, o = _hyp_pair()
+    ctx = hy.Context(**prm, max_batch=64)
+    level, n = 2, 66
+    rs = [1] * n
+    okey = o.keygen_rot(SK, EK, 1)
+    key = evk_dev(okey, ctx)
+    cts = [_fresh_ct(ctx, o, "hyp", level, 500 + i) for i in range(n)]
+    got = ctx.hrot_sum([key] * n, [c[0] for c in cts], level, rs)
+    want = o.hrot_sum([c[1] for c in cts], [okey] * n, rs)
+    assert np.array_equal(to_np(got), want.data)
