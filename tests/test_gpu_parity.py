@@ -398,3 +398,23 @@ def test_hrot_sum_long_batch():
     got = ctx.hrot_sum([key] * n, [c[0] for c in cts], level, rs)
     want = o.hrot_sum([c[1] for c in cts], [okey] * n, rs)
     assert np.array_equal(to_np(got), want.data)
+
+
+@pytest.mark.parametrize("level", [0, 1, 5, 12, 23])
+def test_hrot_random_levels(level):
+    """Plain batch, hoisted and lazy-sum HRot at levels from 0 (one limb, one digit of one limb) to the full chain,
+    with random rotation amounts of both signs (including |r| > n/2): bit-exact vs the oracle."""
+    ctx, o = _hyp_pair()
+    g = np.random.default_rng(1000 + level)
+    rs = [int(x) for x in g.integers(1, o.n, 3) * g.choice([-1, 1], 3)]
+    okeys = [o.keygen_rot(SK, EK, r) for r in rs]
+    keys = [evk_dev(k, ctx) for k in okeys]
+    cts = [_fresh_ct(ctx, o, "hyp", level, 600 + 10 * level + i) for i in range(3)]
+    outs = ctx.hrot_batch(keys, [c[0] for c in cts], level, rs)
+    for out, (dct, oct_), r, k in zip(outs, cts, rs, okeys):
+        assert np.array_equal(to_np(out), o.hrot(oct_, k, r).data), (level, r)
+    hout = ctx.hrot_hoisted(keys, cts[0][0], level, rs)
+    for a, b in zip(hout, o.hrot_hoisted(cts[0][1], okeys, rs)):
+        assert np.array_equal(to_np(a), b.data), level
+    s = ctx.hrot_sum(keys, [c[0] for c in cts], level, rs)
+    assert np.array_equal(to_np(s), o.hrot_sum([c[1] for c in cts], okeys, rs).data), level
