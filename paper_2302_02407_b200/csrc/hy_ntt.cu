@@ -906,6 +906,98 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final_tma(const __grid_const
                                         blockIdx.z);
 }
 
+// Lazy HRotSum inner product on the bulk-copy ring: u = sum over the G items and their B digits, every
+// extended limb.  One warp per (row, limb u) walks the G x B (item, digit) rows through its NST-stage ring
+// (keys packed, digits in the column-pass format, the own digit's limb from own_g = kappa_g(c1) in the NTT
+// domain); the running sums are re-centred at every item boundary (|a| <= q/2 + 1 + 1.5 B q < 2^52, exact).
+// a.out[0] = u [2][E][N] (accumulate: added to it).  grid (1, R/8, E)
+template <int B>
+__global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constant__ IpFinalArgs a, int G,
+                                                            DevTables dt, int level, int L1, int E, int alpha,
+                                                            int logN, int accumulate) {
+  constexpr int NST = 2;
+  extern __shared__ __align__(128) double dsm[];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t N = (size_t)1 << logN;
+  const int R = (int)(N >> 8);
+  const int row = blockIdx.y * 8 + w, u = blockIdx.z;
+  if (row >= R) return;
+  double* T = dsm + (size_t)w * rows_warp_words(NST);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(dsm + 8 * rows_warp_words(NST)) + NST * w;
+  const int K = E - level - 1;
+  const int t = u <= level ? u : L1 - K + (u - level - 1);
+  const int own_digit = u <= level ? u / alpha : -1;
+  const PrimeConst& pc = dt.pc[t];
+  const double q = pc.qd, qinv = pc.qinv;
+  const size_t roff = (size_t)row * 256;
+  const int last = G * B - 1;
+  auto issue = [&](int it) {
+    const int g = it / B, j = it % B;
+    double* b = T + 256 + 768 * (it % NST);
+    uint64_t* mb = mbar + it % NST;
+    const uint64_t* e0 = evk_limb(a.evk[g], (size_t)(j * 2) * L1 + t, N) + roff / 4 * 3;
+    const uint64_t* e1 = evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + t, N) + roff / 4 * 3;
+    const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)u * N : a.ext[g] + ((size_t)j * E + u) * N) + roff;
+    tma::mbar_expect(mb, 2 * 1536 + 2048);
+    tma::bulk_row(b, e0, mb, 1536);
+    tma::bulk_row(b + 256, e1, mb, 1536);
+    tma::bulk_row(b + 512, xs, mb);
+  };
+  if (l == 0) {
+    for (int s = 0; s < NST; ++s) tma::mbar_init(mbar + s);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NST - 1 && s <= last; ++s) issue(s);
+  }
+  load_twiddles_warp(T, dt.tw + (size_t)t * N, (uint32_t)R + (uint32_t)row, l);
+  __syncwarp();
+  double a0[8], a1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a0[k] = a1[k] = 0.0;
+#pragma unroll 1
+  for (int it = 0; it <= last; ++it) {
+    if (l == 0 && it + NST - 1 <= last) issue(it + NST - 1);
+    const int j = it % B;
+    double* b = T + 256 + 768 * (it % NST);
+    tma::mbar_wait(mbar + it % NST, (uint32_t)(it / NST) & 1);
+    double x[8];
+    const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
+    if (j == own_digit) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = u2d(xb[elem<3>(l, k)]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = raw2d(xb[elem<1>(l, k)]);
+      __syncwarp();
+      rows_forward_l3(x, l, b + 512, T, q, qinv);
+    }
+    const uint64_t* e0 = reinterpret_cast<const uint64_t*>(b);
+    const uint64_t* e1 = reinterpret_cast<const uint64_t*>(b + 256);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = 3 * (l + 32 * h);
+      uint64_t v0[4], v1[4];
+      evk_unpack4(e0[o], e0[o + 1], e0[o + 2], v0[0], v0[1], v0[2], v0[3]);
+      evk_unpack4(e1[o], e1[o + 1], e1[o + 2], v1[0], v1[1], v1[2], v1[3]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        a0[4 * h + m] += fmulmod(x[4 * h + m], u2d(v0[m]), q, qinv);
+        a1[4 * h + m] += fmulmod(x[4 * h + m], u2d(v1[m]), q, qinv);
+      }
+    }
+    if (j == B - 1) {  // item boundary: re-centre
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a0[k] = fred(a0[k], q, qinv);
+        a1[k] = fred(a1[k], q, qinv);
+      }
+    }
+    tma::proxy_fence();
+    __syncwarp();
+  }
+  store_l3(a.out[0] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
+  store_l3(a.out[0] + ((size_t)E + u) * N + roff, l, a1, q, qinv, accumulate);
+}
+
 // P limbs of the IP (split ModDown) on the same bulk-copy ring: grid (G, R/8, K); a.out[g] = v_g [2][K][N]
 template <int B, bool HOIST>
 __global__ void __launch_bounds__(256, 2) k_rows_ip_p_tma(const __grid_constant__ IpFinalArgs a, DevTables dt,
@@ -1177,6 +1269,41 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
   }
   dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, nu);
   KTimer kt(c, FAM_NTT_IP, s);
+  // HY_SUMTMA (default on): the lazy HRotSum IP (all limbs summed over the items) on the bulk-copy ring
+  static const bool sumtma = getenv("HY_SUMTMA") == nullptr || atoi(getenv("HY_SUMTMA")) != 0;
+  if (sumtma && sum && !hoist && !inv_p && u0 == 0) {
+    IpFinalArgs fa{};
+    for (int g = 0; g < G; ++g) {
+      fa.ext[g] = a.ext[g];
+      fa.own[g] = a.own[g];
+      fa.evk[g] = a.evk[g];
+    }
+    fa.out[0] = a.u[0];
+    const size_t smem = rows_tma_smem(2);
+    const int L1s = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
+#define HY_ST(BB)                                                                                              \
+  case BB: {                                                                                                   \
+    static bool at = false;                                                                                    \
+    if (!at) {                                                                                                 \
+      cudaFuncSetAttribute(k_rows_ip_sum_tma<BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+      at = true;                                                                                               \
+    }                                                                                                          \
+    k_rows_ip_sum_tma<BB><<<grid, 256, smem, s>>>(fa, G, c->dt, lv, L1s, E, al, lg, accumulate ? 1 : 0);      \
+  } break;
+    switch (beta) {
+      HY_ST(1)
+      HY_ST(2)
+      HY_ST(3)
+      HY_ST(4)
+      HY_ST(5)
+      HY_ST(6)
+      HY_ST(7)
+      default:
+        HY_ST(8)
+    }
+#undef HY_ST
+    return;
+  }
   // HY_PTMA (default on): the split-ModDown P limbs on the bulk-copy ring of the Q-limb kernel
   static const bool ptma = getenv("HY_PTMA") == nullptr || atoi(getenv("HY_PTMA")) != 0;
   if (ptma && !sum && !accumulate && inv_p && u0 == n) {
