@@ -229,6 +229,9 @@ struct RowsAutArgs {
   uint64_t k[kG];
 };
 void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t level, cudaStream_t s);
+// the summed (lazy HRotSum) IP runs on the bulk-copy ring (HY_SUMTMA, default on); it can read the own digit
+// through kappa, so the lazy path then fuses kappa into the inverse row pass
+bool sum_tma_on();
 // one NTT row pass (forward: reads the between-pass format; inverse: writes it)
 void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices

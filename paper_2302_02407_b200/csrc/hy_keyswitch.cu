@@ -424,7 +424,8 @@ void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* ou
 // row pass / IP (hy_ntt.cu)
 void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
-                    cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr, bool rows_done = false) {
+                    cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr, bool rows_done = false,
+                    const uint64_t* own_k = nullptr) {
   if (modup_cols_ok(c)) {
     if (!rows_done) {  // rows_done: d already holds the inverse row pass (launch_ntt_rows_inv_aut)
       LimbList L;
@@ -449,6 +450,7 @@ void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64
     ra.evk[g] = evk[g];
     ra.u[g] = u[sum ? 0 : g];
     ra.v[g] = v ? v[g] : nullptr;
+    ra.kx[g] = own_k ? own_k[g] : 1;  // own_k: the own digit is read from own_g through kappa (summed IP only)
   }
   launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0, v != nullptr);
 }
@@ -1053,10 +1055,22 @@ hy_status hrot_sum_state(hy_ctx* c, const uint64_t* const* evks, const uint64_t*
       kt.bytes = ((uint64_t)G + 2) * nl * N * 8;
       k_automorph_sum<<<grid, kT, 0, s>>>(ai, ak, G, acc0, c->log_n, (int)nl, c->dt);
     }
-    automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
-    if (fuse_ip()) {
+    if (fuse_ip() && modup_cols_ok(c) && sum_tma_on()) {
+      // kappa fused into the inverse row pass of c1 and into the own-digit reads of the summed IP: kappa(c1) is
+      // never stored
+      RowsAutArgs ra{};
+      for (int g = 0; g < G; ++g) {
+        ra.src[g] = c1[g];
+        ra.dst[g] = d[g];
+        ra.k[g] = kk[g];
+      }
+      launch_ntt_rows_inv_aut(c, ra, G, level, s);
+      modup_ip_fused(c, level, G, d, ext, c1, keys, &u, !first, true, s, 0, nullptr, true, kk);
+    } else if (fuse_ip()) {
+      automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
       modup_ip_fused(c, level, G, d, ext, rc1c, keys, &u, !first, true, s);
     } else {
+      automorph_batch(c, G, c1, rc1, kk, nl, nl, false, s);
       intt_polys(c, G, rc1c, d, level, s);
       modup_batch(c, level, G, d, ext, s);
       ip_batch(c, level, G, ext, rc1c, keys, &u, nullptr, !first, false, true, s);

@@ -937,7 +937,10 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
     uint64_t* mb = mbar + it % NST;
     const uint64_t* e0 = evk_limb(a.evk[g], (size_t)(j * 2) * L1 + t, N) + roff / 4 * 3;
     const uint64_t* e1 = evk_limb(a.evk[g], (size_t)(j * 2 + 1) * L1 + t, N) + roff / 4 * 3;
-    const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)u * N : a.ext[g] + ((size_t)j * E + u) * N) + roff;
+    // the own digit's limb: own_g itself, through kappa_{kx_g} (one source row) when kx_g != 1
+    const uint64_t kx = a.kx[g];
+    const size_t srow = (j == own_digit && kx != 1) ? (size_t)(aut_index((uint32_t)roff, kx, logN) >> 8) * 256 : roff;
+    const uint64_t* xs = (j == own_digit ? a.own[g] + (size_t)u * N : a.ext[g] + ((size_t)j * E + u) * N) + srow;
     tma::mbar_expect(mb, 2 * 1536 + 2048);
     tma::bulk_row(b, e0, mb, 1536);
     tma::bulk_row(b + 256, e1, mb, 1536);
@@ -962,8 +965,12 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
     double x[8];
     const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
     if (j == own_digit) {
+      const uint64_t kx = a.kx[it / B];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = u2d(xb[elem<3>(l, k)]);
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
+        x[k] = u2d(xb[(kx != 1 ? aut_index(xi, kx, logN) : xi) & 255]);
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = raw2d(xb[elem<1>(l, k)]);
@@ -1256,6 +1263,11 @@ void launch_ntt_cols(hy_ctx* c, const LimbBatch& b, cudaStream_t s) {
   else k_ntt_cols_small<true><<<gA, 256, 0, s>>>(b, c->dt, logN);
 }
 
+bool sum_tma_on() {
+  static const bool on = getenv("HY_SUMTMA") == nullptr || atoi(getenv("HY_SUMTMA")) != 0;
+  return on;
+}
+
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
                         cudaStream_t s, int u0, bool inv_p, bool hoist) {
   if (G <= 0) return;
@@ -1270,13 +1282,13 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
   dim3 grid(sum ? 1 : G, R / 8 > 0 ? R / 8 : 1, nu);
   KTimer kt(c, FAM_NTT_IP, s);
   // HY_SUMTMA (default on): the lazy HRotSum IP (all limbs summed over the items) on the bulk-copy ring
-  static const bool sumtma = getenv("HY_SUMTMA") == nullptr || atoi(getenv("HY_SUMTMA")) != 0;
-  if (sumtma && sum && !hoist && !inv_p && u0 == 0) {
+  if (sum_tma_on() && sum && !hoist && !inv_p && u0 == 0) {
     IpFinalArgs fa{};
     for (int g = 0; g < G; ++g) {
       fa.ext[g] = a.ext[g];
       fa.own[g] = a.own[g];
       fa.evk[g] = a.evk[g];
+      fa.kx[g] = a.kx[g] ? a.kx[g] : 1;
     }
     fa.out[0] = a.u[0];
     const size_t smem = rows_tma_smem(2);
