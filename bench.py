@@ -181,6 +181,49 @@ def oracle_keyswitch_rate(n_rot: int, level: int = LEVEL, seed: int = 0):
     return n_rot / dt, dt
 
 
+def oracle_conv_layer_extrapolated(name="L2_ds"):
+    """ResNet-18 layer on the CPU oracle (too slow to run whole): time output 0, then outputs
+    {0, 1}; the difference is the per-output cost, the rest the shared Slide_f, and the layer time is extrapolated
+    linearly in n_o.  Data-independent work on seeded residues, as in oracle_conv_layers."""
+    import oracle
+    from oracle import hyphen as H
+    o = oracle.Oracle(**synth.PARAMS["hyp"])
+    chain_all = list(range(o.nq + o.np_))
+    evk = synth.residues(7, (o.dnum * 2, len(chain_all), o.N), [int(o.moduli[t]) for t in chain_all]) \
+        .reshape(o.dnum, 2, len(chain_all), o.N)
+
+    class AnyKey(dict):
+        def __missing__(self, r):
+            return evk
+
+    sp_t = {nm: sp for nm, sp, _ in R18_LAYERS}[name]
+    sp = H.ConvSpec(*sp_t[:10], S=sp_t[10] if len(sp_t) > 10 else 1)
+    K = synth.conv_weight(3000, sp.co, sp.ci, sp.f)
+    plan = H.plan_caconv(sp, K) if sp.algo == "CA" else H.plan_raconv(sp, K)
+    level = CA_LEVEL if sp.algo == "CA" else RA_LEVEL
+    pts = {}
+
+    def encode(v, lv):
+        if lv not in pts:
+            pts[lv] = oracle.Pt(synth.residues(8 + lv, (lv + 1, o.N), o.q[: lv + 1]), lv, float(o.q[lv]))
+        return pts[lv]
+
+    cts = [oracle.Ct(synth.residues(100 + i, (2, level + 1, o.N), o.q[: level + 1]), level, 2.0**42)
+           for i in range(plan.n_in)]
+    times = []
+    for outs in ([0], [0, 1]):
+        enc = H.EncConv(o, plan, AnyKey())
+        enc.encode = encode
+        t0 = time.perf_counter()
+        enc.run(cts, outs)
+        times.append(time.perf_counter() - t0)
+    per_out = max(times[1] - times[0], 0.0)
+    shared = max(times[0] - per_out, 0.0)
+    return {"layer": f"ResNet-18 {name}", "n_out": plan.n_out, "oracle_ms_measured": [1000 * t for t in times],
+            "oracle_ms_extrapolated": 1000 * (shared + plan.n_out * per_out), "level_in": level,
+            "method": "outputs {0} and {0, 1} timed; layer = shared Slide_f + n_o x per-output (extrapolated)"}
+
+
 def oracle_conv_layers(names=("L1_ca", "L1_ra")):
     """Time the CPU oracle's encrypted execution (oracle/hyphen.py EncConv, the plain C RNS-CKKS underneath) of
     whole ResNet-20 layers at the bench's levels, all outputs, on the host cores.  The oracle's work is
@@ -682,6 +725,11 @@ def run_ours(args, ws, rank, local):
                 x["oracle_over_gpu"] = x["oracle_ms"] / x["gpu_ms"]
             cpu["resnet20_layers"] = {"layers": lay, "cores": os.cpu_count(),
                                       "sample": "whole layers (every output ct), oracle EncConv on the host cores"}
+        if conv18 is not None:
+            x = oracle_conv_layer_extrapolated("L2_ds")
+            x["gpu_ms"] = conv18["layers"]["L2_ds"]["ms"]
+            x["oracle_over_gpu"] = x["oracle_ms_extrapolated"] / x["gpu_ms"]
+            cpu["resnet18_layer"] = x
 
     if rank == 0:
         line = {
