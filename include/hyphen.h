@@ -128,6 +128,10 @@ hy_status hy_ntt(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, const uint3
 /* Automorphism X -> X^k in the NTT domain, same permutation on every limb.
  * k: odd Galois element.  d_in/d_out [n_limbs][N], must not alias. */
 hy_status hy_automorph(hy_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, uint32_t n_limbs, uint64_t k, void* stream);
+/* PRot (SPEC prot): plaintext rotation by r slots, the automorphism kappa_{5^r} applied to the
+ * NTT-domain plaintext d_pt [l+1][N] -> d_out (no key switch: the plaintext is public).  r = 0 copies.
+ * Must not alias.  The conv layers fuse PRot into the PMult-accumulate as a gather instead (PRCR). */
+hy_status hy_prot(hy_ctx* ctx, const uint64_t* d_pt, uint32_t level, int32_t r, uint64_t* d_out, void* stream);
 /* Galois element of a left rotation by r slots: 5^(r mod n) mod 2N. */
 uint64_t hy_galois_elt(const hy_ctx* ctx, int64_t r);
 

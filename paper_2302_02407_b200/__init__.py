@@ -62,6 +62,7 @@ SIGNATURES = {
     "hy_ntt": (C.c_int, [_P, _P, _P, C.POINTER(_U32), _U32, C.c_int, _P]),
     "hy_automorph": (C.c_int, [_P, _P, _P, _U32, _U64, _P]),
     "hy_galois_elt": (_U64, [_P, C.c_int64]),
+    "hy_prot": (C.c_int, [_P, _P, _U32, C.c_int32, _P, _P]),
     "hy_modup": (C.c_int, [_P, _U32, _P, _P, _P]),
     "hy_ks_inner_product": (C.c_int, [_P, _U32, _P, _P, _P, _P]),
     "hy_moddown": (C.c_int, [_P, _U32, _P, _P, _P]),
@@ -274,6 +275,12 @@ class Context:
         return out
 
     # -- key switching ---------------------------------------------------
+    def prot(self, pt, level, r, out=None):
+        """PRot: plaintext rotation by r slots (hy_prot)"""
+        out = self.empty(level + 1, self.N) if out is None else out
+        _check(lib().hy_prot(self._c, _ptr(pt), level, int(r), _ptr(out), self._stream()))
+        return out
+
     def modup(self, level, d_coeff):
         ext = self.empty(self.n_digits(level), level + 1 + self.n_p, self.N)
         _check(lib().hy_modup(self._c, level, _ptr(d_coeff), _ptr(ext), self._stream()))

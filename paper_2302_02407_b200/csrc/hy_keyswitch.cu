@@ -844,6 +844,19 @@ extern "C" hy_status hy_automorph(hy_ctx* c, const uint64_t* in, uint64_t* out, 
   return cuda_check("hy_automorph");
 }
 
+extern "C" hy_status hy_prot(hy_ctx* c, const uint64_t* pt, uint32_t level, int32_t r, uint64_t* out, void* stream) {
+  if (!c || !pt || !out) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  if (pt == out) return fail(HY_E_ARG, "prot cannot run in place");
+  const uint64_t k = hy_galois_elt(c, r);
+  if (k == 1) {
+    cudaMemcpyAsync(out, pt, (size_t)(level + 1) * c->N * 8, cudaMemcpyDeviceToDevice, st(stream));
+  } else {
+    automorph(c, pt, out, level + 1, 1, k, false, st(stream));
+  }
+  return cuda_check("hy_prot");
+}
+
 extern "C" hy_status hy_modup(hy_ctx* c, uint32_t level, const uint64_t* d, uint64_t* ext, void* stream) {
   hy_status s0 = check_level(c, level);
   if (s0 != HY_OK) return s0;

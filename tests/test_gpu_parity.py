@@ -418,3 +418,22 @@ def test_hrot_random_levels(level):
         assert np.array_equal(to_np(a), b.data), level
     s = ctx.hrot_sum(keys, [c[0] for c in cts], level, rs)
     assert np.array_equal(to_np(s), o.hrot_sum([c[1] for c in cts], okeys, rs).data), level
+
+
+def test_prot(pair):
+    """PRot (P:126) = the oracle's coefficient-domain automorphism of the plaintext (the EncConv reference), bit-exact;
+    decodes to the left-rotated slots; r = 0 copies."""
+    name, ctx, o = pair
+    level = min(2, o.nq - 1)
+    z = synth.slots_uniform(35, o.n)
+    scale = 2 ** synth.PARAMS[name]["log_scale"]
+    pt = ctx.encode(z, scale, level)
+    opt = to_np(pt)
+    for r in (0, 1, -3, o.n // 2 + 5):
+        got = to_np(ctx.prot(pt, level, r))
+        k = o.galois_elt(r)
+        want = np.stack([o.ntt(o.automorph_coeff(o.intt(opt[i], i), i, k), i) for i in range(level + 1)]) \
+            if r % o.n else opt
+        assert np.array_equal(got, want), r
+    zr = np.real(ctx.decode(ctx.prot(pt, level, 3), level, scale))
+    assert np.max(np.abs(zr - np.roll(z, -3))) < 2**-20
