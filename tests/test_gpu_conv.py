@@ -2,6 +2,8 @@
 against the oracle's encrypted execution of its own plan: bit-exact on every RNS
 limb.  Toy layers (N = 2^12) run in full; ResNet-20 layers at Set_hyp (N = 2^16)
 are checked on sampled output ciphertexts at the conv levels (l+1 = 10 / 7)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -85,12 +87,21 @@ def test_toy_layers_bit_exact(ctx_toy, orc_toy, spec):
 
 
 R18 = {"r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8),
+       # PRCR RAConv over 64 input ciphertexts (PRot-gathered weights, lazy HRotSum), stage-4 CAConv at (8, 8)
+       "r18_L1_ra_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "RA", S=8),
+       "r18_L4_ca_S8": H.ConvSpec(512, 512, 7, 3, 1, 64, 8, 8, 8, "CA", S=8),
        # ResNet-18 stage-4 shortcut: 1x1 stride-2 pconv from plan (4,4) at gap 4 to RA(8,8) at gap 8
        "r18_L4_pconv": H.ConvSpec(256, 512, 14, 1, 2, 64, 4, 4, 4, "CA")}
 
 
+# r18_L1_ra_S8 (64 input ciphertexts through the oracle: ~4 min) runs only with HY_SLOW_TESTS=1; its last run is
+# recorded in profiles/r01_slow_parity.log
+_SLOW = pytest.mark.skipif(os.environ.get("HY_SLOW_TESTS") != "1", reason="slow oracle case (HY_SLOW_TESTS=1)")
+
+
 @pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1]), ("r18_L1_ca_S8", [5]),
-                                          ("r18_L4_pconv", [1])])
+                                          ("r18_L4_pconv", [1]), ("r18_L4_ca_S8", [7]),
+                                          pytest.param("r18_L1_ra_S8", [3], marks=_SLOW)])
 def test_resnet_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
     spec = R20[name] if name in R20 else R18[name]
     level = 9 if spec.algo == "CA" else 6      # l+1 = 10 for CAConv, 7 for RAConv (DESIGN R-LEVELS)
