@@ -748,7 +748,8 @@ def run_ours(args, ws, rank, local):
             "resnet20_blocks": blocks,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches,
+            "gpu_launches": launches * args.steps,  # our kernels launched inside the timed region (K steps)
+            "gpu_launches_per_step": launches,
             "clocks": clocks,
             "hrot_variants": variants,
             "hoisted": {"value": BATCH * ws * 1000.0 / ms_h, "unit": UNIT, "ms_per_step": ms_h,
