@@ -62,7 +62,8 @@ __device__ __forceinline__ uint32_t bitrev32(uint32_t x, int bits) { return __br
 // plaintexts fused into their consumers as a gather.
 __device__ __forceinline__ uint32_t aut_index(uint32_t p, uint64_t k, int logN) {
   uint32_t e = 2 * bitrev32(p, logN) + 1;
-  uint32_t e2 = (uint32_t)(((uint64_t)e * k) & ((2ull << logN) - 1));
+  // only the low logN + 1 bits of e k are needed, so a 32-bit product suffices (k < 2N <= 2^17)
+  uint32_t e2 = (e * (uint32_t)k) & ((2u << logN) - 1);
   return bitrev32((e2 - 1) >> 1, logN);
 }
 
