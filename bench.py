@@ -333,6 +333,66 @@ R18_LAYERS = [
 ]
 
 
+def ks_fp64_ops(level: int, variant: str, alpha: int = 4, kp: int = 4) -> float:
+    """FP64-pipe operations of one key switch at `level` in this implementation's algorithm (DESIGN.md section 5
+    op counting: an NTT pass = 8 stages x N/2 butterflies x 8 ops, a BConv word 7a+2, an IP MAC 7 ops).
+    variant: plain | hoisted (per rotation, the shared ModUp excluded) | modup (the shared ModUp of a hoisted
+    group) | lazy_term (ModUp + IP of one HRotSum term) | moddown (one ModDown with its epilogue)."""
+    n = level + 1
+    E = n + kp
+    P = 8 * (N // 2) * 8
+    digits = [min(alpha, n - j * alpha) for j in range((n + alpha - 1) // alpha)]
+    beta = len(digits)
+    modup = n * P + n * P + sum((E - a) * (P + (7 * a + 2) * N) for a in digits)    # iNTT rows+cols, BConv, NTT cols
+    modup_rows = sum((E - a) * P for a in digits)                                   # the digits' NTT row passes
+    ip = 2 * beta * E * 7 * N
+    moddown = 2 * kp * P + 2 * (kp * P + n * (P + (7 * kp + 2) * N)) + 2 * n * (P + 4 * N)
+    if variant == "plain":
+        return modup + modup_rows + ip + moddown
+    if variant == "hoisted":
+        return ip + moddown
+    if variant == "modup":
+        return modup + modup_rows
+    if variant == "lazy_term":
+        return modup + modup_rows + ip
+    if variant == "moddown":
+        return moddown
+    raise ValueError(variant)
+
+
+def layer_roofline(p, algo: str, level: int, ms: float, kp: int = 4, alpha: int = 4):
+    """Per-layer roofline fractions: HBM -- algorithmic bytes (input cts, the stored weight
+    plaintexts and mask, one read of every distinct evaluation-key slice the layer uses, output cts; intermediates
+    excluded) over the layer time vs MEASURED_PEAKS hbm_gbs; FP64 -- the layer's key switches by variant (CAConv
+    Slide: hoisted groups, RAConv Slide: lazy HRotSum, RaS / RaS_g / IR_g: plain) + PMult terms + rescales, in
+    FP64-pipe ops, vs 148 x 64 x 1.965 GHz."""
+    pk = peaks()
+    n = level + 1
+    out_level = p.out_level(level)
+    beta = (n + alpha - 1) // alpha
+    ct = lambda lv: 2 * (lv + 1) * N * 8  # noqa: E731
+    key_slice = 2 * beta * (n + kp) * N * 6
+    alg = p.n_in * ct(level) + p.n_pt * n * N * 8 + (level * N * 8 if p.has_mask else 0) + \
+        len(p.rots) * key_slice + p.n_out * ct(out_level)
+    c = p.counts
+    lv2 = level - 1  # RaS / RaS_g / IR_g run after the SISO rescale
+    ops = 0.0
+    if algo == "CA":
+        if c["Slide"]:
+            ops += p.n_in * ks_fp64_ops(level, "modup") + c["Slide"] * ks_fp64_ops(level, "hoisted")
+    else:
+        ops += c["Slide"] * ks_fp64_ops(level, "lazy_term") + p.n_out * ks_fp64_ops(level, "moddown")
+    ops += (c["RaS"] + c["RaS_g"] + c["IR_g"]) * ks_fp64_ops(lv2, "plain")
+    ops += c["PMult"] * 2 * n * N * 7
+    resc = 2 * (2 * 8 * (N // 2) * 8 * 2) + 2 * n * (2 * 8 * (N // 2) * 8)  # per rescale: 2 iNTT + 2l NTT limbs
+    ops += (p.n_out + (p.n_out if p.has_mask else 0)) * resc
+    t = ms * 1e-3
+    fp64_peak = 148 * 64 * 1.965e9
+    return {"alg_bytes": alg, "hbm_gbs": alg / t / 1e9, "hbm_frac": alg / t / 1e9 / pk["hbm_gbs"],
+            "fp64_ops": ops, "fp64_tops": ops / t / 1e12, "fp64_frac": ops / t / fp64_peak,
+            "bound": "fp64" if ops / fp64_peak > alg / (pk["hbm_gbs"] * 1e9) else "hbm"}
+
+
 def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet-20"):
     """Per-layer device time of every conv layer type (fresh encryption at its scheduled level,
     outputs sharded over ranks + all-gathered), and the network's conv total."""
@@ -390,6 +450,7 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
                 fams[fn] = round(t, 3)
         ctx.time_kernels(0)
         layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
+                        "roofline": layer_roofline(p, algo, level, ms),
                         "sharding": "taps (all-reduce)" if tap_shard else ("outputs (all-gather)" if ws > 1 else None),
                         "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S,
                         "family_ms": fams}
@@ -460,6 +521,77 @@ def bench_blocks(ctx, ws, rank, steps, warmup, timed):
         torch.cuda.empty_cache()
     return {"blocks": out, "note": "CAConv -> x^2 -> RAConv per stage (Alg. 3, P:739-765), device time; the "
                                    "square is MulCt + relinearization + rescale of the n_o CAConv outputs"}
+
+
+# --------------------------------------------------------------------------- C1 (BASELINE configs[0])
+C1_SPEC = (4, 4, 8, 3, 1, 8, 1, 1, 1, "RA")  # single 3x3 RAConv 4->4, 8x8, N=2^12
+
+
+def bench_c1(device, steps, warmup, timed_fn, with_oracle=True):
+    """BASELINE configs[0]: one 3x3 RAConv 4 -> 4 channels on an 8x8 image, N = 2^12, 3 RNS limbs + 1 special
+    prime (toy set), inputs encrypted at l = 2: device time per layer call, and the CPU oracle's time for the same
+    layer (full oracle, all outputs) on the host cores."""
+    import torch
+
+    import paper_2302_02407_b200 as hy
+    prm = synth.PARAMS["toy"]
+    ctx = hy.Context(**prm, device=device)
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    p = hy.ConvPlan(ctx, *C1_SPEC)
+    level = len(prm["q_bits"]) - 1
+    X = synth.image(1, 4, 8)
+    K = synth.conv_weight(2, 4, 4, 3)
+    scale = 2 ** prm["log_scale"]
+    # the layer's work is data-independent: seeded uniform slots stand in for the packed image on the GPU leg
+    cts = [ctx.encrypt(sk, 900, i, ctx.encode(synth.slots_uniform(40 + i, ctx.n), scale, level), level)
+           for i in range(p.n_in)]
+    evks = [ctx.keygen_rot(sk, ek, r) for r in p.rots]
+    pts = p.encode_weights(K, level)
+    scratch = p.scratch(level)
+    outs = [ctx.empty(*ctx.ct_shape(p.out_level(level)))]
+    ms, launches = timed_fn(lambda: p.run(evks, cts, level, pts, scratch, 0, 1, outs), steps, warmup)
+    torch.cuda.synchronize()
+    res = {"workload": "C1: 3x3 RAConv 4->4, 8x8, N=2^12, 3 limbs + 1 special prime, l = 2 (BASELINE configs[0])",
+           "ms": ms, "gpu_launches": launches, "rotations": p.counts, "n_in": p.n_in, "n_out": p.n_out}
+    if with_oracle:  # the cpu_baseline leg: the oracle's encrypted execution of the same layer
+        import oracle
+        from oracle import hyphen as H
+        o = oracle.Oracle(**prm)
+        plan = H.plan_raconv(H.ConvSpec(*C1_SPEC, n=o.n), K)
+        octs = [o.encrypt(sk, 900, i, o.encode(v, scale, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+        oevks = {r: o.keygen_rot(sk, ek, r) for r in H.rotation_amounts(plan, o.n)}
+        enc = H.EncConv(o, plan, oevks)
+        enc.run(octs)  # warm (weight encoding cache)
+        t0 = time.perf_counter()
+        n_rep = 3
+        for _ in range(n_rep):
+            enc.run(octs)
+        res["oracle_ms"] = 1000.0 * (time.perf_counter() - t0) / n_rep
+        res["oracle_cores"] = os.cpu_count()
+        res["oracle_over_gpu"] = res["oracle_ms"] / ms
+    del ctx
+    return res
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_rate_threads(n_rot: int, threads: int):
+    """oracle_keyswitch_rate in a fresh process with OMP_NUM_THREADS = threads (the C oracle's OpenMP pool is
+    sized when the library loads)."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    code = ("import json, bench; r, dt = bench.oracle_keyswitch_rate(%d); print(json.dumps([r, dt]))" % n_rot)
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=900)
+    r, dt = json.loads(out.stdout.strip().splitlines()[-1])
+    return r, dt
 
 
 # --------------------------------------------------------------------------- our arm
@@ -573,34 +705,66 @@ def run_ours(args, ws, rank, local):
     ctx.time_kernels(0)
     dominant = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
     pk = peaks()
+    alpha, kp = 4, 4
+    n_l = LEVEL + 1
+    E = n_l + kp
+    digits = [min(alpha, n_l - j * alpha) for j in range((n_l + alpha - 1) // alpha)]
+    # SURVEY 8(d).2 algorithmic bytes of one rotation: ct in + the evaluation-key slice it reads + ct out;
+    # intermediates (extended digits, partial sums, conversion rows) excluded.  The key is stored 6 bytes per
+    # word; frac_8byte_key_equiv counts it at the paper's 8 bytes per word (168 MB).
+    ct_bytes = 2 * n_l * N * 8
+    key_slice = 2 * len(digits) * E * N * 6
+    key_slice8 = 2 * len(digits) * E * N * 8
+    alg_rot = {"plain": (2 * ct_bytes + key_slice, 2 * ct_bytes + key_slice8),
+               "hoisted": (ct_bytes + key_slice + ct_bytes / BATCH, ct_bytes + key_slice8 + ct_bytes / BATCH)}
 
-    def hbm_roof(fam_name):
-        d = breakdown[fam_name]
-        achieved = d["alg_bytes_per_launch"] / (d["avg_us"] * 1e-6) / 1e9
+    def ncu_step_bytes(fam_name):
+        t = ncu_traffic(fam_name)
+        if t is None:
+            return None
+        # the capture summary holds the per-launch average of the family's kernels
+        return t["bytes_per_launch"] * breakdown[fam_name]["launches_per_step"]
+
+    def hbm_roof(fam_name, variant="plain", bd=None):
+        bd = bd or breakdown
+        d = bd[fam_name]
+        alg, alg8 = (BATCH * x for x in alg_rot[variant])
+        t_s = d["ms_per_step"] * 1e-3
+        achieved = alg / t_s / 1e9
+        model = d["alg_bytes_per_launch"] * d["launches_per_step"] / t_s / 1e9
+        tr = ncu_step_bytes(fam_name) if bd is breakdown else None
         return {"bound": "hbm", "kernel_family": fam_name, "achieved": achieved, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], **traffic_fields(fam_name),
+                "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                "frac_8byte_key_equiv": alg8 / t_s / 1e9 / pk["hbm_gbs"],
+                "alg_bytes_per_launch": alg / d["launches_per_step"],
+                "alg_bytes_def": "SURVEY 8(d).2: (ct in + key slice read + ct out) per rotation x 64 rotations per "
+                                 "step, attributed to this family's launches (intermediates excluded)",
+                "dram_model_gbs": model,
+                "dram_model_note": "the same launches' modelled DRAM bytes including intermediates (extended "
+                                   "digits, conversion rows) over their time: achieved DRAM rate, not the roofline",
+                **traffic_fields(fam_name),
+                "traffic_over_alg": None if tr is None else tr / alg,
                 "share_of_step": d["ms_per_step"] / ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
 
     fp64_peak = 148 * 64 * 1.965e9 / 1e12  # FP64 lanes x SMs x max clock (B200 unit counts)
 
-    def alu_roof(fam_name, ops_per_launch, what):
-        d = breakdown[fam_name]
+    def alu_roof(fam_name, ops_per_launch, what, bd=None):
+        d = (bd or breakdown)[fam_name]
         achieved = ops_per_launch / (d["avg_us"] * 1e-6) / 1e12
+        tr = ncu_step_bytes(fam_name) if bd is None else None
         return {"bound": "alu", "kernel_family": fam_name, "achieved": achieved, "peak": fp64_peak,
                 "unit": "TFP64op/s", "frac": achieved / fp64_peak, **traffic_fields(fam_name),
+                "traffic_over_model": None if tr is None else tr / (d["alg_bytes_per_launch"] * d["launches_per_step"]),
                 "share_of_step": d["ms_per_step"] / ms, "work": what,
                 "peak_source": "148 SM x 64 FP64 lanes x 1.965 GHz (DESIGN.md section 5); one DFMA/DMUL/DADD = 1 op"}
 
     # algorithmic FP64-pipe work: an NTT column / row pass = 8 stages x N/2
     # butterflies x 8 ops (fmulmod 6 + add + sub); a fast-BConv output word = alpha fmulmods + alpha-1 adds
     # + one fred (3 ops) = 7 alpha + 2
-    alpha, kp = 4, 4
-    n_l = LEVEL + 1
-    E = n_l + kp
-    digits = [min(alpha, n_l - j * alpha) for j in range((n_l + alpha - 1) // alpha)]
     pass_ops = 8 * (N // 2) * 8
     modup_item = n_l * pass_ops + sum((E - a) * (pass_ops + N * (7 * a + 2)) for a in digits)
+    moddown_item = 2 * (kp * pass_ops + n_l * (pass_ops + N * (7 * kp + 2)))
     roofs = {}
     if "modup" in breakdown:
         items = BATCH // breakdown["modup"]["launches_per_step"]
@@ -609,7 +773,6 @@ def run_ours(args, ws, rank, local):
                                   "(BConv word + forward column pass), per item")
     if "moddown" in breakdown:  # the fused ModDown column kernel
         items = BATCH // breakdown["moddown"]["launches_per_step"]
-        moddown_item = 2 * (kp * pass_ops + n_l * (pass_ops + N * (7 * kp + 2)))
         roofs["moddown"] = alu_roof("moddown", items * moddown_item,
                                     "fused ModDown columns: per poly K inverse column passes + (l+1) x (BConv word "
                                     "+ forward column pass), per item")
@@ -621,21 +784,26 @@ def run_ours(args, ws, rank, local):
             limbs = breakdown[f]["alg_bytes_per_launch"] / (2 * N * 8)
             roofs[f] = alu_roof(f, limbs * pass_ops, "NTT pass: 8 stages x N/2 butterflies x 8 ops per limb")
     roof = roofs.get(dominant) or hbm_roof(dominant)
+    # the hoisted batch's dominant family on the same definitions
+    roofs_hoisted = {}
+    if "ntt_ip" in breakdown_h:
+        roofs_hoisted["ntt_ip"] = hbm_roof("ntt_ip", "hoisted", breakdown_h)
+    if "moddown" in breakdown_h:
+        items = BATCH // breakdown_h["moddown"]["launches_per_step"]
+        roofs_hoisted["moddown"] = alu_roof("moddown", items * moddown_item, "fused ModDown columns", breakdown_h)
     # whole-HRot HBM fraction (the metric's "HBM GB/s vs peak"): the bytes a rotation must move -- input ct,
     # its evaluation key, output ct -- over the measured time per rotation (north_star target >= 60 %)
-    ct_bytes = 2 * n_l * N * 8
-    evk_bytes = 2 * len(digits) * E * N * 6  # the key slice a rotation reads, 6-byte packed words
     hrot_hbm = {}
-    for name_, t_ms, moved in (("plain", ms, 2 * ct_bytes + evk_bytes), ("hoisted", ms_h, ct_bytes + evk_bytes)):
+    for name_, t_ms in (("plain", ms), ("hoisted", ms_h)):
+        moved, moved8 = alg_rot[name_]
         gbs = moved * BATCH / (t_ms * 1e-3) / 1e9
-        # the same rotation rate with the key counted at 8 bytes per word (the paper's 168 MB key)
-        moved8 = moved + 2 * len(digits) * E * N * 2
         hrot_hbm[name_] = {"alg_bytes_per_rotation": moved, "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                            "frac": gbs / pk["hbm_gbs"],
                            "frac_8byte_key_equiv": moved8 * BATCH / (t_ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
-    hrot_hbm["note"] = ("plain: ct in + evk (6-byte packed words) + ct out per rotation; hoisted: the shared input is read once per batch, "
-                        "so evk + ct out; the FP64-pipe NTT/BConv work bounds plain HRot below the HBM roofline "
-                        "(DESIGN.md section 5)")
+    hrot_hbm["note"] = ("plain: ct in + evk (6-byte packed words) + ct out per rotation; hoisted: the shared input is "
+                        "read once per batch, so evk + ct out; frac_8byte_key_equiv counts the key at 8 bytes per "
+                        "word (the paper's 168 MB key); the FP64-pipe NTT/BConv work bounds plain HRot below the HBM "
+                        "roofline (DESIGN.md section 5)")
     ntt_ms = sum(breakdown[k]["ms_per_step"] for k in ("ntt_a", "ntt_b") if k in breakdown)
 
     # e2e through the public API with host buffers: pinned H2D of the 64 input cts, D2H of the outputs
@@ -713,11 +881,23 @@ def run_ours(args, ws, rank, local):
         conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18")
         blocks = bench_blocks(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
 
+    c1 = None
+    if not args.no_c1:
+        c1 = bench_c1(local, max(3, args.steps), 2, timed, with_oracle=ws == 1 and not args.no_cpu_baseline)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, dt = oracle_keyswitch_rate(args.cpu_rotations)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{args.cpu_rotations} plain HRot(s) at full level (Set_hyp, N=2^16), {dt:.1f} s"}
+        nproc = os.cpu_count()
+        rate, dt = oracle_rate_threads(args.cpu_rotations, nproc)
+        rate1, dt1 = oracle_rate_threads(max(1, args.cpu_rotations // 15), 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": nproc, "kind": "oracle", "cpu_model": cpu_model(),
+               "sample": f"{args.cpu_rotations} plain HRot(s) at full level (Set_hyp, N=2^16), {dt:.1f} s, "
+                         f"OMP_NUM_THREADS={nproc}",
+               "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                              "sample": f"{max(1, args.cpu_rotations // 15)} plain HRot(s), {dt1:.1f} s, "
+                                        "OMP_NUM_THREADS=1"}}
+        if c1 is not None:
+            cpu["c1"] = {"oracle_ms": c1.get("oracle_ms"), "gpu_ms": c1["ms"], "cores": nproc}
         if conv is not None:  # the same ResNet-20 layers, whole, through the oracle beside the GPU times
             lay = oracle_conv_layers()
             for nm, x in lay.items():
@@ -742,10 +922,12 @@ def run_ours(args, ws, rank, local):
                        "l2": "inputs larger than L2 (64 x 126 MiB packed evaluation keys streamed per step)"},
             "roofline": roof,
             "roofline_families": roofs,
+            "roofline_hoisted": roofs_hoisted,
             "hrot_hbm": hrot_hbm,
             "resnet20_conv": conv,
             "resnet18_conv": conv18,
             "resnet20_blocks": blocks,
+            "c1_raconv": c1,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,  # our kernels launched inside the timed region (K steps)
@@ -773,6 +955,7 @@ def main():
     ap.add_argument("--no-conv", action="store_true", help="skip the ResNet-20 / ResNet-18 conv-layer timings")
     ap.add_argument("--no-r18", action="store_true", help="skip the ResNet-18 (PRCR) conv-layer timings")
     ap.add_argument("--no-variants", action="store_true", help="skip the HRot variant x level table")
+    ap.add_argument("--no-c1", action="store_true", help="skip the BASELINE configs[0] RAConv timing")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":

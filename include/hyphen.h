@@ -65,7 +65,8 @@ typedef enum {
   HY_E_MISSING_KEY = 8,     /* no evaluation key given for a needed rotation */
   HY_E_CUDA = 9,            /* CUDA runtime error */
   HY_E_WORKSPACE = 10,      /* workspace missing or too small */
-  HY_E_NO_DEVICE = 11       /* no usable sm_100 device */
+  HY_E_NO_DEVICE = 11,      /* no usable sm_100 device */
+  HY_E_SCALE_MISMATCH = 12  /* operand scales differ (SPEC: AddCt / AddPt need equal scales) */
 } hy_status;
 
 typedef struct hy_ctx hy_ctx;
@@ -73,11 +74,12 @@ typedef struct hy_ctx hy_ctx;
 typedef struct {
   uint32_t log_n;          /* N = 2^log_n, 10 <= log_n <= 16 */
   uint32_t n_q;            /* L+1 ciphertext primes (Set_hyp: 24) */
-  uint32_t n_p;            /* K special primes (>= alpha) */
+  uint32_t n_p;            /* K special primes, alpha <= K <= 8 (checked: HY_E_ARG) */
   uint32_t dnum;           /* key-switching digits (Set_hyp: 6) */
   uint32_t hamming_weight; /* secret key weight (192) */
-  const uint32_t* q_bits;  /* n_q bit sizes (< 62) */
-  const uint32_t* p_bits;  /* n_p bit sizes (< 62) */
+  const uint32_t* q_bits;  /* n_q bit sizes, each in [20, 48] (DESIGN R-PRIMES: residues are exact doubles for
+                              the FP64-pipe arithmetic, R-FP64; checked: HY_E_ARG) */
+  const uint32_t* p_bits;  /* n_p bit sizes, each in [20, 48] */
 } hy_params;
 
 /* ---- context ---------------------------------------------------------- */
@@ -89,6 +91,10 @@ hy_status hy_ctx_create(const hy_params* params, int cuda_device, hy_ctx** out);
 void hy_ctx_destroy(hy_ctx* ctx);
 /* chain moduli: n_q + n_p words (host) */
 hy_status hy_ctx_moduli(const hy_ctx* ctx, uint64_t* out);
+/* Device bytes of a ciphertext [2][l+1][N] / a plaintext [l+1][N] at level l (with_p: [l+1+K][N], the
+ * extended basis Q_l u P); 0 for a NULL context or l >= n_q. */
+size_t hy_ct_bytes(const hy_ctx* ctx, uint32_t level);
+size_t hy_pt_bytes(const hy_ctx* ctx, uint32_t level, int with_p);
 uint32_t hy_ctx_alpha(const hy_ctx* ctx);
 uint32_t hy_ctx_n_digits(const hy_ctx* ctx, uint32_t level); /* beta = ceil((l+1)/alpha) */
 /* Bytes of workspace the context needs to run every operation up to level max_level
@@ -150,7 +156,9 @@ hy_status hy_moddown(hy_ctx* ctx, uint32_t level, const uint64_t* d_u, uint64_t*
 /* plain: ModUp(kappa(c1)).  r = 0 (mod n) copies the input. */
 hy_status hy_hrot(hy_ctx* ctx, const uint64_t* d_evk, const uint64_t* d_ct, uint32_t level, int32_t r,
                   uint64_t* d_out, void* stream);
-/* non-hoisted batch: out_i = HRot_{r_i}(ct_i) with key evk_i (host arrays of device pointers) */
+/* non-hoisted batch: out_i = HRot_{r_i}(ct_i) with key evk_i (host arrays of device pointers).  No output may
+ * overlap any input of the batch (the items run in key-switch chunks and r = 0 items are copied first):
+ * HY_E_ARG.  Items sharing a key pointer stream it from HBM once per chunk. */
 hy_status hy_hrot_batch(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* const* d_cts, uint32_t level,
                         const int32_t* r, uint32_t n, uint64_t* const* d_outs, void* stream);
 /* hoisted (Slide_f): one ModUp of c1 shared by n rotations of the same ciphertext. */
@@ -185,6 +193,11 @@ hy_status hy_pmult_acc(hy_ctx* ctx, const uint64_t* const* d_cts, const uint64_t
 /* out = a + b over npoly polynomials ([npoly][l+1][N]); in-place allowed. */
 hy_status hy_add(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t npoly, uint32_t level,
                  uint64_t* d_out, void* stream);
+/* AddPt ("AddPt 0.169 ms" P:148; the conv bias): out = (c0 + pt, c1) at level l, [2][l+1][N] and
+ * [l+1][N]; in-place allowed (out == ct).  The scales are the caller's bookkeeping (the ABI carries none): they
+ * must agree to 2^-30 relative, else HY_E_SCALE_MISMATCH (SPEC add_ct / add_pt); the output has ct_scale. */
+hy_status hy_add_pt(hy_ctx* ctx, const uint64_t* d_ct, double ct_scale, const uint64_t* d_pt, double pt_scale,
+                    uint32_t level, uint64_t* d_out, void* stream);
 /* Level alignment (SPEC level_down; P:102-112 levels): [2][l+1][N] -> [2][l'+1][N], l' <= l, by dropping the
  * limbs above l' (reduction mod Q_l'); scale unchanged, no rounding.  out must not alias ct unless l' == l.
  * Errors: HY_E_ARG, HY_E_LEVEL_MISMATCH (l' > l). */
@@ -218,6 +231,9 @@ typedef struct {
                         segment G (F = wp^2/S slots) rows of channel k c_n S m + ((G + im) mod c_n S) m + mu;
                         one weight plaintext per family, used as PRot(P, shift); needs S | wp/gap,
                         e = 1, stride 1, wp/gap >= w + (f-1)/2; adds an output-valid mask step. */
+  uint32_t bias;     /* 1: the layer adds a per-output-channel bias b (Y = conv2d(X, K) + b; BN biases fused into
+                        the conv): AddPt of the output format's packing of b after the layer's last
+                        rescale, at the output level and scale (DESIGN R-BIAS). 0 = none. */
 } hy_conv_spec;
 typedef struct hy_conv_plan hy_conv_plan;
 /* Rotation amounts, weight/mask plaintext contents and counts for one layer.  Errors:
@@ -235,16 +251,23 @@ hy_status hy_conv_plan_query(const hy_conv_plan* plan, uint32_t* n_in, uint32_t*
 /* Slot values (host, N/2 doubles) of weight plaintext idx < n_pt, or of the mask (idx == n_pt).
  * K: host [co][ci][f][f] float64. */
 hy_status hy_conv_weight_slots(const hy_conv_plan* plan, const double* K, uint32_t idx, double* slots);
-/* Device words of the encoded weights at input level l: n_pt x [l+1][N] then the mask [l][N]. */
+/* Slot values (host, N/2 doubles) of the bias plaintext of output ciphertext out_index < n_out: b[c] at every
+ * valid slot of output channel c in the output format (every replica), 0 elsewhere.  bias: host [co]. */
+hy_status hy_conv_bias_slots(const hy_conv_plan* plan, const double* bias, uint32_t out_index, double* slots);
+/* Device words of the encoded weights at input level l: n_pt x [l+1][N], then the mask [l][N] (has_mask), then
+ * (spec.bias) n_out bias plaintexts [l_out+1][N] at the output level l_out = l - 1 - has_mask. */
 size_t hy_conv_weight_words(const hy_ctx* ctx, const hy_conv_plan* plan, uint32_t level);
 /* Device scratch words hy_caconv / hy_raconv need at input level l. */
 size_t hy_conv_scratch_words(const hy_ctx* ctx, const hy_conv_plan* plan, uint32_t level);
 /* Encode every weight plaintext at scale q_l (level l) and the mask at scale q_{l-1} (level
- * l-1), so each rescale returns the ciphertext scale exactly (DESIGN R-SCALE). */
-hy_status hy_conv_encode_weights(hy_ctx* ctx, const hy_conv_plan* plan, const double* K, uint32_t level,
-                                 uint64_t* d_pts, void* stream);
+ * l-1), so each rescale returns the ciphertext scale exactly (DESIGN R-SCALE); with spec.bias, the n_out bias
+ * plaintexts at level l_out and scale bias_scale (the exact integer scale of the layer's input ciphertexts, which
+ * every rescale returns to).  K: host [co][ci][f][f]; bias: host [co] (NULL iff spec.bias == 0).
+ * Errors: HY_E_ARG (null, bias missing), HY_E_LEVEL_EXHAUSTED, HY_E_PLAN, HY_E_WORKSPACE. */
+hy_status hy_conv_encode_weights(hy_ctx* ctx, const hy_conv_plan* plan, const double* K, const double* bias,
+                                 uint64_t bias_scale, uint32_t level, uint64_t* d_pts, void* stream);
 /* Run the layer on n_in input ciphertexts at level l, producing outputs [out_begin, out_end)
- * (the multi-GPU shard) at level l - 1 - has_mask.  d_evks: one key per rotation amount in
+ * (the multi-GPU shard) at level l - 1 - has_mask (plus the bias AddPt when spec.bias).  d_evks: one key per rotation amount in
  * hy_conv_plan_query order.  Outputs must not alias inputs.  HY_E_PLAN when the plan's algo
  * does not match the call. */
 hy_status hy_caconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
@@ -325,6 +348,15 @@ hy_status hy_pt_from_coeffs(hy_ctx* ctx, const int64_t* h_coeffs, uint32_t level
  * Errors: HY_E_ARG (null, level, scale <= 0), HY_E_CAPACITY (n_slots > N/2), HY_E_WORKSPACE. */
 hy_status hy_decode(hy_ctx* ctx, const uint64_t* d_pt, uint32_t level, double scale, uint32_t n_slots,
                     double* h_re, double* h_im, void* stream);
+/* Coefficient-domain wire format (parity dumps independent of the NTT order): n_limbs limbs
+ * [n_limbs][N], limb u on chain index chain[u] (host array; q_0.. then p_0..).  Export: NTT-domain device limbs
+ * -> coefficient-domain host limbs in [0, q) (an inverse NTT on the device into the workspace, then a copy;
+ * synchronous).  Import: the reverse (host coefficients in [0, q) -> NTT-domain device limbs).  Errors: HY_E_ARG
+ * (null, chain index >= n_q + n_p, import word >= its modulus), HY_E_WORKSPACE. */
+hy_status hy_export_coeff(hy_ctx* ctx, const uint64_t* d_ntt, const uint32_t* chain, uint32_t n_limbs,
+                          uint64_t* h_coeff, void* stream);
+hy_status hy_import_coeff(hy_ctx* ctx, const uint64_t* h_coeff, const uint32_t* chain, uint32_t n_limbs,
+                          uint64_t* d_ntt, void* stream);
 /* Host-only part of hy_decode: real coefficients (host, N doubles) -> slots. */
 hy_status hy_decode_coeffs(uint32_t log_n, const double* h_coeffs, double scale, uint32_t n_slots, double* h_re,
                            double* h_im);

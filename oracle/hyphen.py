@@ -387,8 +387,25 @@ def rot(v, r):
     return np.roll(v, -r)
 
 
-def simulate(plan: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
-    """Run the plan on cleartext slot vectors (exact rotations, float products)."""
+def bias_slots(plan: Plan, bias) -> list[np.ndarray]:
+    """The layer's bias as output-format slot vectors (DESIGN R-BIAS; "BN fused into the conv"): the
+    packing, in the output format, of the image B[c][h][w] = b[c] over the wo x wo output pixels.  Adding it to
+    the conv's output ciphertexts (AddPt) turns conv2d(X, K) into conv2d(X, K) + b at every valid slot."""
+    sp = plan.spec
+    B = np.broadcast_to(np.asarray(bias, np.float64)[:, None, None], (sp.co, sp.wo, sp.wo))
+    vs = pack(np.ascontiguousarray(B), plan.fout)
+    return vs + [np.zeros(plan.fout.n)] * max(0, plan.n_out - len(vs))
+
+
+def simulate(plan: Plan, xs: list[np.ndarray], bias=None) -> list[np.ndarray]:
+    """Run the plan on cleartext slot vectors (exact rotations, float products); bias: added after the layer."""
+    outs = _simulate(plan, xs)
+    if bias is not None:
+        outs = [v + b for v, b in zip(outs, bias_slots(plan, bias))]
+    return outs
+
+
+def _simulate(plan: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
     sp = plan.spec
     if sp.algo == "CA":
         slid = [[rot(x, r) for r in plan.taps] for x in xs]       # Slide_f per input (hoisted)
@@ -441,8 +458,10 @@ class EncConv:
     level they are consumed at and masks at q_{l-1}, so each rescale returns the scale to
     the ciphertext scale exactly (DESIGN R-SCALE).  evks: rotation amount -> key."""
 
-    def __init__(self, o, plan: Plan, evks: dict):
-        self.o, self.plan, self.evks = o, plan, evks
+    def __init__(self, o, plan: Plan, evks: dict, bias=None):
+        """bias: optional per-output-channel bias [co], added by AddPt after the layer's last rescale at the
+        output ciphertext's level and scale (DESIGN R-BIAS)."""
+        self.o, self.plan, self.evks, self.bias = o, plan, evks, bias
 
     def key(self, r):
         r %= self.o.n
@@ -480,9 +499,20 @@ class EncConv:
 
     def run(self, cts, outputs=None):
         """outputs: optional list of output ciphertext indices to compute (sampling); default all."""
+        outs_wanted = list(range(self.plan.n_out)) if outputs is None else list(outputs)
+        outs = self._run(cts, outs_wanted)
+        if self.bias is None:
+            return outs
+        bs = bias_slots(self.plan, self.bias)
+        res = []
+        for j, c in zip(outs_wanted, outs):
+            pt = self.o.encode(bs[j], int(round(c.scale)), c.level)
+            res.append(self.o.add_pt(c, pt))
+        return res
+
+    def _run(self, cts, outs_wanted):
         o, p, sp = self.o, self.plan, self.plan.spec
         level = cts[0].level
-        outs_wanted = list(range(p.n_out)) if outputs is None else list(outputs)
         if sp.algo == "CA":
             grp = set(outs_wanted) if sp.s == 1 else {g for J in outs_wanted for g in (2 * J, 2 * J + 1)}
         else:

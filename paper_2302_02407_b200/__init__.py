@@ -38,7 +38,7 @@ class _Params(C.Structure):
 
 class _ConvSpec(C.Structure):
     _fields_ = [(k, C.c_uint32) for k in ("ci", "co", "w", "f", "stride", "wp", "gap", "m", "d", "algo",
-                                          "segments")]
+                                          "segments", "bias")]
 
 
 _lib = None
@@ -101,7 +101,14 @@ SIGNATURES = {
     "hy_conv_weight_slots": (C.c_int, [_P, C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
     "hy_conv_weight_words": (C.c_size_t, [_P, _P, _U32]),
     "hy_conv_scratch_words": (C.c_size_t, [_P, _P, _U32]),
-    "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), _U32, _P, _P]),
+    "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double), _U64, _U32, _P,
+                                         _P]),
+    "hy_conv_bias_slots": (C.c_int, [_P, C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
+    "hy_add_pt": (C.c_int, [_P, _P, C.c_double, _P, C.c_double, _U32, _P, _P]),
+    "hy_ct_bytes": (C.c_size_t, [_P, _U32]),
+    "hy_pt_bytes": (C.c_size_t, [_P, _U32, C.c_int]),
+    "hy_export_coeff": (C.c_int, [_P, _P, C.POINTER(_U32), _U32, C.POINTER(_U64), _P]),
+    "hy_import_coeff": (C.c_int, [_P, C.POINTER(_U64), C.POINTER(_U32), _U32, _P, _P]),
     "hy_caconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
     "hy_raconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
     "hy_raconv_partial_words": (C.c_size_t, [_P, _U32]),
@@ -412,6 +419,36 @@ class Context:
                                self._stream()))
         return re + 1j * im
 
+    def add_pt(self, ct, ct_scale, pt, pt_scale, level, out=None):
+        """AddPt (hy_add_pt): (c0 + pt, c1); HY_E_SCALE_MISMATCH when the scales differ."""
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_add_pt(self._c, _ptr(ct), float(ct_scale), _ptr(pt), float(pt_scale), level, _ptr(out),
+                               self._stream()))
+        return out
+
+    def ct_bytes(self, level):
+        return int(lib().hy_ct_bytes(self._c, level))
+
+    def pt_bytes(self, level, with_p=False):
+        return int(lib().hy_pt_bytes(self._c, level, int(with_p)))
+
+    def export_coeff(self, x, chain):
+        """NTT-domain device limbs [len(chain)][N] -> coefficient-domain host uint64 array (hy_export_coeff)"""
+        ch = (_U32 * len(chain))(*chain)
+        out = np.empty((len(chain), self.N), np.uint64)
+        _check(lib().hy_export_coeff(self._c, _ptr(x), ch, len(chain), out.ctypes.data_as(C.POINTER(_U64)),
+                                     self._stream()))
+        return out
+
+    def import_coeff(self, a, chain, out=None):
+        """coefficient-domain host limbs -> NTT-domain device limbs (hy_import_coeff)"""
+        a = np.ascontiguousarray(a, np.uint64).reshape(len(chain), self.N)
+        ch = (_U32 * len(chain))(*chain)
+        out = self.empty(len(chain), self.N) if out is None else out
+        _check(lib().hy_import_coeff(self._c, a.ctypes.data_as(C.POINTER(_U64)), ch, len(chain), _ptr(out),
+                                     self._stream()))
+        return out
+
     def pt_from_coeffs(self, coeffs, level, out=None):
         out = self.empty(level + 1, self.N) if out is None else out
         cf = np.ascontiguousarray(coeffs, np.int64)
@@ -425,12 +462,14 @@ class ConvPlan:
 
     CA, RA = 0, 1
 
-    def __init__(self, ctx, ci, co, w, f, stride, wp, gap, m, d, algo, log_n=None, S=1):
-        """ctx may be None (host-only plan inspection) when log_n is given."""
+    def __init__(self, ctx, ci, co, w, f, stride, wp, gap, m, d, algo, log_n=None, S=1, bias=False):
+        """ctx may be None (host-only plan inspection) when log_n is given.  bias: the layer adds a per-output-
+        channel bias (AddPt after its last rescale, DESIGN R-BIAS)."""
         self.ctx = ctx
         self.n = 1 << ((log_n if log_n is not None else ctx.log_n) - 1)
         self.algo = {"CA": 0, "RA": 1}.get(algo, algo)
-        spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo, S)
+        self.bias = bool(bias)
+        spec = _ConvSpec(ci, co, w, f, stride, wp, gap, m, d, self.algo, S, int(self.bias))
         h = C.c_void_p()
         self._lib = lib()
         _check(self._lib.hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
@@ -458,15 +497,28 @@ class ConvPlan:
                                           out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    def bias_slots(self, b, idx):
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.zeros(self.n)
+        _check(lib().hy_conv_bias_slots(self._p, b.ctypes.data_as(C.POINTER(C.c_double)), idx,
+                                        out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def out_level(self, level):
         return level - 1 - int(self.has_mask)
 
-    def encode_weights(self, K, level):
+    def encode_weights(self, K, level, bias=None, bias_scale=0):
+        """weights (and mask) at `level`; with a bias plan, the bias plaintexts at the output level and scale
+        bias_scale (the layer's ciphertext scale, an integer)."""
         words = int(lib().hy_conv_weight_words(self.ctx._c, self._p, level))
-        pts = self.ctx.empty(words)
+        pts = self.ctx.empty(max(words, 1))
         K = np.ascontiguousarray(K, np.float64)
-        _check(lib().hy_conv_encode_weights(self.ctx._c, self._p, K.ctypes.data_as(C.POINTER(C.c_double)), level,
-                                            _ptr(pts), self.ctx._stream()))
+        bp = None
+        if bias is not None:
+            b = np.ascontiguousarray(bias, np.float64)
+            bp = b.ctypes.data_as(C.POINTER(C.c_double))
+        _check(lib().hy_conv_encode_weights(self.ctx._c, self._p, K.ctypes.data_as(C.POINTER(C.c_double)), bp,
+                                            int(bias_scale), level, _ptr(pts), self.ctx._stream()))
         return pts
 
     def scratch(self, level):

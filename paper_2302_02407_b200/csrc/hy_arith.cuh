@@ -1,9 +1,10 @@
-// hy_arith.cuh -- 64-bit modular arithmetic on the integer pipes (sm_100a).
+// hy_arith.cuh -- modular arithmetic of the product path (sm_100a).
 //
-// All moduli are < 2^62.  Shoup multiplication by a precomputed constant w
-// (w' = floor(w * 2^64 / q)) is the workhorse of the NTT and of every
-// basis-conversion constant; products of two variables (key-switch inner
-// product, PMult) are accumulated in 128 bits and reduced once.
+// Every prime is < 2^48 (DESIGN R-PRIMES), so residues are exact doubles and the hot
+// kernels (NTT, BConv, key-switch inner product, ModDown, PMult) run on B200's full-rate
+// FP64 pipe with the six-operation fmulmod below (DESIGN R-FP64).  The 64-bit integer
+// helpers (Shoup / Barrett / 128-bit accumulation) serve the cold paths: key generation,
+// encryption, decryption and the 48-bit wire-format conversions.
 #pragma once
 #include <stdint.h>
 
@@ -81,8 +82,11 @@ __device__ __forceinline__ double u2d(uint64_t v) {  // v < 2^52
 __device__ __forceinline__ uint64_t d2u(double d) {  // d integer in [0, 2^52)
   return (uint64_t)__double_as_longlong(d + kTwo52) & 0xFFFFFFFFFFFFFull;
 }
-// b*w mod q as an integer-valued double r with |r| <= 1.5 q, for |b| <= 16 q, 0 <= w < q < 2^48:
-// h + l = b*w exactly (FMA error term), c = rint(h/q), r = (h - c q) + l, every step exact.
+// b*w mod q as an integer-valued double r, for 0 <= w < q < 2^48 and |b * w / q| < 2^51 (the magic-rounding
+// range; |b| < 2^51 suffices): h + l = b*w exactly (FMA error term), c = rint(fl(h * qinv)), r = (h - c q) + l,
+// every step exact, and |r| <= q/2 + |b| q 2^-52 (c is off round(h/q) by at most |h/q| 2^-53 and |l| <= |h| 2^-53).
+// For the 48-bit primes that is |r| <= (1/2 + beta/16) q for |b| <= beta q; DESIGN R-FP64 derives from it the
+// growth bound of the unreduced forward passes (largest operand 6.62 q < 2^51, tests/test_fp64_bound_cpu.py).
 __device__ __forceinline__ double fmulmod(double b, double w, double q, double qinv) {
   const double h = b * w;
   const double l = fma(b, w, -h);

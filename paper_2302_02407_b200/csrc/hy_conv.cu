@@ -79,6 +79,7 @@ struct hy_conv_plan {
   int64_t n_in, n_groups, n_out;
   std::vector<int64_t> ras, ras_g, ir_g;
   bool has_mask = false, has_combine = false;
+  bool has_bias = false;  // AddPt of a per-output-channel bias after the layer (DESIGN R-BIAS)
   int64_t combine = 0;
   std::vector<int64_t> rots;  // distinct nonzero rotation amounts mod n (key order)
   uint32_t counts[5] = {0, 0, 0, 0, 0};
@@ -88,6 +89,11 @@ struct hy_conv_plan {
   int64_t n_w_in() const { return s.algo == HY_CONV_CA ? n_in / S : n_in; }
   int64_t n_w_grp() const { return s.algo == HY_CONV_CA ? n_groups : n_groups / S; }
   int64_t n_pt() const { return n_w_grp() * n_w_in() * f2(); }
+  // device words of the weight buffer before the bias plaintexts: n_pt x [l+1][N], then the mask [l][N]
+  size_t bias_offset(uint32_t level, size_t N) const {
+    return ((size_t)n_pt() * (level + 1) + (has_mask ? level : 0)) * N;
+  }
+  uint32_t out_level(uint32_t level) const { return level - 1 - (has_mask ? 1 : 0); }
   // (stored plaintext index, PRot amount) of term (group/output grp, input ct i, tap t):
   // PRCR shares one plaintext per family, member im using PRot(P, r_t + im F) on the CA input
   // side and PRot(P, im F - r_t) on the RA output side (DESIGN R-PRCR)
@@ -185,6 +191,17 @@ void weight_slots(const hy_conv_plan& p, const double* K, int64_t idx, double* v
   }
 }
 
+// bias slot vector of output ciphertext j: b[c] at every valid slot (pixel inside the wo x wo output, every
+// replica) of output channel c in the layer's output format, 0 elsewhere -- the output format's packing of the
+// image B[c][h][w] = b[c] (DESIGN R-BIAS), so AddPt of it adds the conv bias of Y = conv2d(X, K) + b
+void bias_slots(const hy_conv_plan& p, const double* bias, int64_t j, double* v) {
+  for (int64_t x = 0; x < p.n; ++x) {
+    const Layout::Pos q = p.out.at(x);
+    const int64_t c = p.out.channel(j, q, x);
+    v[x] = (q.h < p.wo && q.w < p.wo && c < (int64_t)p.s.co) ? bias[c] : 0.0;
+  }
+}
+
 // ------------------------------------------------------------------ device orchestration
 struct Ctx {
   hy_ctx* c;
@@ -263,6 +280,7 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
     return fail(HY_E_CAPACITY, "channel block does not divide the slot count");
   }
   p->S = s.segments > 1 ? s.segments : 1;
+  p->has_bias = s.bias != 0;
   if (p->S > 1) {  // PRCR preconditions (DESIGN R-PRCR)
     const char* why = nullptr;
     if (!pow2(p->S) || (s.wp / s.gap) % p->S) why = "PRCR: |S| must be a power of two dividing wp/gap";
@@ -363,9 +381,17 @@ extern "C" hy_status hy_conv_weight_slots(const hy_conv_plan* p, const double* K
   return HY_OK;
 }
 
+extern "C" hy_status hy_conv_bias_slots(const hy_conv_plan* p, const double* bias, uint32_t out_index,
+                                        double* slots) {
+  if (!p || !bias || !slots) return fail(HY_E_ARG, "null");
+  if ((int64_t)out_index >= p->n_out) return fail(HY_E_ARG, "output index");
+  bias_slots(*p, bias, out_index, slots);
+  return HY_OK;
+}
+
 extern "C" size_t hy_conv_weight_words(const hy_ctx* c, const hy_conv_plan* p, uint32_t level) {
-  if (!c || !p) return 0;
-  return ((size_t)p->n_pt() * (level + 1) + (p->has_mask ? level : 0)) * c->N;
+  if (!c || !p || level < 1u + (p->has_mask ? 1u : 0u)) return 0;
+  return p->bias_offset(level, c->N) + (p->has_bias ? (size_t)p->n_out * (p->out_level(level) + 1) * c->N : 0);
 }
 
 extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, uint32_t level) {
@@ -379,38 +405,52 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   return (p->n_out * (f2 + 1) + 8) * ct;                          // tap accumulators + one sum per output
 }
 
-extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, const double* K, uint32_t level,
-                                            uint64_t* d_pts, void* stream) {
+extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, const double* K, const double* bias,
+                                            uint64_t bias_scale, uint32_t level, uint64_t* d_pts, void* stream) {
   if (!c || !p || !K || !d_pts) return fail(HY_E_ARG, "null");
   if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
   if (p->n != (int64_t)c->N / 2) return fail(HY_E_PLAN, "plan ring size differs from the context's");
+  if (p->has_bias && (!bias || bias_scale == 0)) return fail(HY_E_ARG, "the plan adds a bias: bias and its scale needed");
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
   // Slot vectors are built on the host (the plan's weight placement, OpenMP), uploaded in batches and
   // encoded on the device (hy_encode_dev.cu; the same rounding as hy_encode_coeffs, DESIGN R-ENCODE).
-  // Weights at scale q_level, the mask at q_{level-1}: each rescale restores the ciphertext scale.
+  // Weights at scale q_level, the mask at q_{level-1}: each rescale restores the ciphertext scale; the bias
+  // plaintexts at the layer's output level and the output ciphertext scale bias_scale (DESIGN R-BIAS).
   cudaStream_t s = st(stream);
-  const int64_t npt = p->n_pt() + (p->has_mask ? 1 : 0);
   const size_t n = (size_t)p->n, per = n * 8 + n * 32 + (size_t)c->N * 8 + 64;
-  const int64_t B = std::min<int64_t>({64, npt, (int64_t)((c->ws_bytes - 4096) / per)});
-  if (B < 1) return fail(HY_E_WORKSPACE, "workspace too small for weight encoding");
+  if (c->ws_bytes < 4096 + per) return fail(HY_E_WORKSPACE, "workspace too small for weight encoding");
+  const int64_t B = std::min<int64_t>(64, (int64_t)((c->ws_bytes - 4096) / per));
   double* h_slots = nullptr;
   if (cudaMallocHost(&h_slots, (size_t)B * n * 8) != cudaSuccess) return fail(HY_E_CUDA, "pinned slot buffer");
   double* d_slots = reinterpret_cast<double*>(c->ws);
   uint8_t* ws_rest = c->ws + (((size_t)B * n * 8 + 255) & ~(size_t)255);
   const size_t rest_bytes = c->ws_bytes - (size_t)(ws_rest - c->ws);
-  const size_t stride = (size_t)(level + 1) * c->N;
   hy_status err = HY_OK;
-  for (int64_t k0 = 0; k0 < npt && err == HY_OK;) {
-    // a batch never mixes the mask (level - 1 limbs, scale q_{level-1}) with the weights
-    const bool mask = p->has_mask && k0 == p->n_pt();
-    const int64_t cnt = mask ? 1 : std::min<int64_t>(B, p->n_pt() - k0);
+  // one segment = cnt plaintexts of nl limbs at one scale, written stride words apart from dst
+  auto segment = [&](int64_t cnt, uint32_t nl, uint64_t scale, uint64_t* dst, size_t stride, auto&& slots_of) {
+    for (int64_t k0 = 0; k0 < cnt && err == HY_OK;) {
+      const int64_t m = std::min<int64_t>(B, cnt - k0);
 #pragma omp parallel for schedule(dynamic)
-    for (int64_t k = 0; k < cnt; ++k) weight_slots(*p, K, k0 + k, h_slots + (size_t)k * n);
-    cudaMemcpyAsync(d_slots, h_slots, (size_t)cnt * n * 8, cudaMemcpyHostToDevice, s);
-    std::vector<uint64_t> sc((size_t)cnt, mask ? c->mod[level - 1] : c->mod[level]);
-    err = encode_batch_device(c, d_slots, sc.data(), (uint32_t)cnt, mask ? level : level + 1,
-                              d_pts + (size_t)k0 * stride, stride, ws_rest, rest_bytes, s);
-    k0 += cnt;
+      for (int64_t k = 0; k < m; ++k) slots_of(k0 + k, h_slots + (size_t)k * n);
+      cudaMemcpyAsync(d_slots, h_slots, (size_t)m * n * 8, cudaMemcpyHostToDevice, s);
+      std::vector<uint64_t> sc((size_t)m, scale);
+      err = encode_batch_device(c, d_slots, sc.data(), (uint32_t)m, nl, dst + (size_t)k0 * stride, stride, ws_rest,
+                                rest_bytes, s);
+      // the pinned slot buffer is rewritten by the next batch: wait for its upload
+      cudaStreamSynchronize(s);
+      k0 += m;
+    }
+  };
+  const size_t stride = (size_t)(level + 1) * c->N;
+  segment(p->n_pt(), level + 1, c->mod[level], d_pts, stride,
+          [&](int64_t idx, double* v) { weight_slots(*p, K, idx, v); });
+  if (p->has_mask)
+    segment(1, level, c->mod[level - 1], d_pts + (size_t)p->n_pt() * stride, 0,
+            [&](int64_t, double* v) { weight_slots(*p, K, p->n_pt(), v); });
+  if (p->has_bias) {
+    const uint32_t lo = p->out_level(level);
+    segment(p->n_out, lo + 1, bias_scale, d_pts + p->bias_offset(level, c->N), (size_t)(lo + 1) * c->N,
+            [&](int64_t j, double* v) { bias_slots(*p, bias, j, v); });
   }
   cudaFreeHost(h_slots);
   if (err != HY_OK) return err;
@@ -458,9 +498,9 @@ hy_status ra_taps(const Ctx& x, const uint64_t* const* in, uint32_t level, const
   return HY_OK;
 }
 
-hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
-                   uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
-                   uint64_t* const* out, void* stream) {
+hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
+                    uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
+                    uint64_t* const* out, void* stream) {
   if (!c || !p || !evks || !in || !pts || !scratch || !out) return fail(HY_E_ARG, "null");
   if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
   if (ob > oe || oe > p->n_out) return fail(HY_E_PLAN, "output range outside the plan");
@@ -620,6 +660,27 @@ hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks
   return cuda_check("hy_raconv");
 }
 
+// the layer's bias (DESIGN R-BIAS): AddPt of bias plaintext o into c0 of output o, at the output level
+hy_status add_bias(hy_ctx* c, const hy_conv_plan* p, uint32_t level, const uint64_t* pts, uint32_t ob, uint32_t oe,
+                   uint64_t* const* out, void* stream) {
+  if (!p->has_bias) return HY_OK;
+  const uint32_t lo = p->out_level(level);
+  const uint64_t* bias = pts + p->bias_offset(level, c->N);
+  for (uint32_t o = ob; o < oe; ++o) {
+    hy_status st = hy_add(c, out[o - ob], bias + (size_t)o * (lo + 1) * c->N, 1, lo, out[o - ob], stream);
+    if (st != HY_OK) return st;
+  }
+  return HY_OK;
+}
+
+hy_status conv_run(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
+                   uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
+                   uint64_t* const* out, void* stream) {
+  hy_status st = conv_core(c, p, evks, in, level, pts, scratch, ob, oe, out, stream);
+  if (st != HY_OK) return st;
+  return add_bias(c, p, level, pts, ob, oe, out, stream);
+}
+
 }  // namespace
 
 extern "C" hy_status hy_caconv(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
@@ -707,6 +768,7 @@ extern "C" hy_status hy_raconv_finish(hy_ctx* c, const hy_conv_plan* p, const ui
   std::vector<const uint64_t*> sums{sum};
   std::vector<uint64_t*> dst{p->has_mask ? dstb : out};
   stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out, scratch + 3 * ct_l, ct_l);
+  if (stt == HY_OK) stt = add_bias(c, p, level, pts, out_index, out_index + 1, &out, stream);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv_finish");
 }

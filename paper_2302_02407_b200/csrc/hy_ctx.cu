@@ -94,6 +94,9 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
     return fail(HY_E_ARG, "bad chain length / dnum");
   uint32_t alpha = (prm->n_q + prm->dnum - 1) / prm->dnum;
   if (alpha > 8 || prm->n_p > 8 || prm->n_p < 1) return fail(HY_E_ARG, "alpha and n_p must be in [1,8]");
+  // hybrid key switching needs P >= every digit's product D_j (the KS noise bound, DESIGN R-KSBOUND): with
+  // primes of at most 48 bits and digits of alpha primes that means K >= alpha special primes
+  if (prm->n_p < alpha) return fail(HY_E_ARG, "n_p (K special primes) must be >= alpha = ceil(n_q/dnum)");
   if (prm->n_q + prm->n_p > (uint32_t)kMaxExt) return fail(HY_E_ARG, "chain too long");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cuda_device) {

@@ -911,8 +911,15 @@ extern "C" hy_status hy_hrot_batch(hy_ctx* c, const uint64_t* const* evks, const
   hy_status s0 = check_level(c, level);
   if (s0 != HY_OK) return s0;
   if (!evks || !cts || !r || !outs) return fail(HY_E_ARG, "null");
-  for (uint32_t i = 0; i < n; ++i)
-    if (cts[i] == outs[i]) return fail(HY_E_ARG, "hrot cannot run in place");
+  // no output may overlap any input of the batch: items run in key-switch chunks and r = 0 items are copied
+  // first, so an output over another item's input would corrupt it (include/hyphen.h)
+  const size_t ctw = 2ull * (level + 1) * c->N;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!outs[i] || !cts[i]) return fail(HY_E_ARG, "null ciphertext");
+    for (uint32_t j = 0; j < n; ++j)
+      if (outs[i] < cts[j] + ctw && cts[j] < outs[i] + ctw)
+        return fail(HY_E_ARG, i == j ? "hrot cannot run in place" : "an output overlaps another item's input");
+  }
   s0 = hrot_multi(c, evks, cts, level, r, n, outs, nullptr, st(stream));
   if (s0 != HY_OK) return s0;
   return cuda_check("hy_hrot_batch");

@@ -44,8 +44,10 @@ __device__ __forceinline__ int kbit(int s) {
 // Run stages [s_lo, s_hi] (forward: descending, inverse: ascending) on the 8
 // register values of one thread in layout LAY, on the FP64 pipe.  Twiddles come
 // from a shared-memory "heap" table T[li], li = (256 + e) >> (s+1) in [1, 256).
-//   forward (CT):  a' = a + b w, b' = a - b w   with |b w mod q| <= 1.5 q, no reduction
-//                  inside a pass (|v| < q + 8 * 1.5 q < 16 q, see fmulmod);
+//   forward (CT):  a' = a + b w, b' = a - b w   with |b w mod q| <= (1/2 + beta/16) q for |b| <= beta q
+//                  (hy_arith.cuh fmulmod), no reduction inside a pass: 8 stages from |v| <= q take the
+//                  operand bound to 6.62 q (from the between-pass format |v| <= q/2 + 1: 5.81 q), below
+//                  fmulmod's 2^51 / q_max = 8 (DESIGN R-FP64, tests/test_fp64_bound_cpu.py);
 //   inverse (GS):  a' = a + b, b' = (a - b) w; sums double per stage, so every
 //                  register round ends with a reduction (fred) of all 8 values.
 template <int LAY, bool FWD>
@@ -345,8 +347,8 @@ __global__ void __launch_bounds__(256) k_ntt_cols_small(LimbBatch b, DevTables d
 }
 
 // ---------------------------------------------------------------- pass B fused with the key-switch IP
-// The forward row stages of one 256-word row, layout L1 in -> layout L3 out (values |v| < 13 q,
-// not canonicalised), S = the warp's transpose buffer, T = the row's twiddle heap.
+// The forward row stages of one 256-word row, layout L1 in -> layout L3 out (values |v| <= 5.81 q from the
+// between-pass format, DESIGN R-FP64; not canonicalised), S = the warp's transpose buffer, T = the row's twiddle heap.
 __device__ __forceinline__ void rows_forward_l3(double (&x)[8], int l, double* S, const double* T, double q,
                                                 double qinv) {
   run_stages<1, true>(x, l, 7, 5, T, q, qinv);
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(256, 2) k_ntt_rows_ip(const __grid_constant__ 
 
 // ---------------------------------------------------------------- pass B fused with the ModDown epilogue
 // One warp per (item g, poly c, limb i <= level, row): the row stages of w_g[c][i] (column pass done),
-// then in layout L3: (u - w) P^{-1} (fmulmod, |u - w| < 14 q) plus the optional addends, canonicalised
+// then in layout L3: (u - w) P^{-1} (fmulmod, |u - w| <= q + 5.81 q) plus the optional addends, canonicalised
 // once.  grid (R/8, l+1, npoly * G), blockIdx.z = g * npoly + c.
 __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ RowsFinalArgs a, int npoly, int E,
                                                         const ModDownConst* md, DevTables dt, int level, int logN) {
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(256) k_ntt_rows_final(const __grid_constant__ 
 // One warp per (item g, limb i <= level, row), both polys: the inner product of the digits' row i with the
 // evk rows (plain: row pass of the column-pass output; hoisted: NTT-domain digits gathered through kx_g),
 // kept in registers; then for c = 0, 1 the row pass of the conversion w_g[c][i] and
-// out = (fred(acc_c) - w) P^{-1} (+ addends), canonicalised once.  |fred(acc) - w| < q/2 + 1 + 13 q.
+// out = (fred(acc_c) - w) P^{-1} (+ addends), canonicalised once.  |fred(acc) - w| <= q/2 + 1 + 5.81 q.
 // grid (G, R/8, l+1): the item index is the fastest grid dimension (hoisted items share their digits).
 template <int B, bool HOIST>
 __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant__ IpFinalArgs a, DevTables dt,

@@ -2,6 +2,7 @@
 // client-side key generation, encryption and decryption (
 // DESIGN R-SK, R-EVK, R-ENC, R-PRNG), all as device kernels.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -741,4 +742,61 @@ extern "C" hy_status hy_unpack48(hy_ctx* c, const uint64_t* d_in, uint64_t* d_ou
   kt.bytes = n_words * 14;
   k_unpack48<<<(unsigned)((n4 + 255) / 256), 256, 0, st(stream)>>>(d_in, d_out, n4);
   return cuda_check("hy_unpack48");
+}
+
+// ---------------------------------------------------------------- AddPt, sizes, coefficient wire format
+extern "C" hy_status hy_add_pt(hy_ctx* c, const uint64_t* ct, double ct_scale, const uint64_t* pt, double pt_scale,
+                               uint32_t level, uint64_t* out, void* stream) {
+  if (!c || !ct || !pt || !out) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q) return fail(HY_E_ARG, "level out of range");
+  if (!(ct_scale > 0.0) || !(pt_scale > 0.0) || std::fabs(ct_scale - pt_scale) > ct_scale * 0x1p-30)
+    return fail(HY_E_SCALE_MISMATCH, "AddPt: ciphertext and plaintext scales differ");
+  const size_t limb = (size_t)(level + 1) * c->N;
+  if (out != ct)  // c1 unchanged
+    cudaMemcpyAsync(out + limb, ct + limb, limb * 8, cudaMemcpyDeviceToDevice, st(stream));
+  return hy_add(c, ct, pt, 1, level, out, stream);
+}
+
+extern "C" size_t hy_ct_bytes(const hy_ctx* c, uint32_t level) {
+  return (!c || level >= c->n_q) ? 0 : 2ull * (level + 1) * c->N * 8;
+}
+
+extern "C" size_t hy_pt_bytes(const hy_ctx* c, uint32_t level, int with_p) {
+  return (!c || level >= c->n_q) ? 0 : (size_t)(level + 1 + (with_p ? c->n_p : 0)) * c->N * 8;
+}
+
+extern "C" hy_status hy_export_coeff(hy_ctx* c, const uint64_t* d_ntt, const uint32_t* chain, uint32_t n_limbs,
+                                     uint64_t* h_coeff, void* stream) {
+  if (!c || !d_ntt || !chain || !h_coeff) return fail(HY_E_ARG, "null");
+  for (uint32_t u = 0; u < n_limbs; ++u)
+    if (chain[u] >= c->n_q + c->n_p) return fail(HY_E_ARG, "chain index out of range");
+  if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
+  const size_t N = c->N, per = std::min<size_t>(c->ws_bytes / (N * 8), (size_t)kMaxBatch);
+  if (per == 0) return fail(HY_E_WORKSPACE, "workspace smaller than one limb");
+  cudaStream_t s = st(stream);
+  uint64_t* buf = reinterpret_cast<uint64_t*>(c->ws);
+  for (uint32_t u0 = 0; u0 < n_limbs; u0 += (uint32_t)per) {
+    const uint32_t m = std::min<uint32_t>((uint32_t)per, n_limbs - u0);
+    ntt_contig(c, d_ntt + (size_t)u0 * N, buf, chain + u0, m, true, s);
+    cudaMemcpyAsync(h_coeff + (size_t)u0 * N, buf, (size_t)m * N * 8, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("hy_export_coeff");
+  }
+  return cuda_check("hy_export_coeff");
+}
+
+extern "C" hy_status hy_import_coeff(hy_ctx* c, const uint64_t* h_coeff, const uint32_t* chain, uint32_t n_limbs,
+                                     uint64_t* d_ntt, void* stream) {
+  if (!c || !d_ntt || !chain || !h_coeff) return fail(HY_E_ARG, "null");
+  const size_t N = c->N;
+  for (uint32_t u = 0; u < n_limbs; ++u) {
+    if (chain[u] >= c->n_q + c->n_p) return fail(HY_E_ARG, "chain index out of range");
+    const uint64_t q = c->mod[chain[u]];
+    for (size_t x = 0; x < N; ++x)
+      if (h_coeff[(size_t)u * N + x] >= q) return fail(HY_E_ARG, "coefficient not reduced mod its prime");
+  }
+  cudaStream_t s = st(stream);
+  cudaMemcpyAsync(d_ntt, h_coeff, (size_t)n_limbs * N * 8, cudaMemcpyHostToDevice, s);
+  ntt_contig(c, d_ntt, d_ntt, chain, n_limbs, false, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("hy_import_coeff");  // host buffer released
+  return cuda_check("hy_import_coeff");
 }

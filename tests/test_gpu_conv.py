@@ -2,8 +2,6 @@
 against the oracle's encrypted execution of its own plan: bit-exact on every RNS
 limb.  Toy layers (N = 2^12) run in full; ResNet-20 layers at Set_hyp (N = 2^16)
 are checked on sampled output ciphertexts at the conv levels (l+1 = 10 / 7)."""
-import os
-
 import numpy as np
 import pytest
 
@@ -94,14 +92,10 @@ R18 = {"r18_L1_ca_S8": H.ConvSpec(64, 64, 56, 3, 1, 64, 1, 1, 1, "CA", S=8),
        "r18_L4_pconv": H.ConvSpec(256, 512, 14, 1, 2, 64, 4, 4, 4, "CA")}
 
 
-# r18_L1_ra_S8 (64 input ciphertexts through the oracle: ~4 min) runs only with HY_SLOW_TESTS=1; its last run is
-# recorded in profiles/r01_slow_parity.log
-_SLOW = pytest.mark.skipif(os.environ.get("HY_SLOW_TESTS") != "1", reason="slow oracle case (HY_SLOW_TESTS=1)")
-
 
 @pytest.mark.parametrize("name,outputs", [("L1_ra", [0]), ("L3_ca", [3]), ("L3_ds", [1]), ("r18_L1_ca_S8", [5]),
                                           ("r18_L4_pconv", [1]), ("r18_L4_ca_S8", [7]),
-                                          pytest.param("r18_L1_ra_S8", [3], marks=_SLOW)])
+                                          ("r18_L1_ra_S8", [3])])
 def test_resnet_layers_sampled(ctx_hyp, orc_hyp, name, outputs):
     spec = R20[name] if name in R20 else R18[name]
     level = 9 if spec.algo == "CA" else 6      # l+1 = 10 for CAConv, 7 for RAConv (DESIGN R-LEVELS)
@@ -181,3 +175,50 @@ def test_block_mini_bit_exact():
     res = H.unpack(dec, ra.fout, 4, 4, 4)
     ref = H.conv2d(H.conv2d(X, K1) ** 2, K2)
     assert np.max(np.abs(res - ref)) / np.max(np.abs(ref)) < 2**-10
+
+
+@pytest.mark.parametrize("spec", [TOY[0], TOY[5], TOY[7]], ids=["C1_raconv", "dsconv", "prcr_ca"])
+def test_toy_layers_bias_bit_exact(ctx_toy, orc_toy, spec):
+    """the conv bias (hy_conv_spec.bias, hy_conv_encode_weights' bias plaintexts, AddPt after the layer; DESIGN
+    R-BIAS) bit-exact vs the oracle's EncConv with bias, and decrypting to conv2d(X, K) + b within 2^-10"""
+    import paper_2302_02407_b200 as hy
+    level = orc_toy.nq - 1
+    X = synth.image(13, spec.ci, spec.w)
+    K = synth.conv_weight(14, spec.co, spec.ci, spec.f)
+    b = synth.conv_bias(15, spec.co)
+    p = hy.ConvPlan(ctx_toy, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo,
+                    S=spec.S, bias=True)
+    fin = H.Fmt("CA" if spec.algo == "CA" else "RA", spec.n, spec.wp, spec.g, spec.m, spec.d, spec.S)
+    cts = [ctx_toy.encrypt(SK, 902, i, ctx_toy.encode(v, 2**40, level), level) for i, v in enumerate(H.pack(X, fin))]
+    evks = {r: ctx_toy.keygen_rot(SK, EK, r) for r in p.rots}
+    outs = p.run(evks, cts, level, p.encode_weights(K, level, bias=b, bias_scale=2**40))
+    o = orc_toy
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    octs = [o.encrypt(SK, 902, i, o.encode(v, 2**40, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+    oevks = {r: o.keygen_rot(SK, EK, r) for r in H.rotation_amounts(plan, o.n)}
+    ref = H.EncConv(o, plan, oevks, bias=b).run(octs)
+    for a, r in zip(outs, ref):
+        assert np.array_equal(to_np(a), r.data)
+    dec = [np.real(o.decode(o.decrypt(SK, r))) for r in ref]
+    got = H.unpack(dec, plan.fout, spec.co, spec.wo, spec.wo)
+    want = H.conv2d(X, K, spec.s, bias=b)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10
+
+
+def test_raconv_tap_sharding_with_bias(ctx_toy):
+    """hy_raconv_finish adds the bias too: tap-sharded = hy_raconv, bit for bit"""
+    import paper_2302_02407_b200 as hy
+    spec, level = TOY[0], 2
+    p = hy.ConvPlan(ctx_toy, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo,
+                    bias=True)
+    cts = [ctx_toy.encrypt(SK, 903, i, ctx_toy.encode(synth.slots_uniform(50 + i, 2048), 2**40, level), level)
+           for i in range(p.n_in)]
+    evks = {r: ctx_toy.keygen_rot(SK, EK, r) for r in p.rots}
+    pts = p.encode_weights(synth.conv_weight(16, 4, 4, 3), level, bias=synth.conv_bias(17, 4), bias_scale=2**40)
+    want = p.run(evks, cts, level, pts)[0]
+    total = p.partial_state(level)
+    for b_, e_ in [(0, 4), (4, 9)]:
+        st = p.partial_state(level)
+        p.raconv_partial(evks, cts, level, pts, 0, b_, e_, st)
+        total += st
+    assert np.array_equal(to_np(p.raconv_finish(evks, level, pts, total, 0)), to_np(want))

@@ -437,3 +437,61 @@ def test_prot(pair):
         assert np.array_equal(got, want), r
     zr = np.real(ctx.decode(ctx.prot(pt, level, 3), level, scale))
     assert np.max(np.abs(zr - np.roll(z, -3))) < 2**-20
+
+
+def test_add_pt_and_scale_check(pair):
+    """hy_add_pt: (c0 + pt, c1) bit-exact vs the oracle's AddPt, in place and out of place; mismatched scales are
+    HY_E_SCALE_MISMATCH (12)"""
+    import paper_2302_02407_b200 as hy
+    name, ctx, o = pair
+    level = o.nq - 1 if name != "hyp" else 5
+    a = rand_limbs(o, 110, list(range(level + 1)) * 2).reshape(2, level + 1, o.N)
+    p = rand_limbs(o, 111, list(range(level + 1)))
+    want = o.add_pt(oracle.Ct(a, level, 2.0**40), oracle.Pt(p, level, 2.0**40)).data
+    da, dp = to_dev(a, ctx), to_dev(p, ctx)
+    assert np.array_equal(to_np(ctx.add_pt(da, 2.0**40, dp, 2.0**40, level)), want)
+    ctx.add_pt(da, 2.0**40, dp, 2.0**40, level, out=da)
+    assert np.array_equal(to_np(da), want)
+    with pytest.raises(hy.HyError) as e:
+        ctx.add_pt(da, 2.0**40, dp, 2.0**41, level)
+    assert e.value.code == 12
+
+
+def test_coeff_wire_format_and_sizes(pair):
+    """hy_export_coeff / hy_import_coeff (coefficient domain, limbs q_0.. then p_0..) = the oracle's
+    iNTT / NTT, round trip exact; hy_ct_bytes / hy_pt_bytes; unreduced imports are HY_E_ARG"""
+    import paper_2302_02407_b200 as hy
+    name, ctx, o = pair
+    chain = list(range(o.nq)) + list(range(o.nq, o.nq + o.np_))
+    a = rand_limbs(o, 120, chain)
+    coeff = ctx.export_coeff(to_dev(a, ctx), chain)
+    assert np.array_equal(coeff, np.stack([o.intt(a[i], t) for i, t in enumerate(chain)]))
+    back = ctx.import_coeff(coeff, chain)
+    assert np.array_equal(to_np(back), a)
+    bad = coeff.copy()
+    bad[0, 0] = int(o.moduli[0])
+    with pytest.raises(hy.HyError) as e:
+        ctx.import_coeff(bad, chain)
+    assert e.value.code == 1
+    lv = min(3, o.nq - 1)
+    assert ctx.ct_bytes(lv) == 2 * (lv + 1) * o.N * 8
+    assert ctx.pt_bytes(lv) == (lv + 1) * o.N * 8 and ctx.pt_bytes(lv, True) == (lv + 1 + o.np_) * o.N * 8
+    assert ctx.ct_bytes(o.nq) == 0
+
+
+def test_ctx_and_batch_argument_checks():
+    """K < alpha special primes is HY_E_ARG at context creation; an hrot_batch output overlapping
+    another item's input is HY_E_ARG"""
+    import paper_2302_02407_b200 as hy
+    prm = dict(synth.PARAMS["mini"])
+    prm["p_bits"] = [48]          # alpha = 2 > K = 1
+    with pytest.raises(hy.HyError) as e:
+        hy.Context(**prm)
+    assert e.value.code == 1
+    ctx, o = _hyp_pair()
+    level = 2
+    key = ctx.keygen_rot(SK, EK, 1)
+    a, b = ctx.zeros(*ctx.ct_shape(level)), ctx.zeros(*ctx.ct_shape(level))
+    with pytest.raises(hy.HyError) as e:
+        ctx.hrot_batch([key, key], [a, b], level, [1, 1], outs=[b, ctx.empty(*ctx.ct_shape(level))])
+    assert e.value.code == 1

@@ -253,3 +253,19 @@ def test_resnet18_ras_total_matches_paper():
     assert sum(m for _, m in specs) == 19 and siso == 1024
     assert ras == 4512
     assert ir == 1632
+
+
+@pytest.mark.parametrize("name", ["stem", "L1_ra", "L2_ds", "L3_pconv", "L3_ca"])
+def test_simulated_plan_with_bias_equals_conv2d_bias(name):
+    """DESIGN R-BIAS (BN fused into the conv): the plan followed by AddPt of the output-format packing of
+    b equals conv2d(X, K) + b on every valid slot and every replica"""
+    spec = R20[name]
+    X = synth.image(3, spec.ci, spec.w)
+    K = synth.conv_weight(4, spec.co, spec.ci, spec.f)
+    b = synth.conv_bias(5, spec.co)
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    ys = H.simulate(plan, H.pack(X, plan.fin), bias=b)
+    want = H.conv2d(X, K, spec.s, bias=b)
+    for rep in range(plan.fout.d):
+        got = H.unpack(ys, plan.fout, spec.co, spec.wo, spec.wo, rep)
+        assert np.max(np.abs(got - want)) < 1e-9

@@ -65,3 +65,94 @@ def test_encrypted_block_mini():
     got = H.unpack(dec, ra.fout, 4, 4, 4)
     want = H.conv2d(H.conv2d(X, K1) ** 2, K2)
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2**-10
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Pins of the oracle's conv2d (the reference every layer test decrypts against), VERDICT r01 "weak" 1.
+def test_conv2d_matches_torch():
+    """oracle conv2d = torch.nn.functional.conv2d (cross-correlation, zero padding (f-1)/2, stride s, bias): an
+    independent implementation, f in {1, 3}, s in {1, 2}, even and odd image sizes, several channel counts."""
+    import torch
+    import torch.nn.functional as F
+    g = np.random.default_rng(17)
+    for ci, co, w, f, s in [(1, 1, 4, 3, 2), (3, 16, 32, 3, 1), (16, 32, 32, 3, 2), (16, 32, 32, 1, 2),
+                            (4, 4, 7, 3, 2), (8, 4, 5, 3, 1), (2, 3, 9, 1, 1), (5, 2, 6, 5, 1)]:
+        X = g.uniform(-1, 1, (ci, w, w))
+        K = g.normal(0, 1, (co, ci, f, f))
+        b = g.uniform(-1, 1, co)
+        want = F.conv2d(torch.from_numpy(X)[None], torch.from_numpy(K), torch.from_numpy(b), stride=s,
+                        padding=(f - 1) // 2)[0].numpy()
+        got = H.conv2d(X, K, s, bias=b)
+        assert got.shape == want.shape
+        assert np.max(np.abs(got - want)) < 1e-12
+
+
+def _golden_fig2d():
+    import os
+    taps, pos = {}, {}
+    path = os.path.join(os.path.dirname(__file__), "golden", "fig2d_stride2.txt")
+    for line in open(path):
+        line = line.split("#")[0].split()
+        if not line:
+            continue
+        if line[0] == "pos":
+            for it in line[1:]:
+                o, rc = it.split(":")
+                pos[o] = tuple(int(x) for x in rc.split(","))
+        else:
+            taps[line[0]] = [tuple(it.split(":")) for it in line[1:]]
+    return taps, pos
+
+
+def test_conv2d_fig2d_stride2_worked_example():
+    """Fig. 2(d): with one-hot image a_i and one-hot filter k_t, the stride-2 pad-1 conv2d output is
+    one-hot at exactly the output the figure pairs (k_t, a_i) with, and zero where the figure's filter slot is 0;
+    outputs c1..c4 are the even grid positions, i.e. Y[row/2, col/2]."""
+    taps, pos = _golden_fig2d()
+    for k, pairs in taps.items():
+        t = int(k[1:]) - 1
+        K = np.zeros((1, 1, 3, 3))
+        K[0, 0, t // 3, t % 3] = 1.0
+        listed = {}
+        for o, a in pairs:
+            listed[a] = o
+        for i in range(16):
+            X = np.zeros((1, 4, 4))
+            X[0, i // 4, i % 4] = 1.0
+            Y = H.conv2d(X, K, 2)[0]
+            assert Y.shape == (2, 2)
+            want = np.zeros((2, 2))
+            if f"a{i + 1}" in listed:
+                r, c = pos[listed[f"a{i + 1}"]]
+                assert r % 2 == 0 and c % 2 == 0
+                want[r // 2, c // 2] = 1.0
+            # outputs the figure shows for this tap hold only the listed inputs
+            for o, (r, c) in pos.items():
+                if o in listed.values() and f"a{i + 1}" not in listed:
+                    assert Y[r // 2, c // 2] == 0.0
+            if f"a{i + 1}" in listed:
+                assert np.array_equal(Y, want), (k, i)
+    # and every output position of the figure receives k1 only from a6 (the rest reads the padding)
+    K = np.zeros((1, 1, 3, 3))
+    K[0, 0, 0, 0] = 1.0
+    X = np.arange(1, 17, dtype=float).reshape(1, 4, 4)
+    assert np.array_equal(H.conv2d(X, K, 2)[0], np.array([[0.0, 0.0], [0.0, 6.0]]))
+
+
+@pytest.mark.parametrize("spec", [H.ConvSpec(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", n=2048),
+                                  H.ConvSpec(4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", n=2048)], ids=["C1_raconv", "dsconv"])
+def test_encrypted_conv_with_bias(orc_toy, spec):
+    """AddPt of the bias plaintexts after the layer (DESIGN R-BIAS): decrypts to conv2d(X, K) + b within 2^-10"""
+    o = orc_toy
+    level = o.nq - 1
+    X = synth.image(8, spec.ci, spec.w)
+    K = synth.conv_weight(9, spec.co, spec.ci, spec.f)
+    b = synth.conv_bias(10, spec.co)
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    cts = [o.encrypt(SK, 900, i, o.encode(v, 2**40, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+    evks = {r: o.keygen_rot(SK, EK, r) for r in H.rotation_amounts(plan, o.n)}
+    outs = H.EncConv(o, plan, evks, bias=b).run(cts)
+    dec = [np.real(o.decode(o.decrypt(SK, c))) for c in outs]
+    got = H.unpack(dec, plan.fout, spec.co, spec.wo, spec.wo)
+    want = H.conv2d(X, K, spec.s, bias=b)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10

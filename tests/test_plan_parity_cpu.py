@@ -43,3 +43,19 @@ def test_plan_matches_oracle(hy, name):
         assert np.array_equal(p.weight_slots(K, idx), o.weights[key]), (name, key)
     if o.mask is not None:
         assert np.array_equal(p.weight_slots(K, p.n_pt), o.mask)
+
+
+@pytest.mark.parametrize("name", ["C1_raconv", "toy_dsconv", "L1_ca", "L2_ra", "L3_ds", "r18_L4_pconv"]
+                         + [k for k in PRCR][:2])
+def test_bias_slots_match_oracle(hy, name):
+    """DESIGN R-BIAS: the product's bias plaintext slots (hy_conv_bias_slots) = the oracle's packing of the bias
+    image in the output format, for every output ciphertext"""
+    s = CASES[name]
+    log_n = (2 * s.n).bit_length() - 1
+    b = synth.conv_bias(9, s.co)
+    p = hy.ConvPlan(None, s.ci, s.co, s.w, s.f, s.s, s.wp, s.g, s.m, s.d, s.algo, log_n=log_n, S=s.S, bias=True)
+    o = (H.plan_caconv if s.algo == "CA" else H.plan_raconv)(s, synth.conv_weight(7, s.co, s.ci, s.f),
+                                                              with_weights=False)
+    want = H.bias_slots(o, b)
+    for j in range(p.n_out):
+        assert np.array_equal(p.bias_slots(b, j), want[j]), (name, j)
