@@ -430,15 +430,25 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
 
         def step():
             if tap_shard:  # every rank ends with every output: no gather
-                for o in range(p.n_out):
-                    raconv_tap_sharded(p, evks, cts, level, pts, o, scratch)
-                return
+                return [raconv_tap_sharded(p, evks, cts, level, pts, o, scratch) for o in range(p.n_out)]
             if e > b:
                 p.run(evks, cts, level, pts, scratch, b, e, outs)
             if ws > 1:
-                all_gather_cts(outs, p.n_out, like)
+                return all_gather_cts(outs, p.n_out, like)
+            return outs
 
         ms, launches = timed(step, steps, warmup)
+        identity = None
+        if ws > 1:
+            # the sharded, combined result equals a single-rank run bit for bit -- rank 0
+            # recomputes the last output (owned by the last rank, or tap-sharded) alone and compares its limbs
+            got = step()
+            j = p.n_out - 1
+            if rank == 0:
+                alone = p.run(evks, cts, level, pts, scratch, j, j + 1)[0]
+                identity = {"output": j, "bit_identical": bool(torch.equal(got[j], alone)),
+                            "how": "rank 0 recomputes the output alone and compares every limb"}
+            barrier(ws)
         # one extra instrumented run: device ms per kernel family (CUDA events on the launching stream)
         ctx.time_kernels(sum(ctx.FAMILIES.values()))
         step()
@@ -453,6 +463,7 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
                         "roofline": layer_roofline(p, algo, level, ms),
                         "sharding": "taps (all-reduce)" if tap_shard else ("outputs (all-gather)" if ws > 1 else None),
                         "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S,
+                        "multi_gpu_check": identity,
                         "family_ms": fams}
         total += mult * ms
         del pts, cts, outs, scratch
@@ -549,8 +560,11 @@ def bench_c1(device, steps, warmup, timed_fn, with_oracle=True):
     pts = p.encode_weights(K, level)
     scratch = p.scratch(level)
     outs = [ctx.empty(*ctx.ct_shape(p.out_level(level)))]
-    ms, launches = timed_fn(lambda: p.run(evks, cts, level, pts, scratch, 0, 1, outs), steps, warmup)
+    ms, _ = timed_fn(lambda: p.run(evks, cts, level, pts, scratch, 0, 1, outs), steps, warmup)
     torch.cuda.synchronize()
+    l0 = ctx.launch_count()  # this context's kernels per layer call (timed_fn counts the bench context's)
+    p.run(evks, cts, level, pts, scratch, 0, 1, outs)
+    launches = ctx.launch_count() - l0
     res = {"workload": "C1: 3x3 RAConv 4->4, 8x8, N=2^12, 3 limbs + 1 special prime, l = 2 (BASELINE configs[0])",
            "ms": ms, "gpu_launches": launches, "rotations": p.counts, "n_in": p.n_in, "n_out": p.n_out}
     if with_oracle:  # the cpu_baseline leg: the oracle's encrypted execution of the same layer

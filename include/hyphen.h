@@ -248,6 +248,27 @@ void hy_conv_plan_destroy(hy_conv_plan* plan);
  * pointer may be NULL. */
 hy_status hy_conv_plan_query(const hy_conv_plan* plan, uint32_t* n_in, uint32_t* n_out, uint32_t* n_pt,
                              uint32_t* has_mask, uint32_t* n_rot, int32_t* rots, uint32_t* counts);
+/* ---- limited rotation-key sets ("frequently used rotation keys for Slide are loaded ... other
+ * irregular rotation keys used in IR are not loaded; instead, these rotation indices are synthesized using the
+ * already loaded key indices"; DESIGN R-KEYSET).  A key set is a list of loaded rotation amounts (taken mod N/2).
+ * An amount r that is not loaded is synthesized as the shortest sequence of loaded amounts summing to r mod N/2
+ * (HRot_{a+b} = HRot_a o HRot_b, one key switch per step): breadth-first search from 0 over Z_{N/2} with the
+ * loaded amounts as edges in ascending order and a FIFO queue, the first discovery fixing a node's parent.
+ * Host only. */
+typedef struct hy_keyset hy_keyset;
+hy_status hy_keyset_create(uint32_t log_n, const int32_t* amounts, uint32_t n_amounts, hy_keyset** out);
+void hy_keyset_destroy(hy_keyset* keyset);
+/* steps (application order, each a loaded amount in [1, N/2)) of amount r; r = 0 -> 0 steps; a loaded r -> 1 step
+ * (r itself).  steps may be NULL (count only).  Errors: HY_E_MISSING_KEY (r unreachable), HY_E_ARG. */
+hy_status hy_keyset_decompose(const hy_keyset* keyset, int32_t r, int32_t* steps, uint32_t max_steps,
+                              uint32_t* n_steps);
+/* Restrict a conv plan to a key set (NULL: every key the plan needs, the default): its Slide amounts must be loaded
+ * (HY_E_MISSING_KEY otherwise: they are hoisted); every other amount not loaded is synthesized.  Afterwards
+ * hy_conv_plan_query reports the loaded amounts the layer uses (the keys hy_caconv / hy_raconv take) and
+ * hy_conv_scratch_words the larger scratch; hy_conv_plan_eff_counts gives counts[5] with each synthesized rotation
+ * counted once per step ("eff. total"). */
+hy_status hy_conv_plan_set_keyset(hy_conv_plan* plan, const hy_keyset* keyset);
+hy_status hy_conv_plan_eff_counts(const hy_conv_plan* plan, uint32_t* counts);
 /* Slot values (host, N/2 doubles) of weight plaintext idx < n_pt, or of the mask (idx == n_pt).
  * K: host [co][ci][f][f] float64. */
 hy_status hy_conv_weight_slots(const hy_conv_plan* plan, const double* K, uint32_t idx, double* slots);

@@ -452,16 +452,82 @@ def _simulate(plan: Plan, xs: list[np.ndarray]) -> list[np.ndarray]:
     return outs
 
 
+# --------------------------------------------------------------------------- limited key sets
+class KeySet:
+    """Loaded rotation keys and the synthesis of the others ("other irregular rotation keys used in
+    IR are not loaded; instead, these rotation indices are synthesized using the already loaded key indices").
+    Reading (DESIGN R-KEYSET): an amount r is synthesized as the shortest sequence of loaded amounts summing to r
+    mod n -- breadth-first search from 0 over Z_n, the loaded amounts as edges in ascending order, FIFO queue,
+    the first discovery of a node fixing its parent -- and HRot_r = HRot_{a_k} o ... o HRot_{a_1}."""
+
+    def __init__(self, n: int, amounts):
+        self.n = n
+        self.loaded = sorted({int(a) % n for a in amounts} - {0})
+        parent = {0: None}
+        queue = [0]
+        h = 0
+        while h < len(queue):
+            u = queue[h]
+            h += 1
+            for a in self.loaded:
+                v = (u + a) % n
+                if v not in parent:
+                    parent[v] = (u, a)
+                    queue.append(v)
+        self.parent = parent
+
+    def steps(self, r: int) -> list:
+        v = int(r) % self.n
+        out = []
+        while v != 0:
+            if v not in self.parent:
+                raise KeyError(f"rotation {r} cannot be synthesized from the key set")
+            u, a = self.parent[v]
+            out.append(a)
+            v = u
+        return out[::-1]
+
+
+def eff_counts(plan: "Plan", keyset: "KeySet") -> dict:
+    """rotation counts with every synthesized rotation counted once per step ("eff. total")."""
+    n = plan.fin.n
+
+    def cost(rs):
+        return sum(len(keyset.steps(r)) if r % n and r % n not in keyset.loaded else int(r % n != 0) for r in rs)
+
+    c = dict(plan.counts)
+    c["RaS"] = cost(plan.ras) * plan.n_groups
+    c["RaS_g"] = cost(plan.ras_g) * plan.n_groups
+    c["IR_g"] = cost(plan.ir_g) * plan.n_out + (cost([plan.combine]) * plan.n_out if plan.combine is not None else 0)
+    return c
+
+
+def keyset_amounts(plan: "Plan", keyset: "KeySet") -> list:
+    """the loaded amounts a plan uses under a key set (Slide taps must be loaded: they are hoisted)."""
+    n = plan.fin.n
+    need = set()
+    for r in plan.taps:
+        if r % n:
+            assert r % n in keyset.loaded, "Slide amounts must be loaded"
+            need.add(r % n)
+    for r in plan.ras + plan.ras_g + plan.ir_g + ([plan.combine] if plan.combine is not None else []):
+        if r % n == 0:
+            continue
+        need |= {r % n} if r % n in keyset.loaded else set(keyset.steps(r))
+    return sorted(need)
+
+
 # --------------------------------------------------------------------------- encrypted execution
 class EncConv:
     """Runs a plan on oracle ciphertexts.  Weight plaintexts are encoded at scale q_l of the
     level they are consumed at and masks at q_{l-1}, so each rescale returns the scale to
     the ciphertext scale exactly (DESIGN R-SCALE).  evks: rotation amount -> key."""
 
-    def __init__(self, o, plan: Plan, evks: dict, bias=None):
+    def __init__(self, o, plan: Plan, evks: dict, bias=None, keyset: "KeySet | None" = None):
         """bias: optional per-output-channel bias [co], added by AddPt after the layer's last rescale at the
-        output ciphertext's level and scale (DESIGN R-BIAS)."""
-        self.o, self.plan, self.evks, self.bias = o, plan, evks, bias
+        output ciphertext's level and scale (DESIGN R-BIAS).  keyset: optional limited key set; rotations by
+        amounts it does not load are synthesized step by step (DESIGN R-KEYSET)."""
+        self.o, self.plan, self.evks, self.bias, self.keyset = o, plan, evks, bias, keyset
 
     def key(self, r):
         r %= self.o.n
@@ -469,6 +535,10 @@ class EncConv:
 
     def hrot(self, ct, r):
         if r % self.o.n == 0:
+            return ct
+        if self.keyset is not None and r % self.o.n not in self.keyset.loaded:
+            for a in self.keyset.steps(r):
+                ct = self.o.hrot(ct, self.key(a), a)
             return ct
         return self.o.hrot(ct, self.key(r), r)
 

@@ -104,6 +104,11 @@ SIGNATURES = {
     "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double), _U64, _U32, _P,
                                          _P]),
     "hy_conv_bias_slots": (C.c_int, [_P, C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
+    "hy_keyset_create": (C.c_int, [_U32, C.POINTER(C.c_int32), _U32, C.POINTER(_P)]),
+    "hy_keyset_destroy": (None, [_P]),
+    "hy_keyset_decompose": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), _U32, C.POINTER(_U32)]),
+    "hy_conv_plan_set_keyset": (C.c_int, [_P, _P]),
+    "hy_conv_plan_eff_counts": (C.c_int, [_P, C.POINTER(_U32)]),
     "hy_add_pt": (C.c_int, [_P, _P, C.c_double, _P, C.c_double, _U32, _P, _P]),
     "hy_ct_bytes": (C.c_size_t, [_P, _U32]),
     "hy_pt_bytes": (C.c_size_t, [_P, _U32, C.c_int]),
@@ -457,6 +462,31 @@ class Context:
         return out
 
 
+class KeySet:
+    """A limited set of loaded rotation keys (hy_keyset_create, DESIGN R-KEYSET); other amounts are synthesized
+    as the shortest sums of loaded ones."""
+
+    def __init__(self, log_n, amounts):
+        self.n = 1 << (log_n - 1)
+        a = (C.c_int32 * max(1, len(amounts)))(*[int(x) for x in amounts])
+        h = C.c_void_p()
+        self._lib = lib()
+        _check(self._lib.hy_keyset_create(log_n, a, len(amounts), C.byref(h)))
+        self._k = h
+
+    def __del__(self):
+        if getattr(self, "_k", None) and getattr(self, "_lib", None) is not None:
+            self._lib.hy_keyset_destroy(self._k)
+            self._k = None
+
+    def decompose(self, r):
+        n = C.c_uint32()
+        _check(lib().hy_keyset_decompose(self._k, int(r), None, 0, C.byref(n)))
+        st = (C.c_int32 * max(1, n.value))()
+        _check(lib().hy_keyset_decompose(self._k, int(r), st, n.value, C.byref(n)))
+        return [int(st[i]) for i in range(n.value)]
+
+
 class ConvPlan:
     """A HyPHEN convolution layer (CAConv / RAConv_Reorder) on one context (include/hyphen.h)."""
 
@@ -474,6 +504,10 @@ class ConvPlan:
         self._lib = lib()
         _check(self._lib.hy_conv_plan_create(log_n if log_n is not None else ctx.log_n, C.byref(spec), C.byref(h)))
         self._p = h
+        self._query()
+        self.f = f
+
+    def _query(self):
         ni, no, npt, hm, nr = (C.c_uint32() for _ in range(5))
         counts = (C.c_uint32 * 5)()
         _check(lib().hy_conv_plan_query(self._p, C.byref(ni), C.byref(no), C.byref(npt), C.byref(hm), C.byref(nr),
@@ -483,7 +517,15 @@ class ConvPlan:
         self.n_in, self.n_out, self.n_pt, self.has_mask = ni.value, no.value, npt.value, bool(hm.value)
         self.rots = [int(rots[i]) for i in range(nr.value)]
         self.counts = dict(zip(["Slide", "RaS", "RaS_g", "IR_g", "PMult"], [int(x) for x in counts]))
-        self.f = f
+        eff = (C.c_uint32 * 5)()
+        _check(lib().hy_conv_plan_eff_counts(self._p, eff))
+        self.eff_counts = dict(zip(["Slide", "RaS", "RaS_g", "IR_g", "PMult"], [int(x) for x in eff]))
+
+    def set_keyset(self, keyset):
+        """Restrict the layer to a limited rotation-key set (hy_conv_plan_set_keyset): a KeySet or
+        None (every key loaded).  self.rots becomes the loaded amounts the layer uses."""
+        _check(lib().hy_conv_plan_set_keyset(self._p, keyset._k if keyset is not None else None))
+        self._query()
 
     def __del__(self):
         if getattr(self, "_p", None) and getattr(self, "_lib", None) is not None:

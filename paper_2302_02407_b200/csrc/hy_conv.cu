@@ -71,6 +71,27 @@ struct Layout {
 
 }  // namespace
 
+// A limited rotation-key set: the loaded amounts and, over Z_n, the breadth-first tree from 0
+// whose edges are the loaded amounts (DESIGN R-KEYSET): the shortest decomposition of any amount into loaded ones,
+// ties broken by discovery order (FIFO queue, amounts ascending).
+struct hy_keyset {
+  int64_t n = 0;
+  std::vector<int64_t> loaded;          // ascending, canonical in (0, n)
+  std::vector<int32_t> parent_amount;   // per node: the loaded amount of its tree edge (-1: root / unreached)
+  std::vector<int32_t> parent;          // per node: its tree parent
+  std::vector<int64_t> steps(int64_t r) const {  // application order; empty if unreachable (r != 0)
+    std::vector<int64_t> out;
+    int64_t v = ((r % n) + n) % n;
+    while (v != 0) {
+      if (parent_amount[v] < 0) return {};
+      out.push_back(parent_amount[v]);
+      v = parent[v];
+    }
+    std::reverse(out.begin(), out.end());
+    return out;
+  }
+};
+
 struct hy_conv_plan {
   hy_conv_spec s;
   int64_t n, pad, wo;
@@ -83,6 +104,17 @@ struct hy_conv_plan {
   int64_t combine = 0;
   std::vector<int64_t> rots;  // distinct nonzero rotation amounts mod n (key order)
   uint32_t counts[5] = {0, 0, 0, 0, 0};
+  // limited key set (hy_conv_plan_set_keyset): amount -> its loaded steps, for every non-Slide amount that is not
+  // loaded itself (empty map: every key the plan needs is loaded); eff_counts = counts with those rotations
+  // counted once per step ("eff. total")
+  std::map<int64_t, std::vector<int64_t>> decomp;
+  uint32_t eff_counts[5] = {0, 0, 0, 0, 0};
+  std::vector<int64_t> steps_of(int64_t r) const {
+    const int64_t rr = ((r % n) + n) % n;
+    auto it = decomp.find(rr);
+    if (it != decomp.end()) return it->second;
+    return {r};
+  }
   int64_t S = 1;              // PRCR segments
   int64_t f2() const { return (int64_t)s.f * s.f; }
   // stored weight plaintexts: CA [group][input or family][tap]; RA [output or family][input][tap]
@@ -215,22 +247,48 @@ struct Ctx {
   }
 };
 
+// out_g = HRot_r(in_g) (+ addct_g) for all g at once -- one batched HRot per loaded step of r (an
+// amount whose key is not loaded is synthesized from loaded ones, HRot_{a+b} = HRot_a o HRot_b); the intermediate
+// steps ping-pong through tmp_a / tmp_b (G ciphertexts each, tmp_stride words apart), the last step adds addct.
+// Same aliasing rules as hrot_multi (out may alias in and addct).
+hy_status hrot_steps(const Ctx& x, int64_t r, uint32_t level, const std::vector<const uint64_t*>& in,
+                     const std::vector<uint64_t*>& out, const std::vector<const uint64_t*>* addct, uint64_t* tmp_a,
+                     uint64_t* tmp_b, size_t tmp_stride) {
+  const size_t G = in.size();
+  const std::vector<int64_t> steps = x.p->steps_of(r);
+  if (steps.size() > 1 && (!tmp_a || !tmp_b)) return hy::fail(HY_E_WORKSPACE, "no scratch for a synthesized rotation");
+  std::vector<const uint64_t*> cur(in);
+  for (size_t k = 0; k < steps.size(); ++k) {
+    const bool last = k + 1 == steps.size();
+    std::vector<uint64_t*> dst(G);
+    for (size_t g = 0; g < G; ++g) dst[g] = last ? out[g] : ((k & 1) ? tmp_b : tmp_a) + g * tmp_stride;
+    std::vector<const uint64_t*> keys(G, x.key(steps[k]));
+    std::vector<int32_t> rr(G, (int32_t)steps[k]);
+    hy_status st = hy::hrot_multi(x.c, keys.data(), cur.data(), level, rr.data(), (uint32_t)G, dst.data(),
+                                  last && addct ? addct->data() : nullptr, x.s);
+    if (st != HY_OK) return st;
+    cur.assign(dst.begin(), dst.end());
+  }
+  return HY_OK;
+}
+
 // x_g += HRot_r(x_g) for every r in rs, in order, for all ciphertexts x_g at once: each step is one
 // batched HRot whose evaluation key is shared by every item (RaS / RaS_g / IR_g)
 // tmp (optional): v.size() scratch ciphertexts (stride tmp_stride words): the steps ping-pong between v and tmp
 // (out = in + HRot(in) never aliases its input, so the key switch reads c1 / c0 through kappa without first
-// copying the permuted ciphertext), and an odd final position is copied back into v.
+// copying the permuted ciphertext), and an odd final position is copied back into v.  syn_a / syn_b (limited key
+// sets): v.size() scratch ciphertexts each, syn_stride words apart, for the intermediate steps of synthesized
+// rotations.
 hy_status ras_all(const Ctx& x, const std::vector<uint64_t*>& v, uint32_t level, const std::vector<int64_t>& rs,
-                  uint64_t* tmp = nullptr, size_t tmp_stride = 0) {
+                  uint64_t* tmp = nullptr, size_t tmp_stride = 0, uint64_t* syn_a = nullptr,
+                  uint64_t* syn_b = nullptr, size_t syn_stride = 0) {
   if (v.empty() || rs.empty()) return HY_OK;
   const size_t G = v.size(), bytes = 2ull * (level + 1) * x.c->N * 8;
   std::vector<uint64_t*> cur(v.begin(), v.end()), nxt(G);
   for (size_t g = 0; g < G; ++g) nxt[g] = tmp ? tmp + g * tmp_stride : v[g];
   for (int64_t r : rs) {
-    std::vector<const uint64_t*> keys(G, x.key(r)), in_c(cur.begin(), cur.end());
-    std::vector<int32_t> rr(G, (int32_t)r);
-    hy_status st = hy::hrot_multi(x.c, keys.data(), in_c.data(), level, rr.data(), (uint32_t)G, nxt.data(),
-                                  in_c.data(), x.s);
+    std::vector<const uint64_t*> in_c(cur.begin(), cur.end());
+    hy_status st = hrot_steps(x, r, level, in_c, nxt, &in_c, syn_a, syn_b, syn_stride);
     if (st != HY_OK) return st;
     if (tmp) std::swap(cur, nxt);
   }
@@ -354,11 +412,116 @@ extern "C" hy_status hy_conv_plan_create(uint32_t log_n, const hy_conv_spec* spe
   p->counts[2] = (uint32_t)(p->ras_g.size() * p->n_groups);
   p->counts[3] = (uint32_t)(p->ir_g.size() * p->n_out + (p->has_combine ? p->n_out : 0));
   p->counts[4] = (uint32_t)(p->n_groups * p->n_in * p->f2());  // PMult terms (PRCR reuses plaintexts)
+  memcpy(p->eff_counts, p->counts, sizeof(p->counts));
   *out = p;
   return HY_OK;
 }
 
 extern "C" void hy_conv_plan_destroy(hy_conv_plan* p) { delete p; }
+
+// ------------------------------------------------------------------ limited key sets (DESIGN R-KEYSET)
+extern "C" hy_status hy_keyset_create(uint32_t log_n, const int32_t* amounts, uint32_t n_amounts, hy_keyset** out) {
+  if (!out || (!amounts && n_amounts) || log_n < 4 || log_n > 17) return fail(HY_E_ARG, "null / log_n");
+  auto* k = new hy_keyset();
+  k->n = (1ll << log_n) / 2;
+  for (uint32_t i = 0; i < n_amounts; ++i) {
+    const int64_t r = (((int64_t)amounts[i] % k->n) + k->n) % k->n;
+    if (r) k->loaded.push_back(r);
+  }
+  std::sort(k->loaded.begin(), k->loaded.end());
+  k->loaded.erase(std::unique(k->loaded.begin(), k->loaded.end()), k->loaded.end());
+  // breadth-first search from 0 over Z_n, edges = the loaded amounts in ascending order, FIFO queue: the first
+  // discovery of a node fixes its parent (the shortest decomposition, deterministic tie-break)
+  k->parent.assign(k->n, -1);
+  k->parent_amount.assign(k->n, -1);
+  std::vector<int64_t> q;
+  q.reserve(k->n);
+  std::vector<char> seen(k->n, 0);
+  seen[0] = 1;
+  q.push_back(0);
+  for (size_t h = 0; h < q.size(); ++h) {
+    const int64_t u = q[h];
+    for (int64_t a : k->loaded) {
+      const int64_t v = (u + a) % k->n;
+      if (seen[v]) continue;
+      seen[v] = 1;
+      k->parent[v] = (int32_t)u;
+      k->parent_amount[v] = (int32_t)a;
+      q.push_back(v);
+    }
+  }
+  *out = k;
+  return HY_OK;
+}
+
+extern "C" void hy_keyset_destroy(hy_keyset* k) { delete k; }
+
+extern "C" hy_status hy_keyset_decompose(const hy_keyset* k, int32_t r, int32_t* steps, uint32_t max_steps,
+                                         uint32_t* n_steps) {
+  if (!k || !n_steps) return fail(HY_E_ARG, "null");
+  const std::vector<int64_t> st = k->steps(r);
+  if (st.empty() && (((int64_t)r % k->n) + k->n) % k->n) return fail(HY_E_MISSING_KEY, "amount not reachable");
+  *n_steps = (uint32_t)st.size();
+  if (steps) {
+    if (st.size() > max_steps) return fail(HY_E_ARG, "steps buffer too small");
+    for (size_t i = 0; i < st.size(); ++i) steps[i] = (int32_t)st[i];
+  }
+  return HY_OK;
+}
+
+extern "C" hy_status hy_conv_plan_set_keyset(hy_conv_plan* p, const hy_keyset* k) {
+  if (!p) return fail(HY_E_ARG, "null plan");
+  p->decomp.clear();
+  // rebuild the key list from the plan's amounts: Slide taps must be loaded (they are hoisted: one ModUp shared
+  // by the tap rotations); every other amount is used directly when loaded, else through its decomposition
+  std::vector<int64_t> keys;
+  auto canon = [&](int64_t r) { return ((r % p->n) + p->n) % p->n; };
+  for (int64_t t : p->taps) {
+    const int64_t rr = canon(t);
+    if (!rr) continue;
+    if (k && !std::binary_search(k->loaded.begin(), k->loaded.end(), rr))
+      return fail(HY_E_MISSING_KEY, "a Slide (tap) amount is not in the key set");
+    keys.push_back(rr);
+  }
+  std::vector<int64_t> other = p->ras;
+  other.insert(other.end(), p->ras_g.begin(), p->ras_g.end());
+  other.insert(other.end(), p->ir_g.begin(), p->ir_g.end());
+  if (p->has_combine) other.push_back(p->combine);
+  for (int64_t r : other) {
+    const int64_t rr = canon(r);
+    if (!rr) continue;
+    if (!k || std::binary_search(k->loaded.begin(), k->loaded.end(), rr)) {
+      keys.push_back(rr);
+      continue;
+    }
+    if (k->n != p->n) return fail(HY_E_PLAN, "key set ring size differs from the plan's");
+    const std::vector<int64_t> st = k->steps(rr);
+    if (st.empty()) return fail(HY_E_MISSING_KEY, "an amount cannot be synthesized from the key set");
+    p->decomp[rr] = st;
+    keys.insert(keys.end(), st.begin(), st.end());
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  p->rots = keys;
+  // effective counts: each rotation counted once per step
+  auto eff = [&](const std::vector<int64_t>& rs) {
+    int64_t c = 0;
+    for (int64_t r : rs) c += (int64_t)p->steps_of(r).size() * (canon(r) != 0);
+    return c;
+  };
+  p->eff_counts[0] = p->counts[0];
+  p->eff_counts[1] = (uint32_t)(eff(p->ras) * p->n_groups);
+  p->eff_counts[2] = (uint32_t)(eff(p->ras_g) * p->n_groups);
+  p->eff_counts[3] = (uint32_t)(eff(p->ir_g) * p->n_out + (p->has_combine ? eff({p->combine}) * p->n_out : 0));
+  p->eff_counts[4] = p->counts[4];
+  return HY_OK;
+}
+
+extern "C" hy_status hy_conv_plan_eff_counts(const hy_conv_plan* p, uint32_t* counts) {
+  if (!p || !counts) return fail(HY_E_ARG, "null");
+  memcpy(counts, p->eff_counts, sizeof(p->eff_counts));
+  return HY_OK;
+}
 
 extern "C" hy_status hy_conv_plan_query(const hy_conv_plan* p, uint32_t* n_in, uint32_t* n_out, uint32_t* n_pt,
                                         uint32_t* has_mask, uint32_t* n_rot, int32_t* rots, uint32_t* counts) {
@@ -401,8 +564,9 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   // CA: slid inputs + acc + (up to) two ciphertexts per SISO group (group sums, masked groups)
   // (8 = one block of MulFilter&Sum accumulators)
   // (+ n_groups ping-pong ciphertexts for the RaS / RaS_g / IR_g steps)
-  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + 3 * p->n_groups) * ct;
-  return (p->n_out * (f2 + 1) + 8) * ct;                          // tap accumulators + one sum per output
+  // (+ 2 n_groups for the intermediate steps of synthesized rotations with a limited key set)
+  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + (p->decomp.empty() ? 3 : 5) * p->n_groups) * ct;
+  return (std::max<size_t>(p->n_out * (f2 + 1), 6) + 8) * ct;     // tap accumulators + one sum per output
 }
 
 extern "C" hy_status hy_conv_encode_weights(hy_ctx* c, const hy_conv_plan* p, const double* K, const double* bias,
@@ -465,15 +629,15 @@ namespace {
 // pp / pp_stride: no ping-pong ciphertexts for the RaS_g / IR_g steps (nullptr: in place).
 hy_status ra_tail(const Ctx& x, std::vector<const uint64_t*>& sums, std::vector<uint64_t*>& dst, uint32_t level,
                   const uint64_t* mask, uint64_t* tmp, size_t ct_l, uint64_t* const* out, uint64_t* pp = nullptr,
-                  size_t pp_stride = 0) {
+                  size_t pp_stride = 0, uint64_t* sa = nullptr, uint64_t* sb = nullptr) {
   const hy_conv_plan* p = x.p;
   const size_t no = sums.size();
   hy_status stt = rescale_multi(x.c, sums.data(), (uint32_t)no, level, dst.data(), x.s);
-  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g, pp, pp_stride);
+  if (stt == HY_OK) stt = ras_all(x, dst, level - 1, p->ras_g, pp, pp_stride, sa, sb, pp_stride);
   if (stt == HY_OK && p->has_mask) {
     std::vector<uint64_t*> fin(out, out + no);
     stt = mask_rescale(x, dst, mask, level - 1, tmp, ct_l, fin);
-    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g, pp, pp_stride);
+    if (stt == HY_OK) stt = ras_all(x, fin, level - 2, p->ir_g, pp, pp_stride, sa, sb, pp_stride);
   }
   return stt;
 }
@@ -589,8 +753,11 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
       if (stt != HY_OK) return stt;
     }
     uint64_t* pp = gbuf + 2 * G * ct_m;  // G ping-pong ciphertexts (hy_conv_scratch_words)
-    stt = ras_all(x, gp, level - 1, p->ras, pp, ct_m);                        // RaS over C_a
-    if (stt == HY_OK) stt = ras_all(x, gp, level - 1, p->ras_g, pp, ct_m);    // RaS_g over C_g
+    // limited key sets: 2 G more for the intermediate steps of synthesized rotations
+    uint64_t* sa = p->decomp.empty() ? nullptr : pp + G * ct_m;
+    uint64_t* sb = p->decomp.empty() ? nullptr : pp + 2 * G * ct_m;
+    stt = ras_all(x, gp, level - 1, p->ras, pp, ct_m, sa, sb, ct_m);                        // RaS over C_a
+    if (stt == HY_OK) stt = ras_all(x, gp, level - 1, p->ras_g, pp, ct_m, sa, sb, ct_m);    // RaS_g over C_g
     if (stt != HY_OK || (!p->has_mask && !ds)) return stt == HY_OK ? cuda_check("hy_caconv") : stt;
     // IR_g: mask (one level) ...
     std::vector<uint64_t*> masked(G);
@@ -600,16 +767,15 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
     std::vector<uint64_t*> fin(out, out + (oe - ob));
     if (ds) {  // ... merge the two groups of each output into the doubled gap (DESIGN R-DSCONV) ...
       const size_t J = oe - ob;
-      std::vector<const uint64_t*> keys(J, x.key(p->combine)), b(J), a(J);
-      std::vector<int32_t> rr(J, (int32_t)p->combine);
+      std::vector<const uint64_t*> b(J), a(J);
       for (size_t j = 0; j < J; ++j) {
         a[j] = masked[2 * j];
         b[j] = masked[2 * j + 1];
       }
-      stt = hrot_multi(c, keys.data(), b.data(), level - 2, rr.data(), (uint32_t)J, fin.data(), a.data(), x.s);
+      stt = hrot_steps(x, p->combine, level - 2, b, fin, &a, sa, sb, ct_m);
       if (stt != HY_OK) return stt;
     }
-    stt = ras_all(x, fin, level - 2, p->ir_g, pp, ct_m);           // ... and replicate
+    stt = ras_all(x, fin, level - 2, p->ir_g, pp, ct_m, sa, sb, ct_m);           // ... and replicate
     if (stt != HY_OK) return stt;
     return cuda_check("hy_caconv");
   }
@@ -655,7 +821,10 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
   }
   // ping-pong buffers: the second tap accumulator of every output (consumed by its HRotSum; f^2 >= 2)
   const bool ppok = f2 >= 2;
-  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, out, ppok ? accs + ct_l : nullptr, f2 * ct_l);
+  // limited key sets: the third and fourth tap accumulators hold the intermediate steps (f^2 >= 4)
+  const bool syn = !p->decomp.empty() && f2 >= 4;
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, out, ppok ? accs + ct_l : nullptr, f2 * ct_l,
+                syn ? accs + 2 * ct_l : nullptr, syn ? accs + 3 * ct_l : nullptr);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv");
 }
@@ -767,7 +936,8 @@ extern "C" hy_status hy_raconv_finish(hy_ctx* c, const hy_conv_plan* p, const ui
   if (stt != HY_OK) return stt;
   std::vector<const uint64_t*> sums{sum};
   std::vector<uint64_t*> dst{p->has_mask ? dstb : out};
-  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out, scratch + 3 * ct_l, ct_l);
+  stt = ra_tail(x, sums, dst, level, mask, tmp, ct_l, &out, scratch + 3 * ct_l, ct_l, scratch + 4 * ct_l,
+                scratch + 5 * ct_l);
   if (stt == HY_OK) stt = add_bias(c, p, level, pts, out_index, out_index + 1, &out, stream);
   if (stt != HY_OK) return stt;
   return cuda_check("hy_raconv_finish");

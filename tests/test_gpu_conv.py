@@ -222,3 +222,57 @@ def test_raconv_tap_sharding_with_bias(ctx_toy):
         p.raconv_partial(evks, cts, level, pts, 0, b_, e_, st)
         total += st
     assert np.array_equal(to_np(p.raconv_finish(evks, level, pts, total, 0)), to_np(want))
+
+
+@pytest.mark.parametrize("idx", [3, 4, 5], ids=["ra21", "ca_g2", "dsconv"])
+def test_toy_layers_limited_keyset_bit_exact(ctx_toy, orc_toy, idx):
+    """a limited rotation-key set (DESIGN R-KEYSET): the Slide amounts plus {1, 3 W_p, 7}; every
+    RaS / RaS_g / IR_g / combine amount is synthesized as a chain of loaded rotations -- bit-exact vs the oracle's
+    composition (the same BFS decomposition), and decrypting to conv2d within 2^-10"""
+    import paper_2302_02407_b200 as hy
+    spec, level = TOY[idx], orc_toy.nq - 1
+    X = synth.image(18, spec.ci, spec.w)
+    K = synth.conv_weight(19, spec.co, spec.ci, spec.f)
+    plan = H.plan_caconv(spec, K) if spec.algo == "CA" else H.plan_raconv(spec, K)
+    amounts = [r % spec.n for r in plan.taps if r % spec.n] + [1, 3 * spec.wp, 7]
+    p = hy.ConvPlan(ctx_toy, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo)
+    p.set_keyset(hy.KeySet(12, amounts))
+    ks = H.KeySet(spec.n, amounts)
+    assert sum(p.eff_counts.values()) > sum(p.counts.values())   # something is synthesized
+    fin = H.Fmt("CA" if spec.algo == "CA" else "RA", spec.n, spec.wp, spec.g, spec.m, spec.d)
+    cts = [ctx_toy.encrypt(SK, 904, i, ctx_toy.encode(v, 2**40, level), level) for i, v in enumerate(H.pack(X, fin))]
+    outs = p.run({r: ctx_toy.keygen_rot(SK, EK, r) for r in p.rots}, cts, level, p.encode_weights(K, level))
+    o = orc_toy
+    octs = [o.encrypt(SK, 904, i, o.encode(v, 2**40, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+    oevks = {r: o.keygen_rot(SK, EK, r) for r in H.keyset_amounts(plan, ks)}
+    ref = H.EncConv(o, plan, oevks, keyset=ks).run(octs)
+    for a, r in zip(outs, ref):
+        assert np.array_equal(to_np(a), r.data)
+    dec = [np.real(o.decode(o.decrypt(SK, r))) for r in ref]
+    got = H.unpack(dec, plan.fout, spec.co, spec.wo, spec.wo)
+    want = H.conv2d(X, K, spec.s)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 2 ** -10
+
+
+def test_resnet20_layer_positive_power_keyset(ctx_hyp, orc_hyp):
+    """ResNet-20 stage-2 CAConv at N = 2^16 with the Slide keys + positive powers of two loaded: the negative IR_g
+    amounts are synthesized; a sampled output bit-exact vs the oracle"""
+    import paper_2302_02407_b200 as hy
+    spec, level, j = R20["L2_ca"], 9, 1
+    K = synth.conv_weight(24, spec.co, spec.ci, spec.f)
+    plan = H.plan_caconv(spec, K)
+    amounts = [r % spec.n for r in plan.taps if r % spec.n] + [1 << i for i in range(15)]
+    p = hy.ConvPlan(ctx_hyp, spec.ci, spec.co, spec.w, spec.f, spec.s, spec.wp, spec.g, spec.m, spec.d, spec.algo)
+    p.set_keyset(hy.KeySet(16, amounts))
+    ks = H.KeySet(spec.n, amounts)
+    assert p.eff_counts["IR_g"] > p.counts["IR_g"]
+    X = synth.image(25, spec.ci, spec.w)
+    fin = H.Fmt("CA", spec.n, spec.wp, spec.g, spec.m, spec.d)
+    cts = [ctx_hyp.encrypt(SK, 905, i, ctx_hyp.encode(v, 2**42, level), level) for i, v in enumerate(H.pack(X, fin))]
+    out = p.run({r: ctx_hyp.keygen_rot(SK, EK, r) for r in p.rots}, cts, level, p.encode_weights(K, level),
+                out_begin=j, out_end=j + 1)[0]
+    o = orc_hyp
+    octs = [o.encrypt(SK, 905, i, o.encode(v, 2**42, level)) for i, v in enumerate(H.pack(X, plan.fin))]
+    oevks = {r: o.keygen_rot(SK, EK, r) for r in H.keyset_amounts(plan, ks)}
+    ref = H.EncConv(o, plan, oevks, keyset=ks).run(octs, [j])[0]
+    assert np.array_equal(to_np(out), ref.data)
