@@ -393,6 +393,68 @@ def layer_roofline(p, algo: str, level: int, ms: float, kp: int = 4, alpha: int 
             "bound": "fp64" if ops / fp64_peak > alg / (pk["hbm_gbs"] * 1e9) else "hbm"}
 
 
+def keyset_report(log_n: int = 16):
+    """f2 (tb:Rot and Boot P:1147-1168): the networks' conv rotations under limited
+    rotation-key sets (host-side plans; DESIGN R-KEYSET).  Readings of the loaded set: every key the plans need;
+    the Slide keys + both-sign powers of two (bootstrapping's power-of-two rotation keys); the Slide keys + positive
+    powers of two only; the Slide keys only.  Reported: loaded keys, their memory (6-byte packed and at the paper's
+    168 MB), conv rotations and "eff. total" (each synthesized rotation counted once per key switch)."""
+    import paper_2302_02407_b200 as hy
+    n = 1 << (log_n - 1)
+    pow2 = [1 << i for i in range(log_n - 1)]
+    key_mib = 2 * 6 * 28 * (1 << log_n) * 6 / 2**20
+    out = {}
+    for net, layers in (("ResNet-20", R20_LAYERS), ("ResNet-18", R18_LAYERS)):
+        plans = []
+        slide = set()
+        for name, spec, mult in layers:
+            S = spec[10] if len(spec) > 10 else 1
+            plans.append((name, hy.ConvPlan(None, *spec[:10], log_n=log_n, S=S), mult))
+            slide |= {t % n for t in _tap_amounts(spec) if t % n}
+        slide = sorted(slide)
+        rows = {}
+        for kname, extra in (("all_needed", None), ("slide+pm2i", pow2 + [n - x for x in pow2]),
+                             ("slide+p2i", pow2), ("slide_only", [])):
+            ks = None if extra is None else hy.KeySet(log_n, slide + extra)
+            tot = eff = 0
+            used = set()
+            for name, p, mult in plans:
+                p.set_keyset(ks)
+                c, e = p.counts, p.eff_counts
+                tot += mult * sum(c[k] for k in ("Slide", "RaS", "RaS_g", "IR_g"))
+                eff += mult * sum(e[k] for k in ("Slide", "RaS", "RaS_g", "IR_g"))
+                used |= set(p.rots)
+            nk = len(used)
+            rows[kname] = {"loaded_keys_used": nk, "conv_rotations": tot, "eff_total": eff,
+                           "evk_gib_packed": nk * key_mib / 1024, "evk_gib_8byte_words": nk * 168 / 1024}
+        out[net] = rows
+    out["paper"] = {"ResNet-20": {"total": 919, "eff_total": 1002}, "ResNet-18": {"total": 7359, "eff_total": 9095},
+                    "evks": "66 unique Evks = 11.1 GB at Set_hyp (P:1243); one Evk = 2 x 6 x 28 limbs x 512 KiB = "
+                            "168 MiB (P:1208), i.e. 176 MB (P:1240), and 66 x 168 MiB = 11.1 GiB",
+                    "note": "the paper's totals include its IR layout (lost figures, P:996-1000); ours count the "
+                            "plans of DESIGN R-LAYOUT / R-DSCONV (stem excluded for ResNet-18)"}
+    return out
+
+
+def plan_search_report():
+    """f3: the (m, d) plan search of paper_2302_02407_b200.planner over the product's
+    implementable plans, ranked by the paper's per-operation CPU costs (tb:Benchmark P:148); host only."""
+    from paper_2302_02407_b200 import planner as P
+    out = {}
+    for net in (P.RESNET20, P.RESNET18):
+        out[net.name] = [{"mds": p.fmts, "conv_rotations": p.rotations, "pmults": p.pmults, "boots": p.boots,
+                          "modelled_cpu_s": p.time_ms() / 1000} for p in P.search(net)]
+    out["paper_optimal"] = {"ResNet-20": {"mds": [[1, 2], [2, 4], [4, 8]], "boots": 10, "cpu_s": 37.57},
+                            "ResNet-18": {"mds": [[1, 1], [2, 2], [4, 4], [8, 8]], "boots": 65, "cpu_s": 356.97}}
+    return out
+
+
+def _tap_amounts(spec):
+    ci, co, w, f, s, wp, g = spec[:7]
+    pad = (f - 1) // 2
+    return [(j1 - pad) * g * wp + (j2 - pad) * g for j1 in range(f) for j2 in range(f)]
+
+
 def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet-20"):
     """Per-layer device time of every conv layer type (fresh encryption at its scheduled level,
     outputs sharded over ranks + all-gathered), and the network's conv total."""
@@ -942,6 +1004,8 @@ def run_ours(args, ws, rank, local):
             "resnet18_conv": conv18,
             "resnet20_blocks": blocks,
             "c1_raconv": c1,
+            "keyset_f2": keyset_report(),
+            "plan_search_f3": plan_search_report(),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,  # our kernels launched inside the timed region (K steps)
