@@ -360,6 +360,48 @@ def ks_fp64_ops(level: int, variant: str, alpha: int = 4, kp: int = 4) -> float:
     raise ValueError(variant)
 
 
+NVLINK_GBS = 700.0  # measured all-gather / peer-copy class bandwidth per direction (B200_PROFILING.md: 725-770 GB/s)
+
+
+def scaling_model(p, algo: str, level: int, ms: float, hoisted_rate: float, plain_rate: float):
+    """Per-rank cost model of a conv layer on G GPUs from its measured 1-GPU time:
+    t_G = t_repeated + (t_1 - t_repeated) / G + t_comm(G), with
+      CAConv, n_in < G (ResNet-20): Slide_f is repeated on every rank (n_in (f^2 - 1) hoisted rotations at the
+        measured hoisted rate); outputs all-gathered;
+      CAConv, n_in >= G (ResNet-18): Slide sharded by input; slid ciphertexts and outputs all-gathered;
+      RAConv, n_o < G (ResNet-20): taps sharded; one all-reduce of the lazy-sum state, then the ModDown, rescale,
+        RaS_g / IR_g repeated on every rank (their plain rotations at the measured plain rate);
+      RAConv, n_o >= G: outputs sharded and all-gathered.
+    Transfers at NVLINK_GBS per direction; all-gather moves (G-1)/G of the data into each rank."""
+    N_ = N
+    ct_in = 2 * (level + 1) * N_ * 8
+    ct_out = 2 * (p.out_level(level) + 1) * N_ * 8
+    f2 = p.f * p.f
+    out = {}
+    for G in (2, 4, 8):
+        frac = (G - 1) / G
+        if algo == "CA":
+            if p.n_in >= G:
+                rep = 0.0
+                comm = frac * (p.n_in * f2 * ct_in + p.n_out * ct_out) / (NVLINK_GBS * 1e9) * 1e3
+            else:
+                rep = 1e3 * p.n_in * (f2 - 1) / hoisted_rate if f2 > 1 else 0.0
+                comm = frac * p.n_out * ct_out / (NVLINK_GBS * 1e9) * 1e3
+        else:
+            if p.n_out < G:
+                tail = p.counts["RaS_g"] + p.counts["IR_g"]
+                rep = 1e3 * (p.n_out + tail) / plain_rate
+                state = (2 * (level + 1 + 4) + 2 * (level + 1)) * N_ * 8 * p.n_out
+                comm = 2 * frac * state / (NVLINK_GBS * 1e9) * 1e3
+            else:
+                rep = 0.0
+                comm = frac * p.n_out * ct_out / (NVLINK_GBS * 1e9) * 1e3
+        rep = min(rep, ms)
+        tg = rep + (ms - rep) / G + comm
+        out[f"G{G}"] = {"ms": tg, "speedup": ms / tg, "repeated_ms": rep, "comm_ms": comm}
+    return out
+
+
 def layer_roofline(p, algo: str, level: int, ms: float, kp: int = 4, alpha: int = 4):
     """Per-layer roofline fractions: HBM -- algorithmic bytes (input cts, the stored weight
     plaintexts and mask, one read of every distinct evaluation-key slice the layer uses, output cts; intermediates
@@ -455,13 +497,14 @@ def _tap_amounts(spec):
     return [(j1 - pad) * g * wp + (j2 - pad) * g for j1 in range(f) for j2 in range(f)]
 
 
-def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet-20"):
+def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet-20", rates=(41000.0, 30000.0)):
     """Per-layer device time of every conv layer type (fresh encryption at its scheduled level,
-    outputs sharded over ranks + all-gathered), and the network's conv total."""
+    outputs sharded over ranks + all-gathered), and the network's conv total.  rates: measured hoisted (l+1 = 10)
+    and plain (l+1 = 7) keyswitch/s for the scaling model."""
     import torch
 
     import paper_2302_02407_b200 as hy
-    from paper_2302_02407_b200.dist import all_gather_cts, raconv_tap_sharded, shard
+    from paper_2302_02407_b200.dist import all_gather_cts, caconv_slide_sharded, raconv_tap_sharded, shard
 
     sk, ek = synth.SEED_SK, synth.SEED_EVK
     keys = {}
@@ -489,10 +532,15 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
         evks = [keys[r] for r in p.rots]
 
         tap_shard = algo == "RA" and ws > 1 and p.n_out < ws  # ResNet-20 RAConv: one output, shard the taps
+        # CAConv with at least one input per rank (ResNet-18): shard Slide_f by input and all-gather the slid
+        # ciphertexts instead of repeating every Slide rotation on every rank
+        slide_shard = algo == "CA" and ws > 1 and p.n_in >= ws
 
         def step():
             if tap_shard:  # every rank ends with every output: no gather
                 return [raconv_tap_sharded(p, evks, cts, level, pts, o, scratch) for o in range(p.n_out)]
+            if slide_shard:
+                return caconv_slide_sharded(p, evks, cts, level, pts, scratch)
             if e > b:
                 p.run(evks, cts, level, pts, scratch, b, e, outs)
             if ws > 1:
@@ -523,7 +571,10 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
         ctx.time_kernels(0)
         layers[name] = {"ms": ms, "mult": mult, "n_in": p.n_in, "n_out": p.n_out, "level_in": level,
                         "roofline": layer_roofline(p, algo, level, ms),
-                        "sharding": "taps (all-reduce)" if tap_shard else ("outputs (all-gather)" if ws > 1 else None),
+                        "scaling_model": scaling_model(p, algo, level, ms, rates[0], rates[1]) if ws == 1 else None,
+                        "sharding": "taps (all-reduce)" if tap_shard else (
+                            "Slide by input + outputs (two all-gathers)" if slide_shard else (
+                                "outputs (all-gather)" if ws > 1 else None)),
                         "rotations": p.counts, "gpu_launches": launches, "weight_pts": p.n_pt, "prcr_segments": S,
                         "multi_gpu_check": identity,
                         "family_ms": fams}
@@ -543,7 +594,14 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
     n_keys = len(keys)
     key_info = {"distinct_rotation_keys": n_keys, "gib_at_full_level": n_keys * ctx.evk_bytes() / 2**30,
                 "non_slide_amounts_all_power_of_two": True}
-    return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note, "keys": key_info}
+    model = None
+    if ws == 1:
+        model = {}
+        for G in (2, 4, 8):
+            tg = sum(v["mult"] * v["scaling_model"][f"G{G}"]["ms"] for v in layers.values())
+            model[f"G{G}"] = {"total_ms": tg, "speedup": total / tg}
+    return {"layers": layers, "total_ms": total, "n_gpus": ws, "network": net, "note": note, "keys": key_info,
+            "scaling_model": model}
 
 
 def bench_blocks(ctx, ws, rank, steps, warmup, timed):
@@ -953,8 +1011,11 @@ def run_ours(args, ws, rank, local):
     if not args.no_conv:
         del evks, cts, outs, houts
         torch.cuda.empty_cache()
-        conv = bench_conv(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
-        conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18")
+        rates = (41000.0, 30000.0)
+        if variants:
+            rates = (variants["l+1=10"]["hoisted"]["keyswitch_per_s"], variants["l+1=7"]["plain"]["keyswitch_per_s"])
+        conv = bench_conv(ctx, ws, rank, max(2, args.steps // 2), 1, timed, rates=rates)
+        conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18", rates)
         blocks = bench_blocks(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
 
     c1 = None

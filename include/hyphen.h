@@ -297,6 +297,18 @@ hy_status hy_caconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const
 hy_status hy_raconv(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
                     const uint64_t* const* d_in, uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch,
                     uint32_t out_begin, uint32_t out_end, uint64_t* const* d_out, void* stream);
+/* CAConv Slide sharding (multi-GPU): Slide_f is the part of a CAConv every output
+ * needs, so output-sharded ranks would all repeat it.  hy_caconv_slide runs the hoisted Slide of inputs
+ * [in_begin, in_end) into d_slid: ciphertext (i - in_begin) * f^2 + t at level l ([2][l+1][N] each, the identity
+ * tap a copy of the input); ranks slide disjoint input ranges and all-gather the buffers, and hy_caconv_slid runs
+ * the rest of the layer (MulFilter&Sum, rescale, RaS, IR, bias) for outputs [out_begin, out_end) from the complete
+ * slid buffer [n_in][f^2] -- bit-identical to hy_caconv.  Errors as hy_caconv. */
+hy_status hy_caconv_slide(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks,
+                          const uint64_t* const* d_in, uint32_t level, uint32_t in_begin, uint32_t in_end,
+                          uint64_t* d_slid, void* stream);
+hy_status hy_caconv_slid(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t* const* d_evks, const uint64_t* d_slid,
+                         uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch, uint32_t out_begin,
+                         uint32_t out_end, uint64_t* const* d_out, void* stream);
 /* RAConv tap sharding: the multi-GPU exchange step for layers with fewer outputs than GPUs (ResNet-20
  * RAConv has one output ciphertext).  An output of RAConv_Reorder is
  * sum_t HRot_{r_t}(acc_t) over the f^2 taps with ONE ModDown (Alg. P:727-733).  hy_raconv_partial

@@ -116,6 +116,8 @@ SIGNATURES = {
     "hy_import_coeff": (C.c_int, [_P, C.POINTER(_U64), C.POINTER(_U32), _U32, _P, _P]),
     "hy_caconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
     "hy_raconv": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _PP, _P]),
+    "hy_caconv_slide": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _U32, _P, _P]),
+    "hy_caconv_slid": (C.c_int, [_P, _P, _PP, _P, _U32, _P, _P, _U32, _U32, _PP, _P]),
     "hy_raconv_partial_words": (C.c_size_t, [_P, _U32]),
     "hy_raconv_partial": (C.c_int, [_P, _P, _PP, _PP, _U32, _P, _P, _U32, _U32, _U32, _P, _P]),
     "hy_raconv_finish": (C.c_int, [_P, _P, _PP, _U32, _P, _P, _P, _U32, _P, _P]),
@@ -577,6 +579,31 @@ class ConvPlan:
         fn = lib().hy_caconv if self.algo == 0 else lib().hy_raconv
         _check(fn(self.ctx._c, self._p, _ptr_array(evks), _ptr_array(cts), level, _ptr(pts), _ptr(scratch),
                   out_begin, out_end, _ptr_array(outs), self.ctx._stream()))
+        return outs
+
+    # ---- CAConv Slide sharding (include/hyphen.h hy_caconv_slide / hy_caconv_slid)
+    def slide(self, evks, cts, level, in_begin=0, in_end=None, out=None):
+        """Slide_f of inputs [in_begin, in_end) -> [(in_end - in_begin) * f^2][2][l+1][N] (hy_caconv_slide)"""
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        in_end = self.n_in if in_end is None else in_end
+        f2 = self.f * self.f
+        out = self.ctx.empty((in_end - in_begin) * f2, *self.ctx.ct_shape(level)) if out is None else out
+        if in_end > in_begin:
+            _check(lib().hy_caconv_slide(self.ctx._c, self._p, _ptr_array(evks), _ptr_array(cts), level, in_begin,
+                                         in_end, _ptr(out), self.ctx._stream()))
+        return out
+
+    def run_slid(self, evks, slid, level, pts, scratch=None, out_begin=0, out_end=None, outs=None):
+        """the layer from a complete slid buffer (hy_caconv_slid)"""
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        out_end = self.n_out if out_end is None else out_end
+        lo = self.out_level(level)
+        outs = [self.ctx.empty(*self.ctx.ct_shape(lo)) for _ in range(out_end - out_begin)] if outs is None else outs
+        scratch = self.scratch(level) if scratch is None else scratch
+        _check(lib().hy_caconv_slid(self.ctx._c, self._p, _ptr_array(evks), _ptr(slid), level, _ptr(pts),
+                                    _ptr(scratch), out_begin, out_end, _ptr_array(outs), self.ctx._stream()))
         return outs
 
     # ---- RAConv tap sharding (include/hyphen.h hy_raconv_partial / hy_raconv_finish)

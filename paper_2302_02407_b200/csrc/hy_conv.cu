@@ -662,14 +662,17 @@ hy_status ra_taps(const Ctx& x, const uint64_t* const* in, uint32_t level, const
   return HY_OK;
 }
 
+// pre_slid (CAConv only): a complete Slide_f result [n_in][f^2] ciphertexts (hy_caconv_slide layout); the Slide
+// step is then skipped (multi-GPU Slide sharding) and `in` is not read
 hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks, const uint64_t* const* in,
                     uint32_t level, const uint64_t* pts, uint64_t* scratch, uint32_t ob, uint32_t oe,
-                    uint64_t* const* out, void* stream) {
-  if (!c || !p || !evks || !in || !pts || !scratch || !out) return fail(HY_E_ARG, "null");
+                    uint64_t* const* out, void* stream, const uint64_t* pre_slid = nullptr) {
+  if (!c || !p || !evks || (!in && !pre_slid) || !pts || !scratch || !out) return fail(HY_E_ARG, "null");
   if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
   if (ob > oe || oe > p->n_out) return fail(HY_E_PLAN, "output range outside the plan");
-  for (int64_t i = 0; i < p->n_in; ++i)
-    if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
+  if (!pre_slid)
+    for (int64_t i = 0; i < p->n_in; ++i)
+      if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
   Ctx x{c, p, evks, st(stream)};
   const size_t N = c->N, f2 = (size_t)p->s.f * p->s.f;
   const size_t ct_l = 2 * (level + 1) * N;
@@ -689,7 +692,9 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
     // Slide_f: hoisted rotations of every input
     std::vector<std::vector<const uint64_t*>> slid(p->n_in, std::vector<const uint64_t*>(f2));
     uint64_t* sbuf = scratch;
-    for (int64_t i = 0; i < p->n_in; ++i) {
+    for (int64_t i = 0; i < p->n_in && pre_slid; ++i)
+      for (size_t t = 0; t < f2; ++t) slid[i][t] = pre_slid + ((size_t)i * f2 + t) * ct_l;
+    for (int64_t i = 0; i < p->n_in && !pre_slid; ++i) {
       std::vector<int32_t> rs;
       std::vector<const uint64_t*> ks;
       std::vector<uint64_t*> outs;
@@ -864,6 +869,48 @@ extern "C" hy_status hy_raconv(hy_ctx* c, const hy_conv_plan* p, const uint64_t*
                                uint32_t out_begin, uint32_t out_end, uint64_t* const* out, void* stream) {
   if (p && p->s.algo != HY_CONV_RA) return fail(HY_E_PLAN, "plan is not an RAConv plan");
   return conv_run(c, p, evks, in, level, pts, scratch, out_begin, out_end, out, stream);
+}
+
+extern "C" hy_status hy_caconv_slide(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
+                                     const uint64_t* const* in, uint32_t level, uint32_t in_begin, uint32_t in_end,
+                                     uint64_t* slid, void* stream) {
+  if (!c || !p || !evks || !in || !slid) return fail(HY_E_ARG, "null");
+  if (p->s.algo != HY_CONV_CA) return fail(HY_E_PLAN, "plan is not a CAConv plan");
+  if (level >= c->n_q || level < 1u + (p->has_mask ? 1u : 0u)) return fail(HY_E_LEVEL_EXHAUSTED, "level too low");
+  if (in_begin > in_end || in_end > p->n_in) return fail(HY_E_PLAN, "input range outside the plan");
+  const size_t f2 = (size_t)p->s.f * p->s.f, ct_l = 2ull * (level + 1) * c->N;
+  Ctx x{c, p, evks, st(stream)};
+  for (uint32_t i = in_begin; i < in_end; ++i) {
+    if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
+    std::vector<int32_t> rs;
+    std::vector<const uint64_t*> ks;
+    std::vector<uint64_t*> outs;
+    for (size_t t = 0; t < f2; ++t) {
+      uint64_t* o = slid + ((size_t)(i - in_begin) * f2 + t) * ct_l;
+      if (p->taps[t] % p->n == 0) {
+        cudaMemcpyAsync(o, in[i], ct_l * 8, cudaMemcpyDeviceToDevice, x.s);
+        continue;
+      }
+      rs.push_back((int32_t)p->taps[t]);
+      ks.push_back(x.key(p->taps[t]));
+      outs.push_back(o);
+    }
+    if (!rs.empty()) {
+      hy_status stt = hy_hrot_hoisted(c, ks.data(), in[i], level, rs.data(), (uint32_t)rs.size(), outs.data(), stream);
+      if (stt != HY_OK) return stt;
+    }
+  }
+  return cuda_check("hy_caconv_slide");
+}
+
+extern "C" hy_status hy_caconv_slid(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evks,
+                                    const uint64_t* slid, uint32_t level, const uint64_t* pts, uint64_t* scratch,
+                                    uint32_t out_begin, uint32_t out_end, uint64_t* const* out, void* stream) {
+  if (!slid) return fail(HY_E_ARG, "null slid buffer");
+  if (p && p->s.algo != HY_CONV_CA) return fail(HY_E_PLAN, "plan is not a CAConv plan");
+  hy_status st = conv_core(c, p, evks, nullptr, level, pts, scratch, out_begin, out_end, out, stream, slid);
+  if (st != HY_OK) return st;
+  return add_bias(c, p, level, pts, out_begin, out_end, out, stream);
 }
 
 extern "C" size_t hy_raconv_partial_words(const hy_ctx* c, uint32_t level) {

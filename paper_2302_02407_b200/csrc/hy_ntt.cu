@@ -705,32 +705,6 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_final(const __grid_constant_
 // row's stage buffer doubles as the warp's transpose buffer once it is in registers.  Hoisted: the Galois
 // permutation maps a 256-word row onto one row (the high index bits of kappa depend only on high bits), so
 // the source row is copied whole and gathered from shared memory.
-namespace tma {
-__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(saddr(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint64_t* b, uint32_t bytes = 2048) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   saddr(dst)),
-               "l"(src), "r"(bytes), "r"(saddr(b))
-               : "memory");
-}
-__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-}  // namespace tma
 
 // per warp: twiddle heap + NST stages x (e0, e1, x) rows, and NST mbarriers
 __host__ __device__ constexpr int rows_warp_words(int nst) { return 256 * (1 + 3 * nst); }

@@ -80,6 +80,157 @@ __global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBl
     }
 }
 
+// The same block with the PRot gathers staged through shared memory (PRCR reuses one stored weight
+// plaintext per family through PRot).  In the NTT domain the Galois permutation maps every 256-word row onto ONE
+// source row (its high index bits depend only on the row, hy_arith.cuh aut_index), so a CTA = one row x of limb i
+// loads, per operand j, the M source rows of its terms with coalesced 2 KB reads (instead of M scattered 8-byte
+// gathers per thread, one 32-byte sector each) into a double-buffered shared tile, then gathers from shared memory.
+// The next operand's ciphertext words and weight rows are loaded into registers while the current one is
+// multiplied.  grid (N/256, l+1), CTA = 256 threads (one row).
+template <int M>
+__global__ void __launch_bounds__(256) k_pmult_rows(const __grid_constant__ PBlock b, int J, DevTables dt, int level,
+                                                    int logN, int accumulate) {
+  __shared__ double W[2][M][256];
+  const size_t N = (size_t)1 << logN;
+  const int t = threadIdx.x;
+  const uint32_t r = blockIdx.x, x = r * 256 + t;
+  const int i = blockIdx.y;
+  const size_t n = level + 1;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  double acc[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  uint64_t pw[M], p0, p1;
+  auto load = [&](int j) {
+    p0 = __ldcs(b.ct[j] + (size_t)i * N + x);
+    p1 = __ldcs(b.ct[j] + (n + i) * N + x);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t sr = k != 1 ? aut_index(r * 256u, k, logN) >> 8 : r;
+      pw[m] = b.pt_base[((size_t)b.pt_idx[m][j] * n + i) * N + (size_t)sr * 256 + t];
+    }
+  };
+  load(0);
+#pragma unroll
+  for (int m = 0; m < M; ++m) W[0][m][t] = u2d(pw[m]);
+  double c0 = u2d(p0), c1 = u2d(p1);
+  __syncthreads();
+  for (int j = 0; j < J; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < J) load(j + 1);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t pos = k != 1 ? aut_index(x, k, logN) & 255u : (uint32_t)t;
+      const double w = W[buf][m][pos];
+      acc[m][0] += fmulmod(c0, w, q, qinv);
+      acc[m][1] += fmulmod(c1, w, q, qinv);
+    }
+    if ((j & 3) == 3) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        acc[m][0] = fred(acc[m][0], q, qinv);
+        acc[m][1] = fred(acc[m][1], q, qinv);
+      }
+    }
+    if (j + 1 < J) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) W[buf ^ 1][m][t] = u2d(pw[m]);
+      c0 = u2d(p0);
+      c1 = u2d(p1);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      uint64_t* o = b.out[m] + ((size_t)p * n + i) * N + x;
+      double v = acc[m][p];
+      if (accumulate) v += u2d(*o);
+      *o = d2u(fcanon(v, q, qinv));
+    }
+}
+
+// The same with every row moved by the TMA bulk engine: per operand j one stage of the NST-deep shared ring holds
+// the operand's c0 and c1 rows and the M source rows of its weight terms (2 KB each, cp.async.bulk issued by one
+// thread, completion on the stage's mbarrier), so NST - 1 operands are in flight while one is multiplied -- the
+// PRCR stream re-reads each stored weight row once per family member from L2 and needs that memory parallelism.
+constexpr int kPbStages = 4;
+template <int M>
+constexpr size_t pmult_ring_smem() { return (size_t)kPbStages * (M + 2) * 2048 + 8 * kPbStages; }
+template <int M>
+__global__ void __launch_bounds__(256) k_pmult_ring(const __grid_constant__ PBlock b, int J, DevTables dt, int level,
+                                                    int logN, int accumulate) {
+  extern __shared__ __align__(128) double ring[];  // [NST][M + 2][256] then the NST mbarriers
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + (size_t)kPbStages * (M + 2) * 256);
+  const size_t N = (size_t)1 << logN;
+  const int t = threadIdx.x;
+  const uint32_t r = blockIdx.x, x = r * 256 + t;
+  const int i = blockIdx.y;
+  const size_t n = level + 1;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  auto issue = [&](int j) {  // thread 0
+    const int st = j % kPbStages;
+    uint64_t* dst = reinterpret_cast<uint64_t*>(ring + (size_t)st * (M + 2) * 256);
+    tma::mbar_expect(mbar + st, (M + 2) * 2048);
+    tma::bulk_row(dst, b.ct[j] + (size_t)i * N + (size_t)r * 256, mbar + st);
+    tma::bulk_row(dst + 256, b.ct[j] + (n + i) * N + (size_t)r * 256, mbar + st);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t sr = k != 1 ? aut_index(r * 256u, k, logN) >> 8 : r;
+      tma::bulk_row(dst + 256 * (2 + m), b.pt_base + ((size_t)b.pt_idx[m][j] * n + i) * N + (size_t)sr * 256,
+                    mbar + st);
+    }
+  };
+  if (t == 0) {
+    for (int st = 0; st < kPbStages; ++st) tma::mbar_init(mbar + st);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < kPbStages - 1 && j < J; ++j) issue(j);
+  }
+  __syncthreads();
+  double acc[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const int st = j % kPbStages;
+    if (t == 0 && j + kPbStages - 1 < J) issue(j + kPbStages - 1);  // its stage was released at the end of j - 1
+    tma::mbar_wait(mbar + st, (uint32_t)(j / kPbStages) & 1);
+    const uint64_t* S = reinterpret_cast<const uint64_t*>(ring + (size_t)st * (M + 2) * 256);
+    const double c0 = u2d(S[t]), c1 = u2d(S[256 + t]);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t pos = k != 1 ? aut_index(x, k, logN) & 255u : (uint32_t)t;
+      const double w = u2d(S[256 * (2 + m) + pos]);
+      acc[m][0] += fmulmod(c0, w, q, qinv);
+      acc[m][1] += fmulmod(c1, w, q, qinv);
+    }
+    if ((j & 3) == 3) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        acc[m][0] = fred(acc[m][0], q, qinv);
+        acc[m][1] = fred(acc[m][1], q, qinv);
+      }
+    }
+    tma::proxy_fence();  // this thread's reads of the stage precede the next bulk write into it
+    __syncthreads();
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      uint64_t* o = b.out[m] + ((size_t)p * n + i) * N + x;
+      double v = acc[m][p];
+      if (accumulate) v += u2d(*o);
+      *o = d2u(fcanon(v, q, qinv));
+    }
+}
+
 // out[p][i][x] (+)= sum_m ct_m[p][i][x] * pt_m[i][x] mod q_i.  grid (N/256, l+1, 2)
 __global__ void k_pmult_acc(const __grid_constant__ TermPtrs tp, int nterm, uint64_t* __restrict__ out, DevTables dt, int level, int logN,
                             int accumulate) {
@@ -340,6 +491,56 @@ hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_
     KTimer kt(c, FAM_ELEM, s);
     // cts (2 polys) once, every term's weight limb once, outputs written (and read when accumulating)
     kt.bytes = ((uint64_t)jn * 2 + (uint64_t)M * jn + (uint64_t)M * 2 * (acc ? 2 : 1)) * (level + 1) * c->N * 8;
+    // HY_PMB_ROWS=0: the per-thread gather kernel (A/B)
+    // Kernel choice (r02 A/B): blocks without PRot gathers (every non-PRCR layer) stream their
+    // operand and weight rows through the bulk-copy ring (R18 L2_ds MulFilter&Sum 19.5 -> 14.7 ms); PRCR blocks keep
+    // the per-thread gather kernel, whose L1-served gathers beat staging rows for the 8-fold reuse of each stored
+    // weight row (R18 L1_ca 5.8 ms vs 9.2 ms staged).  HY_PMB_ROWS forces 2 (ring), 1 (register-prefetch rows) or
+    // 0 (per-thread gathers).
+    bool any_prot = false;
+    for (uint32_t m = 0; m < M; ++m)
+      for (uint32_t j = 0; j < jn; ++j) any_prot |= b.prot[m][j] != 1;
+    static const int forced = getenv("HY_PMB_ROWS") ? atoi(getenv("HY_PMB_ROWS")) : -1;
+    const int rows = forced >= 0 ? forced : (any_prot ? 0 : 2);
+    if (rows == 2) {
+#define HY_PR(MM)                                                                                                 \
+  case MM: {                                                                                                    \
+    static bool at = false;                                                                                     \
+    if (!at) {                                                                                                  \
+      cudaFuncSetAttribute(k_pmult_ring<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pmult_ring_smem<MM>()); \
+      at = true;                                                                                                \
+    }                                                                                                           \
+    k_pmult_ring<MM><<<g, kT, pmult_ring_smem<MM>(), s>>>(b, (int)jn, c->dt, level, c->log_n, acc);             \
+  } break;
+      switch (M) {
+        HY_PR(1)
+        HY_PR(2)
+        HY_PR(3)
+        HY_PR(4)
+        HY_PR(5)
+        HY_PR(6)
+        HY_PR(7)
+        default:
+          HY_PR(8)
+      }
+#undef HY_PR
+      done += jn;
+      continue;
+    }
+    if (rows == 1) {
+      switch (M) {
+        case 1: k_pmult_rows<1><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 2: k_pmult_rows<2><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 3: k_pmult_rows<3><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 4: k_pmult_rows<4><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 5: k_pmult_rows<5><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 6: k_pmult_rows<6><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        case 7: k_pmult_rows<7><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+        default: k_pmult_rows<8><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      }
+      done += jn;
+      continue;
+    }
     switch (M) {
       case 1: k_pmult_block<1><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
       case 2: k_pmult_block<2><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;

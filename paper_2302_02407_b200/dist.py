@@ -70,3 +70,33 @@ def raconv_tap_sharded(plan, evks, cts, level, pts, out_index: int, scratch=None
         return plan.raconv_finish(evks, level, pts, st, out_index, scratch=scratch)
 
     return tap_sharded(partial, finish, plan.f * plan.f, group)
+
+
+def caconv_slide_sharded(plan, evks, cts, level, pts, scratch=None, group=None):
+    """A CAConv layer with its Slide_f sharded by input (include/hyphen.h hy_caconv_slide / hy_caconv_slid): each
+    rank slides its contiguous input range, the slid ciphertexts are all-gathered (every output needs all of
+    them), each rank computes its contiguous output range from the full slid set, and the outputs are
+    all-gathered.  Modular arithmetic is exact and order-free, so the result is bit-identical to one GPU
+    (Slide is no longer repeated on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    f2 = plan.f * plan.f
+    ib, ie = shard(plan.n_in, rank, world)
+    like = cts[0]
+    mine = plan.slide(evks, cts, level, ib, ie)
+    # all-gather of variable input ranges: pad every rank's block to the largest
+    cap = max(e - b for b, e in (shard(plan.n_in, r, world) for r in range(world))) * f2
+    send = torch.zeros((cap,) + tuple(like.shape), dtype=like.dtype, device=like.device)
+    if mine.shape[0]:
+        send[: mine.shape[0]].copy_(mine)
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    slid = torch.cat([recv[r][: (e - b) * f2] for r, (b, e) in
+                      enumerate(shard(plan.n_in, r, world) for r in range(world))], 0)
+    ob, oe = shard(plan.n_out, rank, world)
+    local = plan.run_slid(evks, slid, level, pts, scratch, ob, oe) if oe > ob else []
+    lo = plan.out_level(level)
+    return all_gather_cts(local, plan.n_out, plan.ctx.empty(*plan.ctx.ct_shape(lo)), group)

@@ -32,7 +32,7 @@ def _worker(rank, world, port, pset, layer, q):
 
         import paper_2302_02407_b200 as hy
         import synth
-        from paper_2302_02407_b200.dist import all_gather_cts, shard, tap_sharded
+        from paper_2302_02407_b200.dist import all_gather_cts, caconv_slide_sharded, shard, tap_sharded
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,6 +57,11 @@ def _worker(rank, world, port, pset, layer, q):
             got = all_gather_cts([t.cpu() for t in mine], p.n_out, full[0].cpu())
             ok &= len(got) == p.n_out
             ok &= all(np.array_equal(a.numpy(), x.cpu().numpy()) for a, x in zip(got, full))
+        if algo == "CA" and p.n_in >= 2:  # Slide sharded by input, slid ciphertexts all-gathered
+            got = caconv_slide_sharded(p, evks, cts, level, pts)
+            torch.cuda.synchronize()
+            ok &= len(got) == p.n_out
+            ok &= all(np.array_equal(a.cpu().numpy(), x.cpu().numpy()) for a, x in zip(got, full))
         if algo == "RA":
             scratch = p.scratch(level)
             for j in range(p.n_out):
@@ -82,6 +87,10 @@ LAYERS = {
     # toy (N = 2^12): CAConv with 4 output groups over 2 ranks; BASELINE config 1 RAConv (1 output: taps sharded)
     "toy_ca": ("toy", (8, 8, 8, 3, 1, 8, 1, 1, 2, "CA", 1)),
     "toy_C1_ra": ("toy", (4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", 1)),
+    # toy PRCR CAConv with 2 input ciphertexts: output sharding and Slide sharding by input
+    "toy_prcr_ca": ("toy", (64, 8, 6, 3, 1, 8, 1, 1, 1, "CA", 2)),
+    # ResNet-18 stage-4 CAConv (8 inputs, 64 outputs, PRCR |S| = 8) at N = 2^16: both shardings
+    "r18_L4_ca": ("hyp", (512, 512, 7, 3, 1, 64, 8, 8, 8, "CA", 8)),
     # Set_hyp (N = 2^16): ResNet-20 stage-3 CAConv (8 outputs) and RAConv (1 output, taps sharded), both with bias
     "r20_L3_ca": ("hyp", (64, 64, 8, 3, 1, 32, 4, 4, 8, "CA", 1)),
     "r20_L3_ra": ("hyp", (64, 64, 8, 3, 1, 32, 4, 8, 4, "RA", 1)),
