@@ -1010,8 +1010,13 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_p_tma(const __grid_constant_
 template <int A>
 __host__ __device__ constexpr int cols_smem_words() { return 8 * 256 + 2 * 256 + kMaxExt * A; }
 
-// (strip bx, group j, item g); sm = cols_smem_words<A>() doubles of shared memory
-template <int A, bool DOWN>
+// YS (round 2): the source words y_1 .. y_{A-1} live in shared memory ([A-1][8][256] doubles after the strip, the
+// twiddles and the constants) instead of registers, so the kernel fits 3 CTAs (24 warps) per SM
+template <int A>
+__host__ __device__ constexpr int cols_ys_words() { return (A - 1) * 8 * 256; }
+
+// (strip bx, group j, item g); sm = cols_smem_words<A>() (+ cols_ys_words<A>() with YS) doubles of shared memory
+template <int A, bool DOWN, bool YS = false>
 __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const ModUpConst* mc, const ModDownConst* md,
                                                 const DevTables& dt, int level, int n_q, int E, int logN,
                                                 double* sm, int bx, int j, int g) {
@@ -1044,11 +1049,16 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
     return dt.tw + (size_t)tgt_chain(target(p)) * N;
   };
   if (tid > 0 && tid < 256) T[tid] = table(0)[tid];
-  double y[A][8];
+  constexpr int AR = YS ? 1 : A;  // sources held in registers
+  double y[AR][8];
+  double* ysm = sm + cols_smem_words<A>();  // YS: [A-1][8][256], word (i, k) of thread tid at ysm[(i*8+k)*256+tid]
 #pragma unroll
-  for (int i = 0; i < A; ++i)
+  for (int i = 0; i < AR; ++i)
 #pragma unroll
     for (int k = 0; k < 8; ++k) y[i][k] = 0.0;
+  if constexpr (YS) {
+    for (int w = tid; w < cols_ys_words<A>(); w += blockDim.x) ysm[w] = 0.0;
+  }
   __syncthreads();
   for (int p = 0; p < nph; ++p) {
     const double tw_next = (p + 1 < nph && tid > 0 && tid < 256) ? table(p + 1)[tid] : 0.0;
@@ -1084,7 +1094,9 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const double v = fcanon(fmulmod(x[k], cst, q, qinv), q, qinv);
-            y[i][k] = center && v > half ? v - q : v;
+            const double yv = center && v > half ? v - q : v;
+            if (i < AR) y[i < AR ? i : 0][k] = yv;
+            else ysm[((i - 1) * 8 + k) * 256 + tid] = yv;
           }
         }
     } else {  // BConv to target u, then the forward column pass
@@ -1098,7 +1110,8 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
       for (int k = 0; k < 8; ++k) {
         double acc = 0.0;
 #pragma unroll
-        for (int i = 0; i < A; ++i) acc += fmulmod(y[i][k], h[i], q, qinv);
+        for (int i = 0; i < A; ++i)
+          acc += fmulmod(i < AR ? y[i < AR ? i : 0][k] : ysm[((i - 1) * 8 + k) * 256 + tid], h[i], q, qinv);
         x[k] = fred(acc, q, qinv);
       }
       run_stages<1, true>(x, l, 7, 5, Tp, q, qinv);
@@ -1130,6 +1143,31 @@ __global__ void __launch_bounds__(256, 2) k_bconv_cols(const __grid_constant__ M
                                                        int level, int n_q, int E, int logN) {
   __shared__ double sm[cols_smem_words<A>()];
   bconv_cols_body<A, DOWN>(a, mc, md, dt, level, n_q, E, logN, sm, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// the YS variant: 3 CTAs per SM (<= 85 registers), dynamic shared memory
+template <int A, bool DOWN>
+__global__ void __launch_bounds__(256, 3) k_bconv_cols_ys(const __grid_constant__ ModUpColsArgs a,
+                                                          const ModUpConst* mc, const ModDownConst* md, DevTables dt,
+                                                          int level, int n_q, int E, int logN) {
+  extern __shared__ __align__(16) double dsm_cols[];
+  bconv_cols_body<A, DOWN, true>(a, mc, md, dt, level, n_q, E, logN, dsm_cols, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+template <int A>
+constexpr size_t cols_ys_smem() { return (size_t)(cols_smem_words<A>() + cols_ys_words<A>()) * 8; }
+bool cols_ys_on() {
+  static const bool on = getenv("HY_COLS_YS") != nullptr && atoi(getenv("HY_COLS_YS")) != 0;  // A/B only: slower (r02h)
+  return on;
+}
+template <int A, bool DOWN>
+void launch_cols_ys(dim3 grid, cudaStream_t s, const ModUpColsArgs& a, const ModUpConst* mc, const ModDownConst* md,
+                    const DevTables& dt, int lv, int nq, int E, int lg) {
+  static bool at = false;
+  if (!at) {
+    cudaFuncSetAttribute(k_bconv_cols_ys<A, DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_ys_smem<A>());
+    at = true;
+  }
+  k_bconv_cols_ys<A, DOWN><<<grid, 256, cols_ys_smem<A>(), s>>>(a, mc, md, dt, lv, nq, E, lg);
 }
 
 }  // namespace
@@ -1171,7 +1209,10 @@ void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level,
     case 1: k_bconv_cols<1, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
     case 2: k_bconv_cols<2, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
     case 3: k_bconv_cols<3, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
-    case 4: k_bconv_cols<4, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg); break;
+    case 4:
+      if (cols_ys_on()) launch_cols_ys<4, false>(grid, s, a, mc, nullptr, c->dt, lv, nq, E, lg);
+      else k_bconv_cols<4, false><<<grid, 256, 0, s>>>(a, mc, nullptr, c->dt, lv, nq, E, lg);
+      break;
     default: break;  // callers check modup_cols_ok
   }
 }
@@ -1189,7 +1230,10 @@ void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t leve
     case 1: k_bconv_cols<1, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
     case 2: k_bconv_cols<2, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
     case 3: k_bconv_cols<3, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
-    case 4: k_bconv_cols<4, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg); break;
+    case 4:
+      if (cols_ys_on()) launch_cols_ys<4, true>(grid, s, a, nullptr, md, c->dt, lv, nq, E, lg);
+      else k_bconv_cols<4, true><<<grid, 256, 0, s>>>(a, nullptr, md, c->dt, lv, nq, E, lg);
+      break;
     default: break;  // callers check moddown_cols_ok
   }
 }

@@ -37,7 +37,11 @@ struct TermPtrs {
 // (instead of once per term) and each gathered weight word serves both polys.  Products on the FP64 pipe
 // (fmulmod, |r| <= 1.5 q for canonical operands), summed exactly in a double and re-centred with fred
 // every 4 operands (|acc| < 6.5 q), canonicalised once per output word.  grid (N/256, l+1)
-template <int M>
+// KM (round 2): how the PRot Galois elements of a block vary -- 0: per term; 1: per operand only (CAConv PRCR: the
+// shift r_t + im F depends on the input member, not the output), the gather index computed once per operand for
+// all M terms; 2: per output only (RAConv PRCR: im F - r_t depends on the output member), the M gather indices
+// computed once per launch.  Products are re-centred every 8 operands (8 x 0.57 q + q/2 < 2^51: exact).
+template <int M, int KM>
 __global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBlock b, int J, DevTables dt, int level,
                                                      int logN, int accumulate) {
   const size_t N = (size_t)1 << logN;
@@ -49,19 +53,41 @@ __global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBl
   double acc[M][2];
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  uint32_t xm[KM == 2 ? M : 1];
+  if constexpr (KM == 2) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][0];
+      xm[m] = (uint32_t)i * (uint32_t)N + (k != 1 ? aut_index(x, k, logN) : x);
+    }
+  }
+  const uint64_t* ct_lo = nullptr;
   // unrolled so that the loads of several operands are in flight together (the stream is HBM-bound)
 #pragma unroll 4
   for (int j = 0; j < J; ++j) {
-    const double c0 = u2d(b.ct[j][(size_t)i * N + x]), c1 = u2d(b.ct[j][(n + i) * N + x]);
+    ct_lo = b.ct[j] + (size_t)i * N + x;
+    const double c0 = u2d(__ldcs(ct_lo)), c1 = u2d(__ldcs(ct_lo + n * N));
+    uint32_t xj = 0;
+    if constexpr (KM == 1) {
+      const uint32_t k = b.prot[0][j];
+      xj = (uint32_t)i * (uint32_t)N + (k != 1 ? aut_index(x, k, logN) : x);
+    }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const uint32_t k = b.prot[m][j];
-      const uint32_t xs = k != 1 ? aut_index(x, k, logN) : x;
-      const double w = u2d(b.pt_base[((size_t)b.pt_idx[m][j] * n + i) * N + xs]);
+      uint32_t off;
+      if constexpr (KM == 0) {
+        const uint32_t k = b.prot[m][j];
+        off = (uint32_t)i * (uint32_t)N + (k != 1 ? aut_index(x, k, logN) : x);
+      } else if constexpr (KM == 1) {
+        off = xj;
+      } else {
+        off = xm[m];
+      }
+      const double w = u2d(b.pt_base[(size_t)b.pt_idx[m][j] * n * N + off]);
       acc[m][0] += fmulmod(c0, w, q, qinv);
       acc[m][1] += fmulmod(c1, w, q, qinv);
     }
-    if ((j & 3) == 3) {
+    if ((j & 7) == 7) {
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         acc[m][0] = fred(acc[m][0], q, qinv);
@@ -541,16 +567,32 @@ hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_
       done += jn;
       continue;
     }
+    // the PRot structure of the block (KM, see k_pmult_block)
+    bool per_j = true, per_m = true;
+    for (uint32_t m = 0; m < M; ++m)
+      for (uint32_t j = 0; j < jn; ++j) {
+        per_j &= b.prot[m][j] == b.prot[0][j];
+        per_m &= b.prot[m][j] == b.prot[m][0];
+      }
+    const int km = per_j ? 1 : (per_m ? 2 : 0);
+#define HY_PB(MM)                                                                                 \
+  case MM:                                                                                        \
+    if (km == 1) k_pmult_block<MM, 1><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc);  \
+    else if (km == 2) k_pmult_block<MM, 2><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); \
+    else k_pmult_block<MM, 0><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc);           \
+    break;
     switch (M) {
-      case 1: k_pmult_block<1><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 2: k_pmult_block<2><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 3: k_pmult_block<3><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 4: k_pmult_block<4><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 5: k_pmult_block<5><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 6: k_pmult_block<6><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      case 7: k_pmult_block<7><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
-      default: k_pmult_block<8><<<g, kT, 0, s>>>(b, (int)jn, c->dt, level, c->log_n, acc); break;
+      HY_PB(1)
+      HY_PB(2)
+      HY_PB(3)
+      HY_PB(4)
+      HY_PB(5)
+      HY_PB(6)
+      HY_PB(7)
+      default:
+        HY_PB(8)
     }
+#undef HY_PB
     done += jn;
   }
   return cuda_check("pmult_block");
