@@ -728,6 +728,36 @@ def oracle_rate_threads(n_rot: int, threads: int):
     return r, dt
 
 
+def bench_boot_linear(ctx, steps, warmup, timed):
+    """The bootstrapping linear steps (partial; DESIGN R-LINTRANS) at Set_hyp: ModRaise of a
+    level-0 ciphertext to level 23, and one BSGS diagonal linear transform at level 23 with 32 diagonals (a radix-32
+    CoeffToSlot layer's shape: d = 0..31 x stride 1, baby-step size 8: 7 hoisted baby rotations, 3 giant rotations in
+    one lazy HRotSum, 32 PMults, one rescale).  Device time per call; random diagonals (the work is data-independent)."""
+    import numpy as np
+
+    import paper_2302_02407_b200 as hy
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    lv = LEVEL
+    scale = 2 ** synth.PARAMS["hyp"]["log_scale"]
+    ct = ctx.encrypt(sk, synth.SEED_ENC, 77, ctx.encode(synth.slots_uniform(77, ctx.n), scale, lv), lv)
+    ct0 = ctx.level_down(ct, lv, 0)
+    raised = ctx.empty(*ctx.ct_shape(lv))
+    ms_raise, l_raise = timed(lambda: ctx.mod_raise(ct0, lv, raised), steps, warmup)
+    ds = list(range(32))
+    lt = hy.LinTrans(ctx, ds, 8)
+    keys = {r: ctx.keygen_rot(sk, ek, r) for r in lt.rots}
+    g = np.random.default_rng(5)
+    pts = lt.encode([g.uniform(-1, 1, ctx.n) + 1j * g.uniform(-1, 1, ctx.n) for _ in ds], lv)
+    out = ctx.empty(*ctx.ct_shape(lv - 1))
+    scratch = ctx.empty(int(hy.lib().hy_lintrans_scratch_words(ctx._c, lt._p, lv)))
+    ms_lt, l_lt = timed(lambda: lt.apply(keys, raised, lv, pts, scratch, out), steps, warmup)
+    return {"mod_raise_ms": ms_raise, "mod_raise_launches": l_raise, "lintrans_ms": ms_lt, "lintrans_launches": l_lt,
+            "lintrans": {"diagonals": len(ds), "baby_steps": lt.n_baby, "giant_steps": lt.n_giant, "level": lv,
+                         "keys": len(lt.rots)},
+            "note": "ModRaise + one BSGS diagonal transform (CoeffToSlot / SlotToCoeff building block); EvalMod is "
+                    "not built, so there is no end-to-end bootstrapping time"}
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, ws, rank, local):
     import torch
@@ -1018,6 +1048,10 @@ def run_ours(args, ws, rank, local):
         conv18 = None if args.no_r18 else bench_conv(ctx, ws, rank, 2, 1, timed, R18_LAYERS, "ResNet-18", rates)
         blocks = bench_blocks(ctx, ws, rank, max(2, args.steps // 2), 1, timed)
 
+    boot = None
+    if not args.no_conv:
+        boot = bench_boot_linear(ctx, max(3, args.steps), 2, timed)
+
     c1 = None
     if not args.no_c1:
         c1 = bench_c1(local, max(3, args.steps), 2, timed, with_oracle=ws == 1 and not args.no_cpu_baseline)
@@ -1065,6 +1099,7 @@ def run_ours(args, ws, rank, local):
             "resnet18_conv": conv18,
             "resnet20_blocks": blocks,
             "c1_raconv": c1,
+            "boot_linear_f4": boot,
             "keyset_f2": keyset_report(),
             "plan_search_f3": plan_search_report(),
             "cpu_baseline": cpu,

@@ -331,6 +331,33 @@ hy_status hy_raconv_finish(hy_ctx* ctx, const hy_conv_plan* plan, const uint64_t
                            const uint64_t* d_pts, uint64_t* d_state, uint64_t* d_scratch, uint32_t out_index,
                            uint64_t* d_out, void* stream);
 
+/* ---- the linear steps of bootstrapping (partial; DESIGN R-LINTRANS) --
+ * ModRaise: a ciphertext at level 0 [2][1][N] -> level l [2][l+1][N]: each coefficient's centred representative mod
+ * q_0 reduced mod q_0..q_l (NTT domain in and out); it then decrypts to m + q_0 I with a small integer polynomial I.
+ * Must not alias.  Errors: HY_E_ARG, HY_E_WORKSPACE. */
+hy_status hy_mod_raise(hy_ctx* ctx, const uint64_t* d_ct0, uint32_t level, uint64_t* d_out, void* stream);
+/* Homomorphic diagonal linear transform y = M x on the slots (CoeffToSlot / SlotToCoeff are such transforms):
+ * y = sum_{d in D} diag_d (.) Rot_d(x), diag_d[j] = M[j][(j + d) mod n], evaluated baby-step / giant-step with
+ * baby-step size bs: d = g bs + b, y = sum_g Rot_{g bs}(sum_b Rot_{-g bs}(diag_{g bs + b}) (.) Rot_b(x)) -- the baby
+ * steps as one hoisted HRot batch, the inner sums as MulFilter&Sum blocks, the giant steps as one lazy HRotSum, then
+ * a rescale (plaintexts at scale q_l: level l -> l - 1, scale unchanged).  A plan lists its diagonals D (amounts
+ * mod n = N/2); query reports the plaintext count (|D| + one zero plaintext), baby / giant step counts and the key
+ * amounts in ascending order (the order apply takes keys in).  encode: host complex diagonals re/im [|D|][n] in
+ * ascending canonical d order (im may be NULL) -> d_pts (hy_lintrans_pt_words).  apply: ct at level l >= 1 -> out at
+ * level l - 1, scratch hy_lintrans_scratch_words.  Errors: HY_E_ARG, HY_E_LEVEL_EXHAUSTED, HY_E_PLAN,
+ * HY_E_MISSING_KEY. */
+typedef struct hy_lintrans hy_lintrans;
+hy_status hy_lintrans_create(uint32_t log_n, const int32_t* diags, uint32_t n_diag, uint32_t bs, hy_lintrans** out);
+void hy_lintrans_destroy(hy_lintrans* plan);
+hy_status hy_lintrans_query(const hy_lintrans* plan, uint32_t* n_pt, uint32_t* n_baby, uint32_t* n_giant,
+                            uint32_t* n_rot, int32_t* rots);
+size_t hy_lintrans_pt_words(const hy_ctx* ctx, const hy_lintrans* plan, uint32_t level);
+size_t hy_lintrans_scratch_words(const hy_ctx* ctx, const hy_lintrans* plan, uint32_t level);
+hy_status hy_lintrans_encode(hy_ctx* ctx, const hy_lintrans* plan, const double* h_re, const double* h_im,
+                             uint32_t level, uint64_t* d_pts, void* stream);
+hy_status hy_lintrans_apply(hy_ctx* ctx, const hy_lintrans* plan, const uint64_t* const* d_evks, const uint64_t* d_ct,
+                            uint32_t level, const uint64_t* d_pts, uint64_t* d_scratch, uint64_t* d_out, void* stream);
+
 /* ---- client side: keys, encode, encrypt, decrypt (untimed) ------- */
 /* Rotation key for Galois element of a left rotation by r (DESIGN R-EVK, R-PRNG):
  * secret from sk_seed, randomness from ek_seed.  d_evk: [dnum][2][n_q+n_p][N]. */
@@ -371,6 +398,10 @@ hy_status hy_encode_batch(hy_ctx* ctx, const double* h_slots, uint32_t P, uint64
 /* Host-only part of hy_encode: the N integer coefficients (no device needed). */
 hy_status hy_encode_coeffs(uint32_t log_n, const double* h_slots, uint32_t n_slots, uint64_t scale,
                            int64_t* h_coeffs);
+/* The same for complex slots z_j = slots[j] + i slots_im[j] (slots_im may be NULL): m_k = round(scale (2/N) Re
+ * sum_j z_j zeta^{-5^j k}) -- R-ENCODE with complex values (the bootstrapping linear transforms' diagonals). */
+hy_status hy_encode_coeffs_complex(uint32_t log_n, const double* h_slots, const double* h_slots_im, uint32_t n_slots,
+                                   uint64_t scale, int64_t* h_coeffs);
 /* Signed integer coefficients (host, N words) -> NTT-domain plaintext on q_0..q_l. */
 hy_status hy_pt_from_coeffs(hy_ctx* ctx, const int64_t* h_coeffs, uint32_t level, uint64_t* d_pt, void* stream);
 /* CKKS decode (client side, the inverse of R-ENCODE; P:98-100 canonical embedding):

@@ -104,6 +104,17 @@ SIGNATURES = {
     "hy_conv_encode_weights": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double), _U64, _U32, _P,
                                          _P]),
     "hy_conv_bias_slots": (C.c_int, [_P, C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
+    "hy_encode_coeffs_complex": (C.c_int, [_U32, C.POINTER(C.c_double), C.POINTER(C.c_double), _U32, _U64,
+                                           C.POINTER(C.c_int64)]),
+    "hy_mod_raise": (C.c_int, [_P, _P, _U32, _P, _P]),
+    "hy_lintrans_create": (C.c_int, [_U32, C.POINTER(C.c_int32), _U32, _U32, C.POINTER(_P)]),
+    "hy_lintrans_destroy": (None, [_P]),
+    "hy_lintrans_query": (C.c_int, [_P, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
+                                     C.POINTER(C.c_int32)]),
+    "hy_lintrans_pt_words": (C.c_size_t, [_P, _P, _U32]),
+    "hy_lintrans_scratch_words": (C.c_size_t, [_P, _P, _U32]),
+    "hy_lintrans_encode": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double), _U32, _P, _P]),
+    "hy_lintrans_apply": (C.c_int, [_P, _P, _PP, _P, _U32, _P, _P, _P, _P]),
     "hy_keyset_create": (C.c_int, [_U32, C.POINTER(C.c_int32), _U32, C.POINTER(_P)]),
     "hy_keyset_destroy": (None, [_P]),
     "hy_keyset_decompose": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), _U32, C.POINTER(_U32)]),
@@ -456,11 +467,75 @@ class Context:
                                      self._stream()))
         return out
 
+    def mod_raise(self, ct0, level, out=None):
+        """ModRaise (hy_mod_raise): level-0 ciphertext -> level `level`"""
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_mod_raise(self._c, _ptr(ct0), level, _ptr(out), self._stream()))
+        return out
+
+    def encode_complex(self, z, scale, level):
+        """complex slots -> NTT-domain plaintext (hy_encode_coeffs_complex + hy_pt_from_coeffs)"""
+        z = np.asarray(z, np.complex128)
+        re, im = np.ascontiguousarray(z.real), np.ascontiguousarray(z.imag)
+        cf = np.zeros(self.N, np.int64)
+        _check(lib().hy_encode_coeffs_complex(self.log_n, re.ctypes.data_as(C.POINTER(C.c_double)),
+                                              im.ctypes.data_as(C.POINTER(C.c_double)), len(z), int(scale),
+                                              cf.ctypes.data_as(C.POINTER(C.c_int64))))
+        return self.pt_from_coeffs(cf, level)
+
     def pt_from_coeffs(self, coeffs, level, out=None):
         out = self.empty(level + 1, self.N) if out is None else out
         cf = np.ascontiguousarray(coeffs, np.int64)
         _check(lib().hy_pt_from_coeffs(self._c, cf.ctypes.data_as(C.POINTER(C.c_int64)), level, _ptr(out),
                                        self._stream()))
+        return out
+
+
+class LinTrans:
+    """Homomorphic diagonal linear transform y = M x (bootstrapping's CoeffToSlot / SlotToCoeff building block;
+    include/hyphen.h hy_lintrans_*, DESIGN R-LINTRANS): diagonals `diags` (amounts mod n), baby-step size bs."""
+
+    def __init__(self, ctx, diags, bs, log_n=None):
+        self.ctx = ctx
+        log_n = log_n if log_n is not None else ctx.log_n
+        self.n = 1 << (log_n - 1)
+        d = (C.c_int32 * len(diags))(*[int(x) for x in diags])
+        h = C.c_void_p()
+        self._lib = lib()
+        _check(self._lib.hy_lintrans_create(log_n, d, len(diags), int(bs), C.byref(h)))
+        self._p = h
+        npt, nb, ng, nr = (C.c_uint32() for _ in range(4))
+        _check(lib().hy_lintrans_query(self._p, C.byref(npt), C.byref(nb), C.byref(ng), C.byref(nr), None))
+        rots = (C.c_int32 * max(1, nr.value))()
+        _check(lib().hy_lintrans_query(self._p, None, None, None, None, rots))
+        self.n_pt, self.n_baby, self.n_giant = npt.value, nb.value, ng.value
+        self.rots = [int(rots[i]) for i in range(nr.value)]
+        self.diags = sorted({int(x) % self.n for x in diags})
+
+    def __del__(self):
+        if getattr(self, "_p", None) and getattr(self, "_lib", None) is not None:
+            self._lib.hy_lintrans_destroy(self._p)
+            self._p = None
+
+    def encode(self, diag_values, level):
+        """diag_values: complex [len(diags)][n] in ascending canonical d order"""
+        v = np.asarray(diag_values)
+        re = np.ascontiguousarray(np.real(v), np.float64)
+        im = np.ascontiguousarray(np.imag(v), np.float64)
+        pts = self.ctx.empty(int(lib().hy_lintrans_pt_words(self.ctx._c, self._p, level)))
+        _check(lib().hy_lintrans_encode(self.ctx._c, self._p, re.ctypes.data_as(C.POINTER(C.c_double)),
+                                        im.ctypes.data_as(C.POINTER(C.c_double)), level, _ptr(pts),
+                                        self.ctx._stream()))
+        return pts
+
+    def apply(self, evks, ct, level, pts, scratch=None, out=None):
+        if isinstance(evks, dict):
+            evks = [evks[r] for r in self.rots]
+        out = self.ctx.empty(*self.ctx.ct_shape(level - 1)) if out is None else out
+        scratch = self.ctx.empty(int(lib().hy_lintrans_scratch_words(self.ctx._c, self._p, level))) \
+            if scratch is None else scratch
+        _check(lib().hy_lintrans_apply(self.ctx._c, self._p, _ptr_array(evks), _ptr(ct), level, _ptr(pts),
+                                       _ptr(scratch), _ptr(out), self.ctx._stream()))
         return out
 
 

@@ -130,14 +130,15 @@ int64_t round_dd(DD x) {
 
 }  // namespace
 
-extern "C" hy_status hy_encode_coeffs(uint32_t log_n, const double* slots, uint32_t n_slots, uint64_t scale,
-                                      int64_t* out) {
+extern "C" hy_status hy_encode_coeffs_complex(uint32_t log_n, const double* slots, const double* slots_im,
+                                              uint32_t n_slots, uint64_t scale, int64_t* out) {
   if (!slots || !out || log_n < 2 || log_n > 17) return HY_E_ARG;
   const uint64_t N = 1ull << log_n, n = N / 2, M = 2 * N;
   if (n_slots > n) return HY_E_CAPACITY;
   auto T = tables(log_n);
   std::vector<CDD> v(n);
-  for (uint64_t j = 0; j < n; ++j) v[j] = {{j < n_slots ? slots[j] : 0.0, 0.0}, {0.0, 0.0}};
+  for (uint64_t j = 0; j < n; ++j)
+    v[j] = {{j < n_slots ? slots[j] : 0.0, 0.0}, {(j < n_slots && slots_im) ? slots_im[j] : 0.0, 0.0}};
   // special inverse FFT over the orbit of 5
   for (uint64_t len = n; len >= 2; len >>= 1) {
     const uint64_t lenh = len >> 1, lenq = len << 2, gap = M / lenq;
@@ -170,6 +171,11 @@ extern "C" hy_status hy_encode_coeffs(uint32_t log_n, const double* slots, uint3
     out[i + n] = round_dd(im);
   }
   return HY_OK;
+}
+
+extern "C" hy_status hy_encode_coeffs(uint32_t log_n, const double* slots, uint32_t n_slots, uint64_t scale,
+                                      int64_t* out) {
+  return hy_encode_coeffs_complex(log_n, slots, nullptr, n_slots, scale, out);
 }
 
 // CKKS decode (client side, untimed): the inverse of R-ENCODE.  The N real coefficients m_i

@@ -1,0 +1,114 @@
+"""GPU parity of the bootstrapping linear steps (partial; DESIGN R-LINTRANS): complex encoding,
+ModRaise and the BSGS diagonal linear transform through the C ABI, bit-exact on every limb against oracle/boot.py,
+and CoeffToSlot / SlotToCoeff (dense special-FFT matrices) moving coefficients to slots and back."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import boot as B
+
+pytestmark = pytest.mark.gpu
+SK, EK = synth.SEED_SK, synth.SEED_EVK
+
+
+def to_np(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def to_dev(a, ctx):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(ctx.device)
+
+
+_P = {}
+
+
+def pair(name):
+    if name not in _P:
+        import paper_2302_02407_b200 as hy
+        prm = synth.PARAMS[name]
+        _P[name] = (hy.Context(**prm), oracle.Oracle(**prm))
+    return _P[name]
+
+
+@pytest.mark.parametrize("name", ["mini", "toy", "hyp"])
+def test_encode_complex(name):
+    ctx, o = pair(name)
+    z = synth.slots_uniform(1, o.n) + 1j * synth.slots_uniform(2, o.n)
+    lv = min(3, o.nq - 1)
+    for scale in (2**40, int(o.q[lv])):
+        assert np.array_equal(to_np(ctx.encode_complex(z, scale, lv)), o.encode(z, scale, lv).data)
+
+
+@pytest.mark.parametrize("name", ["mini", "toy", "hyp"])
+def test_mod_raise(name):
+    ctx, o = pair(name)
+    top = o.nq - 1
+    z = synth.slots_uniform(3, o.n)
+    ct0 = o.level_down(o.encrypt(SK, 7, 1, o.encode(z, 2**40, top)), 0)
+    got = to_np(ctx.mod_raise(to_dev(ct0.data, ctx), top))
+    assert np.array_equal(got, B.mod_raise(o, ct0, top).data)
+
+
+def _lintrans_case(ctx, o, ds, bs, seed, level):
+    import paper_2302_02407_b200 as hy
+    n = o.n
+    g = np.random.default_rng(seed)
+    dsc = sorted({d % n for d in ds})
+    vals = [g.uniform(-1, 1, n) + 1j * g.uniform(-1, 1, n) for _ in dsc]
+    lt = hy.LinTrans(ctx, dsc, bs)
+    keys = {r: ctx.keygen_rot(SK, EK, r) for r in lt.rots}
+    okeys = {r: o.keygen_rot(SK, EK, r) for r in lt.rots}
+    z = synth.slots_uniform(seed, n) + 1j * synth.slots_uniform(seed + 1, n)
+    oct_ = o.encrypt(SK, 9, seed, o.encode(z, 2**40, level))
+    y = lt.apply(keys, to_dev(oct_.data, ctx), level, lt.encode(vals, level))
+    want = B.lintrans(o, oct_, dict(zip(dsc, vals)), bs, okeys)
+    assert np.array_equal(to_np(y), want.data)
+    return lt, want, z, dict(zip(dsc, vals))
+
+
+@pytest.mark.parametrize("name,ds,bs", [("mini", [0, 1, 3, 9, -1, 64], 4), ("toy", [0, 2, 5, 33, -7, 100, 1023], 8),
+                                        ("hyp", [0, 1, 2, 3, 8, 16, -8], 4)])
+def test_lintrans_bit_exact(name, ds, bs):
+    ctx, o = pair(name)
+    lv = o.nq - 1 if name != "hyp" else 9
+    lt, want, z, diags = _lintrans_case(ctx, o, ds, bs, 20, lv)
+    # and it is the matrix-vector product on the slots
+    n = o.n
+    j = np.arange(n)
+    ref = sum(v * z[(j + d) % n] for d, v in diags.items())
+    got = o.decode(o.decrypt(SK, want))
+    assert np.max(np.abs(got - ref)) < 2**-18 * np.max(np.abs(ref))
+
+
+def test_coeff_to_slot_to_coeff_mini():
+    """ModRaise of a level-0 ciphertext, CoeffToSlot (V^{-1}, 512 diagonals, bs = 32) and SlotToCoeff (V): bit-exact
+    vs the oracle; CoeffToSlot's slots are the raised plaintext's complex-packed coefficients / scale and
+    SlotToCoeff returns the raised slots"""
+    import paper_2302_02407_b200 as hy
+    ctx, o = pair("mini")
+    n, top = o.n, o.nq - 1
+    V = B.special_fft_matrix(o.N)
+    Vi = np.linalg.inv(V)
+    ds = list(range(n))
+    z = synth.slots_uniform(30, n) * 0.01
+    ct0 = o.level_down(o.encrypt(SK, 7, 2, o.encode(z, 2**40, top)), 0)
+    up = B.mod_raise(o, ct0, top)
+    d_up = ctx.mod_raise(to_dev(ct0.data, ctx), top)
+    assert np.array_equal(to_np(d_up), up.data)
+    c2s = hy.LinTrans(ctx, ds, 32)
+    keys = {r: ctx.keygen_rot(SK, EK, r) for r in c2s.rots}
+    okeys = {r: o.keygen_rot(SK, EK, r) for r in c2s.rots}
+    y = c2s.apply(keys, d_up, top, c2s.encode(B.diagonals(Vi, ds), top))
+    oy = B.lintrans(o, up, dict(zip(ds, B.diagonals(Vi, ds))), 32, okeys)
+    assert np.array_equal(to_np(y), oy.data)
+    m = np.array(o.crt_coeffs(o.decrypt(SK, up).data, top), dtype=float)
+    u = (m[:n] + 1j * m[n:]) / 2**40
+    assert np.max(np.abs(o.decode(o.decrypt(SK, oy)) - u)) < 2**-20 * np.max(np.abs(u))
+    s2c = hy.LinTrans(ctx, ds, 32)
+    w = s2c.apply(keys, y, top - 1, s2c.encode(B.diagonals(V, ds), top - 1))
+    ow = B.lintrans(o, oy, dict(zip(ds, B.diagonals(V, ds))), 32, okeys)
+    assert np.array_equal(to_np(w), ow.data)
+    back = o.decode(o.decrypt(SK, ow))
+    assert np.max(np.abs(back - o.decode(o.decrypt(SK, up)))) < 2**-12

@@ -1,0 +1,95 @@
+"""Pins of the bootstrapping linear steps in the oracle (oracle/boot.py, partial), CPU only:
+ModRaise decrypts to m + q_0 I with a small integer polynomial I (big-int check); the BSGS linear transform decrypts
+to the plaintext matrix-vector product M z; the special-FFT matrix is the encoder's embedding (decode of a known
+coefficient vector), and CoeffToSlot / SlotToCoeff built from it move coefficients to slots and back."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import boot as B
+
+SK, EK = synth.SEED_SK, synth.SEED_EVK
+
+
+@pytest.fixture(scope="module")
+def mini():
+    return oracle.Oracle(**synth.PARAMS["mini"])
+
+
+def test_special_fft_matrix_is_the_embedding(mini):
+    o = mini
+    V = B.special_fft_matrix(o.N)
+    g = np.random.default_rng(3)
+    m = g.integers(-1000, 1000, o.N)
+    pt = oracle.Pt(o.coeffs_to_pt(m, o.nq - 1), o.nq - 1, 1.0)
+    z = o.decode(pt)
+    u = m[: o.n] + 1j * m[o.n:]
+    assert np.max(np.abs(V @ u - z)) < 1e-9 * np.max(np.abs(z))
+
+
+def test_mod_raise(mini):
+    o = mini
+    z = synth.slots_uniform(5, o.n)
+    ct0 = o.level_down(o.encrypt(SK, 7, 0, o.encode(z, 2**40, o.nq - 1)), 0)
+    up = B.mod_raise(o, ct0, o.nq - 1)
+    m0 = o.crt_coeffs(o.decrypt(SK, ct0).data, 0)
+    m1 = o.crt_coeffs(o.decrypt(SK, up).data, o.nq - 1)
+    q0 = int(o.q[0])
+    I = [(b - a) // q0 for a, b in zip(m0, m1)]
+    assert all((b - a) % q0 == 0 for a, b in zip(m0, m1))
+    assert max(abs(x) for x in I) <= (o.h + 1) // 2 + 1
+
+
+def _rand_diag_matrix(n, ds, seed):
+    g = np.random.default_rng(seed)
+    M = np.zeros((n, n), complex)
+    j = np.arange(n)
+    for d in ds:
+        M[j, (j + d) % n] = g.uniform(-1, 1, n) + 1j * g.uniform(-1, 1, n)
+    return M
+
+
+def test_lintrans_is_matrix_product(mini):
+    o = mini
+    n = o.n
+    ds = [0, 1, 2, 5, 7, 9, n - 1, n - 8, 64]
+    M = _rand_diag_matrix(n, ds, 11)
+    bs = 4
+    dsc = sorted(d % n for d in ds)
+    diags = dict(zip(dsc, B.diagonals(M, dsc)))
+    need = sorted({d % bs for d in dsc if d % bs} | {(d // bs) * bs for d in dsc if d // bs})
+    evks = {r: o.keygen_rot(SK, EK, r) for r in need}
+    z = synth.slots_uniform(12, n) + 1j * synth.slots_uniform(13, n)
+    lv = o.nq - 1
+    ct = o.encrypt(SK, 8, 0, o.encode(z, 2**40, lv))
+    y = B.lintrans(o, ct, diags, bs, evks)
+    assert y.level == lv - 1 and abs(y.scale - 2**40) < 1e-3
+    got = o.decode(o.decrypt(SK, y))
+    want = M @ z
+    assert np.max(np.abs(got - want)) < 2**-18 * np.max(np.abs(want))
+
+
+def test_coeff_to_slot_and_back(mini):
+    """CoeffToSlot = V^{-1} on the slots (dense, n diagonals, bs = 32): the slots become the complex-packed
+    coefficients / scale; SlotToCoeff = V brings the slots back"""
+    o = mini
+    n = o.n
+    V = B.special_fft_matrix(o.N)
+    Vi = np.linalg.inv(V)
+    ds = list(range(n))
+    bs = 32
+    need = sorted({d % bs for d in ds if d % bs} | {(d // bs) * bs for d in ds if d // bs})
+    evks = {r: o.keygen_rot(SK, EK, r) for r in need}
+    z = synth.slots_uniform(14, n)
+    lv = o.nq - 1
+    pt = o.encode(z, 2**40, lv)
+    ct = o.encrypt(SK, 9, 0, pt)
+    c2s = B.lintrans(o, ct, dict(zip(ds, B.diagonals(Vi, ds))), bs, evks)
+    m = np.array(o.crt_coeffs(pt.data, lv), dtype=float)
+    u = (m[:n] + 1j * m[n:]) / 2**40
+    got = o.decode(o.decrypt(SK, c2s))
+    assert np.max(np.abs(got - u)) < 2**-20 * max(1.0, np.max(np.abs(u)))
+    s2c = B.lintrans(o, c2s, dict(zip(ds, B.diagonals(V, ds))), bs, evks)
+    back = o.decode(o.decrypt(SK, s2c))
+    assert np.max(np.abs(back - z)) < 2**-15
