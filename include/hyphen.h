@@ -161,6 +161,11 @@ hy_status hy_hrot(hy_ctx* ctx, const uint64_t* d_evk, const uint64_t* d_ct, uint
  * HY_E_ARG.  Items sharing a key pointer stream it from HBM once per chunk. */
 hy_status hy_hrot_batch(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* const* d_cts, uint32_t level,
                         const int32_t* r, uint32_t n, uint64_t* const* d_outs, void* stream);
+/* Key switch by any Galois element k (odd, < 2N): out = kappa_k(ct) switched back to s with the key from
+ * hy_keygen_galois(k) -- k = 2N - 1 is the conjugation bootstrapping needs; k = 1 copies.  Plain variant,
+ * not in place. */
+hy_status hy_hrot_galois(hy_ctx* ctx, const uint64_t* d_evk, const uint64_t* d_ct, uint32_t level, uint64_t k,
+                         uint64_t* d_out, void* stream);
 /* hoisted (Slide_f): one ModUp of c1 shared by n rotations of the same ciphertext. */
 hy_status hy_hrot_hoisted(hy_ctx* ctx, const uint64_t* const* d_evks, const uint64_t* d_ct, uint32_t level,
                           const int32_t* r, uint32_t n, uint64_t* const* d_outs, void* stream);
@@ -192,6 +197,9 @@ hy_status hy_pmult_acc(hy_ctx* ctx, const uint64_t* const* d_cts, const uint64_t
                        uint32_t level, uint64_t* d_out, int accumulate, void* stream);
 /* out = a + b over npoly polynomials ([npoly][l+1][N]); in-place allowed. */
 hy_status hy_add(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t npoly, uint32_t level,
+                 uint64_t* d_out, void* stream);
+/* out = a - b over npoly polynomials (mod q_i limbwise); in-place allowed. */
+hy_status hy_sub(hy_ctx* ctx, const uint64_t* d_a, const uint64_t* d_b, uint32_t npoly, uint32_t level,
                  uint64_t* d_out, void* stream);
 /* AddPt ("AddPt 0.169 ms" P:148; the conv bias): out = (c0 + pt, c1) at level l, [2][l+1][N] and
  * [l+1][N]; in-place allowed (out == ct).  The scales are the caller's bookkeeping (the ABI carries none): they

@@ -107,6 +107,8 @@ SIGNATURES = {
     "hy_encode_coeffs_complex": (C.c_int, [_U32, C.POINTER(C.c_double), C.POINTER(C.c_double), _U32, _U64,
                                            C.POINTER(C.c_int64)]),
     "hy_mod_raise": (C.c_int, [_P, _P, _U32, _P, _P]),
+    "hy_sub": (C.c_int, [_P, _P, _P, _U32, _U32, _P, _P]),
+    "hy_hrot_galois": (C.c_int, [_P, _P, _P, _U32, _U64, _P, _P]),
     "hy_lintrans_create": (C.c_int, [_U32, C.POINTER(C.c_int32), _U32, _U32, C.POINTER(_P)]),
     "hy_lintrans_destroy": (None, [_P]),
     "hy_lintrans_query": (C.c_int, [_P, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
@@ -465,6 +467,17 @@ class Context:
         out = self.empty(len(chain), self.N) if out is None else out
         _check(lib().hy_import_coeff(self._c, a.ctypes.data_as(C.POINTER(_U64)), ch, len(chain), _ptr(out),
                                      self._stream()))
+        return out
+
+    def sub(self, a, b, level, out=None, npoly=2):
+        out = self.empty(npoly, level + 1, self.N) if out is None else out
+        _check(lib().hy_sub(self._c, _ptr(a), _ptr(b), npoly, level, _ptr(out), self._stream()))
+        return out
+
+    def hrot_galois(self, evk, ct, level, k, out=None):
+        """key switch by Galois element k (hy_hrot_galois; k = 2N - 1: conjugation)"""
+        out = self.empty(*self.ct_shape(level)) if out is None else out
+        _check(lib().hy_hrot_galois(self._c, _ptr(evk), _ptr(ct), level, int(k), _ptr(out), self._stream()))
         return out
 
     def mod_raise(self, ct0, level, out=None):

@@ -243,9 +243,10 @@ void ntt_contig(hy_ctx* c, const uint64_t* in, uint64_t* out, const uint32_t* ch
 hy_status hrot_plain(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, int32_t r, uint64_t* out,
                      cudaStream_t s, const uint64_t* addct);
 // batched plain HRot: out_g = HRot_{r_g}(ct_g) (+ addct_g); identical evk pointers share one key stream
+// gal (optional): the Galois elements of the items (then r is ignored) -- any automorphism, e.g. conjugation
 hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* const* ct, uint32_t level,
                      const int32_t* r, uint32_t n_items, uint64_t* const* out, const uint64_t* const* addct,
-                     cudaStream_t s);
+                     cudaStream_t s, const uint64_t* gal = nullptr);
 // Lazy HRotSum split at its ModDown (RAConv tap sharding, hy_conv.cu):
 //   hrot_sum_partial: u [2][l+1+K][N] = sum of the terms' key-switch inner products (NTT, canonical; zero if no
 //                     term is switched), acc [2][l+1][N] = (sum kappa_t(c0_t), sum of the r = 0 terms' c1)

@@ -648,12 +648,12 @@ hy_status check_level(hy_ctx* c, uint32_t level) {
 // out_g may alias ct_g and addct_g (ct_g is consumed into the workspace before the final write).
 hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* const* ct, uint32_t level,
                      const int32_t* r, uint32_t n_items, uint64_t* const* out, const uint64_t* const* addct,
-                     cudaStream_t s) {
+                     cudaStream_t s, const uint64_t* gal) {
   const size_t n = level + 1, N = c->N;
   // rotations by 0 first (copies / adds), then key switches in chunks
   std::vector<uint32_t> ks;
   for (uint32_t i = 0; i < n_items; ++i) {
-    const uint64_t k = hy_galois_elt(c, r[i]);
+    const uint64_t k = gal ? gal[i] : hy_galois_elt(c, r[i]);
     if (k != 1) {
       if (!evk[i]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
       ks.push_back(i);
@@ -696,7 +696,7 @@ hy_status hrot_multi(hy_ctx* c, const uint64_t* const* evk, const uint64_t* cons
       ext[g] = it[g].ext;
       u[g] = it[g].u;
       keys[g] = evk[i];
-      kk[g] = hy_galois_elt(c, r[i]);
+      kk[g] = gal ? gal[i] : hy_galois_elt(c, r[i]);
       shared &= evk[i] == evk[ks[done]];
       // kappa(c0) is gathered by the ModDown epilogue straight from ct (unless out aliases ct)
       di[g] = alias ? DownItem{it[g].u, out[i], it[g].rc, 1, nullptr, addct ? addct[i] : nullptr, it[g].v, it[g].w}
@@ -923,6 +923,19 @@ extern "C" hy_status hy_hrot_batch(hy_ctx* c, const uint64_t* const* evks, const
   s0 = hrot_multi(c, evks, cts, level, r, n, outs, nullptr, st(stream));
   if (s0 != HY_OK) return s0;
   return cuda_check("hy_hrot_batch");
+}
+
+extern "C" hy_status hy_hrot_galois(hy_ctx* c, const uint64_t* evk, const uint64_t* ct, uint32_t level, uint64_t k,
+                                    uint64_t* out, void* stream) {
+  hy_status s0 = check_level(c, level);
+  if (s0 != HY_OK) return s0;
+  if (!ct || !out) return fail(HY_E_ARG, "null");
+  if (!(k & 1) || k >= 2ull * c->N) return fail(HY_E_ARG, "Galois element must be odd and < 2N");
+  if (out == ct) return fail(HY_E_ARG, "the key switch cannot run in place");
+  const int32_t r0 = 0;
+  s0 = hrot_multi(c, &evk, &ct, level, &r0, 1, &out, nullptr, st(stream), &k);
+  if (s0 != HY_OK) return s0;
+  return cuda_check("hy_hrot_galois");
 }
 
 extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, const uint64_t* ct, uint32_t level,

@@ -622,6 +622,29 @@ extern "C" hy_status hy_add(hy_ctx* c, const uint64_t* a, const uint64_t* b, uin
   return cuda_check("hy_add");
 }
 
+// out = a - b mod q over [npoly][l+1][N].  grid (N/256, (l+1)*npoly)
+namespace hy {
+namespace {
+__global__ void k_sub(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
+                      DevTables dt, int nlimb) {
+  const size_t N = (size_t)gridDim.x * blockDim.x;
+  const size_t o = (size_t)blockIdx.y * N + blockIdx.x * blockDim.x + threadIdx.x;
+  out[o] = sub_mod(a[o], b[o], dt.pc[blockIdx.y % nlimb].q);
+}
+}  // namespace
+}  // namespace hy
+
+extern "C" hy_status hy_sub(hy_ctx* c, const uint64_t* a, const uint64_t* b, uint32_t npoly, uint32_t level,
+                            uint64_t* out, void* stream) {
+  if (!c || !a || !b || !out) return fail(HY_E_ARG, "null");
+  if (level >= c->n_q || npoly == 0) return fail(HY_E_ARG, "level/npoly out of range");
+  dim3 g(c->N / kT, (level + 1) * npoly);
+  KTimer kt(c, FAM_ELEM, st(stream));
+  kt.bytes = 3ull * (level + 1) * npoly * c->N * 8;
+  k_sub<<<g, kT, 0, st(stream)>>>(a, b, out, c->dt, level + 1);
+  return cuda_check("hy_sub");
+}
+
 extern "C" hy_status hy_level_down(hy_ctx* c, const uint64_t* ct, uint32_t level, uint32_t new_level,
                                    uint64_t* out, void* stream) {
   if (!c || !ct || !out) return fail(HY_E_ARG, "null");

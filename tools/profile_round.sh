@@ -3,7 +3,7 @@
 # usage: tools/profile_round.sh <tag>   (run from the repo root under gpurun; then tools/ncu_round.py <tag>)
 TAG=${1:-r01}
 export HY_NCU_TIMED=1
-B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-conv --no-variants"
+B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-conv --no-variants --no-c1"
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --kernel-name-base demangled --log-file gpurun_out/launches_${TAG}.csv $B > /dev/null 2>&1
 # one full capture per distinct kernel (first launch in the timed region, which is the plain step's chunk 0
