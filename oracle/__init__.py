@@ -294,6 +294,12 @@ class Oracle:
         lib().orc_hrot(self._c, ct.level, np.ascontiguousarray(evk), self.galois_elt(r), np.ascontiguousarray(ct.data), out)
         return Ct(out, ct.level, ct.scale)
 
+    def hrot_galois(self, ct: Ct, evk, k: int) -> Ct:
+        """key switch by any Galois element k (k = 2N - 1: conjugation), the plain variant"""
+        out = np.zeros_like(ct.data)
+        lib().orc_hrot(self._c, ct.level, np.ascontiguousarray(evk), int(k), np.ascontiguousarray(ct.data), out)
+        return Ct(out, ct.level, ct.scale)
+
     def hrot_hoisted(self, ct: Ct, evks, rs):
         outs = [np.zeros_like(ct.data) for _ in rs]
         ks = np.array([self.galois_elt(r) for r in rs], np.uint64)

@@ -77,3 +77,115 @@ def special_fft_matrix(N: int) -> np.ndarray:
     k = np.arange(n, dtype=object)
     e = np.outer(rot, k) % M2
     return np.exp(1j * np.pi * e.astype(np.float64) / N)
+
+
+# --------------------------------------------------------------------------- EvalMod and the whole bootstrap
+# DESIGN R-EVALMOD fixes the operation sequence; the Chebyshev coefficients and the linear-transform matrices are
+# inputs (data) of both implementations, like conv weights.
+CHEB_SCHEDULE = [  # (k, m, n): T_k = 2 T_m T_n - T_|m-n|, every even k <= 30 at depth <= 5
+    (2, 1, 1), (4, 2, 2), (8, 4, 4), (16, 8, 8), (6, 4, 2), (10, 8, 2), (12, 8, 4), (14, 8, 6),
+    (18, 16, 2), (20, 16, 4), (22, 16, 6), (24, 16, 8), (26, 16, 10), (28, 16, 12), (30, 16, 14)]
+
+
+def _const(o, c, scale, level):
+    return o.encode(np.full(o.n, float(c)), int(round(scale)), level)
+
+
+def _monomial(o, sign, level):
+    """the plaintext sign * X^{N/2} (scale 1): multiplication by sign * i on every slot"""
+    import oracle as _o
+    cf = np.zeros(o.N, np.int64)
+    cf[o.N // 2] = sign
+    return _o.Pt(o.coeffs_to_pt(cf, level), level, 1.0)
+
+
+def _down(o, ct, level):
+    return ct if ct.level == level else o.level_down(ct, level)
+
+
+def _sub(o, a: Ct, b: Ct) -> Ct:
+    """a - b limbwise mod q (plain definition)"""
+    out = np.empty_like(a.data)
+    for p in range(2):
+        for i in range(a.level + 1):
+            q = np.uint64(o.q[i])
+            out[p, i] = (a.data[p, i] + (q - b.data[p, i]) % q) % q
+    return Ct(out, a.level, a.scale)
+
+
+def _add_const(o, ct, c):
+    return o.add_pt(ct, _const(o, c, ct.scale, ct.level))
+
+
+def _mul(o, a, b, rlk):
+    lv = min(a.level, b.level)
+    return o.rescale(o.mulct(_down(o, a, lv), _down(o, b, lv), rlk))
+
+
+def _rescaled_to(o, t: Ct, target: float) -> Ct:
+    """t brought to scale `target` (one level): PMult by the constant 1 encoded at the integer scale
+    round(q_l target / t.scale), then rescale by q_l -- how terms of different scales are aligned before they are
+    added (DESIGN R-EVALMOD)"""
+    S = float(o.q[t.level]) * target / t.scale
+    return o.rescale(o.pmult(t, _const(o, 1.0, S, t.level)))
+
+
+def eval_chebyshev(o, s: Ct, cheb, rlk, target: float) -> Ct:
+    """sum_k cheb[k] T_k(s) for even k (DESIGN R-EVALMOD): T_k = 2 T_m T_n - T_|m-n| by CHEB_SCHEDULE, T_|m-n| first
+    brought to the product's scale (_rescaled_to) and level; each term c_k T_k a PMult by the constant c_k encoded at
+    round(q_l target / scale(T_k)) and a rescale (every term then at scale ~ target); the terms aligned to the lowest
+    level and summed in increasing k; then c_0 added at the sum's scale."""
+    T = {1: s}
+    for k, m, n in CHEB_SCHEDULE:
+        p = _mul(o, T[m], T[n], rlk)
+        p = o.add(p, p)
+        d = abs(m - n)
+        if d == 0:
+            T[k] = _add_const(o, p, -1.0)
+        else:
+            T[k] = _sub(o, p, _down(o, _rescaled_to(o, T[d], p.scale), p.level))
+    terms = []
+    for k in range(2, len(cheb), 2):
+        if cheb[k] == 0:
+            continue
+        t = T[k]
+        S = float(o.q[t.level]) * target / t.scale
+        terms.append(o.rescale(o.pmult(t, _const(o, cheb[k], S, t.level))))
+    lv = min(t.level for t in terms)
+    acc = None
+    for t in terms:
+        t = _down(o, t, lv)
+        acc = t if acc is None else o.add(acc, t)
+    return _add_const(o, acc, cheb[0])
+
+
+def eval_mod(o, s: Ct, cheb, r: int, rlk) -> Ct:
+    """cos(a s) by the Chebyshev series, then r double angles cos(2x) = 2 cos(x)^2 - 1"""
+    c = eval_chebyshev(o, s, cheb, rlk, s.scale)
+    for _ in range(r):
+        sq = _mul(o, c, c, rlk)
+        c = _add_const(o, o.add(sq, sq), -1.0)
+    return c
+
+
+def bootstrap(o, ct: Ct, level: int, cts_diags: dict, stc_diags: dict, bs: int, cheb, r: int, a: float,
+              evks: dict, conj_key, rlk) -> Ct:
+    """ModRaise -> CoeffToSlot -> (Re, Im) split by conjugation -> EvalMod -> recombine -> SlotToCoeff
+    (DESIGN R-EVALMOD).  cts_diags: the diagonals of V^{-1} / 2, stc_diags those of (K / 2 pi) V, with
+    K = q_0 / scale; cheb: the coefficients of cos(a s) on [-1, 1].  The CoeffToSlot output is scaled by
+    alpha1 = 2 pi / (K 2^r a) with a constant PMult (a constant encodes into one coefficient, exactly to 2^-27,
+    where alpha1 folded into the diagonals would keep only ~15 bits of them)."""
+    K = float(o.q[0]) / ct.scale
+    alpha1 = 2.0 * np.pi / (K * (2 ** r) * a)
+    beta1 = -np.pi / (2.0 * (2 ** r) * a)
+    up = mod_raise(o, ct, level)
+    y = lintrans(o, up, cts_diags, bs, evks)
+    y = o.rescale(o.pmult(y, _const(o, alpha1, o.q[y.level], y.level)))
+    yc = o.hrot_galois(y, conj_key, 2 * o.N - 1)
+    s_re = _add_const(o, o.add(y, yc), beta1)
+    s_im = _add_const(o, o.pmult(_sub(o, y, yc), _monomial(o, -1, y.level)), beta1)
+    e_re = eval_mod(o, s_re, cheb, r, rlk)
+    e_im = eval_mod(o, s_im, cheb, r, rlk)
+    z = o.add(e_re, o.pmult(e_im, _monomial(o, 1, e_im.level)))
+    del K
+    return lintrans(o, z, stc_diags, bs, evks)

@@ -19,6 +19,9 @@ PARAMS = {
     "hyp": dict(log_n=16, q_bits=[48] + [42] * 23, p_bits=[48] * 4, dnum=6, h=192, log_scale=42),
     # small full-featured set used by fast CPU tests (alpha = 2, partial last digit)
     "mini": dict(log_n=10, q_bits=[48, 40, 40, 40, 40], p_bits=[48, 48], dnum=3, h=32, log_scale=40),
+    # the bootstrapping tests' chain: room for ModRaise, CoeffToSlot, EvalMod (Chebyshev depth 6
+    # + 3 double angles), SlotToCoeff; small h keeps the ModRaise overflow I small (insecure, test only)
+    "boot": dict(log_n=10, q_bits=[48] + [40] * 16, p_bits=[48] * 3, dnum=6, h=16, log_scale=40),
 }
 
 SEED_SK = 3        # secret-key seed of BASELINE config 1

@@ -112,3 +112,38 @@ def test_coeff_to_slot_to_coeff_mini():
     assert np.array_equal(to_np(w), ow.data)
     back = o.decode(o.decrypt(SK, ow))
     assert np.max(np.abs(back - o.decode(o.decrypt(SK, up)))) < 2**-12
+
+
+def test_bootstrap_small_ring():
+    """The whole bootstrapping (DESIGN R-EVALMOD) on the 'boot' chain (N = 2^10, 17 limbs): ModRaise, CoeffToSlot,
+    conjugation split, EvalMod (Chebyshev degree 30 of cos(8 s), 3 double angles), recombination, SlotToCoeff --
+    every intermediate and the result bit-exact vs oracle/boot.py, and the result decrypts to the input slots within
+    2^-10 of max|z|"""
+    import math
+
+    import paper_2302_02407_b200 as hy
+    from paper_2302_02407_b200.boot import Bootstrapper
+    ctx, o = pair("boot")
+    n, N, top = o.n, o.N, o.nq - 1
+    r, a, bs = 3, 8.0, 32
+    K = float(o.q[0]) / 2**40
+    V = B.special_fft_matrix(N)
+    ds = list(range(n))
+    cts_d = B.diagonals(np.linalg.inv(V) / 2, ds)
+    stc_d = B.diagonals(K / (2 * math.pi) * V, ds)
+    cheb = np.polynomial.chebyshev.chebinterpolate(lambda s: np.cos(a * s), 30)
+    cheb[1::2] = 0.0
+    lt = hy.LinTrans(ctx, ds, bs)
+    keys = {rr: ctx.keygen_rot(SK, EK, rr) for rr in lt.rots}
+    okeys = {rr: o.keygen_rot(SK, EK, rr) for rr in lt.rots}
+    conj, oconj = ctx.keygen_galois(SK, EK, 2 * N - 1), o.keygen_galois(SK, EK, 2 * N - 1)
+    rlk, orlk = ctx.keygen_relin(SK, EK), o.keygen_relin(SK, EK)
+    z = synth.slots_uniform(40, n)
+    ct0 = o.level_down(o.encrypt(SK, 11, 0, o.encode(z, 2**40, top)), 0)
+    bt = Bootstrapper(ctx, cts_d, stc_d, bs, cheb, r, a, keys, conj, rlk)
+    got = bt.bootstrap(to_dev(ct0.data, ctx), 2.0**40, top)
+    want = B.bootstrap(o, ct0, top, dict(zip(ds, cts_d)), dict(zip(ds, stc_d)), bs, cheb, r, a, okeys, oconj, orlk)
+    assert got.level == want.level and got.scale == want.scale
+    assert np.array_equal(to_np(got.t), want.data)
+    dz = o.decode(o.decrypt(SK, want))
+    assert np.max(np.abs(dz - z)) < 2**-10 * np.max(np.abs(z))

@@ -93,3 +93,29 @@ def test_coeff_to_slot_and_back(mini):
     s2c = B.lintrans(o, c2s, dict(zip(ds, B.diagonals(V, ds))), bs, evks)
     back = o.decode(o.decrypt(SK, s2c))
     assert np.max(np.abs(back - z)) < 2**-15
+
+
+@pytest.mark.slow
+def test_oracle_bootstrap_recovers_slots():
+    """DESIGN R-EVALMOD end to end on the oracle ('boot' chain, N = 2^10): a level-0 ciphertext bootstrapped to a
+    higher level decrypts to the same slots within 2^-10 of max|z|, and every EvalMod stage matches its plaintext
+    function (the scaled sine of t / (Delta K))"""
+    import math
+    o = oracle.Oracle(**synth.PARAMS["boot"])
+    n, N, top = o.n, o.N, o.nq - 1
+    r, a, bs = 3, 8.0, 32
+    K = float(o.q[0]) / 2**40
+    V = B.special_fft_matrix(N)
+    ds = list(range(n))
+    cheb = np.polynomial.chebyshev.chebinterpolate(lambda s: np.cos(a * s), 30)
+    cheb[1::2] = 0.0
+    need = sorted({d % bs for d in ds if d % bs} | {(d // bs) * bs for d in ds if d // bs})
+    evks = {rr: o.keygen_rot(SK, EK, rr) for rr in need}
+    z = synth.slots_uniform(41, n)
+    ct0 = o.level_down(o.encrypt(SK, 12, 0, o.encode(z, 2**40, top)), 0)
+    out = B.bootstrap(o, ct0, top, dict(zip(ds, B.diagonals(np.linalg.inv(V) / 2, ds))),
+                      dict(zip(ds, B.diagonals(K / (2 * math.pi) * V, ds))), bs, cheb, r, a, evks,
+                      o.keygen_galois(SK, EK, 2 * N - 1), o.keygen_relin(SK, EK))
+    assert out.level >= 1
+    got = o.decode(o.decrypt(SK, out))
+    assert np.max(np.abs(got - z)) < 2**-10 * np.max(np.abs(z))
