@@ -751,11 +751,56 @@ def bench_boot_linear(ctx, steps, warmup, timed):
     out = ctx.empty(*ctx.ct_shape(lv - 1))
     scratch = ctx.empty(int(hy.lib().hy_lintrans_scratch_words(ctx._c, lt._p, lv)))
     ms_lt, l_lt = timed(lambda: lt.apply(keys, raised, lv, pts, scratch, out), steps, warmup)
+    small = bench_bootstrap_small(steps, warmup, timed)
     return {"mod_raise_ms": ms_raise, "mod_raise_launches": l_raise, "lintrans_ms": ms_lt, "lintrans_launches": l_lt,
+            "bootstrap_n1024": small,
             "lintrans": {"diagonals": len(ds), "baby_steps": lt.n_baby, "giant_steps": lt.n_giant, "level": lv,
                          "keys": len(lt.rots)},
-            "note": "ModRaise + one BSGS diagonal transform (CoeffToSlot / SlotToCoeff building block); EvalMod is "
-                    "not built, so there is no end-to-end bootstrapping time"}
+            "note": "Set_hyp: ModRaise + one BSGS diagonal transform (the CoeffToSlot / SlotToCoeff building block); "
+                    "the whole bootstrapping runs at N = 2^10 only (dense transforms, DESIGN R-EVALMOD)"}
+
+
+def bench_bootstrap_small(steps, warmup, timed):
+    """The whole bootstrapping (DESIGN R-EVALMOD) on the 'boot' chain (N = 2^10, 17 limbs), device time per call
+    with every key resident; timed through the bench's own context clock (the launches are this context's)."""
+    import math
+
+    import numpy as np
+    import torch
+
+    import paper_2302_02407_b200 as hy
+    from paper_2302_02407_b200.boot import Bootstrapper
+    prm = synth.PARAMS["boot"]
+    ctx = hy.Context(**prm, device=torch.cuda.current_device())
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    n, N, top = ctx.n, ctx.N, len(prm["q_bits"]) - 1
+    r, a, bs = 3, 8.0, 32
+    K = float(ctx.moduli[0]) / 2**40
+    # the special-FFT matrix V[j][k] = zeta^{k 5^j} (DESIGN R-LINTRANS) and its diagonals
+    rot = np.array([pow(5, j, 2 * N) for j in range(n)], dtype=np.int64)
+    V = np.exp(1j * np.pi * (np.outer(rot, np.arange(n)) % (2 * N)) / N)
+    j = np.arange(n)
+    diag = lambda M: [M[j, (j + d) % n] for d in range(n)]  # noqa: E731
+    cheb = np.polynomial.chebyshev.chebinterpolate(lambda x: np.cos(a * x), 30)
+    cheb[1::2] = 0.0
+    lt = hy.LinTrans(ctx, list(range(n)), bs)
+    keys = {rr: ctx.keygen_rot(sk, ek, rr) for rr in lt.rots}
+    bt = Bootstrapper(ctx, diag(np.linalg.inv(V) / 2), diag(K / (2 * math.pi) * V), bs, cheb, r, a, keys,
+                      ctx.keygen_galois(sk, ek, 2 * N - 1), ctx.keygen_relin(sk, ek))
+    ct = ctx.encrypt(sk, synth.SEED_ENC, 5, ctx.encode(synth.slots_uniform(5, n), 2**40, top), top)
+    ct0 = ctx.level_down(ct, top, 0)
+    bt.bootstrap(ct0, 2.0**40, top)  # encodes the transform plaintexts once (untimed, like weights)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    e0.record()
+    for _ in range(steps):
+        out = bt.bootstrap(ct0, 2.0**40, top)
+    e1.record()
+    torch.cuda.synchronize()
+    return {"ms": e0.elapsed_time(e1) / steps, "launches": (ctx.launch_count() - l0) // steps, "levels_consumed":
+            top - out.level, "ring": "N = 2^10, 17 limbs (synth boot chain)",
+            "note": "host-sequenced C-ABI calls; the transforms are dense (512 diagonals each)"}
 
 
 # --------------------------------------------------------------------------- our arm

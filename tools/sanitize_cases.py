@@ -18,8 +18,10 @@ SK, EK = synth.SEED_SK, synth.SEED_EVK
 def toy():
     prm = synth.PARAMS["toy"]
     ctx = hy.Context(**prm)
-    for spec in [(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA"), (8, 8, 8, 3, 1, 8, 1, 1, 2, "CA"), (4, 8, 8, 3, 2, 8, 1, 1, 2, "CA")]:
-        p = hy.ConvPlan(ctx, *spec, bias=True)
+    for spec in [(4, 4, 8, 3, 1, 8, 1, 1, 1, "RA", 1), (8, 8, 8, 3, 1, 8, 1, 1, 2, "CA", 1),
+                 (4, 8, 8, 3, 2, 8, 1, 1, 2, "CA", 1), (64, 8, 6, 3, 1, 8, 1, 1, 1, "CA", 2),
+                 (8, 64, 6, 3, 1, 8, 1, 1, 1, "RA", 2)]:
+        p = hy.ConvPlan(ctx, *spec[:10], S=spec[10], bias=True)
         level = 2
         cts = [ctx.encrypt(SK, 9, i, ctx.encode(synth.slots_uniform(i, ctx.n), 2**40, level), level)
                for i in range(p.n_in)]
@@ -46,7 +48,25 @@ def hyp():
     print("hyp key switches ok")
 
 
+def boot():
+    """ModRaise, the BSGS transform (hoisted baby steps, MulFilter&Sum, lazy HRotSum), conjugation, MulCt"""
+    prm = synth.PARAMS["boot"]
+    ctx = hy.Context(**prm)
+    top = len(prm["q_bits"]) - 1
+    ct = ctx.encrypt(SK, 9, 0, ctx.encode(synth.slots_uniform(1, ctx.n), 2**40, top), top)
+    up = ctx.mod_raise(ctx.level_down(ct, top, 0), top)
+    lt = hy.LinTrans(ctx, [0, 1, 2, 5, 9, 33], 4)
+    keys = {r: ctx.keygen_rot(SK, EK, r) for r in lt.rots}
+    g = np.random.default_rng(2)
+    y = lt.apply(keys, up, top, lt.encode([g.uniform(-1, 1, ctx.n) + 0j for _ in range(6)], top))
+    ctx.hrot_galois(ctx.keygen_galois(SK, EK, 2 * ctx.N - 1), y, top - 1, 2 * ctx.N - 1)
+    ctx.mulct(ctx.keygen_relin(SK, EK), y, y, top - 1)
+    torch.cuda.synchronize()
+    print("boot steps ok")
+
+
 if __name__ == "__main__":
     toy()
+    boot()
     if "--toy-only" not in sys.argv:
         hyp()
