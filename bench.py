@@ -798,9 +798,33 @@ def bench_bootstrap_small(steps, warmup, timed):
         out = bt.bootstrap(ct0, 2.0**40, top)
     e1.record()
     torch.cuda.synchronize()
-    return {"ms": e0.elapsed_time(e1) / steps, "launches": (ctx.launch_count() - l0) // steps, "levels_consumed":
-            top - out.level, "ring": "N = 2^10, 17 limbs (synth boot chain)",
-            "note": "host-sequenced C-ABI calls; the transforms are dense (512 diagonals each)"}
+    res = {"ms": e0.elapsed_time(e1) / steps, "launches": (ctx.launch_count() - l0) // steps, "levels_consumed":
+           top - out.level, "ring": "N = 2^10, 17 limbs (synth boot chain)",
+           "note": "host-sequenced C-ABI calls; the transforms are dense (512 diagonals each)"}
+    # the same sequence captured once in a CUDA graph and replayed (the small ring is launch-bound)
+    try:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            bt.bootstrap(ct0, 2.0**40, top)  # warm the allocator on the capture stream
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            gout = bt.bootstrap(ct0, 2.0**40, top)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(gout.t, out.t))
+        e0.record()
+        for _ in range(steps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        res["cuda_graph"] = {"ms": e0.elapsed_time(e1) / steps, "replay_equals_eager": ok}
+    except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+        res["cuda_graph"] = {"error": str(ex)[:200]}
+    return res
 
 
 # --------------------------------------------------------------------------- our arm

@@ -41,15 +41,24 @@ class Bootstrapper:
         self.stc = LinTrans(ctx, list(range(n)), bs)
         self._cts_diags, self._stc_diags = cts_diags, stc_diags
         self._pts = {}
+        self._consts = {}
 
     # ---- helpers (each one C-ABI call, scales tracked as the oracle's Ct does)
     def _const(self, c, scale, level):
-        return self.ctx.encode(np.full(self.ctx.n, float(c)), int(round(scale)), level), float(int(round(scale)))
+        """the constant plaintext c at integer scale round(scale), encoded once and kept on the device (so that a
+        bootstrap issues only device work and can be captured in a CUDA graph)"""
+        key = (float(c), int(round(scale)), level)
+        if key not in self._consts:
+            self._consts[key] = self.ctx.encode(np.full(self.ctx.n, float(c)), key[1], level)
+        return self._consts[key], float(key[1])
 
     def _monomial(self, sign, level):
-        cf = np.zeros(self.ctx.N, np.int64)
-        cf[self.ctx.N // 2] = sign
-        return self.ctx.pt_from_coeffs(cf, level)
+        key = ("X^{N/2}", sign, level)
+        if key not in self._consts:
+            cf = np.zeros(self.ctx.N, np.int64)
+            cf[self.ctx.N // 2] = sign
+            self._consts[key] = self.ctx.pt_from_coeffs(cf, level)
+        return self._consts[key]
 
     def _down(self, x: CT, level):
         return x if x.level == level else CT(self.ctx.level_down(x.t, x.level, level), level, x.scale)
