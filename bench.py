@@ -534,7 +534,7 @@ def bench_conv(ctx, ws, rank, steps, warmup, timed, layers_def=None, net="ResNet
         tap_shard = algo == "RA" and ws > 1 and p.n_out < ws  # ResNet-20 RAConv: one output, shard the taps
         # CAConv with at least one input per rank (ResNet-18): shard Slide_f by input and all-gather the slid
         # ciphertexts instead of repeating every Slide rotation on every rank
-        slide_shard = algo == "CA" and ws > 1 and p.n_in >= ws
+        slide_shard = algo == "CA" and ws > 1 and p.n_in >= ws and f > 1  # pconv (f = 1) has no Slide
 
         def step():
             if tap_shard:  # every rank ends with every output: no gather
