@@ -1006,10 +1006,6 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_p_tma(const __grid_constant_
 // column stages and is stored fred-reduced (between-pass format, for the fused row kernels).  The
 // coefficient-domain sources and the un-transformed conversion never reach HBM.  The next phase's
 // twiddle heap is fetched into a register during the current phase (double-buffered T).
-// HY_BCONV_FRED: whether the BConv sum is re-centred before the forward column stages (device copy of the switch)
-__constant__ int c_bconv_fred = 0;
-__device__ __forceinline__ bool bconv_fred_on() { return c_bconv_fred != 0; }
-
 // shared memory of one column CTA: the 8-column strip, the double-buffered twiddle heap, the BConv constants
 template <int A>
 __host__ __device__ constexpr int cols_smem_words() { return 8 * 256 + 2 * 256 + kMaxExt * A; }
@@ -1053,7 +1049,6 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
     return dt.tw + (size_t)tgt_chain(target(p)) * N;
   };
   if (tid > 0 && tid < 256) T[tid] = table(0)[tid];
-  const bool bconv_fred = bconv_fred_on() || A > 4;
   constexpr int AR = YS ? 1 : A;  // sources held in registers
   double y[AR][8];
   double* ysm = sm + cols_smem_words<A>();  // YS: [A-1][8][256], word (i, k) of thread tid at ysm[(i*8+k)*256+tid]
@@ -1117,10 +1112,7 @@ __device__ __forceinline__ void bconv_cols_body(const ModUpColsArgs& a, const Mo
 #pragma unroll
         for (int i = 0; i < A; ++i)
           acc += fmulmod(i < AR ? y[i < AR ? i : 0][k] : ysm[((i - 1) * 8 + k) * 256 + tid], h[i], q, qinv);
-        // HY_BCONV_FRED=0 (default): the sum of A <= 4 products (|each| <= 0.57 q, R-FP64) enters the forward column
-        // stages unreduced: from |v| <= 2.25 q the 8 stages keep every fmulmod operand below 7.7 q < 2^51 / q_max
-        // (tests/test_fp64_bound_cpu.py); the pass output is stored fred-reduced as before
-        x[k] = bconv_fred ? fred(acc, q, qinv) : acc;
+        x[k] = fred(acc, q, qinv);
       }
       run_stages<1, true>(x, l, 7, 5, Tp, q, qinv);
 #pragma unroll
@@ -1202,17 +1194,8 @@ void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t le
   k_ntt_rows_inv_aut<<<grid, 256, 0, s>>>(a, c->dt, (int)c->log_n);
 }
 
-void set_bconv_fred_switch() {
-  static bool done = false;
-  if (done) return;
-  const int v = getenv("HY_BCONV_FRED") != nullptr && atoi(getenv("HY_BCONV_FRED")) != 0;
-  cudaMemcpyToSymbol(c_bconv_fred, &v, sizeof(v));
-  done = true;
-}
-
 void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
   if (G <= 0) return;
-  set_bconv_fred_switch();
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level);
   dim3 grid(32, beta, G);
   KTimer kt(c, FAM_MODUP, s);
@@ -1236,7 +1219,6 @@ void launch_modup_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level,
 
 void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
   if (G <= 0) return;
-  set_bconv_fred_switch();
   const int n = (int)level + 1, E = n + (int)c->n_p;
   dim3 grid(32, 2, G);
   KTimer kt(c, FAM_MODDOWN, s);
@@ -1258,7 +1240,6 @@ void launch_moddown_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t leve
 
 void launch_rescale_cols(hy_ctx* c, const ModUpColsArgs& a, int G, uint32_t level, cudaStream_t s) {
   if (G <= 0) return;
-  set_bconv_fred_switch();
   dim3 grid(32, 2, G);
   KTimer kt(c, FAM_RESCALE, s);
   // algorithmic bytes: the 2 dropped limbs in, the 2 level conversion limbs out

@@ -95,14 +95,3 @@ def test_inverse_pass_growth():
     so the largest fmulmod operand is a - b with |a|, |b| <= 4 q_max (canonical start): far below 2^51."""
     for _, q in PRIMES:
         assert 8 * q < 2.0**51
-
-
-def test_bconv_sum_unreduced_into_column_pass():
-    """the fast BConv output (a sum of alpha <= 4 fmulmod products of canonical operands, each |r| <= (1/2 + 1/16) q)
-    enters the forward column stages without a re-centring (hy_ntt.cu bconv_cols_body): from 2.25 q the largest
-    stage input after 7 stages stays below 2^51 / q for every prime; the pass output is stored fred-reduced"""
-    for _, q in PRIMES:
-        beta0 = 4 * (0.5 + q * 2.0**-52)
-        b = beta_after(8, beta0, q)
-        assert max(b[:8]) * q < 2.0**51, (q, b)
-    assert abs(beta_after(8, 2.25, 2**48)[7] - 7.66) < 0.01
