@@ -752,12 +752,64 @@ def bench_boot_linear(ctx, steps, warmup, timed):
     scratch = ctx.empty(int(hy.lib().hy_lintrans_scratch_words(ctx._c, lt._p, lv)))
     ms_lt, l_lt = timed(lambda: lt.apply(keys, raised, lv, pts, scratch, out), steps, warmup)
     small = bench_bootstrap_small(steps, warmup, timed)
+    del keys, pts, raised, out, scratch
+    hyp = bench_bootstrap_set_hyp(ctx, steps)
     return {"mod_raise_ms": ms_raise, "mod_raise_launches": l_raise, "lintrans_ms": ms_lt, "lintrans_launches": l_lt,
-            "bootstrap_n1024": small,
+            "bootstrap_n1024": small, "bootstrap_set_hyp": hyp,
             "lintrans": {"diagonals": len(ds), "baby_steps": lt.n_baby, "giant_steps": lt.n_giant, "level": lv,
                          "keys": len(lt.rots)},
             "note": "Set_hyp: ModRaise + one BSGS diagonal transform (the CoeffToSlot / SlotToCoeff building block); "
-                    "the whole bootstrapping runs at N = 2^10 only (dense transforms, DESIGN R-EVALMOD)"}
+                    "the whole bootstrapping at Set_hyp with factorised transforms (bootstrap_set_hyp, DESIGN R-SFFT) "
+                    "and at N = 2^10 with dense ones (bootstrap_n1024)"}
+
+
+def bench_bootstrap_set_hyp(ctx, steps):
+    """The whole bootstrapping at Set_hyp (N = 2^16, L+1 = 24, h = 192; DESIGN R-SFFT,
+    R-EVALMOD): ModRaise 0 -> 23, CoeffToSlot as 3 factorised levels (63/63/32 diagonals), EvalMod (degree-30
+    Chebyshev series of cos(12 s), 4 double angles), SlotToCoeff as 3 levels -> level 6 (L' = 6).  Device
+    time per call with every key and transform plaintext resident (encoded once, untimed, like weights), set beside
+    the paper's Boot = 2160 ms (tb:Benchmark; HEaaN, its own hardware: context, not a target)."""
+    import math
+
+    import numpy as np
+    import torch
+
+    from paper_2302_02407_b200.boot import Bootstrapper, level_bs, sfft_levels, transform_rots
+    sk, ek = synth.SEED_SK, synth.SEED_EVK
+    N, top = ctx.N, ctx.n_q - 1
+    r, a = 4, 12.0
+    K = float(ctx.moduli[0]) / 2**42
+    cts = sfft_levels(N, [5, 5, 5], inverse=True, scale=0.5)
+    stc = sfft_levels(N, [5, 5, 5], scale=K / (2 * math.pi))
+    bs = ([level_bs(D) for D in cts], [level_bs(D) for D in stc])
+    rots = sorted(set(transform_rots(ctx, cts, bs[0])) | set(transform_rots(ctx, stc, bs[1])))
+    keys = {rr: ctx.keygen_rot(sk, ek, rr) for rr in rots}
+    cheb = np.polynomial.chebyshev.chebinterpolate(lambda x: np.cos(a * x), 30)
+    cheb[1::2] = 0.0
+    bt = Bootstrapper(ctx, cts, stc, bs, cheb, r, a, keys, ctx.keygen_galois(sk, ek, 2 * N - 1),
+                      ctx.keygen_relin(sk, ek))
+    z = synth.slots_uniform(6, ctx.n)
+    ct = ctx.encrypt(sk, synth.SEED_ENC, 6, ctx.encode(z, 2**42, top), top)
+    ct0 = ctx.level_down(ct, top, 0)
+    out = bt.bootstrap(ct0, 2.0**42, top)  # encodes the transform plaintexts once (untimed)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_it = max(1, min(steps, 3))
+    l0 = ctx.launch_count()
+    e0.record()
+    for _ in range(n_it):
+        out = bt.bootstrap(ct0, 2.0**42, top)
+    e1.record()
+    torch.cuda.synchronize()
+    got = ctx.decode(ctx.decrypt(sk, out.t, out.level), out.level, out.scale)
+    err = float(np.max(np.abs(got - z)) / np.max(np.abs(z)))
+    return {"ms": e0.elapsed_time(e1) / n_it, "calls": n_it, "launches": (ctx.launch_count() - l0) // n_it,
+            "levels": [top, out.level], "levels_consumed": top - out.level, "rotation_keys": len(rots),
+            "transform_levels": {"coeff_to_slot": [len(D) for D in cts], "slot_to_coeff": [len(D) for D in stc]},
+            "evalmod": {"cos_a": a, "double_angles": r, "chebyshev_degree": 30},
+            "max_rel_error": err, "paper_boot_ms": 2160.0,
+            "note": "host-sequenced C-ABI calls on the resident keys; the paper's 2160 ms is HEaaN on its own "
+                    "hardware (tb:Benchmark), context only"}
 
 
 def bench_bootstrap_small(steps, warmup, timed):

@@ -1,4 +1,4 @@
-"""Oracle for the linear steps of CKKS bootstrapping (partial) -- TEST INFRASTRUCTURE.
+"""Oracle for CKKS bootstrapping -- TEST INFRASTRUCTURE.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import this (see oracle/__init__.py).
 
@@ -12,7 +12,12 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import 
 * special_fft_matrix: the canonical embedding restricted to CKKS's complex packing, V[j][k] = zeta^{k 5^j}
   (zeta = exp(i pi / N)), so that the slots of a plaintext with coefficients m are V (m_k + i m_{k+n})_k / scale
   (DESIGN R-ENCODE).  CoeffToSlot is V^{-1} on the slots, SlotToCoeff is V.
-EvalMod (the approximate modular reduction between them) is not built.
+* sfft_stage / diag_mul / sfft_levels: V factorised into radix-2 butterfly stages (three diagonals each) grouped
+  into a few levels (DESIGN R-SFFT), so that CoeffToSlot / SlotToCoeff at N = 2^16 take 3 levels and ~42 rotation keys
+  (48 rotation keys) instead of n = 2^15 dense diagonals.  Pinned in tests/test_oracle_boot.py against the
+  dense V and V^{-1} (products of the levels, bit reversal), and the product of two diagonal matrices against dense
+  matmul.
+* eval_chebyshev / eval_mod / bootstrap: EvalMod and the whole bootstrap in the operation order DESIGN R-EVALMOD fixes.
 """
 from __future__ import annotations
 
@@ -77,6 +82,77 @@ def special_fft_matrix(N: int) -> np.ndarray:
     k = np.arange(n, dtype=object)
     e = np.outer(rot, k) % M2
     return np.exp(1j * np.pi * e.astype(np.float64) / N)
+
+
+# --------------------------------------------------------------------------- the special FFT, factorised
+# DESIGN R-SFFT.  V (special_fft_matrix) is evaluated by the radix-2 "special FFT": bit-reverse the input, then for
+# len = 2, 4, ..., n, every block of len slots takes the butterfly (x_j, x_{j+len/2}) -> (x_j + w x_{j+len/2},
+# x_j - w x_{j+len/2}) with w = zeta^{(5^j mod 4 len) N / (2 len)} (zeta = exp(i pi / N)), j < len / 2.  Each stage
+# is a matrix with three diagonals (offsets 0, +len/2, -len/2 mod n); the dense V never has to be formed.
+
+
+def sfft_stage(N: int, length: int, inverse: bool = False) -> dict:
+    """the butterfly stage of half-length h = length / 2 as diagonals {d: diag_d} (diag_d[j] = S[j][(j + d) mod n]);
+    inverse: the stage's inverse, (a, b) -> ((a + b) / 2, (a - b) / (2 w))"""
+    n, h = N // 2, length // 2
+    d0 = np.zeros(n, complex)
+    dp = np.zeros(n, complex)
+    dm = np.zeros(n, complex)
+    for p in range(n):
+        j = p % length
+        jj = j if j < h else j - h
+        e = (pow(5, jj, 4 * length) * (N // (2 * length))) % (2 * N)
+        w = np.exp(1j * np.pi * e / N)
+        if j < h:  # output p = x_p + w x_{p+h}   (inverse: (x_p + x_{p+h}) / 2)
+            d0[p], dp[p] = (0.5, 0.5) if inverse else (1.0, w)
+        else:      # output p = x_{p-h} - w x_p   (inverse: (x_{p-h} - x_p) / (2 w))
+            dm[p], d0[p] = (0.5 / w, -0.5 / w) if inverse else (1.0, -w)
+    out = {0: d0}
+    for d, v in ((h % n, dp), ((n - h) % n, dm)):
+        out[d] = out[d] + v if d in out else v
+    return out
+
+
+def diag_mul(A: dict, B: dict, n: int) -> dict:
+    """the diagonals of the matrix product A B: (A B)[j][j + d] = sum_{a + b = d} A_a[j] B_b[j + a]"""
+    out = {}
+    j = np.arange(n)
+    for a, va in A.items():
+        for b, vb in B.items():
+            d = (a + b) % n
+            t = va * vb[(j + a) % n]
+            out[d] = out[d] + t if d in out else t
+    return out
+
+
+def bit_reverse_perm(n: int) -> np.ndarray:
+    bits = n.bit_length() - 1
+    return np.array([int(format(k, f"0{bits}b")[::-1], 2) if bits else 0 for k in range(n)])
+
+
+def sfft_levels(N: int, groups, inverse: bool = False, scale: complex = 1.0) -> list:
+    """V = S_n ... S_4 S_2 P (P the bit reversal), grouped into len(groups) levels of consecutive stages
+    (groups = stages per level, low half-lengths first, sum = log2 n).  Forward (SlotToCoeff): the levels in the
+    order they are applied to a bit-reversed slot vector, [S_{2^g0} ... S_2, ...] -> scale V P.  Inverse
+    (CoeffToSlot): the order they are applied to the slots, [S_n^{-1} ..., ..., ... S_2^{-1}] -> scale P V^{-1}
+    (output in bit-reversed slot order).  scale multiplies the first level applied."""
+    n = N // 2
+    assert sum(groups) == n.bit_length() - 1
+    lens, at = [], 1
+    for g in groups:
+        lens.append([2 ** (at + k) for k in range(g)])
+        at += g
+    levels = []
+    for ls in lens:
+        M = None
+        for length in ls:  # later stages on the left
+            S = sfft_stage(N, length, inverse)
+            M = S if M is None else (diag_mul(S, M, n) if not inverse else diag_mul(M, S, n))
+        levels.append(M)
+    if inverse:
+        levels = levels[::-1]
+    levels[0] = {d: v * scale for d, v in levels[0].items()}
+    return levels
 
 
 # --------------------------------------------------------------------------- EvalMod and the whole bootstrap
@@ -172,15 +248,20 @@ def bootstrap(o, ct: Ct, level: int, cts_diags: dict, stc_diags: dict, bs: int, 
               evks: dict, conj_key, rlk) -> Ct:
     """ModRaise -> CoeffToSlot -> (Re, Im) split by conjugation -> EvalMod -> recombine -> SlotToCoeff
     (DESIGN R-EVALMOD).  cts_diags: the diagonals of V^{-1} / 2, stc_diags those of (K / 2 pi) V, with
-    K = q_0 / scale; cheb: the coefficients of cos(a s) on [-1, 1].  The CoeffToSlot output is scaled by
+    K = q_0 / scale -- or their factorised forms (lists of levels, bs a tuple of two lists (CoeffToSlot, SlotToCoeff):
+    sfft_levels, DESIGN R-SFFT; the slots
+    between them in bit-reversed order, which the slot-wise EvalMod does not see); cheb: the coefficients of cos(a s) on [-1, 1].  The CoeffToSlot output is scaled by
     alpha1 = 2 pi / (K 2^r a) with a constant PMult (a constant encodes into one coefficient, exactly to 2^-27,
     where alpha1 folded into the diagonals would keep only ~15 bits of them)."""
     K = float(o.q[0]) / ct.scale
     alpha1 = 2.0 * np.pi / (K * (2 ** r) * a)
     beta1 = -np.pi / (2.0 * (2 ** r) * a)
+    bs_c, bs_s = bs if isinstance(bs, tuple) else (bs, bs)
     up = mod_raise(o, ct, level)
-    y = lintrans(o, up, cts_diags, bs, evks)
-    y = o.rescale(o.pmult(y, _const(o, alpha1, o.q[y.level], y.level)))
+    y = lintrans_levels(o, up, cts_diags, bs_c, evks)
+    # alpha1's constant is encoded at scale q_l q_{l-1} / scale(y): s_re / s_im leave at the EvalMod scale q_{l-1}
+    # (DESIGN R-EVALMOD), which the squarings then keep near the primes they rescale by
+    y = o.rescale(o.pmult(y, _const(o, alpha1, float(o.q[y.level]) * float(o.q[y.level - 1]) / y.scale, y.level)))
     yc = o.hrot_galois(y, conj_key, 2 * o.N - 1)
     s_re = _add_const(o, o.add(y, yc), beta1)
     s_im = _add_const(o, o.pmult(_sub(o, y, yc), _monomial(o, -1, y.level)), beta1)
@@ -188,4 +269,14 @@ def bootstrap(o, ct: Ct, level: int, cts_diags: dict, stc_diags: dict, bs: int, 
     e_im = eval_mod(o, s_im, cheb, r, rlk)
     z = o.add(e_re, o.pmult(e_im, _monomial(o, 1, e_im.level)))
     del K
-    return lintrans(o, z, stc_diags, bs, evks)
+    return lintrans_levels(o, z, stc_diags, bs_s, evks)
+
+
+def lintrans_levels(o, ct: Ct, levels, bs, evks: dict) -> Ct:
+    """one dense transform ({d: diag}, bs an int) or a factorised one (a list of {d: diag} levels applied in order,
+    bs a list), one lintrans (one level) each (DESIGN R-SFFT)"""
+    if isinstance(levels, dict):
+        return lintrans(o, ct, levels, bs, evks)
+    for D, b in zip(levels, bs):
+        ct = lintrans(o, ct, D, b, evks)
+    return ct

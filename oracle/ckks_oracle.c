@@ -550,8 +550,9 @@ void orc_ks_inner_product(const orc_ctx* c, int level, const uint64_t* ext, cons
 }
 
 /* ModDown of one polynomial u [E][N] (NTT domain, Q_l u P) -> out [level+1][N] (NTT domain):
- * z_k = [v_k * (P/p_k)^{-1}]_{p_k} with v = iNTT(u on P),
- * out_i = (u_i - NTT_i( sum_k z_k * [(P/p_k) mod q_i] mod q_i )) * [P^{-1}]_{q_i}. */
+ * z_k = [v_k * (P/p_k)^{-1}]_{p_k} with v = iNTT(u on P), taken as the centred remainder in (-p_k/2, p_k/2]
+ * (DESIGN R-MODDOWN: then sum_k z_k (P/p_k) = [u]_P + e P with e symmetric about 0, |e| <= K/2, and the division by
+ * P rounds without bias), out_i = (u_i - NTT_i( sum_k z_k * [(P/p_k) mod q_i] mod q_i )) * [P^{-1}]_{q_i}. */
 void orc_moddown(const orc_ctx* c, int level, const uint64_t* u, uint64_t* out) {
   const int N = c->N, K = c->np, nq_l = level + 1;
   uint64_t* v = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)K * N);
@@ -580,7 +581,12 @@ void orc_moddown(const orc_ctx* c, int level, const uint64_t* u, uint64_t* out) 
     uint64_t* w = (uint64_t*)malloc(sizeof(uint64_t) * N);
     for (int x = 0; x < N; ++x) {
       uint64_t acc = 0;
-      for (int k = 0; k < K; ++k) acc = addmod(acc, mulmod(v[(size_t)k * N + x] % q, hat_mod_q[k], q), q);
+      for (int k = 0; k < K; ++k) {
+        const uint64_t pk = c->mod[c->nq + k], z = v[(size_t)k * N + x];
+        /* centred z: z - p_k when z > (p_k - 1)/2, reduced mod q */
+        const uint64_t zq = z > (pk - 1) / 2 ? (q - (pk - z) % q) % q : z % q;
+        acc = addmod(acc, mulmod(zq, hat_mod_q[k], q), q);
+      }
       w[x] = acc;
     }
     orc_ntt(c, i, w);

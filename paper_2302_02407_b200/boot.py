@@ -5,8 +5,8 @@ r double angles: the scaled sine of the modular reduction) -> recombination -> S
 Every homomorphic step is a C-ABI call into libhyphen.so (hy_mod_raise, hy_lintrans_apply, hy_hrot_galois,
 hy_mulct, hy_pmult, hy_rescale, hy_add, hy_sub, hy_add_pt, hy_level_down); this module only sequences them and tracks
 the scales (as ConvBlock sequences a residual block).  The CoeffToSlot / SlotToCoeff matrices and the Chebyshev
-coefficients are inputs, like conv weights.  The dense transforms need n = N/2 diagonals, so this runs at N <= 2^12;
-the N = 2^16 special FFT would need its level-budgeted radix factorisation (not built).
+coefficients are inputs, like conv weights.  Dense transforms need n = N/2 diagonals (small rings only);
+at N = 2^16 the transforms are factorised into 3 levels of radix-2 butterfly stages (sfft_levels, DESIGN R-SFFT).
 """
 from __future__ import annotations
 
@@ -28,20 +28,24 @@ class CT:
 
 
 class Bootstrapper:
-    def __init__(self, ctx, cts_diags, stc_diags, bs: int, cheb, r: int, a: float, evks: dict, conj_key, rlk):
-        """cts_diags / stc_diags: the n diagonals of V^{-1}/2 and of (K/2pi) V (ascending d); cheb: Chebyshev
-        coefficients of cos(a s) on [-1, 1] (odd ones zero); evks: rotation amount -> key (the transforms' baby and
-        giant steps); conj_key: the Galois key of k = 2N - 1; rlk: the relinearization key."""
-        from . import LinTrans
-        self.ctx, self.bs, self.cheb, self.r, self.a = ctx, bs, list(cheb), r, a
+    def __init__(self, ctx, cts_diags, stc_diags, bs, cheb, r: int, a: float, evks, conj_key, rlk):
+        """cts_diags / stc_diags: the n diagonals of V^{-1}/2 and of (K/2pi) V (ascending d, bs an int), or their
+        factorised forms (lists of {d: diag} levels, bs a list per transform pair: sfft_levels, DESIGN R-SFFT); cheb:
+        Chebyshev coefficients of cos(a s) on [-1, 1] (odd ones zero); evks: rotation amount -> key (the transforms'
+        baby and giant steps, `transform_rots`); conj_key: the Galois key of k = 2N - 1; rlk: the relinearization
+        key."""
+        self.ctx, self.cheb, self.r, self.a = ctx, list(cheb), r, a
         self.evks, self.conj_key, self.rlk = evks, conj_key, rlk
         self.q = ctx.moduli
-        n = ctx.n
-        self.cts = LinTrans(ctx, list(range(n)), bs)
-        self.stc = LinTrans(ctx, list(range(n)), bs)
-        self._cts_diags, self._stc_diags = cts_diags, stc_diags
+        self.cts = _levels(ctx, cts_diags, bs[0] if isinstance(bs, (list, tuple)) else bs)
+        self.stc = _levels(ctx, stc_diags, bs[1] if isinstance(bs, (list, tuple)) else bs)
         self._pts = {}
         self._consts = {}
+
+    @property
+    def rots(self):
+        """every rotation amount the two transforms need a key for"""
+        return sorted({r for lt, _ in self.cts + self.stc for r in lt.rots})
 
     # ---- helpers (each one C-ABI call, scales tracked as the oracle's Ct does)
     def _const(self, c, scale, level):
@@ -88,12 +92,14 @@ class Bootstrapper:
         pt, s = self._const(1.0, float(self.q[x.level]) * target / x.scale, x.level)
         return self._rescale(self._pmult(x, pt, s))
 
-    def _lintrans(self, lt, diags, x: CT):
-        key = (id(lt), x.level)
-        if key not in self._pts:
-            self._pts[key] = lt.encode(diags, x.level)
-        q = self.q[x.level]
-        return CT(lt.apply(self.evks, x.t, x.level, self._pts[key]), x.level - 1, (x.scale * q) / q)
+    def _lintrans(self, levels, x: CT):
+        for lt, diags in levels:
+            key = (id(lt), x.level)
+            if key not in self._pts:
+                self._pts[key] = lt.encode(diags, x.level)
+            q = self.q[x.level]
+            x = CT(lt.apply(self.evks, x.t, x.level, self._pts[key]), x.level - 1, (x.scale * q) / q)
+        return x
 
     # ---- the steps
     def eval_chebyshev(self, s: CT, target: float) -> CT:
@@ -134,8 +140,10 @@ class Bootstrapper:
         alpha1 = 2.0 * math.pi / (K * (2 ** self.r) * self.a)
         beta1 = -math.pi / (2.0 * (2 ** self.r) * self.a)
         up = CT(ctx.mod_raise(ct0, level), level, scale)
-        y = self._lintrans(self.cts, self._cts_diags, up)
-        pt, s = self._const(alpha1, float(self.q[y.level]), y.level)
+        y = self._lintrans(self.cts, up)
+        # alpha1 brings the slots to the EvalMod scale: the next prime q_{l-1} (R-EVALMOD), so that the squarings
+        # of the Chebyshev series and the double angles keep the scale near the primes they rescale by
+        pt, s = self._const(alpha1, float(self.q[y.level]) * float(self.q[y.level - 1]) / y.scale, y.level)
         y = self._rescale(self._pmult(y, pt, s))
         yc = CT(ctx.hrot_galois(self.conj_key, y.t, y.level, 2 * ctx.N - 1), y.level, y.scale)
         s_re = self._add_const(self._add(y, yc), beta1)
@@ -145,4 +153,89 @@ class Bootstrapper:
         e_im = self.eval_mod(s_im)
         ie = CT(ctx.pmult(e_im.t, self._monomial(1, e_im.level), e_im.level), e_im.level, e_im.scale)
         z = self._add(e_re, ie)
-        return self._lintrans(self.stc, self._stc_diags, z)
+        return self._lintrans(self.stc, z)
+
+
+def _levels(ctx, diags, bs):
+    """[(LinTrans, diagonal values in ascending d)] of one dense transform (a list of n diagonals) or of a factorised
+    one (a list of {d: diag} dicts, bs a list)"""
+    from . import LinTrans
+    if isinstance(diags, (list, tuple)) and diags and isinstance(diags[0], dict):
+        out = []
+        for D, b in zip(diags, bs):
+            ds = sorted(D)
+            out.append((LinTrans(ctx, ds, b), [D[d] for d in ds]))
+        return out
+    return [(LinTrans(ctx, list(range(ctx.n)), bs), diags)]
+
+
+def transform_rots(ctx, diags, bs) -> list:
+    """rotation amounts the transform (dense or factorised, as Bootstrapper takes it) needs keys for"""
+    return sorted({r for lt, _ in _levels(ctx, diags, bs) for r in lt.rots})
+
+
+# ---- the special FFT factorised into levels (DESIGN R-SFFT; host-side data of the transforms, like conv weights)
+def sfft_levels(N: int, groups, inverse: bool = False, scale: complex = 1.0) -> list:
+    """The CKKS special FFT V (slots = V (m_k + i m_{k+n})_k) as radix-2 butterfly stages of half-length h
+    = 1, 2, ..., n/2 -- (x_j, x_{j+h}) -> (x_j + w x_{j+h}, x_j - w x_{j+h}), w = zeta^{(5^j mod 4 len) N / (2 len)},
+    len = 2h -- on a bit-reversed input, grouped into len(groups) levels of consecutive stages; each level a dict
+    {offset d: diag_d} with diag_d[j] = M[j][(j + d) mod n].  Forward: the levels of S_n ... S_2 in application order
+    (SlotToCoeff on bit-reversed slots); inverse: those of P V^{-1} (CoeffToSlot, output bit-reversed).  `scale`
+    multiplies the first level applied."""
+    n = N // 2
+    assert sum(groups) == n.bit_length() - 1
+    rot = np.empty(n, np.int64)
+    r = 1
+    for j in range(n):
+        rot[j] = r
+        r = (r * 5) % (2 * N)
+    p = np.arange(n)
+
+    def stage(length):
+        h = length // 2
+        j = p % length
+        first = j < h
+        jj = np.where(first, j, j - h)
+        e = ((rot[jj] % (4 * length)) * (N // (2 * length))) % (2 * N)
+        w = np.exp(1j * np.pi * e / N)
+        if inverse:
+            d0 = np.where(first, 0.5, -0.5 / w)
+            dp = np.where(first, 0.5, 0.0)
+            dm = np.where(first, 0.0, 0.5 / w)
+        else:
+            d0 = np.where(first, 1.0, -w)
+            dp = np.where(first, w, 0.0)
+            dm = np.where(first, 0.0, 1.0)
+        out = {0: d0.astype(complex)}
+        for d, v in ((h % n, dp), ((n - h) % n, dm)):
+            out[d] = out[d] + v if d in out else v.astype(complex)
+        return out
+
+    def mul(A, B):  # diagonals of A B
+        out = {}
+        for a, va in A.items():
+            for b, vb in B.items():
+                d = (a + b) % n
+                t = va * np.roll(vb, -a)
+                out[d] = out[d] + t if d in out else t
+        return out
+
+    levels, at = [], 1
+    for g in groups:
+        M = None
+        for k in range(g):
+            S = stage(2 ** (at + k))
+            M = S if M is None else (mul(M, S) if inverse else mul(S, M))
+        levels.append(M)
+        at += g
+    if inverse:
+        levels = levels[::-1]
+    levels[0] = {d: v * scale for d, v in levels[0].items()}
+    return levels
+
+
+def level_bs(diags) -> int:
+    """baby-step size of a factorised level: 8 x the smallest nonzero offset step, so its offsets m 2^a (|m| < 32)
+    split into <= 8 baby and <= 8 giant rotations"""
+    n_min = min((d & -d) for d in diags if d) if any(diags) else 1
+    return 8 * n_min

@@ -242,7 +242,7 @@ extern "C" hy_status hy_ctx_create(const hy_params* prm, int cuda_device, hy_ctx
       md.p_inv_sh[i] = shoup_pre(md.p_inv[i], qi);
     }
     md.src0 = c->n_q;
-    md.center = 0;
+    md.center = 1;  // R-MODDOWN: the centred remainder (zero-mean rounding; a floor-style lift biases every coefficient)
     RescaleConst& rc = c->h_rescale[lvl];
     memset(&rc, 0, sizeof(rc));
     for (uint32_t i = 0; i < lvl; ++i) {

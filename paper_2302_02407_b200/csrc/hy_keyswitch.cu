@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(256) k_moddown_bconv(const __grid_constant__ A
     const PrimeConst& pc = dt.pc[n_q + k];
     z[k] = fcanon(fmulmod(u2d(v[((size_t)c * KP + k) * N + x]), (double)md->phat_inv[k], pc.qd, pc.qinv), pc.qd,
                   pc.qinv);
+    if (md->center && z[k] > 0.5 * (pc.qd - 1.0)) z[k] -= pc.qd;  // R-MODDOWN: centred remainder in (-p/2, p/2]
   }
   __syncthreads();
   uint64_t* out = w + (size_t)c * n * N + x;

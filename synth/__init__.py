@@ -16,7 +16,11 @@ import numpy as np
 PARAMS = {
     # P:1028 (h = 192), DESIGN R-PRIMES (bit sizes, all <= 48 bits), R-SCALE (log_scale)
     "toy": dict(log_n=12, q_bits=[48, 40, 40], p_bits=[48], dnum=3, h=64, log_scale=40),
-    "hyp": dict(log_n=16, q_bits=[48] + [42] * 23, p_bits=[48] * 4, dnum=6, h=192, log_scale=42),
+    # levels 10..23 are bootstrapping's (DESIGN R-PRIMES, R-SFFT): q_10..q_20 46 bits for EvalMod (its scale follows
+    # the primes; 2^46 with digits 2^8 below P keeps the key-switch noise 2^-31 of it), q_21..q_23 48 bits for
+    # CoeffToSlot's diagonals; every conv layer and block runs at levels <= 9 on the 42-bit primes (R-LEVELS)
+    "hyp": dict(log_n=16, q_bits=[48] + [42] * 9 + [46] * 11 + [48] * 3, p_bits=[48] * 4, dnum=6, h=192,
+                log_scale=42),
     # small full-featured set used by fast CPU tests (alpha = 2, partial last digit)
     "mini": dict(log_n=10, q_bits=[48, 40, 40, 40, 40], p_bits=[48, 48], dnum=3, h=32, log_scale=40),
     # the bootstrapping tests' chain: room for ModRaise, CoeffToSlot, EvalMod (Chebyshev depth 6

@@ -119,3 +119,90 @@ def test_oracle_bootstrap_recovers_slots():
     assert out.level >= 1
     got = o.decode(o.decrypt(SK, out))
     assert np.max(np.abs(got - z)) < 2**-10 * np.max(np.abs(z))
+
+
+def _dense(D, n):
+    M = np.zeros((n, n), complex)
+    j = np.arange(n)
+    for d, v in D.items():
+        M[j, (j + d) % n] += v
+    return M
+
+
+@pytest.mark.parametrize("N,groups", [(16, [1, 2]), (64, [2, 3]), (256, [3, 2, 2]), (1024, [3, 3, 3]), (1024, [4, 5])])
+def test_sfft_levels_factorise_the_embedding(N, groups):
+    """DESIGN R-SFFT pinned to the plain definition: the levels of the forward factorisation, applied in order to a
+    bit-reversed vector, multiply to V P (V = special_fft_matrix, itself pinned to the embedding above; P the bit
+    reversal); the inverse levels multiply to P V^{-1}; each level has the diagonal count of its stages' offsets"""
+    n = N // 2
+    V = B.special_fft_matrix(N)
+    P = np.eye(n)[B.bit_reverse_perm(n)]
+    fwd = B.sfft_levels(N, groups)
+    inv = B.sfft_levels(N, groups, inverse=True, scale=0.5)
+    Mf, Mi = np.eye(n), np.eye(n)
+    for D in fwd:
+        Mf = _dense(D, n) @ Mf
+    for D in inv:
+        Mi = _dense(D, n) @ Mi
+    assert np.abs(Mf - V @ P).max() < 1e-12
+    assert np.abs(Mi - 0.5 * P @ np.linalg.inv(V)).max() < 1e-12
+    at = 0
+    for g, D in zip(groups, fwd):
+        offs = {(m << at) % n for m in range(-(2 ** g - 1), 2 ** g)}
+        assert set(D) == offs
+        at += g
+
+
+def test_bit_reverse_perm():
+    assert list(B.bit_reverse_perm(8)) == [0, 4, 2, 6, 1, 5, 3, 7]
+    assert list(B.bit_reverse_perm(1)) == [0]
+
+
+def test_diag_mul_is_matmul():
+    """the product of two matrices given by their diagonals equals dense matmul (random diagonals, wrap-around)"""
+    n = 16
+    rng = np.random.default_rng(5)
+    A = {d: rng.normal(size=n) + 1j * rng.normal(size=n) for d in (0, 1, 5, 15)}
+    Bm = {d: rng.normal(size=n) + 1j * rng.normal(size=n) for d in (0, 3, 14)}
+    assert np.abs(_dense(B.diag_mul(A, Bm, n), n) - _dense(A, n) @ _dense(Bm, n)).max() < 1e-12
+
+
+def test_product_sfft_levels_match_oracle():
+    """the product's own (vectorised) factorisation gives the oracle's diagonals to the last bit, so bench.py (which
+    may not import oracle/) times the transforms the parity tests check"""
+    from paper_2302_02407_b200 import boot as PB
+    for N, groups in ((64, [2, 3]), (1024, [4, 5]), (4096, [4, 4, 3])):
+        for inv in (False, True):
+            a = B.sfft_levels(N, groups, inv, 0.5)
+            b = PB.sfft_levels(N, groups, inv, 0.5)
+            for x, y in zip(a, b):
+                assert sorted(x) == sorted(y)
+                for d in x:
+                    assert np.array_equal(x[d], y[d])
+
+
+def test_oracle_bootstrap_factorised_recovers_slots():
+    """the whole bootstrap with the factorised transforms (2 CoeffToSlot + 2 SlotToCoeff levels, DESIGN R-SFFT) on
+    the 'boot' chain decrypts to the input slots within 2^-10 of max|z|"""
+    import math
+    o = oracle.Oracle(**synth.PARAMS["boot"])
+    N, top = o.N, o.nq - 1
+    r, a = 3, 8.0
+    K = float(o.q[0]) / 2**40
+    cts = B.sfft_levels(N, [4, 5], inverse=True, scale=0.5)
+    stc = B.sfft_levels(N, [4, 5], scale=K / (2 * math.pi))
+    bsc = [8 * min((d & -d) for d in D if d) for D in cts]
+    bss = [8 * min((d & -d) for d in D if d) for D in stc]
+    cheb = np.polynomial.chebyshev.chebinterpolate(lambda s: np.cos(a * s), 30)
+    cheb[1::2] = 0.0
+    need = set()
+    for D, bs in list(zip(cts, bsc)) + list(zip(stc, bss)):
+        need |= {d % bs for d in D if d % bs} | {(d // bs) * bs for d in D if d // bs}
+    evks = {rr: o.keygen_rot(SK, EK, rr) for rr in sorted(need)}
+    z = synth.slots_uniform(41, o.n)
+    ct0 = o.level_down(o.encrypt(SK, 12, 0, o.encode(z, 2**40, top)), 0)
+    out = B.bootstrap(o, ct0, top, cts, stc, (bsc, bss), cheb, r, a, evks, o.keygen_galois(SK, EK, 2 * N - 1),
+                      o.keygen_relin(SK, EK))
+    assert out.level == top - 14
+    got = o.decode(o.decrypt(SK, out))
+    assert np.max(np.abs(got - z)) < 2**-10 * np.max(np.abs(z))

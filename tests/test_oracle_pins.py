@@ -261,7 +261,9 @@ def test_modup_identity(orc_mini):
 
 
 def test_moddown_identity(orc_mini):
-    """out*P == U - ut_P (mod Q_l), ut_P = [U]_P + v*P with 0 <= v < K (floor-style ModDown)."""
+    """out*P == U - ut_P (mod Q_l) with ut_P = sum_k z_k (P/p_k) exactly, z_k = [U (P/p_k)^{-1}]_{p_k} taken in
+    (-p_k/2, p_k/2] (DESIGN R-MODDOWN, centred), so |ut_P| < K P / 2 and ut_P == U (mod P); and the rounding error
+    ut_P / P has mean ~0 over the sampled coefficients (no floor-style bias)."""
     o = orc_mini
     level = 3
     chain = o.ext_chain(level)
@@ -273,12 +275,22 @@ def test_moddown_identity(orc_mini):
     uc = [o.intt(u[i], chain[i]) for i in range(len(chain))]
     oc = [o.intt(out[i], i) for i in range(level + 1)]
     mods = [int(o.moduli[t]) for t in chain]
+    errs = []
     for x in range(0, o.N, 41):
         U = _lift(uc, mods, x)
         Ot = _lift(oc, o.q[: level + 1], x)
-        r = (U - Ot * P) % (Q * P)  # == ut_P  (as an integer in [0, K*P))
-        assert r % P == U % P
-        assert 0 <= r // P < o.np_
+        r = (U - Ot * P) % (Q * P)
+        r = r - Q * P if r > (Q * P) // 2 else r  # == ut_P, centred
+        want = 0
+        for pk in o.p:
+            pk = int(pk)
+            z = (U % pk) * pow(P // pk, -1, pk) % pk
+            z = z - pk if z > (pk - 1) // 2 else z
+            want += z * (P // pk)
+        assert r == want
+        assert r % P == U % P and abs(r) < o.np_ * P // 2
+        errs.append(r / P)
+    assert abs(np.mean(errs)) < 0.5
 
 
 def test_rescale_is_exact_rounding(orc_mini):
