@@ -803,7 +803,31 @@ def bench_bootstrap_set_hyp(ctx, steps):
     torch.cuda.synchronize()
     got = ctx.decode(ctx.decrypt(sk, out.t, out.level), out.level, out.scale)
     err = float(np.max(np.abs(got - z)) / np.max(np.abs(z)))
-    return {"ms": e0.elapsed_time(e1) / n_it, "calls": n_it, "launches": (ctx.launch_count() - l0) // n_it,
+    ms, launches = e0.elapsed_time(e1) / n_it, (ctx.launch_count() - l0) // n_it
+    graph = {}
+    try:  # the same sequence captured once in a CUDA graph and replayed (no host sequencing in the timed region)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            bt.bootstrap(ct0, 2.0**42, top)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            gout = bt.bootstrap(ct0, 2.0**42, top)
+        g.replay()
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(gout.t, out.t))
+        e0.record()
+        for _ in range(n_it):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph = {"ms": e0.elapsed_time(e1) / n_it, "replay_equals_eager": ok}
+        del g, gout
+    except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+        graph = {"error": str(ex)[:200]}
+    return {"ms": ms, "calls": n_it, "launches": launches, "cuda_graph": graph,
             "levels": [top, out.level], "levels_consumed": top - out.level, "rotation_keys": len(rots),
             "transform_levels": {"coeff_to_slot": [len(D) for D in cts], "slot_to_coeff": [len(D) for D in stc]},
             "evalmod": {"cos_a": a, "double_angles": r, "chebyshev_degree": 30},

@@ -1,3 +1,5 @@
+"""Key-switch noise per parameter set (diagnostic, DESIGN R-MODDOWN): max slot error of a fresh encryption, a
+conjugation and a rotation at a few levels, relative to the scale."""
 import sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2302_02407_b200 as hy, synth
