@@ -213,6 +213,11 @@ hy_status hy_level_down(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint3
                         void* stream);
 /* Rescale (DESIGN R-RESCALE): [2][l+1][N] -> [2][l][N], exact round(c/q_l). */
 hy_status hy_rescale(hy_ctx* ctx, const uint64_t* d_ct, uint32_t level, uint64_t* d_out, void* stream);
+/* Rescale of n ciphertexts at the same level in batched launches (each output bit-identical to hy_rescale of its
+ * input; used by bootstrapping's lockstep EvalMod).  Errors: HY_E_ARG (null, an output aliasing any input),
+ * HY_E_LEVEL_EXHAUSTED (l = 0), HY_E_WORKSPACE. */
+hy_status hy_rescale_batch(hy_ctx* ctx, const uint64_t* const* d_cts, uint32_t n, uint32_t level,
+                           uint64_t* const* d_outs, void* stream);
 
 /* ---- HyPHEN convolution layers ------------------------------- */
 /* Slot layout (DESIGN R-LAYOUT): physical width wp (power of two), gap g, cell kappa in

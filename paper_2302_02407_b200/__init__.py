@@ -85,6 +85,7 @@ SIGNATURES = {
     "hy_unpack48": (C.c_int, [_P, _P, _P, C.c_size_t, _P]),
     "hy_mulct": (C.c_int, [_P, _P, _P, _P, _U32, _P, _P]),
     "hy_mulct_batch": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _PP, _P]),
+    "hy_rescale_batch": (C.c_int, [_P, _PP, _U32, _U32, _PP, _P]),
     "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
     "hy_decrypt": (C.c_int, [_P, _U64, _P, _U32, _P, _P]),
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
@@ -376,6 +377,11 @@ class Context:
         _check(lib().hy_rescale(self._c, _ptr(ct), level, _ptr(out), self._stream()))
         return out
 
+    def rescale_batch(self, cts, level, outs=None):
+        outs = [self.empty(*self.ct_shape(level - 1)) for _ in cts] if outs is None else outs
+        _check(lib().hy_rescale_batch(self._c, _ptr_array(cts), len(cts), level, _ptr_array(outs), self._stream()))
+        return outs
+
     # -- client side -----------------------------------------------------
     def keygen_rot(self, sk_seed, ek_seed, r, out=None):
         out = self.empty(*self.evk_shape()) if out is None else out
@@ -392,6 +398,13 @@ class Context:
         out = self.empty(*self.ct_shape(level)) if out is None else out
         _check(lib().hy_mulct(self._c, _ptr(rlk), _ptr(a), _ptr(b), level, _ptr(out), self._stream()))
         return out
+
+    def mulct_batch(self, rlk, As, Bs, level, outs=None):
+        """a_i * b_i for every pair, MulCt + relinearization in one batched key switch, no rescale (hy_mulct_batch)."""
+        outs = [self.empty(*self.ct_shape(level)) for _ in As] if outs is None else outs
+        _check(lib().hy_mulct_batch(self._c, _ptr(rlk), _ptr_array(As), _ptr_array(Bs), level, len(As),
+                                    _ptr_array(outs), self._stream()))
+        return outs
 
     def square_batch(self, rlk, cts, level, outs=None):
         """x^2 of every ciphertext (AESPA after fusion), MulCt + relinearization, no rescale."""

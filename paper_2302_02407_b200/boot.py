@@ -101,7 +101,52 @@ class Bootstrapper:
             x = CT(lt.apply(self.evks, x.t, x.level, self._pts[key]), x.level - 1, (x.scale * q) / q)
         return x
 
+    def _mul_many(self, As, Bs):
+        """pairwise MulCt + rescale of several ciphertext pairs in lockstep: one batched key switch (hy_mulct_batch;
+        each item bit-identical to its own hy_mulct)"""
+        lv = min(x.level for x in As + Bs)
+        As, Bs = [self._down(a, lv) for a in As], [self._down(b, lv) for b in Bs]
+        outs = self.ctx.mulct_batch(self.rlk, [a.t for a in As], [b.t for b in Bs], lv)
+        res = self.ctx.rescale_batch(outs, lv)
+        return [CT(r, lv - 1, a.scale * b.scale / self.q[lv]) for r, a, b in zip(res, As, Bs)]
+
     # ---- the steps
+    def eval_chebyshev_many(self, xs, targets):
+        """eval_chebyshev of several ciphertexts in lockstep (the real and imaginary parts): the same operation
+        sequence per item as eval_chebyshev, each MulCt of the schedule batched over the items"""
+        T = [{1: x} for x in xs]
+        for k, m, n in CHEB_SCHEDULE:
+            ps = self._mul_many([t[m] for t in T], [t[n] for t in T])
+            for t, p in zip(T, ps):
+                p = self._add(p, p)
+                d = abs(m - n)
+                if d == 0:
+                    t[k] = self._add_const(p, -1.0)
+                else:
+                    t[k] = self._sub(p, self._down(self._rescaled_to(t[d], p.scale), p.level))
+        outs = []
+        for t, target in zip(T, targets):
+            terms = []
+            for k in range(2, len(self.cheb), 2):
+                if self.cheb[k] == 0:
+                    continue
+                pt, sc = self._const(self.cheb[k], float(self.q[t[k].level]) * target / t[k].scale, t[k].level)
+                terms.append(self._rescale(self._pmult(t[k], pt, sc)))
+            lv = min(x.level for x in terms)
+            acc = None
+            for x in terms:
+                x = self._down(x, lv)
+                acc = x if acc is None else self._add(acc, x)
+            outs.append(self._add_const(acc, self.cheb[0]))
+        return outs
+
+    def eval_mod_many(self, xs):
+        cs = self.eval_chebyshev_many(xs, [x.scale for x in xs])
+        for _ in range(self.r):
+            sqs = self._mul_many(cs, cs)
+            cs = [self._add_const(self._add(sq, sq), -1.0) for sq in sqs]
+        return cs
+
     def eval_chebyshev(self, s: CT, target: float) -> CT:
         T = {1: s}
         for k, m, n in CHEB_SCHEDULE:
@@ -149,8 +194,7 @@ class Bootstrapper:
         s_re = self._add_const(self._add(y, yc), beta1)
         d = self._sub(y, yc)
         s_im = self._add_const(CT(ctx.pmult(d.t, self._monomial(-1, d.level), d.level), d.level, d.scale), beta1)
-        e_re = self.eval_mod(s_re)
-        e_im = self.eval_mod(s_im)
+        e_re, e_im = self.eval_mod_many([s_re, s_im])  # the two parts in lockstep (batched MulCts)
         ie = CT(ctx.pmult(e_im.t, self._monomial(1, e_im.level), e_im.level), e_im.level, e_im.scale)
         z = self._add(e_re, ie)
         return self._lintrans(self.stc, z)

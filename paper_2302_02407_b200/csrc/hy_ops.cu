@@ -776,6 +776,15 @@ extern "C" hy_status hy_rescale(hy_ctx* c, const uint64_t* ct, uint32_t level, u
   return rescale_multi(c, &ct, 1, level, &out, st(stream));
 }
 
+extern "C" hy_status hy_rescale_batch(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint32_t level,
+                                      uint64_t* const* outs, void* stream) {
+  if (!c || (n && (!cts || !outs))) return fail(HY_E_ARG, "null");
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < n; ++j)
+      if (outs[i] == cts[j]) return fail(HY_E_ARG, "rescale output aliases an input");
+  return rescale_multi(c, cts, n, level, outs, st(stream));
+}
+
 namespace hy {
 namespace {
 // s^2 in the NTT domain: the pointwise square of NTT(s) (NTT multiplication = negacyclic product)
