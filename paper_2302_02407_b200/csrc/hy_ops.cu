@@ -62,8 +62,9 @@ __global__ void __launch_bounds__(256) k_pmult_block(const __grid_constant__ PBl
     }
   }
   const uint64_t* ct_lo = nullptr;
-  // unrolled so that the loads of several operands are in flight together (the stream is HBM-bound)
-#pragma unroll 4
+  // unrolled by 2 so that the loads of two operands are in flight together (r02r A/B on the ResNet-18 PRCR layers:
+  // unroll 1 / 2 / 4 / 8 -> L1_ra MulFilter&Sum 3.03 / 2.91 / 3.14 / 3.61 ms, L1_ca 5.02 / 5.02 / 5.12 / 5.14 ms)
+#pragma unroll 2
   for (int j = 0; j < J; ++j) {
     ct_lo = b.ct[j] + (size_t)i * N + x;
     const double c0 = u2d(__ldcs(ct_lo)), c1 = u2d(__ldcs(ct_lo + n * N));
