@@ -49,7 +49,8 @@ def hyp():
 
 
 def boot():
-    """ModRaise, the BSGS transform (hoisted baby steps, MulFilter&Sum, lazy HRotSum), conjugation, MulCt"""
+    """ModRaise, the BSGS transform (hoisted baby steps, MulFilter&Sum, lazy HRotSum), conjugation, MulCt, and the
+    batched MulCt / rescale of the lockstep EvalMod"""
     prm = synth.PARAMS["boot"]
     ctx = hy.Context(**prm)
     top = len(prm["q_bits"]) - 1
@@ -60,7 +61,11 @@ def boot():
     g = np.random.default_rng(2)
     y = lt.apply(keys, up, top, lt.encode([g.uniform(-1, 1, ctx.n) + 0j for _ in range(6)], top))
     ctx.hrot_galois(ctx.keygen_galois(SK, EK, 2 * ctx.N - 1), y, top - 1, 2 * ctx.N - 1)
-    ctx.mulct(ctx.keygen_relin(SK, EK), y, y, top - 1)
+    rlk = ctx.keygen_relin(SK, EK)
+    ctx.mulct(rlk, y, y, top - 1)
+    # bootstrapping's lockstep EvalMod: batched MulCt and batched rescale
+    pr = ctx.mulct_batch(rlk, [y, up[:, : top].contiguous()], [y, y], top - 1)
+    ctx.rescale_batch(pr, top - 1)
     torch.cuda.synchronize()
     print("boot steps ok")
 
