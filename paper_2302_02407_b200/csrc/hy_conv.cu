@@ -297,11 +297,13 @@ hy_status ras_all(const Ctx& x, const std::vector<uint64_t*>& v, uint32_t level,
   return HY_OK;
 }
 
-// out_g = Rescale(ct_g (.) mask) for all g, in blocks of 8 through the temporaries tmp[0..7]
+// out_g = Rescale(ct_g (.) mask) for all g, in blocks of `blk` through the temporaries tmp[0..blk-1] (one
+// batched PMult and one batched rescale per block: the rescale's grids are too small to fill the GPU for a few
+// ciphertexts at a low level)
 hy_status mask_rescale(const Ctx& x, const std::vector<uint64_t*>& v, const uint64_t* mask, uint32_t level,
-                       uint64_t* tmp, size_t tmp_stride, const std::vector<uint64_t*>& outs) {
-  for (size_t g0 = 0; g0 < v.size(); g0 += 8) {
-    const size_t M = std::min<size_t>(8, v.size() - g0);
+                       uint64_t* tmp, size_t tmp_stride, const std::vector<uint64_t*>& outs, size_t blk = 8) {
+  for (size_t g0 = 0; g0 < v.size(); g0 += blk) {
+    const size_t M = std::min<size_t>(blk, v.size() - g0);
     std::vector<const uint64_t*> in(v.begin() + g0, v.begin() + g0 + M);
     std::vector<uint64_t*> t(M);
     for (size_t m = 0; m < M; ++m) t[m] = tmp + m * tmp_stride;
@@ -565,7 +567,9 @@ extern "C" size_t hy_conv_scratch_words(const hy_ctx* c, const hy_conv_plan* p, 
   // (8 = one block of MulFilter&Sum accumulators)
   // (+ n_groups ping-pong ciphertexts for the RaS / RaS_g / IR_g steps)
   // (+ 2 n_groups for the intermediate steps of synthesized rotations with a limited key set)
-  if (p->s.algo == HY_CONV_CA) return (p->n_in * f2 + 8 + (p->decomp.empty() ? 3 : 5) * p->n_groups) * ct;
+  // (the accumulators: one per group, at least 8, so that all groups are rescaled in one batched call)
+  if (p->s.algo == HY_CONV_CA)
+    return (p->n_in * f2 + std::max<size_t>(8, p->n_groups) + (p->decomp.empty() ? 3 : 5) * p->n_groups) * ct;
   return (std::max<size_t>(p->n_out * (f2 + 1), 6) + 8) * ct;     // tap accumulators + one sum per output
 }
 
@@ -727,8 +731,9 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
       }
     }
     const size_t G = grps.size();
-    uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;          // 8 block accumulators
-    uint64_t* gbuf = acc + 8 * ct_l;                              // G group ciphertexts (level - 1)
+    const size_t nacc = std::max<size_t>(8, G);
+    uint64_t* acc = sbuf + (size_t)p->n_in * f2 * ct_l;          // one MulFilter&Sum accumulator per group
+    uint64_t* gbuf = acc + nacc * ct_l;                           // G group ciphertexts (level - 1)
     const size_t ct_m = 2 * (size_t)level * N;
     std::vector<uint64_t*> gp(G);
     for (size_t g = 0; g < G; ++g)
@@ -745,16 +750,18 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
       bgal.assign(M * J, 1);
       std::vector<uint64_t*> accs(M);
       for (size_t m = 0; m < M; ++m) {
-        accs[m] = acc + m * ct_l;
+        accs[m] = acc + (g0 + m) * ct_l;
         for (size_t t = 0; t < f2; ++t)
           for (int64_t i = 0; i < p->n_in; ++i) set_term(m, J, t * p->n_in + i, grps[g0 + m], i, (int64_t)t);
       }
       stt = pmult_block(c, ops.data(), (uint32_t)J, accs.data(), (uint32_t)M, wpt, bidx.data(), bgal.data(), level,
                         0, stream);
-      if (stt == HY_OK) {
-        std::vector<const uint64_t*> ac(accs.begin(), accs.end());
-        stt = rescale_multi(c, ac.data(), (uint32_t)M, level, gp.data() + g0, x.s);
-      }
+      if (stt != HY_OK) return stt;
+    }
+    {  // every group's rescale in one batched call (r02t: R18 rescale family 3.15 -> ... ms per ds layer)
+      std::vector<const uint64_t*> ac(G);
+      for (size_t g = 0; g < G; ++g) ac[g] = acc + g * ct_l;
+      stt = rescale_multi(c, ac.data(), (uint32_t)G, level, gp.data(), x.s);
       if (stt != HY_OK) return stt;
     }
     uint64_t* pp = gbuf + 2 * G * ct_m;  // G ping-pong ciphertexts (hy_conv_scratch_words)
@@ -767,7 +774,7 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
     // IR_g: mask (one level) ...
     std::vector<uint64_t*> masked(G);
     for (size_t g = 0; g < G; ++g) masked[g] = ds ? gbuf + (G + g) * ct_m : out[g];
-    stt = mask_rescale(x, gp, mask, level - 1, acc, ct_l, masked);
+    stt = mask_rescale(x, gp, mask, level - 1, acc, ct_l, masked, nacc);
     if (stt != HY_OK) return stt;
     std::vector<uint64_t*> fin(out, out + (oe - ob));
     if (ds) {  // ... merge the two groups of each output into the doubled gap (DESIGN R-DSCONV) ...

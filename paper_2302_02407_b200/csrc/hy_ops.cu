@@ -671,13 +671,16 @@ hy_status rescale_multi(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint3
   if (level == 0) return fail(HY_E_LEVEL_EXHAUSTED, "rescale at level 0");
   if (!c->ws) return fail(HY_E_WORKSPACE, "workspace not set");
   const size_t N = c->N, nl = level + 1;
+  // items per launch set: kG, and what the workspace holds (v [2][N] + w [2][level][N] per item, plus alignment)
+  const size_t per_item = (2 * N + 2 * (size_t)level * N) * 8 + 512;
+  const uint32_t cap = (uint32_t)std::max<size_t>(1, std::min<size_t>(kG, c->ws_bytes / per_item));
   static const bool fused = getenv("HY_FUSE_RESCALE") == nullptr || atoi(getenv("HY_FUSE_RESCALE")) != 0;
   if (fused && moddown_cols_ok(c)) {
     // a ModDown by P = q_level with the centred remainder: inverse row pass of the two dropped limbs, one
     // column kernel (inverse column pass, centred lift, forward column pass of the level targets), one row
     // kernel ((c_i - t_i) q_level^{-1}); the lifted limbs never make an HBM round trip through separate passes
     for (uint32_t done = 0; done < n;) {
-      const int G = (int)std::min<uint32_t>(n - done, kG);
+      const int G = (int)std::min<uint32_t>(n - done, cap);
       Ws ws{c->ws, c->ws_bytes};
       LimbList L;
       ModUpColsArgs ma{};
@@ -706,7 +709,7 @@ hy_status rescale_multi(hy_ctx* c, const uint64_t* const* cts, uint32_t n, uint3
     return cuda_check("rescale");
   }
   for (uint32_t done = 0; done < n;) {
-    const int G = (int)std::min<uint32_t>(n - done, kG);
+    const int G = (int)std::min<uint32_t>(n - done, cap);
     Ws ws{c->ws, c->ws_bytes};
     ItemPtrs a{};
     LimbBatch b;
