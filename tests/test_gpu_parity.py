@@ -275,6 +275,28 @@ def test_rescale_fused_levels(level):
         assert np.array_equal(to_np(ctx.rescale(to_dev(a, ctx), level)), o.rescale(oracle.Ct(a, level, 1.0)).data)
 
 
+def test_rescale_batch_and_mulct_batch():
+    """hy_rescale_batch and hy_mulct_batch (bootstrapping's lockstep EvalMod): every item bit-exact vs the oracle's
+    rescale / MulCt of that item; an output aliasing another item's input is rejected (HY_E_ARG)"""
+    import paper_2302_02407_b200 as hy
+    ctx, o = _hyp_pair()
+    level = 9
+    cts = [rand_limbs(o, 700 + k, list(range(level + 1)) * 2).reshape(2, level + 1, o.N) for k in range(5)]
+    outs = ctx.rescale_batch([to_dev(a, ctx) for a in cts], level)
+    for a, got in zip(cts, outs):
+        assert np.array_equal(to_np(got), o.rescale(oracle.Ct(a, level, 1.0)).data)
+    d = [to_dev(a, ctx) for a in cts[:2]]
+    with pytest.raises(hy.HyError):
+        ctx.rescale_batch(d, level, outs=[d[1][:, :level].contiguous(), d[0]])
+    rlk, orlk = ctx.keygen_relin(SK, EK), o.keygen_relin(SK, EK)
+    z = [synth.slots_uniform(80 + k, o.n) for k in range(3)]
+    ocs = [o.encrypt(SK, 4, 40 + k, o.encode(z[k], 2**42, level)) for k in range(3)]
+    dcs = [to_dev(c.data, ctx) for c in ocs]
+    got = ctx.mulct_batch(rlk, [dcs[0], dcs[1], dcs[2]], [dcs[1], dcs[1], dcs[0]], level)
+    for g, (x, y) in zip(got, [(0, 1), (1, 1), (2, 0)]):
+        assert np.array_equal(to_np(g), o.mulct(ocs[x], ocs[y], orlk).data)
+
+
 _HYP = {}
 
 
