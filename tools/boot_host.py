@@ -1,5 +1,6 @@
+"""Host vs device time per Set_hyp bootstrap call, batched vs single MulCt in EvalMod (diagnostic); MB=<max_batch>."""
 import os, sys, time, math
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import numpy as np, torch
 import paper_2302_02407_b200 as hy, synth
 from paper_2302_02407_b200.boot import Bootstrapper, level_bs, sfft_levels, transform_rots

@@ -1,7 +1,7 @@
 """Key-switch noise per parameter set (diagnostic, DESIGN R-MODDOWN): max slot error of a fresh encryption, a
 conjugation and a rotation at a few levels, relative to the scale."""
 import sys, numpy as np, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_2302_02407_b200 as hy, synth
 SK, EK = synth.SEED_SK, synth.SEED_EVK
 for name in ("boot", "hyp", "toy"):
