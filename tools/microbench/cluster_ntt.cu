@@ -1,0 +1,231 @@
+// A/B for keeping a whole 2^16-word limb on chip across the NTT's column -> row boundary (VERDICT r01 item 3,
+// DESIGN section 11): the forward negacyclic-NTT structure of the product (256 x 256, column pass then row pass,
+// 8 FP64 stages each, the same layouts and twiddle heaps) run
+//   (a) as two kernels with the between-pass limb in HBM (the product's split: a column kernel on 8-column strips of
+//       256 threads with block-wide transposes, then a row kernel with one row per warp), and
+//   (b) as ONE kernel per limb on a thread-block cluster: CTA r holds columns [CW r, CW r + CW) of the limb in shared
+//       memory, each warp transforms whole columns with warp-local transposes, cluster barrier, then each CTA
+//       transforms its CW rows reading the other CTAs' columns through distributed shared memory (ld.shared::cluster);
+//       CW = 64 (4-CTA clusters, 165 KB, one CTA per SM) and CW = 32 (8-CTA clusters, 83 KB, two CTAs per SM).
+// Same twiddles and arithmetic -> identical words (checked); times both over 1536 limbs (64 items x 24 limbs).
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../paper_2302_02407_b200/csrc/hy_arith.cuh"
+using namespace hy;
+namespace cg = cooperative_groups;
+
+// CW columns per CTA (64: a 4-CTA cluster, 165 KB, one CTA per SM; 32: an 8-CTA cluster, 83 KB, two per SM)
+template <int CW>
+struct Cl {
+  static constexpr int RS = CW + 1;  // padded row stride (a warp reading a column meets 2-way bank pairs)
+  static constexpr int NC = 256 / CW;
+  static constexpr int smem = (256 * RS + 16 * 256) * 8;
+};
+
+template <int LAY>
+__device__ __forceinline__ int elem(int l, int k) {
+  if (LAY == 1) return l + 32 * k;
+  if (LAY == 2) return 32 * (l >> 2) + 4 * k + (l & 3);
+  return 4 * (l + 32 * (k >> 2)) + (k & 3);
+}
+template <int LAY>
+__device__ __forceinline__ int kbit(int s) { return LAY == 1 ? s - 5 : (LAY == 2 ? s - 2 : s); }
+template <int LAY>
+__device__ __forceinline__ void stages(double (&x)[8], int l, int s_hi, int s_lo, const double* T, double q,
+                                       double qinv) {
+#pragma unroll
+  for (int it = 0; it <= s_hi - s_lo; ++it) {
+    const int s = s_hi - it, kb = 1 << kbit<LAY>(s);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k & kb) continue;
+      const double w = T[(256 + elem<LAY>(l, k)) >> (s + 1)];
+      const double a = x[k], t = fmulmod(x[k | kb], w, q, qinv);
+      x[k] = a + t;
+      x[k | kb] = a - t;
+    }
+  }
+}
+__device__ __forceinline__ int pidx(int e) { return e ^ ((e >> 2) & 1) ^ (((e >> 4) & 7) << 1); }
+__device__ __forceinline__ int sidx8(int e, int c) { return 8 * (e ^ ((e >> 2) & 1)) + c; }
+// L1 in -> L3 out with a warp-local transpose buffer S
+__device__ __forceinline__ void fwd_l1_l3(double (&x)[8], int l, double* S, const double* T, double q, double qinv) {
+  stages<1>(x, l, 7, 5, T, q, qinv);
+  for (int k = 0; k < 8; ++k) S[pidx(elem<1>(l, k))] = x[k];
+  __syncwarp();
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<2>(l, k))];
+  stages<2>(x, l, 4, 2, T, q, qinv);
+  __syncwarp();
+  for (int k = 0; k < 8; ++k) S[pidx(elem<2>(l, k))] = x[k];
+  __syncwarp();
+  for (int k = 0; k < 8; ++k) x[k] = S[pidx(elem<3>(l, k))];
+  stages<3>(x, l, 1, 0, T, q, qinv);
+  __syncwarp();
+}
+__device__ __forceinline__ void heap_warp(double* T, const double* W, uint32_t hb, int l) {
+  double v[8];
+  for (int k = 0; k < 8; ++k) {
+    const int li = l + 32 * k, m = 31 - __clz(li | 1);
+    v[k] = li ? __ldg(W + ((hb - 1) << m) + (uint32_t)li) : 0.0;
+  }
+  for (int k = 0; k < 8; ++k) T[l + 32 * k] = v[k];
+}
+
+// (a1) column pass on an 8-column strip (the product's thread mapping), limb-major buffers of 65536 doubles
+__global__ void __launch_bounds__(256, 2) k_cols(const double* __restrict__ in, double* __restrict__ mid,
+                                                 const double* __restrict__ W, double q, double qinv) {
+  __shared__ double sm[8 * 256], T[256];
+  const int c = threadIdx.x & 7, l = threadIdx.x >> 3;
+  const size_t base = (size_t)blockIdx.y * 65536;
+  const int col = blockIdx.x * 8 + c;
+  if (threadIdx.x > 0) T[threadIdx.x] = W[threadIdx.x];
+  double x[8];
+  for (int k = 0; k < 8; ++k) x[k] = in[base + (size_t)elem<1>(l, k) * 256 + col];
+  __syncthreads();
+  stages<1>(x, l, 7, 5, T, q, qinv);
+  for (int k = 0; k < 8; ++k) sm[sidx8(elem<1>(l, k), c)] = x[k];
+  __syncthreads();
+  for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<2>(l, k), c)];
+  stages<2>(x, l, 4, 2, T, q, qinv);
+  __syncthreads();
+  for (int k = 0; k < 8; ++k) sm[sidx8(elem<2>(l, k), c)] = x[k];
+  __syncthreads();
+  for (int k = 0; k < 8; ++k) x[k] = sm[sidx8(elem<3>(l, k), c)];
+  stages<3>(x, l, 1, 0, T, q, qinv);
+  for (int k = 0; k < 8; ++k) mid[base + (size_t)elem<3>(l, k) * 256 + col] = fred(x[k], q, qinv);
+}
+// (a2) row pass, one row per warp
+__global__ void __launch_bounds__(256) k_rows(const double* __restrict__ mid, double* __restrict__ out,
+                                              const double* __restrict__ W, double q, double qinv) {
+  __shared__ double S[8][256], TT[8][256];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + w;
+  const size_t base = (size_t)blockIdx.y * 65536 + (size_t)row * 256;
+  heap_warp(TT[w], W, 256 + row, l);
+  double x[8];
+  for (int k = 0; k < 8; ++k) x[k] = mid[base + elem<1>(l, k)];
+  __syncwarp();
+  fwd_l1_l3(x, l, S[w], TT[w], q, qinv);
+  for (int k = 0; k < 8; ++k) out[base + elem<3>(l, k)] = fcanon(x[k], q, qinv);
+}
+
+// (b) one limb per cluster of 256 / CW CTAs
+template <int CW>
+__device__ __forceinline__ void cluster_body(const double* __restrict__ in, double* __restrict__ out,
+                                             const double* __restrict__ W, double q, double qinv) {
+  constexpr int RS = Cl<CW>::RS, NC = Cl<CW>::NC, PW = CW / 8;  // PW columns (and rows) per warp
+  extern __shared__ __align__(16) double dsm[];
+  double* strip = dsm;                                                // [256][RS], columns CW r .. CW r + CW - 1
+  double* S = dsm + 256 * RS + (threadIdx.x >> 5) * 256;             // per-warp transpose buffer
+  double* T = dsm + 256 * RS + 8 * 256 + (threadIdx.x >> 5) * 256;   // per-warp twiddle heap
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank(), w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const size_t base = (size_t)(blockIdx.x / NC) * 65536;
+  for (int i = threadIdx.x; i < 256 * CW; i += 256) {
+    const int row = i / CW, c = i % CW;
+    strip[row * RS + c] = in[base + (size_t)row * 256 + CW * r + c];
+  }
+  heap_warp(T, W, 1, l);
+  __syncthreads();
+  for (int cc = 0; cc < PW; ++cc) {
+    const int c = PW * w + cc;
+    double x[8];
+    for (int k = 0; k < 8; ++k) x[k] = strip[elem<1>(l, k) * RS + c];
+    fwd_l1_l3(x, l, S, T, q, qinv);
+    for (int k = 0; k < 8; ++k) strip[elem<3>(l, k) * RS + c] = fred(x[k], q, qinv);
+  }
+  cl.sync();
+  for (int rr = 0; rr < PW; ++rr) {
+    const int row = CW * r + PW * w + rr;
+    __syncwarp();
+    heap_warp(T, W, 256 + row, l);
+    double x[8];
+    for (int k = 0; k < 8; ++k) {
+      const int e = elem<1>(l, k);
+      const double* pe = cl.map_shared_rank(strip, e / CW);
+      x[k] = pe[row * RS + (e % CW)];
+    }
+    __syncwarp();
+    fwd_l1_l3(x, l, S, T, q, qinv);
+    for (int k = 0; k < 8; ++k) out[base + (size_t)row * 256 + elem<3>(l, k)] = fcanon(x[k], q, qinv);
+  }
+  cl.sync();
+}
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
+    k_cluster4(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ W, double q,
+               double qinv) {
+  cluster_body<64>(in, out, W, q, qinv);
+}
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 2)
+    k_cluster8(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ W, double q,
+               double qinv) {
+  cluster_body<32>(in, out, W, q, qinv);
+}
+
+int main() {
+  const int limbs = 1536;
+  const size_t n = (size_t)limbs * 65536;
+  const double q = 281474976710597.0, qinv = 1.0 / q;
+  double *in, *mid, *o1, *o2, *W;
+  cudaMalloc(&in, n * 8);
+  cudaMalloc(&mid, n * 8);
+  cudaMalloc(&o1, n * 8);
+  cudaMalloc(&o2, n * 8);
+  cudaMalloc(&W, 65536 * 8);
+  double* h = new double[65536];
+  for (int i = 0; i < 65536; ++i) h[i] = (double)(((uint64_t)i * 0x9E3779B97F4A7C15ull) % 281474976710597ull);
+  cudaMemcpy(W, h, 65536 * 8, cudaMemcpyHostToDevice);
+  for (size_t o = 0; o < n; o += 65536) {
+    for (int i = 0; i < 65536; ++i) h[i] = (double)((((uint64_t)(o + i)) * 0xD1B54A32D192ED03ull) % 281474976710597ull);
+    cudaMemcpy(in + o, h, 65536 * 8, cudaMemcpyHostToDevice);
+  }
+  cudaFuncSetAttribute(k_cluster4, cudaFuncAttributeMaxDynamicSharedMemorySize, Cl<64>::smem);
+  cudaFuncSetAttribute(k_cluster8, cudaFuncAttributeMaxDynamicSharedMemorySize, Cl<32>::smem);
+  double* o3;
+  cudaMalloc(&o3, n * 8);
+  float ms3 = 0;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float ms1 = 0, ms2 = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    k_cols<<<dim3(32, limbs), 256>>>(in, mid, W, q, qinv);
+    k_rows<<<dim3(32, limbs), 256>>>(mid, o1, W, q, qinv);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms1, a, b);
+    cudaEventRecord(a);
+    k_cluster4<<<4 * limbs, 256, Cl<64>::smem>>>(in, o2, W, q, qinv);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms2, a, b);
+    cudaEventRecord(a);
+    k_cluster8<<<8 * limbs, 256, Cl<32>::smem>>>(in, o3, W, q, qinv);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms3, a, b);
+  }
+  const cudaError_t err = cudaGetLastError();
+  size_t bad = 0;
+  for (int lb = 0; lb < limbs; lb += 311) {
+    double* r1 = new double[65536];
+    double* r2 = new double[65536];
+    cudaMemcpy(r1, o1 + (size_t)lb * 65536, 65536 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r2, o2 + (size_t)lb * 65536, 65536 * 8, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 65536; ++i) bad += r1[i] != r2[i];
+    cudaMemcpy(r2, o3 + (size_t)lb * 65536, 65536 * 8, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 65536; ++i) bad += r1[i] != r2[i];
+    delete[] r1;
+    delete[] r2;
+  }
+  printf("{\"kernel\":\"two_pass_hbm_round_trip\",\"ms\":%.3f,\"limbs\":%d}\n", ms1, limbs);
+  printf("{\"kernel\":\"cluster4_dsmem_one_pass\",\"ms\":%.3f,\"limbs\":%d,\"smem_bytes\":%d}\n", ms2, limbs, Cl<64>::smem);
+  printf("{\"kernel\":\"cluster8_dsmem_one_pass\",\"ms\":%.3f,\"limbs\":%d,\"smem_bytes\":%d}\n", ms3, limbs, Cl<32>::smem);
+  printf("{\"check\":\"identical words on sampled limbs\",\"mismatches\":%zu,\"cuda\":\"%s\"}\n", bad,
+         cudaGetErrorString(err));
+  return 0;
+}

@@ -3,7 +3,7 @@
 #   bash tools/microbench/run.sh > gpurun_out/microbench.txt
 set -e
 D=$(dirname "$0")
-for f in int_roofline fp_modmul mix_pipes shfl_vs_smem; do
+for f in int_roofline fp_modmul mix_pipes shfl_vs_smem cluster_ntt; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/$f $D/$f.cu
   echo "== $f"
   /tmp/$f
