@@ -6,7 +6,8 @@
 //   (b) as ONE kernel per limb on a thread-block cluster: CTA r holds columns [CW r, CW r + CW) of the limb in shared
 //       memory, each warp transforms whole columns with warp-local transposes, cluster barrier, then each CTA
 //       transforms its CW rows reading the other CTAs' columns through distributed shared memory (ld.shared::cluster);
-//       CW = 64 (4-CTA clusters, 165 KB, one CTA per SM) and CW = 32 (8-CTA clusters, 83 KB, two CTAs per SM).
+//       CW = 64 (4-CTA clusters, 165 KB, one CTA per SM), 32 (8-CTA clusters, 100 KB, two per SM) and 16 (16-CTA
+//       non-portable clusters, 67 KB, three per SM).
 // Same twiddles and arithmetic -> identical words (checked); times both over 1536 limbs (64 items x 24 limbs).
 #include <cooperative_groups.h>
 #include <cstdint>
@@ -164,6 +165,11 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, 2)
                double qinv) {
   cluster_body<32>(in, out, W, q, qinv);
 }
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
+    k_cluster16(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ W, double q,
+                double qinv) {
+  cluster_body<16>(in, out, W, q, qinv);
+}
 
 int main() {
   const int limbs = 1536;
@@ -184,9 +190,13 @@ int main() {
   }
   cudaFuncSetAttribute(k_cluster4, cudaFuncAttributeMaxDynamicSharedMemorySize, Cl<64>::smem);
   cudaFuncSetAttribute(k_cluster8, cudaFuncAttributeMaxDynamicSharedMemorySize, Cl<32>::smem);
+  cudaFuncSetAttribute(k_cluster16, cudaFuncAttributeMaxDynamicSharedMemorySize, Cl<16>::smem);
+  cudaFuncSetAttribute(k_cluster16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   double* o3;
   cudaMalloc(&o3, n * 8);
-  float ms3 = 0;
+  double* o4;
+  cudaMalloc(&o4, n * 8);
+  float ms3 = 0, ms4 = 0;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -208,6 +218,11 @@ int main() {
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms3, a, b);
+    cudaEventRecord(a);
+    k_cluster16<<<16 * limbs, 256, Cl<16>::smem>>>(in, o4, W, q, qinv);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms4, a, b);
   }
   const cudaError_t err = cudaGetLastError();
   size_t bad = 0;
@@ -219,12 +234,15 @@ int main() {
     for (int i = 0; i < 65536; ++i) bad += r1[i] != r2[i];
     cudaMemcpy(r2, o3 + (size_t)lb * 65536, 65536 * 8, cudaMemcpyDeviceToHost);
     for (int i = 0; i < 65536; ++i) bad += r1[i] != r2[i];
+    cudaMemcpy(r2, o4 + (size_t)lb * 65536, 65536 * 8, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 65536; ++i) bad += r1[i] != r2[i];
     delete[] r1;
     delete[] r2;
   }
   printf("{\"kernel\":\"two_pass_hbm_round_trip\",\"ms\":%.3f,\"limbs\":%d}\n", ms1, limbs);
   printf("{\"kernel\":\"cluster4_dsmem_one_pass\",\"ms\":%.3f,\"limbs\":%d,\"smem_bytes\":%d}\n", ms2, limbs, Cl<64>::smem);
   printf("{\"kernel\":\"cluster8_dsmem_one_pass\",\"ms\":%.3f,\"limbs\":%d,\"smem_bytes\":%d}\n", ms3, limbs, Cl<32>::smem);
+  printf("{\"kernel\":\"cluster16_dsmem_one_pass\",\"ms\":%.3f,\"limbs\":%d,\"smem_bytes\":%d}\n", ms4, limbs, Cl<16>::smem);
   printf("{\"check\":\"identical words on sampled limbs\",\"mismatches\":%zu,\"cuda\":\"%s\"}\n", bad,
          cudaGetErrorString(err));
   return 0;
