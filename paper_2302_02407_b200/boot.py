@@ -283,3 +283,29 @@ def level_bs(diags) -> int:
     split into <= 8 baby and <= 8 giant rotations"""
     n_min = min((d & -d) for d in diags if d) if any(diags) else 1
     return 8 * n_min
+
+
+class BlockChain:
+    """ResNet-style conv blocks chained through bootstrapping at Set_hyp (bootstrapping "to chain
+    blocks end to end"): y = RAConv(CAConv(x)^2) + x -- the ConvBlock (Alg. 3, the AESPA square between the
+    two convs) plus the identity shortcut, whose ciphertext is first brought to the block's output scale
+    and level -- and then `refresh`: the scale set to the bootstrapper's input scale (one level), ModRaise ...
+    SlotToCoeff back to L' (R-SFFT, R-EVALMOD).  Only sequencing and scale bookkeeping here; every step is a C-ABI
+    call."""
+
+    def __init__(self, ctx, bt: Bootstrapper, boot_scale: float = 2.0**42):
+        self.ctx, self.bt, self.boot_scale = ctx, bt, boot_scale
+        self.top = ctx.n_q - 1
+
+    def block(self, blk, ca_keys, ra_keys, ca_pts, ra_pts, x: CT) -> CT:
+        bt = self.bt
+        mid, _, out_level = blk.levels(x.level)
+        y = blk.run(ca_keys, ra_keys, bt.rlk, [x.t], x.level, ca_pts, ra_pts)[0]
+        ys = x.scale * x.scale / bt.q[mid]  # CAConv and RAConv keep the scale; the square makes it s^2 / q_mid
+        sc = bt._down(bt._rescaled_to(x, ys), out_level)
+        return bt._add(CT(y, out_level, ys), sc)
+
+    def refresh(self, x: CT) -> CT:
+        bt = self.bt
+        x = bt._down(bt._rescaled_to(x, self.boot_scale), 0)
+        return bt.bootstrap(x.t, x.scale, self.top)

@@ -215,3 +215,48 @@ def test_bootstrap_set_hyp():
     assert np.array_equal(to_np(got.t), want.data)
     dz = o.decode(o.decrypt(SK, want))
     assert np.max(np.abs(dz - z)) < 2**-9 * np.max(np.abs(z))
+
+
+def test_block_chain_set_hyp():
+    """Bootstrapping chaining conv blocks end to end at Set_hyp: ResNet-20 stage-1 shapes (16
+    channels, 32 x 32, CA(1,2) -> RA(2,1) -> CA(1,2)), y = RAConv(CAConv(x)^2) + x at L' = 6 -> level 3, bootstrap back
+    to L' (BlockChain.refresh), a second block; the result decrypts to the plaintext recursion
+    Y1 = conv(conv(X, K1)^2, K2) + X, Y2 = conv(conv(Y1, K3)^2, K4) + Y1 within 2^-8 of max|Y2|."""
+    import paper_2302_02407_b200 as hy
+    from oracle import hyphen as H
+    from paper_2302_02407_b200.boot import CT, BlockChain, Bootstrapper, transform_rots
+    ctx, o = pair("hyp")
+    N, n, top = o.N, o.n, o.nq - 1
+    cts, stc, bs = _factorised(N, [5, 5, 5], float(o.q[0]) / 2**42)
+    rots = sorted(set(transform_rots(ctx, cts, bs[0])) | set(transform_rots(ctx, stc, bs[1])))
+    rlk = ctx.keygen_relin(SK, EK)
+    bt = Bootstrapper(ctx, cts, stc, bs, _cheb(12.0), 4, 12.0, {r: ctx.keygen_rot(SK, EK, r) for r in rots},
+                      ctx.keygen_galois(SK, EK, 2 * N - 1), rlk)
+    ca_s = H.ConvSpec(16, 16, 32, 3, 1, 32, 1, 1, 2, "CA", n=n)
+    ra_s = H.ConvSpec(16, 16, 32, 3, 1, 32, 1, 2, 1, "RA", n=n)
+    X = synth.image(90, 16, 32)
+    Ks = [synth.conv_weight(91 + i, 16, 16, 3) * 0.3 for i in range(4)]
+    fin = H.plan_caconv(ca_s, Ks[0]).fin
+    fout = H.plan_raconv(ra_s, Ks[1]).fout
+    assert fin == fout  # the block's output format is its input's: the shortcut adds slot by slot
+    g_ca = hy.ConvPlan(ctx, 16, 16, 32, 3, 1, 32, 1, 1, 2, "CA")
+    g_ra = hy.ConvPlan(ctx, 16, 16, 32, 3, 1, 32, 1, 2, 1, "RA")
+    blk = hy.ConvBlock(ctx, g_ca, g_ra)
+    L = 6
+    _, ra_level, out_level = blk.levels(L)
+    ca_keys = {r: ctx.keygen_rot(SK, EK, r) for r in g_ca.rots}
+    ra_keys = {r: ctx.keygen_rot(SK, EK, r) for r in g_ra.rots}
+    xs = H.pack(X, fin)
+    assert len(xs) == 1
+    chain = BlockChain(ctx, bt)
+    x = CT(ctx.encrypt(SK, 31, 0, ctx.encode(xs[0], 2**42, L), L), L, 2.0**42)
+    x = chain.block(blk, ca_keys, ra_keys, g_ca.encode_weights(Ks[0], L), g_ra.encode_weights(Ks[1], ra_level), x)
+    assert x.level == out_level
+    x = chain.refresh(x)
+    assert x.level == L
+    x = chain.block(blk, ca_keys, ra_keys, g_ca.encode_weights(Ks[2], L), g_ra.encode_weights(Ks[3], ra_level), x)
+    dec = np.real(ctx.decode(ctx.decrypt(SK, x.t, x.level), x.level, x.scale))
+    res = H.unpack([dec], fout, 16, 32, 32)
+    Y1 = H.conv2d(H.conv2d(X, Ks[0]) ** 2, Ks[1]) + X
+    Y2 = H.conv2d(H.conv2d(Y1, Ks[2]) ** 2, Ks[3]) + Y1
+    assert np.max(np.abs(res - Y2)) < 2**-8 * np.max(np.abs(Y2))
