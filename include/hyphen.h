@@ -193,6 +193,10 @@ hy_status hy_pmult(hy_ctx* ctx, const uint64_t* d_ct, const uint64_t* d_pt, uint
                    void* stream);
 /* MulFilter&Sum: out (+)= sum_i ct_i (.) pt_i, one reduction per output word.
  * accumulate != 0 adds into d_out. */
+/* out_i = ct_i (.) pt for n ciphertexts and ONE plaintext in one launch (each bit-identical to hy_pmult; used by
+ * bootstrapping's lockstep EvalMod).  out_i may alias ct_i, not another item's input (HY_E_ARG). */
+hy_status hy_pmult_batch(hy_ctx* ctx, const uint64_t* const* d_cts, uint32_t n, const uint64_t* d_pt, uint32_t level,
+                         uint64_t* const* d_outs, void* stream);
 hy_status hy_pmult_acc(hy_ctx* ctx, const uint64_t* const* d_cts, const uint64_t* const* d_pts, uint32_t n,
                        uint32_t level, uint64_t* d_out, int accumulate, void* stream);
 /* out = a + b over npoly polynomials ([npoly][l+1][N]); in-place allowed. */

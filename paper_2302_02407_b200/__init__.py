@@ -86,6 +86,7 @@ SIGNATURES = {
     "hy_mulct": (C.c_int, [_P, _P, _P, _P, _U32, _P, _P]),
     "hy_mulct_batch": (C.c_int, [_P, _P, _PP, _PP, _U32, _U32, _PP, _P]),
     "hy_rescale_batch": (C.c_int, [_P, _PP, _U32, _U32, _PP, _P]),
+    "hy_pmult_batch": (C.c_int, [_P, _PP, _U32, _P, _U32, _PP, _P]),
     "hy_encrypt": (C.c_int, [_P, _U64, _U64, _U64, _P, _U32, _P, _P]),
     "hy_decrypt": (C.c_int, [_P, _U64, _P, _U32, _P, _P]),
     "hy_encode": (C.c_int, [_P, C.POINTER(C.c_double), _U32, _U64, _U32, _P, _P]),
@@ -376,6 +377,13 @@ class Context:
         out = self.empty(*self.ct_shape(level - 1)) if out is None else out
         _check(lib().hy_rescale(self._c, _ptr(ct), level, _ptr(out), self._stream()))
         return out
+
+    def pmult_batch(self, cts, pt, level, outs=None):
+        """ct_i (.) pt for every ciphertext, one plaintext, one launch (hy_pmult_batch)"""
+        outs = [self.empty(*self.ct_shape(level)) for _ in cts] if outs is None else outs
+        _check(lib().hy_pmult_batch(self._c, _ptr_array(cts), len(cts), _ptr(pt), level, _ptr_array(outs),
+                                    self._stream()))
+        return outs
 
     def rescale_batch(self, cts, level, outs=None):
         outs = [self.empty(*self.ct_shape(level - 1)) for _ in cts] if outs is None else outs

@@ -111,31 +111,46 @@ class Bootstrapper:
         return [CT(r, lv - 1, a.scale * b.scale / self.q[lv]) for r, a, b in zip(res, As, Bs)]
 
     # ---- the steps
+    def _rescaled_to_many(self, xs, target):
+        """_rescaled_to of ciphertexts in lockstep (equal levels and scales): one constant, one batched PMult
+        (hy_pmult_batch) and one batched rescale; each item bit-identical to its own _rescaled_to"""
+        x0 = xs[0]
+        pt, s = self._const(1.0, float(self.q[x0.level]) * target / x0.scale, x0.level)
+        return self._pmult_rescale_many(xs, pt, s)
+
+    def _pmult_rescale_many(self, xs, pt, s):
+        lv = xs[0].level
+        rs = self.ctx.rescale_batch(self.ctx.pmult_batch([x.t for x in xs], pt, lv), lv)
+        return [CT(r, lv - 1, x.scale * s / self.q[lv]) for r, x in zip(rs, xs)]
+
     def eval_chebyshev_many(self, xs, targets):
         """eval_chebyshev of several ciphertexts in lockstep (the real and imaginary parts): the same operation
-        sequence per item as eval_chebyshev, each MulCt of the schedule batched over the items"""
-        T = [{1: x} for x in xs]
+        sequence per item as eval_chebyshev, every MulCt, scale alignment and coefficient product batched over the
+        items (their levels and scales are equal step by step)"""
+        assert all(t == targets[0] for t in targets) and all(x.scale == xs[0].scale for x in xs)
+        target = targets[0]
+        T = {1: list(xs)}
         for k, m, n in CHEB_SCHEDULE:
-            ps = self._mul_many([t[m] for t in T], [t[n] for t in T])
-            for t, p in zip(T, ps):
-                p = self._add(p, p)
-                d = abs(m - n)
-                if d == 0:
-                    t[k] = self._add_const(p, -1.0)
-                else:
-                    t[k] = self._sub(p, self._down(self._rescaled_to(t[d], p.scale), p.level))
+            ps = [self._add(p, p) for p in self._mul_many(T[m], T[n])]
+            d = abs(m - n)
+            if d == 0:
+                T[k] = [self._add_const(p, -1.0) for p in ps]
+            else:
+                al = self._rescaled_to_many(T[d], ps[0].scale)
+                T[k] = [self._sub(p, self._down(a, p.level)) for p, a in zip(ps, al)]
+        terms = []
+        for k in range(2, len(self.cheb), 2):
+            if self.cheb[k] == 0:
+                continue
+            t0 = T[k][0]
+            pt, sc = self._const(self.cheb[k], float(self.q[t0.level]) * target / t0.scale, t0.level)
+            terms.append(self._pmult_rescale_many(T[k], pt, sc))
+        lv = min(x[0].level for x in terms)
         outs = []
-        for t, target in zip(T, targets):
-            terms = []
-            for k in range(2, len(self.cheb), 2):
-                if self.cheb[k] == 0:
-                    continue
-                pt, sc = self._const(self.cheb[k], float(self.q[t[k].level]) * target / t[k].scale, t[k].level)
-                terms.append(self._rescale(self._pmult(t[k], pt, sc)))
-            lv = min(x.level for x in terms)
+        for i in range(len(xs)):
             acc = None
             for x in terms:
-                x = self._down(x, lv)
+                x = self._down(x[i], lv)
                 acc = x if acc is None else self._add(acc, x)
             outs.append(self._add_const(acc, self.cheb[0]))
         return outs

@@ -612,6 +612,15 @@ extern "C" hy_status hy_pmult(hy_ctx* c, const uint64_t* ct, const uint64_t* pt,
   return hy_pmult_acc(c, a, b, 1, level, out, 0, stream);
 }
 
+extern "C" hy_status hy_pmult_batch(hy_ctx* c, const uint64_t* const* cts, uint32_t n, const uint64_t* pt,
+                                    uint32_t level, uint64_t* const* outs, void* stream) {
+  if (!c || !pt || (n && (!cts || !outs))) return fail(HY_E_ARG, "null");
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < n; ++j)
+      if (i != j && outs[i] == cts[j]) return fail(HY_E_ARG, "an output aliases another item's input");
+  return pmult_many(c, cts, n, pt, level, outs, st(stream));
+}
+
 extern "C" hy_status hy_add(hy_ctx* c, const uint64_t* a, const uint64_t* b, uint32_t npoly, uint32_t level,
                             uint64_t* out, void* stream) {
   if (!c || !a || !b || !out) return fail(HY_E_ARG, "null");
