@@ -276,8 +276,8 @@ def test_rescale_fused_levels(level):
 
 
 def test_rescale_batch_and_mulct_batch():
-    """hy_rescale_batch and hy_mulct_batch (bootstrapping's lockstep EvalMod): every item bit-exact vs the oracle's
-    rescale / MulCt of that item; an output aliasing another item's input is rejected (HY_E_ARG)"""
+    """hy_rescale_batch, hy_pmult_batch and hy_mulct_batch (bootstrapping's lockstep EvalMod): every item bit-exact vs
+    the oracle's rescale / PMult / MulCt of that item; an output aliasing another item's input is rejected (HY_E_ARG)"""
     import paper_2302_02407_b200 as hy
     ctx, o = _hyp_pair()
     level = 9
@@ -288,6 +288,12 @@ def test_rescale_batch_and_mulct_batch():
     d = [to_dev(a, ctx) for a in cts[:2]]
     with pytest.raises(hy.HyError):
         ctx.rescale_batch(d, level, outs=[d[1][:, :level].contiguous(), d[0]])
+    pt = rand_limbs(o, 799, list(range(level + 1)))
+    pm = ctx.pmult_batch([to_dev(a, ctx) for a in cts], to_dev(pt, ctx), level)
+    for a, got in zip(cts, pm):
+        assert np.array_equal(to_np(got), o.pmult(oracle.Ct(a, level, 1.0), oracle.Pt(pt, level, 1.0)).data)
+    with pytest.raises(hy.HyError):
+        ctx.pmult_batch(d, to_dev(pt, ctx), level, outs=[d[1], d[1].clone()])
     rlk, orlk = ctx.keygen_relin(SK, EK), o.keygen_relin(SK, EK)
     z = [synth.slots_uniform(80 + k, o.n) for k in range(3)]
     ocs = [o.encrypt(SK, 4, 40 + k, o.encode(z[k], 2**42, level)) for k in range(3)]

@@ -65,6 +65,7 @@ def boot():
     ctx.mulct(rlk, y, y, top - 1)
     # bootstrapping's lockstep EvalMod: batched MulCt and batched rescale
     pr = ctx.mulct_batch(rlk, [y, up[:, : top].contiguous()], [y, y], top - 1)
+    pr = ctx.pmult_batch(pr, ctx.encode(np.full(ctx.n, 0.5), 2**40, top - 1), top - 1)
     ctx.rescale_batch(pr, top - 1)
     torch.cuda.synchronize()
     print("boot steps ok")
