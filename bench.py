@@ -887,7 +887,30 @@ def bench_block_chain(ctx, bt, sk, ek):
         ms_r = e0.elapsed_time(e1) / 3
         out[name] = {"block_ms": ms_b, "refresh_ms": ms_r, "blocks_in_resnet20": count, "levels": [L, out_level, z.level]}
         del cak, rak, cap, rap
-    return {"stages": out, "level_in": L,
+    # the whole ResNet-20 conv stack end to end (boot.ResNet20Convs): stem, 9 blocks, 8 bootstraps
+    from paper_2302_02407_b200.boot import ResNet20Convs
+    shapes = [((16, 3), 3)] + [((16, 16), 3)] * 6 + [((32, 16), 3), ((32, 32), 3), ((32, 16), 1)] + \
+        [((32, 32), 3)] * 4 + [((64, 32), 3), ((64, 64), 3), ((64, 32), 1)] + [((64, 64), 3)] * 4
+    net = ResNet20Convs(ctx, chain, [synth.conv_weight(200 + i, co, ci, f) * 0.5 for i, ((co, ci), f) in
+                                     enumerate(shapes)], lambda r: ctx.keygen_rot(sk, ek, r))
+    Li = net.input_level
+    x = CT(ctx.encrypt(sk, 32, 0, ctx.encode(synth.slots_uniform(8, ctx.n), 2**42, Li), Li), Li, 2.0**42)
+    y = net.run(x)  # warm-up
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    e0.record()
+    for _ in range(2):
+        y = net.run(x)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e = {"ms": e0.elapsed_time(e1) / 2, "launches": (ctx.launch_count() - l0) // 2, "bootstraps": 8,
+           "convs": 21 + 3, "input_level": Li, "output_level": y.level, "paper_a100_s": 1.40,
+           "note": "stem conv + square, 9 blocks y = RAConv(CAConv(x)^2) + s(x) (dsconv / pconv at the stage "
+                   "boundaries; 1x1 identity RAConvs convert the stem's and the pconvs' RA format), a bootstrap after "
+                   "each of the first 8 blocks; no pooling / FC; random Kaiming weights x 0.5; "
+                   "tests/test_gpu_boot.py::test_resnet20_convs_end_to_end checks the decryption against the "
+                   "plaintext network (8.9e-4 of its max, r02v)"}
+    return {"stages": out, "level_in": L, "resnet20_end_to_end": e2e,
             "note": "y = RAConv(CAConv(x)^2) + x, then bootstrap (BlockChain.refresh) back to L' = 6; device time per "
                     "call, host-sequenced C-ABI calls"}
 
@@ -1252,18 +1275,7 @@ def run_ours(args, ws, rank, local):
     boot = None
     if not args.no_conv:
         boot = bench_boot_linear(ctx, max(3, args.steps), 2, timed)
-        ch = boot.get("resnet20_chain") if boot else None
-        if ch and conv and "layers" in conv:
-            lay = conv["layers"]
-            ds = sum(lay[k]["ms"] for k in ("L2_ds", "L2_pconv", "L3_ds", "L3_pconv") if k in lay)
-            blocks_ms = sum(v["blocks_in_resnet20"] * (v["block_ms"] + v["refresh_ms"]) for v in ch["stages"].values())
-            ch["network_estimate"] = {
-                "ms": lay["stem"]["ms"] + blocks_ms + ds if "stem" in lay else None,
-                "how": "composed from measured parts (an upper estimate): the stem layer; 3 blocks per stage at the "
-                       "stage's measured block + refresh time; the 2 stride-2 blocks counted as regular blocks PLUS "
-                       "their dsconv and pconv layer times from the layer table; one bootstrap per block; no "
-                       "pooling / FC; random Kaiming weights",
-                "paper_a100_s": 1.40}
+
 
     c1 = None
     if not args.no_c1:

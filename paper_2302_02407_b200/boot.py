@@ -312,15 +312,97 @@ class BlockChain:
         self.ctx, self.bt, self.boot_scale = ctx, bt, boot_scale
         self.top = ctx.n_q - 1
 
-    def block(self, blk, ca_keys, ra_keys, ca_pts, ra_pts, x: CT) -> CT:
+    def block(self, blk, ca_keys, ra_keys, ca_pts, ra_pts, x: CT, shortcut=()) -> CT:
+        """y = RAConv(CAConv(x)^2) + s(x), s the identity or (a stride-2 block) the convs `shortcut` = [(ConvPlan,
+        keys, weight pts at its input level), ...] applied in order; the shortcut branch is brought to the main
+        branch's scale and level"""
         bt = self.bt
         mid, _, out_level = blk.levels(x.level)
-        y = blk.run(ca_keys, ra_keys, bt.rlk, [x.t], x.level, ca_pts, ra_pts)[0]
+        y = blk.run(ca_keys, ra_keys, bt.rlk, [x.t], x.level, ca_pts, ra_pts)
+        assert len(y) == 1
         ys = x.scale * x.scale / bt.q[mid]  # CAConv and RAConv keep the scale; the square makes it s^2 / q_mid
-        sc = bt._down(bt._rescaled_to(x, ys), out_level)
-        return bt._add(CT(y, out_level, ys), sc)
+        xs = [x.t]
+        lv = x.level
+        for plan, keys, pts in shortcut:
+            xs, lv = plan.run(keys, xs, lv, pts), plan.out_level(lv)
+        sc = bt._down(bt._rescaled_to(CT(xs[0], lv, x.scale), ys), out_level)
+        return bt._add(CT(y[0], out_level, ys), sc)
 
     def refresh(self, x: CT) -> CT:
         bt = self.bt
         x = bt._down(bt._rescaled_to(x, self.boot_scale), 0)
         return bt.bootstrap(x.t, x.scale, self.top)
+
+
+class ResNet20Convs:
+    """The ResNet-20 (CIFAR-10) conv stack run end to end under encryption at Set_hyp through BlockChain (SURVEY 8(f)
+    row 4): stem conv + square (+ a 1x1 identity RAConv for the format), then 3 stages of 3 blocks y = RAConv(CAConv(x)^2) + s(x) -- the first block of
+    stages 2 and 3 a stride-2 CAConv (dsconv, R-DSCONV) with a 1x1 stride-2 conv (pconv, then a 1x1 identity RAConv
+    for the format) on the shortcut -- with a
+    bootstrap after every block but the last.  Layer shapes and plans as bench.R20_LAYERS (2D-gap
+    (1,2) / (2,4) / (4,8)); no average pooling / FC (outside the conv path).  weights: the 21 conv kernels in order
+    (stem, then per block CAConv, RAConv [, pconv])."""
+
+    SPECS = {  # (ci, co, w, f, stride, wp, gap, m, d, algo)
+        "stem": (3, 16, 32, 3, 1, 32, 1, 1, 2, "CA"),
+        "s1_ca": (16, 16, 32, 3, 1, 32, 1, 1, 2, "CA"), "s1_ra": (16, 16, 32, 3, 1, 32, 1, 2, 1, "RA"),
+        "s2_ds": (16, 32, 32, 3, 2, 32, 1, 1, 2, "CA"), "s2_pc": (16, 32, 32, 1, 2, 32, 1, 1, 2, "CA"),
+        "s2_ca": (32, 32, 16, 3, 1, 32, 2, 2, 4, "CA"), "s2_ra": (32, 32, 16, 3, 1, 32, 2, 4, 2, "RA"),
+        "s3_ds": (32, 64, 16, 3, 2, 32, 2, 2, 4, "CA"), "s3_pc": (32, 64, 16, 1, 2, 32, 2, 2, 4, "CA"),
+        "s3_ca": (64, 64, 8, 3, 1, 32, 4, 4, 8, "CA"), "s3_ra": (64, 64, 8, 3, 1, 32, 4, 8, 4, "RA"),
+        # the pconv shortcut leaves RA(2d, 2m) (8 ciphertexts, R-DSCONV); a 1x1 RAConv with identity weights turns
+        # it into the block output's CA(m, d) (1 ciphertext) so that the two branches add slot by slot
+        "s2_id": (32, 32, 16, 1, 1, 32, 2, 4, 2, "RA"), "s3_id": (64, 64, 8, 1, 1, 32, 4, 8, 4, "RA"),
+        # the same after the stem: its RA(2,1) output (8 ciphertexts) into the first block's CA(1,2)
+        "s1_id": (16, 16, 32, 1, 1, 32, 1, 2, 1, "RA"),
+    }
+    # blocks: (CAConv, RAConv, shortcut conv or None)
+    BLOCKS = [("s1_ca", "s1_ra", None)] * 3 + [("s2_ds", "s2_ra", ("s2_pc", "s2_id"))] + \
+        [("s2_ca", "s2_ra", None)] * 2 + [("s3_ds", "s3_ra", ("s3_pc", "s3_id"))] + [("s3_ca", "s3_ra", None)] * 2
+
+    def __init__(self, ctx, chain: BlockChain, weights, keyfn, level: int = 6):
+        from . import ConvBlock, ConvPlan
+        self.ctx, self.chain, self.level = ctx, chain, level
+        self.plans = {k: ConvPlan(ctx, *v) for k, v in self.SPECS.items()}
+        self.keys = {}
+        for p in self.plans.values():
+            for r in p.rots:
+                if r not in self.keys:
+                    self.keys[r] = keyfn(r)
+        w = iter(weights)
+        # the stem, its square and the identity RAConv into CA(1,2) as one ConvBlock; the client encrypts above L'
+        # so that they land on L' (a fresh ciphertext may start at any level; every block then starts at L', the
+        # level a bootstrap returns to)
+        self.stem = ConvBlock(ctx, self.plans["stem"], self.plans["s1_id"])
+        self.input_level = next(lv for lv in range(level, ctx.n_q) if self.stem.levels(lv)[2] == level)
+        _, id_level, _ = self.stem.levels(self.input_level)
+        self.stem_pts = self.plans["stem"].encode_weights(next(w), self.input_level)
+        self.id_pts = self.plans["s1_id"].encode_weights(np.eye(16).reshape(16, 16, 1, 1), id_level)
+        self.blocks = []
+        lv = level
+        for ca, ra, sc in self.BLOCKS:
+            blk = ConvBlock(ctx, self.plans[ca], self.plans[ra])
+            _, ra_level, _ = blk.levels(lv)
+            cap = self.plans[ca].encode_weights(next(w), lv)
+            rap = self.plans[ra].encode_weights(next(w), ra_level)
+            scp = []
+            if sc:
+                pc, idn = self.plans[sc[0]], self.plans[sc[1]]
+                co = self.SPECS[sc[1]][1]
+                scp = [(pc, pc.encode_weights(next(w), lv)),
+                       (idn, idn.encode_weights(np.eye(co).reshape(co, co, 1, 1), pc.out_level(lv)))]
+            self.blocks.append((blk, cap, rap, scp, lv))
+
+    def run(self, x: CT) -> CT:
+        """x: the packed image, encrypted at self.input_level"""
+        bt = self.chain.bt
+        mid, _, out = self.stem.levels(x.level)
+        # the stem conv, its activation (AESPA square, P:1013-1015), the identity RAConv (format only)
+        y = self.stem.run(self.keys, self.keys, bt.rlk, [x.t], x.level, self.stem_pts, self.id_pts)
+        y = CT(y[0], out, x.scale * x.scale / bt.q[mid])
+        for i, (blk, cap, rap, scp, lv) in enumerate(self.blocks):
+            assert y.level == lv
+            y = self.chain.block(blk, self.keys, self.keys, cap, rap, y, shortcut=[(p, self.keys, w) for p, w in scp])
+            if i + 1 < len(self.blocks):
+                y = self.chain.refresh(y)
+        return y

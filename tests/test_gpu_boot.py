@@ -260,3 +260,40 @@ def test_block_chain_set_hyp():
     Y1 = H.conv2d(H.conv2d(X, Ks[0]) ** 2, Ks[1]) + X
     Y2 = H.conv2d(H.conv2d(Y1, Ks[2]) ** 2, Ks[3]) + Y1
     assert np.max(np.abs(res - Y2)) < 2**-8 * np.max(np.abs(Y2))
+
+
+def test_resnet20_convs_end_to_end():
+    """The ResNet-20 conv stack end to end under encryption at Set_hyp (boot.ResNet20Convs: stem + square, 9 blocks
+    y = RAConv(CAConv(x)^2) + s(x) with dsconv / pconv at the stage boundaries, a bootstrap after each of the first 8
+    blocks): the 64 x 8 x 8 result decrypts to the plaintext network (oracle conv2d) within 2^-7 of its max."""
+    import paper_2302_02407_b200 as hy
+    from oracle import hyphen as H
+    from paper_2302_02407_b200.boot import CT, BlockChain, Bootstrapper, ResNet20Convs, transform_rots
+    ctx, o = pair("hyp")
+    N, n = o.N, o.n
+    cts, stc, bs = _factorised(N, [5, 5, 5], float(o.q[0]) / 2**42)
+    rots = sorted(set(transform_rots(ctx, cts, bs[0])) | set(transform_rots(ctx, stc, bs[1])))
+    bt = Bootstrapper(ctx, cts, stc, bs, _cheb(12.0), 4, 12.0, {r: ctx.keygen_rot(SK, EK, r) for r in rots},
+                      ctx.keygen_galois(SK, EK, 2 * N - 1), ctx.keygen_relin(SK, EK))
+    shapes = [((16, 3), 3)] + [((16, 16), 3)] * 6 + [((32, 16), 3), ((32, 32), 3), ((32, 16), 1)] + \
+        [((32, 32), 3)] * 4 + [((64, 32), 3), ((64, 64), 3), ((64, 32), 1)] + [((64, 64), 3)] * 4
+    Ws = [synth.conv_weight(200 + i, co, ci, f) * (0.5) for i, ((co, ci), f) in enumerate(shapes)]
+    net = ResNet20Convs(ctx, BlockChain(ctx, bt), Ws, lambda r: ctx.keygen_rot(SK, EK, r))
+    X = synth.image(300, 3, 32)
+    spec = ResNet20Convs.SPECS
+    fin = H.plan_caconv(H.ConvSpec(*spec["stem"], n=n), Ws[0]).fin
+    xs = H.pack(X, fin)
+    assert len(xs) == 1
+    L = net.input_level
+    y = net.run(CT(ctx.encrypt(SK, 32, 0, ctx.encode(xs[0], 2**42, L), L), L, 2.0**42))
+    fout = H.plan_raconv(H.ConvSpec(*spec["s3_ra"], n=n), Ws[-1]).fout
+    res = H.unpack([np.real(ctx.decode(ctx.decrypt(SK, y.t, y.level), y.level, y.scale))], fout, 64, 8, 8)
+    it = iter(Ws)
+    Y = H.conv2d(X, next(it)) ** 2
+    for ca, ra, sc in ResNet20Convs.BLOCKS:
+        Kc, Kr = next(it), next(it)
+        stride = spec[ca][4]
+        main = H.conv2d(H.conv2d(Y, Kc, stride) ** 2, Kr)
+        Y = main + (H.conv2d(Y, next(it), 2) if sc else Y)
+    assert res.shape == Y.shape
+    assert np.max(np.abs(res - Y)) < 2**-7 * np.max(np.abs(Y))
