@@ -105,6 +105,8 @@ class Bootstrapper:
         """pairwise MulCt + rescale of several ciphertext pairs in lockstep: one batched key switch (hy_mulct_batch;
         each item bit-identical to its own hy_mulct)"""
         lv = min(x.level for x in As + Bs)
+        # every pair at the level its own _mul would use (a batch must not pull a pair lower than that)
+        assert all(min(a.level, b.level) == lv for a, b in zip(As, Bs))
         As, Bs = [self._down(a, lv) for a in As], [self._down(b, lv) for b in Bs]
         outs = self.ctx.mulct_batch(self.rlk, [a.t for a in As], [b.t for b in Bs], lv)
         res = self.ctx.rescale_batch(outs, lv)
@@ -119,9 +121,24 @@ class Bootstrapper:
         return self._pmult_rescale_many(xs, pt, s)
 
     def _pmult_rescale_many(self, xs, pt, s):
-        lv = xs[0].level
-        rs = self.ctx.rescale_batch(self.ctx.pmult_batch([x.t for x in xs], pt, lv), lv)
-        return [CT(r, lv - 1, x.scale * s / self.q[lv]) for r, x in zip(rs, xs)]
+        return self._pmult_rescale_groups([(xs, pt, s)])[0]
+
+    def _pmult_rescale_groups(self, groups):
+        """[(cts, pt, pt_scale)] -> [[rescale(ct (.) pt)]]: one batched PMult per group (one plaintext each), then
+        one batched rescale per level over every group's products; each item bit-identical to its own PMult +
+        rescale"""
+        prods = [self.ctx.pmult_batch([x.t for x in xs], pt, xs[0].level) for xs, pt, _ in groups]
+        by_level = {}
+        for gi, (xs, _, _) in enumerate(groups):
+            for ii, x in enumerate(xs):
+                by_level.setdefault(x.level, []).append((gi, ii))
+        res = [[None] * len(xs) for xs, _, _ in groups]
+        for lv, idx in by_level.items():
+            outs = self.ctx.rescale_batch([prods[gi][ii] for gi, ii in idx], lv)
+            for (gi, ii), o in zip(idx, outs):
+                xs, _, s = groups[gi]
+                res[gi][ii] = CT(o, lv - 1, xs[ii].scale * s / self.q[lv])
+        return res
 
     def eval_chebyshev_many(self, xs, targets):
         """eval_chebyshev of several ciphertexts in lockstep (the real and imaginary parts): the same operation
@@ -130,21 +147,37 @@ class Bootstrapper:
         assert all(t == targets[0] for t in targets) and all(x.scale == xs[0].scale for x in xs)
         target = targets[0]
         T = {1: list(xs)}
-        for k, m, n in CHEB_SCHEDULE:
-            ps = [self._add(p, p) for p in self._mul_many(T[m], T[n])]
-            d = abs(m - n)
-            if d == 0:
-                T[k] = [self._add_const(p, -1.0) for p in ps]
-            else:
-                al = self._rescaled_to_many(T[d], ps[0].scale)
-                T[k] = [self._sub(p, self._down(a, p.level)) for p, a in zip(ps, al)]
-        terms = []
+        # the schedule in waves of entries whose operands are ready (depth by depth: T2 | T4 | T8, T6 |
+        # T16, T10, T12, T14 | T18 .. T30); a wave's MulCts share one level, so all of them, for every item, run as ONE
+        # batched MulCt + rescale -- 5 sequential key-switch steps instead of 15, each item's operations unchanged
+        todo = list(CHEB_SCHEDULE)
+        while todo:
+            wave = [e for e in todo if all(v in T for v in (e[1], e[2], abs(e[1] - e[2])) if v)]
+            todo = [e for e in todo if e not in wave]
+            ni = len(xs)
+            prods = self._mul_many([a for _, m, _ in wave for a in T[m]], [b for _, _, n in wave for b in T[n]])
+            ps = {k: [self._add(p, p) for p in prods[w * ni:(w + 1) * ni]] for w, (k, _, _) in enumerate(wave)}
+            # the scale alignments of T_|m-n| (one constant per entry), rescaled together level by level
+            al_entries = [(k, abs(m - n)) for k, m, n in wave if m != n]
+            groups = []
+            for k, d in al_entries:
+                x0 = T[d][0]
+                pt, sc = self._const(1.0, float(self.q[x0.level]) * ps[k][0].scale / x0.scale, x0.level)
+                groups.append((T[d], pt, sc))
+            als = dict(zip([k for k, _ in al_entries], self._pmult_rescale_groups(groups)))
+            for k, m, n in wave:
+                if m == n:
+                    T[k] = [self._add_const(p, -1.0) for p in ps[k]]
+                else:
+                    T[k] = [self._sub(p, self._down(a, p.level)) for p, a in zip(ps[k], als[k])]
+        groups = []
         for k in range(2, len(self.cheb), 2):
             if self.cheb[k] == 0:
                 continue
             t0 = T[k][0]
             pt, sc = self._const(self.cheb[k], float(self.q[t0.level]) * target / t0.scale, t0.level)
-            terms.append(self._pmult_rescale_many(T[k], pt, sc))
+            groups.append((T[k], pt, sc))
+        terms = self._pmult_rescale_groups(groups)
         lv = min(x[0].level for x in terms)
         outs = []
         for i in range(len(xs)):
