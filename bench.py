@@ -1381,11 +1381,11 @@ def main():
     ap.add_argument("--no-variants", action="store_true", help="skip the HRot variant x level table")
     ap.add_argument("--no-c1", action="store_true", help="skip the BASELINE configs[0] RAConv timing")
     args = ap.parse_args()
+    if args.impl == "reference":  # the CPU oracle on rank 0; no process group (the other ranks exit 0 at once)
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
     ws, rank, local = dist_setup()
-    if args.impl == "reference":
-        run_reference(args, ws, rank)
-    else:
-        run_ours(args, ws, rank, local)
+    run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
