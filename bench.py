@@ -269,7 +269,9 @@ def run_reference(args, ws, rank):
     """Reference arm: the CPU oracle as it stands, on the host cores (rank 0 only)."""
     if rank != 0:
         return
+    # all host cores (torchrun sets OMP_NUM_THREADS=1 per rank; the oracle's OpenMP reads it when it loads, below)
     cores = os.cpu_count()
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     # warm-up (untimed) and K timed steps, each step = 1 plain HRot at full level (bounded sample)
     for _ in range(args.warmup):
         oracle_keyswitch_rate(1)
