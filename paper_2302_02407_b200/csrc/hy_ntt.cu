@@ -849,9 +849,12 @@ __device__ __forceinline__ void rows_ip_final_tma_body(const IpFinalArgs& a, con
         store_l3(a.out[g] + o, l, x, q, qinv, false);
       }
     }
-    // release the stage: every lane's generic accesses before the next bulk write into it
-    tma::proxy_fence();
-    __syncwarp();
+    // release the stage: every lane's generic accesses before the next bulk write into it (issued at j + 1 only when
+    // j + NST <= LAST; the last iterations skip the fence, whose MEMBAR would wait for the epilogue's global stores)
+    if (j + NST <= LAST) {
+      tma::proxy_fence();
+      __syncwarp();
+    }
   }
   if constexpr (PL) {
     // the P limb's inverse row pass straight from registers (layout L3), stage 0's buffer as transpose space
@@ -974,8 +977,10 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
         a1[k] = fred(a1[k], q, qinv);
       }
     }
-    tma::proxy_fence();
-    __syncwarp();
+    if (it + NST <= last) {  // the stage is refilled at it + 1 (see rows_ip_final_tma_body)
+      tma::proxy_fence();
+      __syncwarp();
+    }
   }
   store_l3(a.out[0] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
   store_l3(a.out[0] + ((size_t)E + u) * N + roff, l, a1, q, qinv, accumulate);

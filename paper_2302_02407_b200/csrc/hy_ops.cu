@@ -188,6 +188,8 @@ __global__ void __launch_bounds__(256) k_pmult_rows(const __grid_constant__ PBlo
 constexpr int kPbStages = 4;
 template <int M>
 constexpr size_t pmult_ring_smem() { return (size_t)kPbStages * (M + 2) * 2048 + 8 * kPbStages; }
+template <int M, int NS = kPbStages>
+constexpr size_t pmult_ring_ws_smem() { return (size_t)NS * (M + 2) * 2048 + 16 * NS; }
 template <int M>
 __global__ void __launch_bounds__(256) k_pmult_ring(const __grid_constant__ PBlock b, int J, DevTables dt, int level,
                                                     int logN, int accumulate) {
@@ -246,6 +248,93 @@ __global__ void __launch_bounds__(256) k_pmult_ring(const __grid_constant__ PBlo
     }
     tma::proxy_fence();  // this thread's reads of the stage precede the next bulk write into it
     __syncthreads();
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      uint64_t* o = b.out[m] + ((size_t)p * n + i) * N + x;
+      double v = acc[m][p];
+      if (accumulate) v += u2d(*o);
+      *o = d2u(fcanon(v, q, qinv));
+    }
+}
+
+// The same ring with a producer warp (round 2): warps 0-7 consume (one thread per word, as above), warp 8 only
+// refills the ring.  A stage is released by one arrival per consumer warp on its "empty" mbarrier, so the consumer
+// warps never wait for each other (no CTA barrier per operand); the producer waits for the 8 arrivals before it
+// reuses a stage.  Same arithmetic, term order and output as k_pmult_ring.
+template <int M, int NS = kPbStages>
+__global__ void __launch_bounds__(288) k_pmult_ring_ws(const __grid_constant__ PBlock b, int J, DevTables dt,
+                                                       int level, int logN, int accumulate) {
+  extern __shared__ __align__(128) double ring[];  // [NST][M + 2][256], then NST full and NST empty mbarriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * (M + 2) * 256);
+  uint64_t* empty = full + NS;
+  const size_t N = (size_t)1 << logN;
+  const int t = threadIdx.x;
+  const uint32_t r = blockIdx.x;
+  const int i = blockIdx.y;
+  const size_t n = level + 1;
+  if (t == 0) {
+    for (int st = 0; st < NS; ++st) {
+      tma::mbar_init(full + st);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tma::saddr(empty + st)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t >= 256) {  // producer warp
+    if (t == 256) {
+      for (int j = 0; j < J; ++j) {
+        const int st = j % NS;
+        if (j >= NS) tma::mbar_wait(empty + st, (uint32_t)(j / NS - 1) & 1);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(ring + (size_t)st * (M + 2) * 256);
+        tma::mbar_expect(full + st, (M + 2) * 2048);
+        tma::bulk_row(dst, b.ct[j] + (size_t)i * N + (size_t)r * 256, full + st);
+        tma::bulk_row(dst + 256, b.ct[j] + (n + i) * N + (size_t)r * 256, full + st);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const uint32_t k = b.prot[m][j];
+          const uint32_t sr = k != 1 ? aut_index(r * 256u, k, logN) >> 8 : r;
+          tma::bulk_row(dst + 256 * (2 + m), b.pt_base + ((size_t)b.pt_idx[m][j] * n + i) * N + (size_t)sr * 256,
+                        full + st);
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t x = r * 256 + t;
+  const PrimeConst& pc = dt.pc[i];
+  const double q = pc.qd, qinv = pc.qinv;
+  double acc[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m][0] = acc[m][1] = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const int st = j % NS;
+    tma::mbar_wait(full + st, (uint32_t)(j / NS) & 1);
+    const uint64_t* S = reinterpret_cast<const uint64_t*>(ring + (size_t)st * (M + 2) * 256);
+    const double c0 = u2d(S[t]), c1 = u2d(S[256 + t]);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint32_t k = b.prot[m][j];
+      const uint32_t pos = k != 1 ? aut_index(x, k, logN) & 255u : (uint32_t)t;
+      const double w = u2d(S[256 * (2 + m) + pos]);
+      acc[m][0] += fmulmod(c0, w, q, qinv);
+      acc[m][1] += fmulmod(c1, w, q, qinv);
+    }
+    if ((j & 3) == 3) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        acc[m][0] = fred(acc[m][0], q, qinv);
+        acc[m][1] = fred(acc[m][1], q, qinv);
+      }
+    }
+    if (j + NS < J) {  // the stage is refilled for j + NST: release it (one arrival per warp)
+      tma::proxy_fence();
+      __syncwarp();
+      if ((t & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tma::saddr(empty + st)) : "memory");
+    }
   }
 #pragma unroll
   for (int m = 0; m < M; ++m)
@@ -530,14 +619,19 @@ hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_
     static const int forced = getenv("HY_PMB_ROWS") ? atoi(getenv("HY_PMB_ROWS")) : -1;
     const int rows = forced >= 0 ? forced : (any_prot ? 0 : 2);
     if (rows == 2) {
+      // HY_PMB_WS=0: the ring without the producer warp (one CTA barrier per operand)
+      static const bool ws = getenv("HY_PMB_WS") == nullptr || atoi(getenv("HY_PMB_WS")) != 0;
 #define HY_PR(MM)                                                                                                 \
   case MM: {                                                                                                    \
     static bool at = false;                                                                                     \
     if (!at) {                                                                                                  \
       cudaFuncSetAttribute(k_pmult_ring<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pmult_ring_smem<MM>()); \
+      cudaFuncSetAttribute(k_pmult_ring_ws<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
+                           (int)pmult_ring_ws_smem<MM>());                                                      \
       at = true;                                                                                                \
     }                                                                                                           \
-    k_pmult_ring<MM><<<g, kT, pmult_ring_smem<MM>(), s>>>(b, (int)jn, c->dt, level, c->log_n, acc);             \
+    if (ws) k_pmult_ring_ws<MM><<<g, kT + 32, pmult_ring_ws_smem<MM>(), s>>>(b, (int)jn, c->dt, level, c->log_n, acc); \
+    else k_pmult_ring<MM><<<g, kT, pmult_ring_smem<MM>(), s>>>(b, (int)jn, c->dt, level, c->log_n, acc);        \
   } break;
       switch (M) {
         HY_PR(1)
