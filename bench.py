@@ -1133,12 +1133,12 @@ def run_ours(args, ws, rank, local):
     alg_rot = {"plain": (2 * ct_bytes + key_slice, 2 * ct_bytes + key_slice8),
                "hoisted": (ct_bytes + key_slice + ct_bytes / BATCH, ct_bytes + key_slice8 + ct_bytes / BATCH)}
 
-    def ncu_step_bytes(fam_name):
-        t = ncu_traffic(fam_name)
+    def ncu_step_bytes(fam_name, bd=None, tfam=None):
+        t = ncu_traffic(tfam or fam_name)
         if t is None:
             return None
         # the capture summary holds the per-launch average of the family's kernels
-        return t["bytes_per_launch"] * breakdown[fam_name]["launches_per_step"]
+        return t["bytes_per_launch"] * (bd or breakdown)[fam_name]["launches_per_step"]
 
     def hbm_roof(fam_name, variant="plain", bd=None):
         bd = bd or breakdown
@@ -1147,7 +1147,9 @@ def run_ours(args, ws, rank, local):
         t_s = d["ms_per_step"] * 1e-3
         achieved = alg / t_s / 1e9
         model = d["alg_bytes_per_launch"] * d["launches_per_step"] / t_s / 1e9
-        tr = ncu_step_bytes(fam_name) if bd is breakdown else None
+        # the hoisted batch's own kernels (tools/ncu_round.py family "<fam>_hoisted") when captured
+        tfam = fam_name if variant == "plain" else fam_name + "_hoisted"
+        tr = ncu_step_bytes(fam_name, bd, tfam)
         return {"bound": "hbm", "kernel_family": fam_name, "achieved": achieved, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                 "frac_8byte_key_equiv": alg8 / t_s / 1e9 / pk["hbm_gbs"],
@@ -1157,7 +1159,7 @@ def run_ours(args, ws, rank, local):
                 "dram_model_gbs": model,
                 "dram_model_note": "the same launches' modelled DRAM bytes including intermediates (extended "
                                    "digits, conversion rows) over their time: achieved DRAM rate, not the roofline",
-                **traffic_fields(fam_name),
+                **traffic_fields(tfam),
                 "traffic_over_alg": None if tr is None else tr / alg,
                 "share_of_step": d["ms_per_step"] / ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback 6.65 TB/s"}
