@@ -16,7 +16,7 @@ namespace {
 constexpr int kT = 256;
 constexpr int kMaxTerms = 64;
 
-constexpr int kPbJ = 64, kPbM = 8;
+constexpr int kPbJ = 128, kPbM = 8;  // up to 128 operands per launch: a 3x3 block of 8 inputs (72) in one
 struct PBlock {
   const uint64_t* ct[kPbJ];
   uint64_t* out[kPbM];
@@ -591,7 +591,10 @@ hy_status pmult_block(hy_ctx* c, const uint64_t* const* cts, uint32_t J, uint64_
   if (M == 0 || M > (uint32_t)kPbM || J == 0) return fail(HY_E_ARG, "block shape");
   cudaStream_t s = st(stream);
   for (uint32_t done = 0; done < J;) {
-    const uint32_t jn = std::min<uint32_t>(J - done, kPbJ);
+    // operands per launch (HY_PMB_J A/B: 64 splits a 72-operand 3x3 block of 8 inputs into 64 + 8)
+    static const uint32_t jcap = getenv("HY_PMB_J") ? (uint32_t)std::max(1, std::min(kPbJ, atoi(getenv("HY_PMB_J"))))
+                                                    : (uint32_t)kPbJ;
+    const uint32_t jn = std::min<uint32_t>(J - done, jcap);
     PBlock b;
     b.pt_base = pt_base;
     for (uint32_t j = 0; j < jn; ++j) b.ct[j] = cts[done + j];
