@@ -821,16 +821,25 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
   const size_t no = oe - ob;
   std::vector<const uint64_t*> sums(no);
   std::vector<uint64_t*> dst(no);
+  std::vector<const uint64_t*> tap_accs(no * f2);
+  std::vector<uint64_t*> sum_out(no);
   for (uint32_t o = ob; o < oe; ++o) {
     uint64_t* oacc = accs + (size_t)(o - ob) * f2 * ct_l;
-    std::vector<const uint64_t*> acc_ptrs(f2);
-    for (size_t t = 0; t < f2; ++t) acc_ptrs[t] = oacc + t * ct_l;
-    uint64_t* sum = tmp + (size_t)(o - ob) * ct_l;
-    stt = hy_hrot_sum(c, keys.data(), acc_ptrs.data(), level, rs.data(), (uint32_t)f2, sum, stream);
-    if (stt != HY_OK) return stt;
-    sums[o - ob] = sum;
+    for (size_t t = 0; t < f2; ++t) tap_accs[(o - ob) * f2 + t] = oacc + t * ct_l;
+    sum_out[o - ob] = tmp + (size_t)(o - ob) * ct_l;
+    sums[o - ob] = sum_out[o - ob];
     dst[o - ob] = p->has_mask ? oacc : out[o - ob];  // the output's consumed tap accumulators
   }
+  // every output's lazy HRotSum in one batched launch set (round 2), else one hy_hrot_sum per output
+  stt = no >= 2 ? hrot_sum_multi(c, keys.data(), tap_accs.data(), level, rs.data(), (uint32_t)f2, (uint32_t)no,
+                                 sum_out.data(), x.s)
+                : HY_E_WORKSPACE;
+  if (stt == HY_E_WORKSPACE)
+    for (size_t o = 0; o < no; ++o) {
+      stt = hy_hrot_sum(c, keys.data(), tap_accs.data() + o * f2, level, rs.data(), (uint32_t)f2, sum_out[o], stream);
+      if (stt != HY_OK) return stt;
+    }
+  if (stt != HY_OK) return stt;
   // ping-pong buffers: the second tap accumulator of every output (consumed by its HRotSum; f^2 >= 2)
   const bool ppok = f2 >= 2;
   // limited key sets: the third and fourth tap accumulators hold the intermediate steps (f^2 >= 4)

@@ -157,7 +157,7 @@ struct RowsIpArgs {
 // inv_p (with u0 = l+1): store the P limbs after their inverse row pass into v instead (split ModDown)
 // hoist: ext holds the NTT-domain digits of one shared ModUp, read through kx_g (hoisted batch)
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0 = 0, bool inv_p = false, bool hoist = false);
+                        cudaStream_t s, int u0 = 0, bool inv_p = false, bool hoist = false, int groups = 1);
 
 // Key-switch inner product on the Q_l limbs fused with the ModDown epilogue (hy_ntt.cu), per item g,
 // limb i <= level, poly c:
@@ -232,6 +232,10 @@ void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t le
 // the summed (lazy HRotSum) IP runs on the bulk-copy ring (HY_SUMTMA, default on); it can read the own digit
 // through kappa, so the lazy path then fuses kappa into the inverse row pass
 bool sum_tma_on();
+// the lazy HRotSums of O outputs over the same n rotations, batched (hy_keyswitch.cu); HY_E_WORKSPACE: not
+// batchable here (nothing launched), call hy_hrot_sum per output
+hy_status hrot_sum_multi(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                         const int32_t* r, uint32_t n, uint32_t O, uint64_t* const* outs, cudaStream_t s);
 // one NTT row pass (forward: reads the between-pass format; inverse: writes it)
 void launch_ntt_rows(hy_ctx* c, const LimbBatch& b, bool inverse, cudaStream_t s);
 // convenience: contiguous [n][N] arrays with chain indices

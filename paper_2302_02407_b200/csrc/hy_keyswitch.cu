@@ -426,7 +426,7 @@ void intt_polys(hy_ctx* c, int G, const uint64_t* const* in, uint64_t* const* ou
 void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64_t* const* ext,
                     const uint64_t* const* own, const uint64_t* const* evk, uint64_t* const* u, bool acc, bool sum,
                     cudaStream_t s, int u0 = 0, uint64_t* const* v = nullptr, bool rows_done = false,
-                    const uint64_t* own_k = nullptr) {
+                    const uint64_t* own_k = nullptr, int groups = 1) {
   if (modup_cols_ok(c)) {
     if (!rows_done) {  // rows_done: d already holds the inverse row pass (launch_ntt_rows_inv_aut)
       LimbList L;
@@ -449,11 +449,11 @@ void modup_ip_fused(hy_ctx* c, uint32_t level, int G, uint64_t* const* d, uint64
     ra.ext[g] = ext[g];
     ra.own[g] = own[g];
     ra.evk[g] = evk[g];
-    ra.u[g] = u[sum ? 0 : g];
+    ra.u[g] = u[sum ? g / (G / groups) : g];  // sum: one u per group of G / groups items
     ra.v[g] = v ? v[g] : nullptr;
     ra.kx[g] = own_k ? own_k[g] : 1;  // own_k: the own digit is read from own_g through kappa (summed IP only)
   }
-  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0, v != nullptr);
+  launch_ntt_rows_ip(c, ra, G, level, sum, acc, s, u0, v != nullptr, false, groups);
 }
 
 // HY_FUSE_IP=0 / HY_FUSE_MD=0 run the unfused ModUp NTT + IP / ModDown NTT + epilogue (A/B measurements)
@@ -1139,6 +1139,101 @@ hy_status hrot_sum_finish(hy_ctx* c, uint32_t level, const uint64_t* u, const ui
   const size_t nl = level + 1, N = c->N;
   DownItem di{u, out, acc, 1, acc + nl * N, nullptr, it[0].v, it[0].w};
   moddown_batch(c, level, 2, 1, &di, s);
+  return HY_OK;
+}
+
+// The lazy HRotSums of O outputs over the same n rotations (RAConv_Reorder: every output sums its f^2 tap
+// accumulators with the same tap amounts): out_o = sum_t HRot_{r_t}(cts[o n + t]).  Each output's terms
+// are the same operations as hy_hrot_sum's (bit-identical), batched over the outputs: one inverse row pass, one
+// ModUp column kernel and one grouped summed IP for all O x T key-switched terms, one ModDown for the O sums.
+// Returns HY_E_WORKSPACE (nothing launched) when the O x T items or the O accumulators do not fit; callers then
+// fall back to hy_hrot_sum per output.
+hy_status hrot_sum_multi(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,
+                         const int32_t* r, uint32_t n, uint32_t O, uint64_t* const* outs, cudaStream_t s) {
+  static const bool on = env_int("HY_SUM_MULTI", 1) != 0;  // HY_SUM_MULTI=0: one hy_hrot_sum per output (A/B)
+  if (!on || !(fuse_ip() && modup_cols_ok(c) && sum_tma_on())) return HY_E_WORKSPACE;
+  const size_t nl = level + 1, N = c->N;
+  std::vector<uint32_t> ks, zero;
+  for (uint32_t t = 0; t < n; ++t) {
+    if (hy_galois_elt(c, r[t]) == 1) {
+      zero.push_back(t);
+    } else {
+      if (!evks[t]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
+      ks.push_back(t);
+    }
+  }
+  const int T = (int)ks.size();
+  const int cap = max_items(c, level);
+  if (T == 0 || cap < 4) return HY_E_WORKSPACE;
+  const uint32_t oc = (uint32_t)std::min(cap / T, cap / 2);  // outputs per launch set
+  if (oc < 2) return HY_E_WORKSPACE;
+  if (O > oc) {  // chunks of oc outputs (stream-ordered: each chunk reuses the workspace after the previous one)
+    for (uint32_t o0 = 0; o0 < O; o0 += oc) {
+      const uint32_t on = std::min(oc, O - o0);
+      hy_status st2 = on >= 2 ? hrot_sum_multi(c, evks, cts + (size_t)o0 * n, level, r, n, on, outs + o0, s)
+                               : HY_E_WORKSPACE;
+      if (st2 == HY_E_WORKSPACE) st2 = hy_hrot_sum(c, evks, cts + (size_t)o0 * n, level, r, n, outs[o0], s);
+      if (st2 != HY_OK) return st2;
+    }
+    return HY_OK;
+  }
+  if (O < 2) return HY_E_WORKSPACE;
+  const int G = (int)O * T;
+  KsItem it[kG];
+  hy_status s0 = carve(c, level, cap, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  // accumulators: (sum_t kappa_t(c0_t) incl. the r = 0 terms' c0, sum of the r = 0 terms' c1) of output o in the
+  // w buffer of item O + o (the summed IP uses only d / ext / u; ModDown's scratch is items 0 .. O - 1)
+  std::vector<uint64_t*> acc(O), u(O);
+  for (uint32_t o = 0; o < O; ++o) {
+    acc[o] = it[O + o].w;
+    u[o] = it[o].u;
+  }
+  uint64_t kk[kG];
+  for (int t = 0; t < T; ++t) kk[t] = hy_galois_elt(c, r[ks[t]]);
+  for (uint32_t o = 0; o < O; ++o) {
+    const uint64_t* const* co = cts + (size_t)o * n;
+    uint64_t* acc0 = acc[o];
+    uint64_t* acc1 = acc[o] + nl * N;
+    cudaMemsetAsync(acc[o], 0, 2 * nl * N * 8, s);
+    for (uint32_t t : zero) {
+      automorph(c, co[t], acc0, nl, nl, 1, true, s);
+      automorph(c, co[t] + nl * N, acc1, nl, nl, 1, true, s);
+    }
+    Arr<const uint64_t*> ai{};
+    Arr<uint64_t> ak{};
+    for (int t = 0; t < T; ++t) {
+      ai.p[t] = co[ks[t]];
+      ak.p[t] = kk[t];
+    }
+    dim3 grid(c->N / kT, nl);
+    KTimer kt(c, FAM_AUT, s);
+    kt.bytes = ((uint64_t)T + 2) * nl * N * 8;
+    k_automorph_sum<<<grid, kT, 0, s>>>(ai, ak, T, acc0, c->log_n, (int)nl, c->dt);
+  }
+  // item g = o T + t: c1 of output o's term ks[t]
+  const uint64_t* c1[kG];
+  uint64_t* d[kG];
+  uint64_t* ext[kG];
+  const uint64_t* keys[kG];
+  uint64_t kg[kG];
+  RowsAutArgs ra{};
+  for (int g = 0; g < G; ++g) {
+    const int o = g / T, t = g % T;
+    c1[g] = cts[(size_t)o * n + ks[t]] + nl * N;
+    d[g] = it[g].d;
+    ext[g] = it[g].ext;
+    keys[g] = evks[ks[t]];
+    kg[g] = kk[t];
+    ra.src[g] = c1[g];
+    ra.dst[g] = d[g];
+    ra.k[g] = kg[g];
+  }
+  launch_ntt_rows_inv_aut(c, ra, G, level, s);
+  modup_ip_fused(c, level, G, d, ext, c1, keys, u.data(), false, true, s, 0, nullptr, true, kg, (int)O);
+  std::vector<DownItem> di(O);
+  for (uint32_t o = 0; o < O; ++o) di[o] = DownItem{u[o], outs[o], acc[o], 1, acc[o] + nl * N, nullptr, it[o].v, it[o].w};
+  moddown_batch(c, level, 2, (int)O, di.data(), s);
   return HY_OK;
 }
 

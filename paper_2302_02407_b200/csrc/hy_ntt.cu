@@ -910,8 +910,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
   const double q = pc.qd, qinv = pc.qinv;
   const size_t roff = (size_t)row * 256;
   const int last = G * B - 1;
+  const int gb = blockIdx.x * G;  // grouped (round 2): output blockIdx.x sums items gb .. gb + G - 1
   auto issue = [&](int it) {
-    const int g = it / B, j = it % B;
+    const int g = gb + it / B, j = it % B;
     double* b = T + 256 + 768 * (it % NST);
     uint64_t* mb = mbar + it % NST;
     const uint64_t* e0 = evk_limb(a.evk[g], (size_t)(j * 2) * L1 + t, N) + roff / 4 * 3;
@@ -944,7 +945,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
     double x[8];
     const uint64_t* xb = reinterpret_cast<const uint64_t*>(b + 512);
     if (j == own_digit) {
-      const uint64_t kx = a.kx[it / B];
+      const uint64_t kx = a.kx[gb + it / B];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t xi = (uint32_t)(roff + elem<3>(l, k));
@@ -982,8 +983,8 @@ __global__ void __launch_bounds__(256, 2) k_rows_ip_sum_tma(const __grid_constan
       __syncwarp();
     }
   }
-  store_l3(a.out[0] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
-  store_l3(a.out[0] + ((size_t)E + u) * N + roff, l, a1, q, qinv, accumulate);
+  store_l3(a.out[blockIdx.x] + (size_t)u * N + roff, l, a0, q, qinv, accumulate);
+  store_l3(a.out[blockIdx.x] + ((size_t)E + u) * N + roff, l, a1, q, qinv, accumulate);
 }
 
 // P limbs of the IP (split ModDown) on the same bulk-copy ring: grid (G, R/8, K); a.out[g] = v_g [2][K][N]
@@ -1294,7 +1295,7 @@ bool sum_tma_on() {
 }
 
 void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, bool sum, bool accumulate,
-                        cudaStream_t s, int u0, bool inv_p, bool hoist) {
+                        cudaStream_t s, int u0, bool inv_p, bool hoist, int groups) {
   if (G <= 0) return;
   const int n = (int)level + 1, E = n + (int)c->n_p, beta = (int)n_digits(c, level), R = (int)(c->N / 256);
   const int nu = E - u0;  // extended limbs produced
@@ -1315,7 +1316,9 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
       fa.evk[g] = a.evk[g];
       fa.kx[g] = a.kx[g] ? a.kx[g] : 1;
     }
-    fa.out[0] = a.u[0];
+    const int per = G / groups;  // items per output (grouped lazy sums)
+    for (int o = 0; o < groups; ++o) fa.out[o] = a.u[o * per];
+    grid.x = groups;
     const size_t smem = rows_tma_smem(2);
     const int L1s = (int)(c->n_q + c->n_p), lv = (int)level, al = (int)c->alpha, lg = (int)c->log_n;
 #define HY_ST(BB)                                                                                              \
@@ -1325,7 +1328,7 @@ void launch_ntt_rows_ip(hy_ctx* c, const RowsIpArgs& a, int G, uint32_t level, b
       cudaFuncSetAttribute(k_rows_ip_sum_tma<BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
       at = true;                                                                                               \
     }                                                                                                          \
-    k_rows_ip_sum_tma<BB><<<grid, 256, smem, s>>>(fa, G, c->dt, lv, L1s, E, al, lg, accumulate ? 1 : 0);      \
+    k_rows_ip_sum_tma<BB><<<grid, 256, smem, s>>>(fa, per, c->dt, lv, L1s, E, al, lg, accumulate ? 1 : 0);    \
   } break;
     switch (beta) {
       HY_ST(1)
