@@ -698,23 +698,37 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
     uint64_t* sbuf = scratch;
     for (int64_t i = 0; i < p->n_in && pre_slid; ++i)
       for (size_t t = 0; t < f2; ++t) slid[i][t] = pre_slid + ((size_t)i * f2 + t) * ct_l;
-    for (int64_t i = 0; i < p->n_in && !pre_slid; ++i) {
+    if (!pre_slid) {
+      // every input rotates by the same tap amounts: one batched hoisted launch set for all inputs (round 2), else
+      // one hy_hrot_hoisted per input
       std::vector<int32_t> rs;
       std::vector<const uint64_t*> ks;
-      std::vector<uint64_t*> outs;
-      for (size_t t = 0; t < f2; ++t) {
-        if (p->taps[t] % p->n == 0) {
-          slid[i][t] = in[i];
-          continue;
+      for (size_t t = 0; t < f2; ++t)
+        if (p->taps[t] % p->n != 0) {
+          rs.push_back((int32_t)p->taps[t]);
+          ks.push_back(x.key(p->taps[t]));
         }
-        uint64_t* o = sbuf + ((size_t)i * f2 + t) * ct_l;
-        slid[i][t] = o;
-        rs.push_back((int32_t)p->taps[t]);
-        ks.push_back(x.key(p->taps[t]));
-        outs.push_back(o);
-      }
+      std::vector<uint64_t*> outs;  // [input][rotation]
+      for (int64_t i = 0; i < p->n_in; ++i)
+        for (size_t t = 0; t < f2; ++t) {
+          if (p->taps[t] % p->n == 0) {
+            slid[i][t] = in[i];
+            continue;
+          }
+          uint64_t* o = sbuf + ((size_t)i * f2 + t) * ct_l;
+          slid[i][t] = o;
+          outs.push_back(o);
+        }
       if (!rs.empty()) {
-        stt = hy_hrot_hoisted(c, ks.data(), in[i], level, rs.data(), (uint32_t)rs.size(), outs.data(), stream);
+        const uint32_t nr = (uint32_t)rs.size();
+        stt = p->n_in >= 2 ? hrot_hoisted_multi(c, ks.data(), in, (uint32_t)p->n_in, level, rs.data(), nr,
+                                                outs.data(), x.s)
+                           : HY_E_WORKSPACE;
+        if (stt == HY_E_WORKSPACE)
+          for (int64_t i = 0; i < p->n_in; ++i) {
+            stt = hy_hrot_hoisted(c, ks.data(), in[i], level, rs.data(), nr, outs.data() + (size_t)i * nr, stream);
+            if (stt != HY_OK) return stt;
+          }
         if (stt != HY_OK) return stt;
       }
     }
@@ -896,25 +910,36 @@ extern "C" hy_status hy_caconv_slide(hy_ctx* c, const hy_conv_plan* p, const uin
   if (in_begin > in_end || in_end > p->n_in) return fail(HY_E_PLAN, "input range outside the plan");
   const size_t f2 = (size_t)p->s.f * p->s.f, ct_l = 2ull * (level + 1) * c->N;
   Ctx x{c, p, evks, st(stream)};
+  std::vector<int32_t> rs;
+  std::vector<const uint64_t*> ks;
+  for (size_t t = 0; t < f2; ++t)
+    if (p->taps[t] % p->n != 0) {
+      rs.push_back((int32_t)p->taps[t]);
+      ks.push_back(x.key(p->taps[t]));
+    }
+  std::vector<uint64_t*> outs;  // [input][rotation]
   for (uint32_t i = in_begin; i < in_end; ++i) {
     if (!in[i]) return fail(HY_E_ARG, "null input ciphertext");
-    std::vector<int32_t> rs;
-    std::vector<const uint64_t*> ks;
-    std::vector<uint64_t*> outs;
     for (size_t t = 0; t < f2; ++t) {
       uint64_t* o = slid + ((size_t)(i - in_begin) * f2 + t) * ct_l;
       if (p->taps[t] % p->n == 0) {
         cudaMemcpyAsync(o, in[i], ct_l * 8, cudaMemcpyDeviceToDevice, x.s);
         continue;
       }
-      rs.push_back((int32_t)p->taps[t]);
-      ks.push_back(x.key(p->taps[t]));
       outs.push_back(o);
     }
-    if (!rs.empty()) {
-      hy_status stt = hy_hrot_hoisted(c, ks.data(), in[i], level, rs.data(), (uint32_t)rs.size(), outs.data(), stream);
-      if (stt != HY_OK) return stt;
-    }
+  }
+  const uint32_t ni = in_end - in_begin, nr = (uint32_t)rs.size();
+  if (nr && ni) {  // the inputs' hoisted Slides batched (as in hy_caconv), else one hy_hrot_hoisted per input
+    hy_status stt = ni >= 2 ? hrot_hoisted_multi(c, ks.data(), in + in_begin, ni, level, rs.data(), nr, outs.data(), x.s)
+                            : HY_E_WORKSPACE;
+    if (stt == HY_E_WORKSPACE)
+      for (uint32_t i = 0; i < ni; ++i) {
+        stt = hy_hrot_hoisted(c, ks.data(), in[in_begin + i], level, rs.data(), nr, outs.data() + (size_t)i * nr,
+                              stream);
+        if (stt != HY_OK) return stt;
+      }
+    if (stt != HY_OK) return stt;
   }
   return cuda_check("hy_caconv_slide");
 }

@@ -232,6 +232,10 @@ void launch_ntt_rows_inv_aut(hy_ctx* c, const RowsAutArgs& a, int G, uint32_t le
 // the summed (lazy HRotSum) IP runs on the bulk-copy ring (HY_SUMTMA, default on); it can read the own digit
 // through kappa, so the lazy path then fuses kappa into the inverse row pass
 bool sum_tma_on();
+// the hoisted rotations of I ciphertexts by the same n amounts, batched (hy_keyswitch.cu); HY_E_WORKSPACE: not
+// batchable here (nothing launched), call hy_hrot_hoisted per input
+hy_status hrot_hoisted_multi(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t I,
+                             uint32_t level, const int32_t* r, uint32_t n, uint64_t* const* outs, cudaStream_t s);
 // the lazy HRotSums of O outputs over the same n rotations, batched (hy_keyswitch.cu); HY_E_WORKSPACE: not
 // batchable here (nothing launched), call hy_hrot_sum per output
 hy_status hrot_sum_multi(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t level,

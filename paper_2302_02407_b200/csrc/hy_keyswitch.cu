@@ -1028,6 +1028,83 @@ extern "C" hy_status hy_hrot_hoisted(hy_ctx* c, const uint64_t* const* evks, con
 
 namespace hy {
 
+// The hoisted rotations of I ciphertexts by the same n amounts (CAConv Slide_f over the layer's inputs),
+// batched: the I ModUps in one launch set, then all I x n (input, rotation) items' P-limb IP, ModDown columns and
+// Q-limb IP + epilogue together; each item's operations are hy_hrot_hoisted's (bit-identical).  outs[i n + t] =
+// HRot_{r_t}(cts[i]); every r_t must need a key switch.  HY_E_WORKSPACE: not batchable here (nothing launched),
+// call hy_hrot_hoisted per input.
+hy_status hrot_hoisted_multi(hy_ctx* c, const uint64_t* const* evks, const uint64_t* const* cts, uint32_t I,
+                             uint32_t level, const int32_t* r, uint32_t n, uint64_t* const* outs, cudaStream_t s) {
+  static const bool on = env_int("HY_HOIST_MULTI", 1) != 0;  // HY_HOIST_MULTI=0: hy_hrot_hoisted per input (A/B)
+  if (!on || I < 2 || n == 0 || !split_moddown() || !moddown_cols_ok(c)) return HY_E_WORKSPACE;
+  const size_t nl = level + 1, N = c->N;
+  for (uint32_t t = 0; t < n; ++t) {
+    if (hy_galois_elt(c, r[t]) == 1) return HY_E_WORKSPACE;
+    if (!evks[t]) return fail(HY_E_MISSING_KEY, "no evaluation key for rotation");
+  }
+  for (size_t k = 0; k < (size_t)I * n; ++k)
+    for (uint32_t i = 0; i < I; ++i)
+      if (outs[k] == cts[i]) return HY_E_WORKSPACE;
+  const int cap = max_items(c, level);
+  const uint32_t ic = cap / (int)n;  // inputs per launch set
+  if (ic < 2) return HY_E_WORKSPACE;
+  if (I > ic) {
+    for (uint32_t i0 = 0; i0 < I; i0 += ic) {
+      const uint32_t in_ = std::min(ic, I - i0);
+      hy_status st2 = in_ >= 2 ? hrot_hoisted_multi(c, evks, cts + i0, in_, level, r, n, outs + (size_t)i0 * n, s)
+                               : HY_E_WORKSPACE;
+      if (st2 == HY_E_WORKSPACE) st2 = hy_hrot_hoisted(c, evks, cts[i0], level, r, n, outs + (size_t)i0 * n, s);
+      if (st2 != HY_OK) return st2;
+    }
+    return HY_OK;
+  }
+  KsItem it[kG];
+  hy_status s0 = carve(c, level, cap, it, nullptr);
+  if (s0 != HY_OK) return s0;
+  // one ModUp per input into item i's d / ext (the rotation items use only their u / v / w)
+  const uint64_t* c1[kG];
+  uint64_t* dd[kG];
+  uint64_t* ee[kG];
+  for (uint32_t i = 0; i < I; ++i) {
+    c1[i] = cts[i] + nl * N;
+    dd[i] = it[i].d;
+    ee[i] = it[i].ext;
+  }
+  intt_polys(c, (int)I, c1, dd, level, s);
+  modup_batch(c, level, (int)I, (const uint64_t* const*)dd, ee, s);
+  const int G = (int)(I * n);
+  RowsIpArgs ra{};
+  IpFinalArgs fa{};
+  uint64_t* u[kG];
+  uint64_t* v[kG];
+  uint64_t* w[kG];
+  for (int g = 0; g < G; ++g) {
+    const uint32_t i = g / n, t = g % n;
+    const uint64_t kk = hy_galois_elt(c, r[t]);
+    u[g] = it[g].u;
+    v[g] = it[g].v;
+    w[g] = it[g].w;
+    ra.ext[g] = ee[i];
+    ra.own[g] = c1[i];
+    ra.evk[g] = evks[t];
+    ra.u[g] = u[g];
+    ra.v[g] = v[g];
+    ra.kx[g] = kk;
+    fa.ext[g] = ee[i];
+    fa.own[g] = c1[i];
+    fa.evk[g] = evks[t];
+    fa.w[g] = w[g];
+    fa.add0[g] = cts[i];
+    fa.k0[g] = kk;
+    fa.out[g] = outs[g];
+    fa.kx[g] = kk;
+  }
+  launch_ntt_rows_ip(c, ra, G, level, false, false, s, (int)nl, true, true);
+  moddown_p(c, level, G, u, v, w, s, true);
+  launch_rows_ip_final(c, fa, G, level, true, s);
+  return HY_OK;
+}
+
 // The lazy HRotSum state of n terms (hy_hrot_sum before its ModDown, DESIGN R-HROT):
 //   u   [2][l+1+K][N]  sum_t of the key-switch inner products IP_t(kappa_t(c1_t)) over Q_l u P (NTT, canonical;
 //                      zero when no term needs a key switch)
