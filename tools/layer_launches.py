@@ -8,7 +8,7 @@ import paper_2302_02407_b200 as hy
 which = sys.argv[1] if len(sys.argv) > 1 else "r18:L1_ca"
 net, lname = which.split(":")
 table = bench.R18_LAYERS if net == "r18" else bench.R20_LAYERS
-ctx = hy.Context(**synth.PARAMS["hyp"])
+ctx = hy.Context(**synth.PARAMS["hyp"], max_batch=64)  # as bench.py
 name, spec, mult = next(l for l in table if l[0] == lname)
 ci, co, w, f, s, wp, g, m, d, algo = spec[:10]
 S = spec[10] if len(spec) > 10 else 1
