@@ -651,16 +651,19 @@ hy_status ra_taps(const Ctx& x, const uint64_t* const* in, uint32_t level, const
                   size_t tb, size_t te, uint64_t* const* accs) {
   const hy_conv_plan* p = x.p;
   const size_t J = (size_t)p->n_in;
-  std::vector<uint32_t> bidx(J);
-  std::vector<uint64_t> bgal(J);
-  for (size_t t = tb; t < te; ++t) {
-    for (size_t i = 0; i < J; ++i) {
-      const auto tm = p->term(o, (int64_t)i, (int64_t)t);
-      bidx[i] = (uint32_t)tm.first;
-      bgal[i] = hy_galois_elt(x.c, tm.second);
-    }
-    uint64_t* dst = accs[t - tb];
-    hy_status st = pmult_block(x.c, in, (uint32_t)J, &dst, 1, wpt, bidx.data(), bgal.data(), level, 0, x.s);
+  // the taps' accumulators share the operands: blocks of up to 8 taps per MulFilter&Sum launch
+  for (size_t t0 = tb; t0 < te; t0 += 8) {
+    const size_t M = std::min<size_t>(8, te - t0);
+    std::vector<uint32_t> bidx(M * J);
+    std::vector<uint64_t> bgal(M * J);
+    for (size_t m = 0; m < M; ++m)
+      for (size_t i = 0; i < J; ++i) {
+        const auto tm = p->term(o, (int64_t)i, (int64_t)(t0 + m));
+        bidx[m * J + i] = (uint32_t)tm.first;
+        bgal[m * J + i] = hy_galois_elt(x.c, tm.second);
+      }
+    hy_status st = pmult_block(x.c, in, (uint32_t)J, accs + (t0 - tb), (uint32_t)M, wpt, bidx.data(), bgal.data(),
+                               level, 0, x.s);
     if (st != HY_OK) return st;
   }
   return HY_OK;
@@ -817,7 +820,28 @@ hy_status conv_core(hy_ctx* c, const hy_conv_plan* p, const uint64_t* const* evk
     keys[t] = (p->taps[t] % p->n) ? x.key(p->taps[t]) : nullptr;
   }
   const size_t J = (size_t)p->n_in;
-  for (size_t t = 0; t < f2; ++t)
+  if (oe - ob < 8) {  // fewer than 8 outputs (ResNet-20 RAConv: one): blocks of 8 (output, tap) accumulators,
+    // which all read the same n_in operands, instead of one launch per tap with the few outputs
+    std::vector<std::pair<uint32_t, size_t>> pr;  // (output, tap)
+    for (uint32_t o = ob; o < oe; ++o)
+      for (size_t t = 0; t < f2; ++t) pr.emplace_back(o, t);
+    for (size_t k0 = 0; k0 < pr.size(); k0 += 8) {
+      const size_t M = std::min<size_t>(8, pr.size() - k0);
+      bidx.assign(M * J, 0);
+      bgal.assign(M * J, 1);
+      std::vector<uint64_t*> outs(M);
+      for (size_t m = 0; m < M; ++m) {
+        const uint32_t o = pr[k0 + m].first;
+        const size_t t = pr[k0 + m].second;
+        outs[m] = accs + ((o - ob) * f2 + t) * ct_l;
+        for (size_t i = 0; i < J; ++i) set_term(m, J, i, o, (int64_t)i, (int64_t)t);
+      }
+      stt = pmult_block(c, in, (uint32_t)J, outs.data(), (uint32_t)M, wpt, bidx.data(), bgal.data(), level, 0,
+                        stream);
+      if (stt != HY_OK) return stt;
+    }
+  }
+  for (size_t t = 0; t < f2 && oe - ob >= 8; ++t)
     for (uint32_t o0 = ob; o0 < oe; o0 += 8) {
       const size_t M = std::min<size_t>(8, oe - o0);
       bidx.assign(M * J, 0);
